@@ -1,0 +1,158 @@
+/*
+ * diaq_b200.h -- C-ABI of the B200-native DiaQ hot path (arXiv 2405.01250).
+ *
+ * The reference (/root/reference/pkg/src/diaqsim) is a pure Python package
+ * with no native ABI; its drop-in boundary is the Python API re-exported by
+ * diaqsim/__init__.py:5-70 (and the `kernel` JSON protocol, cli.py:251-287).
+ * Every entry point below replaces one reference function; the Python host
+ * mirror (paper_2405_01250_b200/) binds them with ctypes exactly the way
+ * INTEGRATION.md shows a diaqsim maintainer would.
+ *
+ * Conventions (reference matrix.py:1-14): d = col - row; diagonal d holds
+ * n-|d| values; element (r, r+d) is at storage position k = r + min(d,0).
+ * On the device a matrix is one complex128 arena (interleaved re,im = one
+ * 16-byte load per element) plus a host offset table:
+ *   - offs[i]   ascending diagonal offsets (int64),
+ *   - starts[i] element index of k=0 of diagonal i inside the arena, chosen
+ *     by diaq_layout() so that row r of every diagonal sits at a 128-byte
+ *     aligned address whenever r % 8 == 0 ("row-aligned" padding),
+ *   - vals      device pointer to the arena (cudaMalloc / torch storage).
+ * State vectors are device complex128 arrays (reference sim.py:36).
+ *
+ * All functions are stream-ordered (cudaStream_t passed as void*), never
+ * synchronise unless documented, are reentrant per stream, and return a
+ * diaq_status (0 = OK).  No CPU fallback exists: without a CUDA device
+ * every compute entry point returns DIAQ_ERR_CUDA.
+ */
+#ifndef DIAQ_B200_H
+#define DIAQ_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes; the Python mirror maps them onto the reference exception
+ * types (reference errors.py:9-46) */
+typedef enum {
+    DIAQ_OK = 0,
+    DIAQ_ERR_SHAPE = 1,     /* -> ShapeError ("not multiplyable: ..."), matrix.py:227-229,262-263 */
+    DIAQ_ERR_VALUE = 2,     /* -> ValueError (bad offset / argument), matrix.py:33-34 */
+    DIAQ_ERR_RESOURCE = 3,  /* -> ResourceError (size guard), sim.py:55-56, gates.py:237-240 */
+    DIAQ_ERR_CUDA = 4,      /* CUDA runtime failure (no device, launch error, OOM) */
+    DIAQ_ERR_UNSUPPORTED = 5
+} diaq_status;
+
+/* complex-multiply rounding of the gate apply: numpy's complex128 multiply
+ * on AVX-512 hosts is re=fma(vr,xr,-(vi*xi)), im=fma(vr,xi,vi*xr)
+ * (reference sim.py:76-78); PLAIN is the textbook four-product form. */
+#define DIAQ_CMUL_PLAIN 0
+#define DIAQ_CMUL_FMA 1
+
+/* a device-resident DiaQ matrix (replaces reference DiaqMatrix,
+ * matrix.py:50-123; the dict of Diagonal objects becomes offs/starts/vals) */
+typedef struct {
+    int64_t n;              /* n_dim */
+    int64_t nd;             /* number of stored diagonals */
+    const int64_t *offs;    /* host, ascending, nd entries */
+    const int64_t *starts;  /* host, element start of diagonal i in vals */
+    void *vals;             /* device complex128 arena */
+} diaq_matrix_t;
+
+/* ---- library / diagnostics ------------------------------------------- */
+int diaq_version(void);
+const char *diaq_last_error(void);               /* thread-local message */
+int diaq_device_count(int *count);
+uint64_t diaq_launch_count(void);                /* kernels launched by this library */
+void diaq_reset_launch_count(void);
+
+/* ---- layout (host only) ----------------------------------------------
+ * Row-aligned storage starts for a diagonal set; returns total arena
+ * elements in *total.  Replaces the per-diagonal aligned_zeros of
+ * reference alloc.py:15-24 / matrix.py:75-76.  Offsets must be strictly
+ * ascending with |d| <= n-1 (reference diag_len, matrix.py:31-35). */
+int diaq_layout(int64_t n, int64_t nd, const int64_t *offs, int64_t *starts, int64_t *total);
+
+/* ---- construction ----------------------------------------------------- */
+/* I_left (x) m (x) I_right into a pre-laid-out `out` whose offs are
+ * m.offs * right (reference kron_identity, matrix.py:358-387). */
+int diaq_kron_identity(int64_t left, const diaq_matrix_t *m, int64_t right, diaq_matrix_t *out,
+                       void *stream);
+
+/* offsets of build_span_unitary(g, positions, span) (reference
+ * gates.py:169-219): g is a HOST dense 2^k x 2^k complex128 row-major
+ * matrix; offs_out has room for 4^k entries. */
+int diaq_span_plan(int k, const double *g_host, const int *positions, int span, int64_t *offs_out,
+                   int64_t *nd_out);
+/* fill a pre-laid-out span matrix on the device */
+int diaq_span_expand(int k, const double *g_host, const int *positions, int span,
+                     diaq_matrix_t *out, void *stream);
+
+/* from_dense (reference matrix.py:135-153), device dense n x n complex128
+ * row-major.  Pass 1 writes keep[d+n-1] in {0,1} for all 2n-1 diagonals
+ * (|re|+|im| > eps anywhere); pass 2 gathers the kept diagonals into `out`. */
+int diaq_from_dense_scan(int64_t n, const void *dense, double eps, uint8_t *keep_dev,
+                         void *stream);
+int diaq_from_dense_fill(const void *dense, diaq_matrix_t *out, void *stream);
+/* to_dense (reference matrix.py:156-167) into a zeroed device n x n buffer */
+int diaq_to_dense(const diaq_matrix_t *a, void *dense, void *stream);
+
+/* ---- spmv (reference matrix.py:253-278) -------------------------------
+ * y = A x, bitwise equal to the reference (ascending d, no FMA). */
+int diaq_spmv(const diaq_matrix_t *a, const void *x, void *y, void *stream);
+
+/* ---- spgemm (reference matrix.py:173-250) -----------------------------
+ * plan (host): candidate result offsets (sorted), nc <= nda*ndb. */
+int diaq_spgemm_plan(int64_t n, int64_t nda, const int64_t *offa, int64_t ndb, const int64_t *offb,
+                     int64_t *offc, int64_t *nc);
+/* device workspace bytes needed by diaq_spgemm for these operands */
+int64_t diaq_spgemm_workspace(int64_t nda, int64_t ndb, int64_t nc);
+/* multiply into the candidate layout `c` and flag keep_dev[i] = 1 iff
+ * candidate i has an element with |re|+|im| > prune_eps (matrix.py:246-249) */
+int diaq_spgemm(const diaq_matrix_t *a, const diaq_matrix_t *b, diaq_matrix_t *c,
+                uint8_t *keep_dev, double prune_eps, void *workspace, int64_t workspace_bytes,
+                void *stream);
+
+/* ---- gate application (reference sim.py:69-105) -----------------------
+ * Generic placement: y = (I_dim_a (x) m (x) I_dim_b) x over the stored
+ * diagonals of m (any m).  y must not alias x. */
+int diaq_apply_placed(int64_t dim_a, const diaq_matrix_t *m, int64_t dim_b, const void *x, void *y,
+                      int cmul_mode, void *stream);
+
+/* Compact Kronecker-structured gate: a k-qubit gate g (HOST dense 2^k x 2^k,
+ * row-major complex128) acting on state bits shifts[0..k-1] (operand 0 =
+ * most significant gate-index bit) of an N = 2^n_bits state.  Equals
+ * apply_placed of the placement compile_circuit builds for it (incl. the
+ * build_span_unitary embedding, gates.py:169-219, 242-245) with the same
+ * per-element summation order.  In place allowed (x == y).  k <= 5. */
+int diaq_apply_gate(int n_bits, int k, const double *g_host, const int *shifts, const void *x,
+                    void *y, int cmul_mode, void *stream);
+
+/* a compiled gate for the native program runner */
+typedef struct {
+    int k;                  /* gate qubits (<= 5) */
+    int shifts[5];          /* state bit of operand i (operand 0 = MSB) */
+    const double *g;        /* HOST dense 2^k x 2^k complex128 */
+} diaq_gate_t;
+
+/* Apply `ngates` compact gates in order to `state` (in place) on one
+ * stream: the device loop of reference run(), sim.py:193-199.  If events
+ * is non-NULL it must hold ngates+1 cudaEvent_t recorded around each gate
+ * (per-gate timings, resolved by the caller after the loop). */
+int diaq_run_gates(int n_bits, int ngates, const diaq_gate_t *gates, void *state, int cmul_mode,
+                   void **events, void *stream);
+
+/* ---- state helpers ------------------------------------------------------ */
+/* |index> (reference init_state, sim.py:53-59) */
+int diaq_init_basis(int64_t n_amps, void *x, int64_t index, void *stream);
+/* sum |x_i|^2 (reference StateVector.norm, sim.py:38-39, squared) into
+ * work_dev[0]; work_dev holds DIAQ_NORM_WORK device doubles (partials in
+ * 1..); fixed two-pass order, so repeated calls are bitwise identical. */
+#define DIAQ_NORM_WORK 1025
+int diaq_norm2(int64_t n_amps, const void *x, double *work_dev, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DIAQ_B200_H */

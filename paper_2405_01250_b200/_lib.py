@@ -1,0 +1,195 @@
+"""ctypes binding of the in-tree CUDA library libdiaq_b200.so (include/diaq_b200.h).
+
+There is no CPU fallback: if the library or a CUDA device is missing, every
+compute call raises DeviceError.  Device memory and streams come from
+PyTorch (plumbing only); pointers and the current stream handle are passed
+to the C-ABI as plain integers.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .errors import DiaqError, ResourceError, ShapeError, UnsupportedFeatureError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdiaq_b200.so")
+
+DIAQ_OK = 0
+DIAQ_ERR_SHAPE = 1
+DIAQ_ERR_VALUE = 2
+DIAQ_ERR_RESOURCE = 3
+DIAQ_ERR_CUDA = 4
+DIAQ_ERR_UNSUPPORTED = 5
+DIAQ_NORM_WORK = 1025
+
+CMUL_PLAIN = 0
+CMUL_FMA = 1
+
+
+class DeviceError(DiaqError, RuntimeError):
+    """The CUDA library is missing or a device call failed."""
+
+
+class Matrix(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int64),
+        ("nd", ctypes.c_int64),
+        ("offs", ctypes.c_void_p),
+        ("starts", ctypes.c_void_p),
+        ("vals", ctypes.c_void_p),
+    ]
+
+
+class Gate(ctypes.Structure):
+    _fields_ = [
+        ("k", ctypes.c_int),
+        ("shifts", ctypes.c_int * 5),
+        ("g", ctypes.c_void_p),
+    ]
+
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_INT = ctypes.c_int
+_MP = ctypes.POINTER(Matrix)
+
+_SIGS = {
+    "diaq_version": ([], _INT),
+    "diaq_last_error": ([], ctypes.c_char_p),
+    "diaq_device_count": ([ctypes.POINTER(_INT)], _INT),
+    "diaq_launch_count": ([], ctypes.c_uint64),
+    "diaq_reset_launch_count": ([], None),
+    "diaq_layout": ([_I64, _I64, _P, _P, _P], _INT),
+    "diaq_kron_identity": ([_I64, _MP, _I64, _MP, _P], _INT),
+    "diaq_span_plan": ([_INT, _P, _P, _INT, _P, _P], _INT),
+    "diaq_span_expand": ([_INT, _P, _P, _INT, _MP, _P], _INT),
+    "diaq_from_dense_scan": ([_I64, _P, ctypes.c_double, _P, _P], _INT),
+    "diaq_from_dense_fill": ([_P, _MP, _P], _INT),
+    "diaq_to_dense": ([_MP, _P, _P], _INT),
+    "diaq_spmv": ([_MP, _P, _P, _P], _INT),
+    "diaq_spgemm_plan": ([_I64, _I64, _P, _I64, _P, _P, _P], _INT),
+    "diaq_spgemm_workspace": ([_I64, _I64, _I64], _I64),
+    "diaq_spgemm": ([_MP, _MP, _MP, _P, ctypes.c_double, _P, _I64, _P], _INT),
+    "diaq_apply_placed": ([_I64, _MP, _I64, _P, _P, _INT, _P], _INT),
+    "diaq_apply_gate": ([_INT, _INT, _P, _P, _P, _P, _INT, _P], _INT),
+    "diaq_run_gates": ([_INT, _INT, ctypes.POINTER(Gate), _P, _INT, _P, _P], _INT),
+    "diaq_init_basis": ([_I64, _P, _I64, _P], _INT),
+    "diaq_norm2": ([_I64, _P, _P, _P], _INT),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+_load_error = None
+
+
+def load():
+    """Load the CUDA library (once); raise DeviceError if it is absent."""
+    global _lib, _load_error
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise DeviceError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2405_01250_b200.build` "
+            "(no CPU fallback exists)")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    msg = load().diaq_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc: int, what: str) -> None:
+    """Map a diaq_status onto the reference's exception types."""
+    if rc == DIAQ_OK:
+        return
+    msg = last_error() or what
+    if rc == DIAQ_ERR_SHAPE:
+        raise ShapeError(msg)
+    if rc == DIAQ_ERR_VALUE:
+        raise ValueError(msg)
+    if rc == DIAQ_ERR_RESOURCE:
+        raise ResourceError(msg)
+    if rc == DIAQ_ERR_UNSUPPORTED:
+        raise UnsupportedFeatureError(msg)
+    raise DeviceError(f"{what}: {msg}")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)
+
+
+def launch_count() -> int:
+    return int(load().diaq_launch_count())
+
+
+# ---- torch plumbing ----------------------------------------------------------
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+        _torch = t
+    return _torch
+
+
+def device():
+    t = torch()
+    if not t.cuda.is_available():
+        raise DeviceError("no CUDA device visible: the DiaQ B200 path has no CPU fallback")
+    return t.device("cuda", t.cuda.current_device())
+
+
+def stream_handle() -> int:
+    return int(torch().cuda.current_stream().cuda_stream)
+
+
+def empty_c128(n: int):
+    t = torch()
+    try:
+        return t.empty(int(n), dtype=t.complex128, device=device())
+    except t.cuda.OutOfMemoryError as e:  # size guard, like the reference's ResourceError
+        raise ResourceError(f"cannot allocate {int(n) * 16} bytes on the device: {e}") from e
+
+
+def to_device_c128(a):
+    """numpy/any array -> device complex128 tensor (contiguous copy)."""
+    t = torch()
+    if isinstance(a, t.Tensor):
+        if a.device.type == "cuda" and a.dtype == t.complex128 and a.is_contiguous():
+            return a
+        return a.to(device=device(), dtype=t.complex128).contiguous()
+    host = np.ascontiguousarray(a, dtype=np.complex128)
+    return t.from_numpy(host).to(device())
+
+
+def host_ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def mat_struct(n: int, offs: np.ndarray, starts: np.ndarray, vals) -> Matrix:
+    return Matrix(int(n), int(len(offs)), offs.ctypes.data if len(offs) else None,
+                  starts.ctypes.data if len(starts) else None,
+                  int(vals.data_ptr()) if vals is not None and vals.numel() else None)
+
+
+def layout(n: int, offs: np.ndarray) -> tuple[np.ndarray, int]:
+    offs = np.ascontiguousarray(offs, dtype=np.int64)
+    starts = np.zeros(len(offs), dtype=np.int64)
+    total = ctypes.c_int64(0)
+    call("diaq_layout", int(n), len(offs), offs.ctypes.data if len(offs) else None,
+         starts.ctypes.data if len(offs) else None, ctypes.addressof(total))
+    return starts, int(total.value)

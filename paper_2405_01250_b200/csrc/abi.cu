@@ -1,0 +1,75 @@
+// abi.cu -- library-level C-ABI entry points: errors, layout, counters.
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "common.cuh"
+
+namespace diaq {
+
+static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+int set_error(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+int check_launch(const char *what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(DIAQ_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return DIAQ_OK;
+}
+
+}  // namespace diaq
+
+using namespace diaq;
+
+extern "C" int diaq_version(void) { return 1; }
+
+extern "C" const char *diaq_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int diaq_device_count(int *count) {
+    int c = 0;
+    const cudaError_t e = cudaGetDeviceCount(&c);
+    if (count) *count = (e == cudaSuccess) ? c : 0;
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(DIAQ_ERR_CUDA, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+    }
+    return DIAQ_OK;
+}
+
+extern "C" uint64_t diaq_launch_count(void) { return g_launches.load(); }
+
+extern "C" void diaq_reset_launch_count(void) { g_launches.store(0); }
+
+// Row-aligned layout: diagonal i starts at an element index s_i with
+// (s_i + min(d_i, 0)) % 8 == 0, so the element of row r is 128-byte aligned
+// whenever r % 8 == 0 (arena base is >= 512-byte aligned).
+extern "C" int diaq_layout(int64_t n, int64_t nd, const int64_t *offs, int64_t *starts, int64_t *total) {
+    if (n < 1) return set_error(DIAQ_ERR_SHAPE, "n_dim must be >= 1, got %lld", (long long)n);
+    if (nd < 0 || (nd > 0 && (!offs || !starts)) || !total) return set_error(DIAQ_ERR_VALUE, "diaq_layout: bad arguments");
+    int64_t cur = 0;
+    for (int64_t i = 0; i < nd; ++i) {
+        const int64_t d = offs[i];
+        const int64_t a = d < 0 ? -d : d;
+        if (a > n - 1)
+            return set_error(DIAQ_ERR_VALUE, "diagonal %lld out of range for n_dim=%lld", (long long)d, (long long)n);
+        if (i > 0 && offs[i - 1] >= d) return set_error(DIAQ_ERR_VALUE, "offsets must be strictly ascending");
+        const int64_t want = (d < 0 ? -d : 0) & 7;  // s % 8 == (-min(d,0)) % 8
+        int64_t s = cur + ((want - (cur & 7)) & 7);
+        starts[i] = s;
+        cur = s + (n - a);
+    }
+    *total = (cur + 7) & ~7ll;
+    return DIAQ_OK;
+}

@@ -1,0 +1,310 @@
+// construct.cu -- building DiaQ matrices on the device (sm_100a).
+//
+//  * kron_identity (reference matrix.py:358-387): closed form.  Output
+//    diagonal d*R, element k: with block = n_m*R and run = len(m_d)*R,
+//    value m_d[(k mod block) / R] if (k mod block) < run else 0 (explicit
+//    zeros kept, never pruned).  Pure streaming writes; m stays in L1/L2.
+//  * build_span_unitary (reference gates.py:169-219): closed form.  For
+//    output diagonal d, row r, column c = r + d: value g[gather(r),
+//    gather(c)] when r and c agree on every non-gate bit and that gate entry
+//    is nonzero (|re|+|im| > 0, gates.py:203-204), else 0.
+//  * from_dense (reference matrix.py:135-153): pass 1 flags every diagonal
+//    holding some |re|+|im| > eps (coalesced row-major read of the dense
+//    matrix); the host lays out the kept set; pass 2 gathers them.
+//  * to_dense (reference matrix.py:156-167): scatter at stride n+1.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+
+namespace diaq {
+
+struct KronDiag {
+    const double2 *src;  // m diagonal (k = 0)
+    double2 *dst;        // output diagonal (k = 0)
+    int64_t len;         // output length n - |d*R|
+    int64_t run;         // len(m_d) * R
+};
+
+struct KronParams {
+    int64_t block, right;
+    int pow2;
+    int block_shift, right_shift;
+    int nd;
+    KronDiag dg[kParamDiags];
+};
+
+__global__ void __launch_bounds__(kThreads) kron_identity_kernel(const __grid_constant__ KronParams p) {
+    const KronDiag &dg = p.dg[blockIdx.y];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < dg.len; k += stride) {
+        int64_t pos, src;
+        if (p.pow2) {
+            pos = k & (p.block - 1);
+            src = pos >> p.right_shift;
+        } else {
+            pos = k % p.block;
+            src = pos / p.right;
+        }
+        double2 v = make_double2(0.0, 0.0);
+        if (pos < dg.run) v = ld_reuse(dg.src + src);
+        st_stream(dg.dst + k, v);
+    }
+}
+
+struct SpanParams {
+    int k, span;
+    int shifts[kParamDiags];   // state bit of gate operand i (operand 0 = MSB)
+    uint64_t free_mask;        // bits of the span that are not gate bits
+    int nd;
+    int64_t off[kParamDiags];
+    double2 *dst[kParamDiags];
+    int64_t len[kParamDiags];
+    double2 g[256];            // dense gate, k <= 4
+};
+
+__device__ __forceinline__ int gather_bits(uint64_t r, const int *shifts, int k) {
+    int out = 0;
+    for (int i = 0; i < k; ++i) out |= (int)((r >> shifts[i]) & 1ull) << (k - 1 - i);
+    return out;
+}
+
+__global__ void __launch_bounds__(kThreads) span_expand_kernel(const __grid_constant__ SpanParams p) {
+    const int i = blockIdx.y;
+    const int64_t d = p.off[i];
+    const int64_t len = p.len[i];
+    const int M = 1 << p.k;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t kk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; kk < len; kk += stride) {
+        const uint64_t r = (uint64_t)(kk - (d < 0 ? d : 0));
+        const uint64_t c = r + (uint64_t)d;
+        double2 v = make_double2(0.0, 0.0);
+        if (((r ^ c) & p.free_mask) == 0) {
+            const int rg = gather_bits(r, p.shifts, p.k);
+            const int cg = gather_bits(c, p.shifts, p.k);
+            const double2 gv = p.g[rg * M + cg];
+            if (fabs(gv.x) + fabs(gv.y) > 0.0) v = gv;
+        }
+        st_stream(p.dst[i] + kk, v);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+from_dense_scan_kernel(const double2 *m, int64_t n, double eps, uint8_t *keep) {
+    const int64_t total = n * n;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+        const double2 v = ld_stream(m + e, policy_evict_first());
+        if (fabs(v.x) + fabs(v.y) > eps) {
+            const int64_t r = e / n, c = e - r * n;
+            keep[c - r + n - 1] = 1;
+        }
+    }
+}
+
+struct GatherDiag {
+    double2 *dst;
+    int64_t len, base;  // dense flat index of k = 0
+};
+
+__global__ void __launch_bounds__(kThreads)
+from_dense_fill_kernel(const double2 *m, int64_t n, const GatherDiag *__restrict__ dg) {
+    const GatherDiag g = dg[blockIdx.y];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < g.len; k += stride)
+        g.dst[k] = m[g.base + k * (n + 1)];
+}
+
+__global__ void __launch_bounds__(kThreads)
+to_dense_kernel(double2 *m, int64_t n, const GatherDiag *__restrict__ dg) {
+    const GatherDiag g = dg[blockIdx.y];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < g.len; k += stride)
+        m[g.base + k * (n + 1)] = g.dst[k];
+}
+
+static int grid_x(int64_t len, int nd) {
+    int dev = 0, sms = kSms;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaGetLastError();
+    const int64_t want = (len + kThreads - 1) / kThreads;
+    const int64_t cap = std::max<int64_t>(1, (int64_t)sms * 8 / std::max(1, nd));
+    return (int)std::max<int64_t>(1, std::min<int64_t>(want, cap));
+}
+
+static bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+static int log2i(int64_t v) { int s = 0; while ((1ll << s) < v) ++s; return s; }
+
+static int64_t embed_idx(int64_t idx, int k, const int *shifts) {
+    int64_t out = 0;
+    for (int i = 0; i < k; ++i) out |= ((idx >> (k - 1 - i)) & 1) << shifts[i];
+    return out;
+}
+
+// temporary device table, freed stream-ordered
+template <typename T>
+static T *upload_table(const std::vector<T> &h, cudaStream_t s) {
+    T *d = nullptr;
+    if (cudaMallocAsync((void **)&d, sizeof(T) * h.size(), s) != cudaSuccess) return nullptr;
+    if (cudaMemcpyAsync(d, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice, s) != cudaSuccess) {
+        cudaFreeAsync(d, s);
+        return nullptr;
+    }
+    return d;
+}
+
+}  // namespace diaq
+
+using namespace diaq;
+
+extern "C" int diaq_kron_identity(int64_t left, const diaq_matrix_t *m, int64_t right, diaq_matrix_t *out,
+                                  void *stream) {
+    if (!m || !out) return set_error(DIAQ_ERR_VALUE, "diaq_kron_identity: null argument");
+    if (left < 1 || right < 1) return set_error(DIAQ_ERR_SHAPE, "left_dim and right_dim must be >= 1");
+    if (out->n != left * m->n * right || out->nd != m->nd)
+        return set_error(DIAQ_ERR_SHAPE, "diaq_kron_identity: output layout mismatch");
+    if (m->nd == 0) return DIAQ_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t block = m->n * right;
+    for (int64_t base = 0; base < m->nd; base += kParamDiags) {
+        const int cnt = (int)std::min<int64_t>(kParamDiags, m->nd - base);
+        KronParams p;
+        p.block = block;
+        p.right = right;
+        p.pow2 = is_pow2(block) && is_pow2(right);
+        p.block_shift = p.pow2 ? log2i(block) : 0;
+        p.right_shift = p.pow2 ? log2i(right) : 0;
+        p.nd = cnt;
+        int64_t maxlen = 0;
+        for (int j = 0; j < cnt; ++j) {
+            const int64_t i = base + j;
+            const int64_t d = m->offs[i];
+            if (out->offs[i] != d * right) return set_error(DIAQ_ERR_SHAPE, "diaq_kron_identity: offset table mismatch");
+            const int64_t dout = d * right;
+            p.dg[j].src = (const double2 *)m->vals + m->starts[i];
+            p.dg[j].dst = (double2 *)out->vals + out->starts[i];
+            p.dg[j].len = out->n - (dout < 0 ? -dout : dout);
+            p.dg[j].run = (m->n - (d < 0 ? -d : d)) * right;
+            maxlen = std::max(maxlen, p.dg[j].len);
+        }
+        dim3 grid(grid_x(maxlen, cnt), cnt);
+        kron_identity_kernel<<<grid, kThreads, 0, s>>>(p);
+        count_launch();
+        const int rc = check_launch("kron_identity_kernel");
+        if (rc) return rc;
+    }
+    return DIAQ_OK;
+}
+
+extern "C" int diaq_span_plan(int k, const double *g, const int *positions, int span, int64_t *offs_out,
+                              int64_t *nd_out) {
+    if (!g || !positions || !offs_out || !nd_out) return set_error(DIAQ_ERR_VALUE, "diaq_span_plan: null argument");
+    if (k < 1 || k > 4) return set_error(DIAQ_ERR_UNSUPPORTED, "diaq_span_plan: gate width %d outside 1..4", k);
+    if (span < k || span > 62) return set_error(DIAQ_ERR_SHAPE, "diaq_span_plan: span %d", span);
+    int shifts[8];
+    for (int i = 0; i < k; ++i) {
+        if (positions[i] < 0 || positions[i] >= span)
+            return set_error(DIAQ_ERR_SHAPE, "positions outside span of %d qubits", span);
+        for (int j = 0; j < i; ++j)
+            if (positions[j] == positions[i]) return set_error(DIAQ_ERR_SHAPE, "need %d distinct positions", k);
+        shifts[i] = span - 1 - positions[i];
+    }
+    const int64_t M = 1ll << k;
+    std::vector<int64_t> v;
+    for (int64_t rg = 0; rg < M; ++rg)
+        for (int64_t cg = 0; cg < M; ++cg) {
+            const double re = g[2 * (rg * M + cg)], im = g[2 * (rg * M + cg) + 1];
+            if (!(std::fabs(re) + std::fabs(im) > 0.0)) continue;
+            v.push_back(embed_idx(cg, k, shifts) - embed_idx(rg, k, shifts));
+        }
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+    for (size_t i = 0; i < v.size(); ++i) offs_out[i] = v[i];
+    *nd_out = (int64_t)v.size();
+    return DIAQ_OK;
+}
+
+extern "C" int diaq_span_expand(int k, const double *g, const int *positions, int span, diaq_matrix_t *out,
+                                void *stream) {
+    if (!g || !positions || !out) return set_error(DIAQ_ERR_VALUE, "diaq_span_expand: null argument");
+    if (k < 1 || k > 4) return set_error(DIAQ_ERR_UNSUPPORTED, "diaq_span_expand: gate width %d outside 1..4", k);
+    if (out->n != (1ll << span)) return set_error(DIAQ_ERR_SHAPE, "diaq_span_expand: output n mismatch");
+    cudaStream_t s = (cudaStream_t)stream;
+    SpanParams p;
+    p.k = k;
+    p.span = span;
+    uint64_t gate_mask = 0;
+    for (int i = 0; i < k; ++i) {
+        p.shifts[i] = span - 1 - positions[i];
+        gate_mask |= 1ull << p.shifts[i];
+    }
+    p.free_mask = (span >= 64 ? ~0ull : ((1ull << span) - 1ull)) & ~gate_mask;
+    const int M = 1 << k;
+    for (int i = 0; i < M * M; ++i) p.g[i] = make_double2(g[2 * i], g[2 * i + 1]);
+    for (int64_t base = 0; base < out->nd; base += kParamDiags) {
+        const int cnt = (int)std::min<int64_t>(kParamDiags, out->nd - base);
+        p.nd = cnt;
+        int64_t maxlen = 0;
+        for (int j = 0; j < cnt; ++j) {
+            const int64_t d = out->offs[base + j];
+            p.off[j] = d;
+            p.len[j] = out->n - (d < 0 ? -d : d);
+            p.dst[j] = (double2 *)out->vals + out->starts[base + j];
+            maxlen = std::max(maxlen, p.len[j]);
+        }
+        dim3 grid(grid_x(maxlen, cnt), cnt);
+        span_expand_kernel<<<grid, kThreads, 0, s>>>(p);
+        count_launch();
+        const int rc = check_launch("span_expand_kernel");
+        if (rc) return rc;
+    }
+    return DIAQ_OK;
+}
+
+extern "C" int diaq_from_dense_scan(int64_t n, const void *dense, double eps, uint8_t *keep_dev, void *stream) {
+    if (!dense || !keep_dev || n < 1) return set_error(DIAQ_ERR_VALUE, "diaq_from_dense_scan: bad arguments");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cudaMemsetAsync(keep_dev, 0, (size_t)(2 * n - 1), s) != cudaSuccess)
+        return set_error(DIAQ_ERR_CUDA, "diaq_from_dense_scan: memset failed");
+    const int grid = grid_x(n * n, 1);
+    from_dense_scan_kernel<<<grid, kThreads, 0, s>>>((const double2 *)dense, n, eps, keep_dev);
+    count_launch();
+    return check_launch("from_dense_scan_kernel");
+}
+
+static int gather_launch(const void *dense, diaq_matrix_t *a, bool to_dense, cudaStream_t s) {
+    if (a->nd == 0) return DIAQ_OK;
+    std::vector<GatherDiag> h((size_t)a->nd);
+    int64_t maxlen = 0;
+    const int64_t n = a->n;
+    for (int64_t i = 0; i < a->nd; ++i) {
+        const int64_t d = a->offs[i];
+        h[i].dst = (double2 *)a->vals + a->starts[i];
+        h[i].len = n - (d < 0 ? -d : d);
+        h[i].base = d >= 0 ? d : -d * n;
+        maxlen = std::max(maxlen, h[i].len);
+    }
+    GatherDiag *dt = upload_table(h, s);
+    if (!dt) return set_error(DIAQ_ERR_CUDA, "gather table upload failed");
+    for (int64_t base = 0; base < a->nd; base += 65535) {
+        const int cnt = (int)std::min<int64_t>(65535, a->nd - base);
+        dim3 grid(grid_x(maxlen, cnt), cnt);
+        if (to_dense) to_dense_kernel<<<grid, kThreads, 0, s>>>((double2 *)dense, n, dt + base);
+        else from_dense_fill_kernel<<<grid, kThreads, 0, s>>>((const double2 *)dense, n, dt + base);
+        count_launch();
+    }
+    const int rc = check_launch(to_dense ? "to_dense_kernel" : "from_dense_fill_kernel");
+    cudaFreeAsync(dt, s);
+    return rc;
+}
+
+extern "C" int diaq_from_dense_fill(const void *dense, diaq_matrix_t *out, void *stream) {
+    if (!dense || !out) return set_error(DIAQ_ERR_VALUE, "diaq_from_dense_fill: null argument");
+    return gather_launch(dense, out, false, (cudaStream_t)stream);
+}
+
+extern "C" int diaq_to_dense(const diaq_matrix_t *a, void *dense, void *stream) {
+    if (!dense || !a) return set_error(DIAQ_ERR_VALUE, "diaq_to_dense: null argument");
+    return gather_launch(dense, const_cast<diaq_matrix_t *>(a), true, (cudaStream_t)stream);
+}

@@ -1,0 +1,337 @@
+"""State-vector simulation on the device (drop-in for diaqsim.sim).
+
+Reference: /root/reference/pkg/src/diaqsim/sim.py.  The diaq backend applies
+every Placement on the B200:
+
+* compact gates (everything compile_circuit emits, and explicit placements
+  whose m is a small power-of-two block) go through the group kernel
+  (apply.cu gate_kernel): read each amplitude once, write it once;
+* any other explicit Placement goes through the diagonal kernel
+  (apply.cu placed_kernel), the direct analogue of _apply_diags_block.
+
+Both reproduce the reference's per-amplitude summation order and numpy's
+complex multiply rounding (CMUL_MODE), so states match the reference
+bitwise on hosts whose numpy uses the same complex multiply (see
+DESIGN.md; the contract is 1e-12 relative L2).
+
+run() compiles on the host, then hands the whole gate list to the native
+loop diaq_run_gates (one C call, in-place updates, CUDA events around every
+gate resolved after the loop -- no per-gate host sync).  Sampling is the
+reference's splitmix64 inverse-CDF sampler on the host over the downloaded
+probabilities (device sampler is the next row).
+"""
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib as L
+from .errors import NormalizationError, ResourceError, ShapeError, UnsupportedFeatureError
+from .gates import Circuit, Placement, compile_circuit, fuse_pass
+from .matrix import kron_identity, spmv, to_dense
+
+MAX_QUBITS = 30
+
+BACKENDS = ("dense", "diaq")
+
+
+def _probe_numpy_cmul() -> int:
+    """Which complex-multiply rounding this host's numpy uses."""
+    rng = np.random.default_rng(7)
+    a = rng.normal(size=64) + 1j * rng.normal(size=64)
+    b = rng.normal(size=64) + 1j * rng.normal(size=64)
+    plain = a.real * b.real - a.imag * b.imag
+    return L.CMUL_PLAIN if np.array_equal((a * b).real, plain) else L.CMUL_FMA
+
+
+# rounding of the gate-apply complex multiply; defaults to this host's numpy
+CMUL_MODE = _probe_numpy_cmul()
+
+
+class StateVector:
+    """2^n complex128 amplitudes, resident on the device.
+
+    `amps` is the host view (downloaded lazily, like the reference's numpy
+    array); `device_amps` the CUDA tensor.  Construct from either.
+    """
+
+    def __init__(self, n_qubits: int, amps):
+        self.n_qubits = int(n_qubits)
+        t = L.torch()
+        if isinstance(amps, t.Tensor) and amps.device.type == "cuda":
+            self._dev = L.to_device_c128(amps.reshape(-1))
+            self._host = None
+        else:
+            self._host = np.ascontiguousarray(amps, dtype=np.complex128).reshape(-1)
+            self._dev = None
+
+    @property
+    def device_amps(self):
+        if self._dev is None:
+            self._dev = L.to_device_c128(self._host)
+        return self._dev
+
+    @property
+    def amps(self) -> np.ndarray:
+        if self._host is None:
+            self._host = self._dev.cpu().numpy()
+        return self._host
+
+    def __len__(self) -> int:
+        return int(self._dev.numel()) if self._host is None else len(self._host)
+
+    def norm(self) -> float:
+        return float(np.sqrt(norm2(self.device_amps)))
+
+
+def norm2(x) -> float:
+    """sum |x_i|^2 of a device vector (deterministic two-pass reduction)."""
+    t = L.torch()
+    work = t.empty(L.DIAQ_NORM_WORK, dtype=t.float64, device=x.device)
+    L.call("diaq_norm2", int(x.numel()), x.data_ptr(), work.data_ptr(), L.stream_handle())
+    return float(work[0].item())
+
+
+@dataclass
+class RunResult:
+    counts: dict[str, int]
+    timings_ns: dict
+    backend: str
+    seed: int
+    shots: int
+    n_qubits: int
+    state: np.ndarray | None = None
+
+
+def init_state(n_qubits: int, max_qubits: int = MAX_QUBITS) -> StateVector:
+    """|0...0>: amplitude 1 at index 0 (sim.py:53-59)."""
+    if not 1 <= n_qubits <= max_qubits:
+        raise ResourceError(f"n_qubits {n_qubits} outside 1..{max_qubits}")
+    x = L.empty_c128(2**n_qubits)
+    L.call("diaq_init_basis", 2**n_qubits, x.data_ptr(), 0, L.stream_handle())
+    return StateVector(n_qubits, x)
+
+
+def _check_dims(p: Placement, x: StateVector) -> None:
+    if p.n_dim != len(x):
+        raise ShapeError(
+            f"placement covers {p.n_dim} amplitudes, state has {len(x)}"
+        )
+
+
+def _apply_into(p: Placement, xd, yd, cmul_mode: int) -> None:
+    """y = placement(x) on the device; y must not alias x for the generic path."""
+    n = int(xd.numel())
+    comp = p.compact()
+    s = L.stream_handle()
+    if comp is not None:
+        g, shifts = comp
+        k = len(shifts)
+        gd = np.ascontiguousarray(g, dtype=np.complex128)
+        sh = np.ascontiguousarray(shifts, dtype=np.int32)
+        L.call("diaq_apply_gate", n.bit_length() - 1, k, gd.ctypes.data, sh.ctypes.data,
+               xd.data_ptr(), yd.data_ptr(), int(cmul_mode), s)
+        return
+    m = p.m
+    if m.diag_count() <= 64:
+        st = m._struct()
+        L.call("diaq_apply_placed", p.dim_a, ctypes.byref(st), p.dim_b, xd.data_ptr(), yd.data_ptr(),
+               int(cmul_mode), s)
+        return
+    raise UnsupportedFeatureError(
+        f"placement with {m.diag_count()} stored diagonals exceeds the 64-diagonal apply kernel")
+
+
+def apply_placed(p: Placement, x: StateVector, threads: int = 1,
+                 cmul_mode: int | None = None) -> StateVector:
+    """Apply I_dim_a (x) m (x) I_dim_b to x on the device (sim.py:81-105).
+
+    Returns a fresh state (x is not modified).  `threads` is accepted for API
+    compatibility; results never depend on it (the reference guarantees the
+    same, sim.py:84-87).
+    """
+    _check_dims(p, x)
+    xd = x.device_amps
+    yd = L.empty_c128(xd.numel())
+    _apply_into(p, xd, yd, CMUL_MODE if cmul_mode is None else cmul_mode)
+    return StateVector(x.n_qubits, yd)
+
+
+def apply_dense(p: Placement, x: StateVector) -> StateVector:
+    """Dense backend: materialise the span operator and contract it (sim.py:108-120).
+
+    Reference/oracle backend only (4^span cost); runs as a torch contraction
+    on the device.
+    """
+    _check_dims(p, x)
+    t = L.torch()
+    g = t.from_numpy(np.ascontiguousarray(to_dense(p.m))).to(L.device())
+    x3 = x.device_amps.reshape(p.dim_a, p.m.n_dim, p.dim_b)
+    y3 = t.tensordot(g, x3, dims=([1], [1])).permute(1, 0, 2).contiguous()
+    return StateVector(x.n_qubits, y3.reshape(-1))
+
+
+# -- sampling ------------------------------------------------------------------
+
+# splitmix64: golden-gamma counter increment and the two mixing constants
+_GAMMA = np.uint64(0x9E3779B97F4A7C15)
+_MIX1 = np.uint64(0xBF58476D1CE4E5B9)
+_MIX2 = np.uint64(0x94D049BB133111EB)
+
+
+def splitmix64_uniforms(seed: int, count: int) -> np.ndarray:
+    """`count` doubles in [0, 1) from the splitmix64 stream for `seed` (sim.py:131-139)."""
+    idx = np.arange(1, count + 1, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = np.uint64(seed & 0xFFFFFFFFFFFFFFFF) + idx * _GAMMA
+        z = (z ^ (z >> np.uint64(30))) * _MIX1
+        z = (z ^ (z >> np.uint64(27))) * _MIX2
+        z = z ^ (z >> np.uint64(31))
+    return (z >> np.uint64(11)).astype(np.float64) * 2.0**-53
+
+
+def measure_all_sample(x: StateVector, shots: int, seed: int) -> dict[str, int]:
+    """Sample `shots` bitstrings (q0..q(n-1), MSB first) from |amps|^2 (sim.py:142-161).
+
+    Probabilities are rounded to 1e-12 before the sequential CDF, exactly as
+    the reference does, so counts match it for states equal to ~1e-13.
+    """
+    if shots < 0:
+        raise ValueError(f"shots must be >= 0, got {shots}")
+    p = np.abs(x.amps) ** 2
+    if abs(p.sum() - 1.0) > 1e-6:
+        raise NormalizationError(f"state norm^2 = {p.sum():.9f}, cannot sample")
+    if shots == 0:
+        return {}
+    cdf = np.cumsum(np.round(p, 12))
+    u = splitmix64_uniforms(seed, shots)
+    hits = np.minimum(np.searchsorted(cdf, u, side="right"), len(p) - 1)
+    outcomes, freq = np.unique(hits, return_counts=True)
+    width = x.n_qubits
+    return {format(int(i), f"0{width}b"): int(c) for i, c in zip(outcomes, freq)}
+
+
+# -- driver ----------------------------------------------------------------------
+
+
+class _GateProgram:
+    """Compact gates packed for diaq_run_gates (keeps host buffers alive)."""
+
+    def __init__(self, comps):
+        self.mats = [np.ascontiguousarray(g, dtype=np.complex128) for g, _ in comps]
+        self.arr = (L.Gate * max(1, len(comps)))()
+        for i, ((_, shifts), g) in enumerate(zip(comps, self.mats)):
+            self.arr[i].k = len(shifts)
+            for j, s in enumerate(shifts):
+                self.arr[i].shifts[j] = int(s)
+            self.arr[i].g = g.ctypes.data
+        self.n = len(comps)
+
+
+def run_gates(state: StateVector, placements: list[Placement], cmul_mode: int | None = None,
+              events: list | None = None, inplace: bool = False) -> StateVector:
+    """Apply placements in order on the device; each maximal run of compact
+    gates goes through one native call (diaq_run_gates, in place).  The input
+    state is left untouched unless inplace=True."""
+    mode = CMUL_MODE if cmul_mode is None else cmul_mode
+    n_bits = len(state).bit_length() - 1
+    xd = state.device_amps
+    if not inplace:
+        xd = xd.clone()
+    i = 0
+    ev_i = 0
+    s = L.stream_handle()
+    while i < len(placements):
+        j = i
+        comps = []
+        while j < len(placements) and placements[j].compact() is not None:
+            comps.append(placements[j].compact())
+            j += 1
+        if comps:
+            prog = _GateProgram(comps)
+            evs = None
+            if events is not None:
+                sub = events[ev_i: ev_i + prog.n + 1]
+                evs = (ctypes.c_void_p * len(sub))(*[e.cuda_event for e in sub])
+            L.call("diaq_run_gates", n_bits, prog.n, prog.arr, xd.data_ptr(), int(mode),
+                   evs, s)
+            ev_i += prog.n
+            i = j
+            continue
+        p = placements[i]
+        yd = L.empty_c128(xd.numel())
+        if events is not None:
+            events[ev_i].record()
+        _apply_into(p, xd, yd, mode)
+        xd = yd
+        if events is not None:
+            events[ev_i + 1].record()
+        ev_i += 1
+        i += 1
+    return StateVector(state.n_qubits, xd)
+
+
+def run(
+    circuit: Circuit,
+    backend: str = "diaq",
+    shots: int = 1024,
+    seed: int = 0,
+    fusion: bool = False,
+    span_limit: int | None = None,
+    emit_state: bool = False,
+    threads: int = 1,
+) -> RunResult:
+    """Compile, apply, and sample a circuit (sim.py:167-221).
+
+    Timings are nanoseconds per phase; per-gate application times come from
+    CUDA events recorded around every gate and resolved after the loop.
+    """
+    if backend not in BACKENDS:
+        raise ValueError(f"backend must be one of {BACKENDS}, got '{backend}'")
+    kwargs = {} if span_limit is None else {"span_limit": span_limit}
+    t = L.torch()
+
+    t0 = time.perf_counter_ns()
+    placements = fuse_pass(compile_circuit(circuit, **kwargs), enabled=fusion)
+    t_compile = time.perf_counter_ns() - t0
+
+    state = init_state(circuit.n_qubits)
+    events = [t.cuda.Event(enable_timing=True) for _ in range(len(placements) + 1)]
+    t0 = time.perf_counter_ns()
+    if backend == "diaq":
+        state = run_gates(state, placements, events=events, inplace=True)
+    else:
+        events[0].record()
+        for i, p in enumerate(placements):
+            state = apply_dense(p, state)
+            events[i + 1].record()
+    events[-1].synchronize()
+    t_apply = time.perf_counter_ns() - t0
+    per_gate = {
+        f"{i}:{p.name}": int(round(events[i].elapsed_time(events[i + 1]) * 1e6))
+        for i, p in enumerate(placements)
+    }
+
+    t0 = time.perf_counter_ns()
+    counts = measure_all_sample(state, shots, seed)
+    t_sample = time.perf_counter_ns() - t0
+
+    timings = {
+        "compile": t_compile,
+        "apply_total": t_apply,
+        "sample": t_sample,
+        "total": t_compile + t_apply + t_sample,
+        "per_gate": per_gate,
+    }
+    return RunResult(
+        counts=counts,
+        timings_ns=timings,
+        backend=backend,
+        seed=seed,
+        shots=shots,
+        n_qubits=circuit.n_qubits,
+        state=state.amps if emit_state else None,
+    )

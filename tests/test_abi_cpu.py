@@ -1,0 +1,149 @@
+"""CPU-side checks of the C-ABI library and the host logic (no GPU needed).
+
+* the in-tree libdiaq_b200.so loads and exports every symbol declared in
+  include/diaq_b200.h;
+* the host-only ABI functions (layout, span plan, spgemm plan) agree with
+  the oracle / reference rules;
+* compile_circuit's compact placements agree with the reference's
+  dims and embedding;
+* compute entry points fail loudly without a device (no CPU fallback).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, dense_from_pairs
+from oracle import oracle as O
+from paper_2405_01250_b200 import _lib as L
+from paper_2405_01250_b200 import build as B
+from paper_2405_01250_b200 import workloads as W
+
+
+@pytest.fixture(scope="module")
+def lib():
+    B.build()
+    return L.load()
+
+
+def header_functions() -> list[str]:
+    with open(os.path.join(ROOT, "include", "diaq_b200.h")) as f:
+        text = f.read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|uint64_t|void|const char \*)\s*\**\s*(diaq_\w+)\s*\(",
+                                 text, flags=re.M)))
+
+
+def test_exports_every_header_symbol(lib):
+    names = header_functions()
+    assert len(names) >= 20
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(L.EXPORTED)
+
+
+def test_version_and_counters(lib):
+    assert lib.diaq_version() == 1
+    lib.diaq_reset_launch_count()
+    assert lib.diaq_launch_count() == 0
+
+
+@pytest.mark.parametrize("n,offs", [(16, [-15, -3, 0, 1, 7, 15]), (2**20, [-(2**19) - 3, -1, 0, 5, 2**19]),
+                                    (9, [0]), (1, [0])])
+def test_layout_row_aligned(lib, n, offs):
+    offs = np.array(offs, dtype=np.int64)
+    starts, total = L.layout(n, offs)
+    prev_end = 0
+    for d, s in zip(offs.tolist(), starts.tolist()):
+        assert s >= prev_end
+        assert (s + min(d, 0)) % 8 == 0          # row r%8==0 sits 128-byte aligned
+        prev_end = s + n - abs(d)
+    assert total >= prev_end and total % 8 == 0
+
+
+def test_layout_rejects_bad_offsets(lib):
+    with pytest.raises(ValueError):
+        L.layout(4, np.array([4]))
+    with pytest.raises(ValueError):
+        L.layout(4, np.array([1, 0]))
+
+
+def test_span_plan_matches_oracle(lib, kats):
+    for case in kats["kats"]["span"]:
+        g = np.ascontiguousarray(dense_from_pairs(case["g"]))
+        k = int(np.log2(g.shape[0]))
+        pos = np.ascontiguousarray(case["positions"], dtype=np.int32)
+        offs = np.zeros(4**k, dtype=np.int64)
+        nd = ctypes.c_int64(0)
+        L.call("diaq_span_plan", k, g.ctypes.data, pos.ctypes.data, case["span"], offs.ctypes.data,
+               ctypes.addressof(nd))
+        assert offs[: nd.value].tolist() == case["offsets"]
+
+
+def test_spgemm_plan_matches_oracle(lib, random_cases):
+    for i in range(48):
+        a = O.from_dense(random_cases[f"mm{i}_a"])
+        b = O.from_dense(random_cases[f"mm{i}_b"])
+        cap = max(1, len(a.offs) * len(b.offs))
+        want = np.zeros(cap, dtype=np.int64)
+        nw = O.lib().oracle_matmul_plan(a.n, len(a.offs), O._p(a.offs), len(b.offs), O._p(b.offs),
+                                        O._p(want))
+        got = np.zeros(cap, dtype=np.int64)
+        nc = ctypes.c_int64(0)
+        L.call("diaq_spgemm_plan", a.n, len(a.offs), a.offs.ctypes.data, len(b.offs), b.offs.ctypes.data,
+               got.ctypes.data, ctypes.addressof(nc))
+        assert got[: nc.value].tolist() == want[:nw].tolist()
+
+
+def test_compile_compact_placements_match_reference_dims():
+    from paper_2405_01250_b200 import Circuit, GateOp, ResourceError, compile_circuit
+    ops = W.random_layered_ops(12, 3, seed=1)
+    c = Circuit(12, [GateOp(*o) for o in ops])
+    pls = compile_circuit(c, span_limit=12)
+    for p, (name, qubits, params) in zip(pls, ops):
+        lo, hi = min(qubits), max(qubits)
+        assert (p.dim_a, p.dim_b, p.span_lo, p.span_hi, p.name) == (2**lo, 2 ** (11 - hi), lo, hi, name)
+        assert p.n_dim == 2**12
+        g, shifts = p.compact()
+        # operand i sits on state bit n-1-q_i (qubit 0 = most significant)
+        assert shifts == [11 - q for q in qubits]
+        assert np.array_equal(g, O.GATES[name](*params))
+    with pytest.raises(ResourceError, match="cx"):
+        compile_circuit(Circuit(8, [GateOp("cx", (0, 7))]), span_limit=4)
+
+
+def test_gateop_validation_errors():
+    from paper_2405_01250_b200 import Circuit, GateOp, ShapeError, UnsupportedGateError
+    with pytest.raises(UnsupportedGateError):
+        GateOp("frobnicate", (0,))
+    with pytest.raises(ShapeError):
+        GateOp("cx", (1, 1))
+    with pytest.raises(ShapeError):
+        GateOp("h", (0,), (0.5,))
+    with pytest.raises(ShapeError):
+        Circuit(2, [GateOp("h", (5,))])
+
+
+def test_diag_len_and_shape_errors():
+    from paper_2405_01250_b200 import DiaqMatrix, ShapeError, diag_len
+    assert diag_len(0, 4) == 4 and diag_len(-3, 4) == 1
+    with pytest.raises(ValueError):
+        diag_len(4, 4)
+    with pytest.raises(ShapeError):
+        DiaqMatrix(0)
+    a = DiaqMatrix(4)
+    with pytest.raises(ShapeError):
+        a.set_diag(1, [1.0, 2.0])
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="checks the no-device path")
+def test_compute_fails_loudly_without_device():
+    from paper_2405_01250_b200 import from_dense, init_state
+    with pytest.raises(L.DeviceError):
+        init_state(3)
+    with pytest.raises(L.DeviceError):
+        from_dense(np.eye(2))

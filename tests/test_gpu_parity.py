@@ -1,0 +1,361 @@
+"""GPU parity: the CUDA path (through the public API / C-ABI) against the
+reference's golden vectors and the pinned CPU oracle.
+
+Bar: bitwise (values equal, signed zeros folded) for spmv, spgemm,
+kron_identity, build_span_unitary, from_dense and -- with the reference
+host's complex-multiply rounding -- gate application.  Where a test states a
+tolerance it is the north-star 1e-12 relative L2.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_2405_01250_b200 as D
+from conftest import GOLDEN, dense_from_pairs, digest, pairs_to_complex, rel_l2
+from oracle import oracle as O
+from paper_2405_01250_b200 import _lib as L
+from paper_2405_01250_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+CORNER = np.array([[1, 0, 0, 2], [0, 3, 0, 0], [0, 0, 4, 0], [5, 0, 0, 6]], dtype=complex)
+CX = np.array([[1, 0, 0, 0], [0, 1, 0, 0], [0, 0, 0, 1], [0, 0, 1, 0]], dtype=complex)
+
+
+@pytest.fixture(scope="module")
+def cmul(configs):
+    return L.CMUL_FMA if configs["meta"]["numpy_cmul"] == "fma" else L.CMUL_PLAIN
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _built(cmul):
+    """Build/load the library and use the golden host's complex-multiply rounding."""
+    from paper_2405_01250_b200 import build
+    build.build()
+    L.load()
+    old = D.sim.CMUL_MODE
+    D.sim.CMUL_MODE = cmul
+    yield
+    D.sim.CMUL_MODE = old
+
+
+def values(m) -> np.ndarray:
+    parts = [dg.re + 1j * dg.im for dg in m.diagonals()]
+    return np.concatenate(parts) if parts else np.zeros(0, np.complex128)
+
+
+def omat(m) -> O.OMat:
+    return O.omat_from_diags(m.n_dim, {dg.index: (dg.re, dg.im) for dg in m.diagonals()})
+
+
+# ---- KATs -------------------------------------------------------------------
+
+def test_corner_layout_and_spmv(kats):
+    a = D.from_dense(CORNER, 0.0)
+    assert a.diag_indices() == [-3, 0, 3]
+    assert a.get(-3).re.tolist() == [5.0]
+    assert a.get(0).re.tolist() == [1.0, 3.0, 4.0, 6.0]
+    assert a.get(3).re.tolist() == [2.0]
+    assert not any(a.get(d).im.any() for d in (-3, 0, 3))
+    y = D.spmv(a, np.ones(4, dtype=complex))
+    assert np.array_equal(y, pairs_to_complex(kats["kats"]["corner_spmv_ones"]))
+    assert np.array_equal(D.to_dense(a), CORNER)
+
+
+def test_cx_layout_and_prune(kats):
+    a = D.from_dense(CX, 0.0)
+    assert a.diag_indices() == [-1, 0, 1]
+    assert a.get(-1).re.tolist() == [0.0, 0.0, 1.0]
+    assert a.get(0).re.tolist() == [1.0, 1.0, 0.0, 0.0]
+    x = D.from_dense(np.array([[0, 1], [1, 0]], dtype=complex), 0.0)
+    assert D.matmul(x, x).diag_indices() == [0]
+    z = D.from_dense(np.diag([1.0, -1.0]), 0.0)
+    zz = D.matmul(z, z)
+    assert zz.diag_indices() == [0] and zz.get(0).re.tolist() == [1.0, 1.0]
+
+
+def test_from_dense_edge_cases():
+    z = D.from_dense(np.zeros((4, 4)), 0.0)
+    assert z.diag_count() == 0
+    assert np.array_equal(D.to_dense(z), np.zeros((4, 4)))
+    assert np.array_equal(D.spmv(z, np.ones(4)), np.zeros(4))
+    m = CORNER.copy()
+    m[0, 3] = 1e-9
+    assert D.from_dense(m, 1e-6).diag_indices() == [-3, 0]
+    one = D.from_dense(np.array([[2.5 - 1j]]), 0.0)
+    assert one.diag_indices() == [0] and one.get(0).im.tolist() == [-1.0]
+    with pytest.raises(D.ShapeError):
+        D.from_dense(np.zeros((2, 3)))
+    rng = np.random.default_rng(3)
+    for n in (1, 2, 3, 5, 16, 64):
+        m = rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))
+        m[np.abs(np.subtract.outer(np.arange(n), np.arange(n))) % 3 == 1] = 0
+        a = D.from_dense(m, 0.0)
+        assert a.diag_indices() == O.from_dense(m).offs.tolist()
+        assert np.array_equal(D.to_dense(a), m)
+
+
+def test_multiply_diagonals_corner(kats):
+    a = D.from_dense(CORNER, 0.0)
+    d_c, diag = D.multiply_diagonals(a.get(3), a.get(-3), 4)
+    k = kats["kats"]["multiply_diagonals_corner"]
+    assert d_c == k["d_c"] == 0
+    assert diag.re.tolist() == k["re"] == [10.0, 0.0, 0.0, 0.0]
+    b = D.DiaqMatrix(4)
+    b.set_diag(3, [1.0])
+    assert D.multiply_diagonals(b.get(3), b.get(3), 4) is None
+
+
+def test_kron_identity_patterns(kats):
+    z = D.from_dense(np.diag([1.0, -1.0]), 0.0)
+    kz = D.kron_identity(2, z, 1)
+    assert kz.diag_indices() == [0] and kz.get(0).re.tolist() == [1.0, -1.0, 1.0, -1.0]
+    h = np.array([[1, 1], [1, -1]]) / np.sqrt(2)
+    kh = D.kron_identity(2, D.from_dense(h, 0.0), 2)
+    assert kh.diag_indices() == kats["kats"]["kron_identity_h"]["offsets"]
+    assert np.array_equal(D.to_dense(kh), dense_from_pairs(kats["kats"]["kron_identity_h"]["dense"]))
+    a = D.from_dense(CORNER, 0.0)
+    assert D.kron_identity(1, a, 1) == a
+    rng = np.random.default_rng(5)
+    for left, right in ((1, 4), (4, 1), (2, 2), (8, 2), (3, 5)):
+        m = rng.normal(size=(4, 4)) + 1j * rng.normal(size=(4, 4))
+        m[0, 2] = m[1, 3] = 0
+        want = O.kron_identity(left, O.from_dense(m), right)
+        got = D.kron_identity(left, D.from_dense(m, 0.0), right)
+        assert got.diag_indices() == want.offs.tolist()
+        assert np.array_equal(D.to_dense(got), want.to_dense())
+
+
+def test_span_embeddings(kats):
+    for case in kats["kats"]["span"]:
+        g = D.from_dense(dense_from_pairs(case["g"]), 0.0)
+        u = D.build_span_unitary(g, case["positions"], case["span"])
+        assert u.diag_indices() == case["offsets"], case["name"]
+        assert np.array_equal(values(u), pairs_to_complex(case["values"])), case["name"]
+    gsw = D.gate_matrix(D.GateOp("swap", (0, 1)))
+    assert D.build_span_unitary(gsw, [0, 1], 2) == gsw
+    with pytest.raises(D.ShapeError):
+        D.build_span_unitary(gsw, [0, 0], 2)
+    with pytest.raises(D.ShapeError):
+        D.build_span_unitary(gsw, [0, 2], 2)
+
+
+def test_catalog_gates(kats):
+    for name, rec in kats["kats"]["catalog"].items():
+        nq = D.GATE_DEFS[name][0]
+        g = D.gate_matrix(D.GateOp(name, tuple(range(nq)), tuple(rec["params"])))
+        assert g.diag_indices() == rec["offsets"], name
+        assert np.array_equal(values(g), pairs_to_complex(rec["values"])), name
+
+
+def test_kernel_protocol_goldens(kats):
+    proto = kats["kernel_protocol"]
+    corner = proto["corner"]
+    a = D.from_dense(dense_from_pairs(corner["dense"]), 0.0)
+    assert D.to_json_dict(a) == corner["wire"]
+    assert np.array_equal(D.to_dense(D.from_json_dict(corner["wire"])), dense_from_pairs(corner["round_trip"]))
+    mc = proto["matmul_case"]
+    a = D.from_json_dict(mc["a"])
+    b = D.from_json_dict(mc["b"])
+    c = D.matmul(a, b)
+    assert D.to_json_dict(c) == mc["c"]
+    assert np.array_equal(D.to_dense(c), dense_from_pairs(mc["c_dense"]))
+    y = D.spmv(a, pairs_to_complex(mc["x"]))
+    assert np.array_equal(y, pairs_to_complex(mc["y"]))
+
+
+# ---- BASELINE configs ------------------------------------------------------
+
+def test_config1_spmv_bitwise():
+    g = np.load(os.path.join(GOLDEN, "config1_spmv.npz"))
+    c1 = W.config1(0)
+    a = D.kron_identity(c1["left"], D.from_dense(c1["u"], 0.0), c1["right"])
+    assert a.diag_indices() == g["offsets"].tolist() == [-32, 0, 32]
+    assert [len(dg) for dg in a.diagonals()] == [16352, 16384, 16352]
+    assert np.array_equal(values(a), g["a_values"])
+    y = D.spmv(a, c1["x"])
+    assert np.array_equal(y, g["y"])
+
+
+def _c2(seed):
+    p = W.config2(seed)
+    span = D.build_span_unitary(D.from_dense(p["u4"], 0.0), p["u4_positions"], p["u4_span"])
+    A = D.kron_identity(p["a_left"], span, p["a_right"])
+    B1 = D.kron_identity(p["b1_left"], D.from_dense(p["u2"], 0.0), p["b1_right"])
+    B0 = D.kron_identity(p["b0_left"], D.from_dense(W.rz(p["theta"]), 0.0), p["b0_right"])
+    B = D.matmul(B1, B0)
+    return A, B1, B0, B, D.matmul(A, B)
+
+
+def test_config2_spgemm_bitwise():
+    g = np.load(os.path.join(GOLDEN, "config2_spgemm.npz"))
+    A, B1, B0, B, C = _c2(0)
+    assert A.diag_indices() == g["a_offsets"].tolist()
+    assert B.diag_indices() == g["b_offsets"].tolist()
+    assert np.array_equal(values(B), g["b_values"])
+    assert C.diag_indices() == g["c_offsets"].tolist()
+    assert C.diag_count() == 27
+    assert np.array_equal(values(C), g["c_values"])
+    assert D.matmul(A, B) == C  # bitwise repeatable
+
+
+def test_config2_sweep_digests(configs):
+    for rec in configs["config2_sweep"]:
+        _, _, _, B, C = _c2(rec["seed"])
+        assert B.diag_indices() == rec["b_offsets"]
+        assert digest(values(B)) == rec["b_digest"]
+        assert C.diag_indices() == rec["c_offsets"]
+        assert digest(values(C)) == rec["c_digest"], rec["seed"]
+
+
+def test_random_kernel_cases(random_cases, cmul):
+    rc = random_cases
+    for i in range(48):
+        c = D.matmul(D.from_dense(rc[f"mm{i}_a"], 0.0), D.from_dense(rc[f"mm{i}_b"], 0.0))
+        assert c.diag_indices() == rc[f"mm{i}_c_offsets"].tolist()
+        assert np.array_equal(values(c), rc[f"mm{i}_c_values"])
+    for i in range(100):
+        y = D.spmv(D.from_dense(rc[f"mv{i}_a"], 0.0), rc[f"mv{i}_x"])
+        assert np.array_equal(y, rc[f"mv{i}_y"]), i
+    for i in range(100):
+        dim_a, dim_b = (int(v) for v in rc[f"ap{i}_dims"])
+        m = D.from_dense(rc[f"ap{i}_m"], 0.0)
+        n_q = int(np.log2(m.n_dim))
+        p = D.Placement(dim_a, m, dim_b, 0, n_q - 1, "rand")
+        x = D.StateVector(int(np.log2(len(rc[f"ap{i}_x"]))), rc[f"ap{i}_x"])
+        y = D.apply_placed(p, x, cmul_mode=cmul).amps
+        assert np.array_equal(y, rc[f"ap{i}_y"]), i
+
+
+def test_generic_placed_kernel_matches_oracle(cmul):
+    """Non-power-of-two placements take the diagonal kernel (apply.cu placed_kernel)."""
+    rng = np.random.default_rng(11)
+    for dim_a, n_m, dim_b in ((3, 5, 2), (1, 7, 1), (5, 3, 4), (2, 33, 3)):
+        m = rng.normal(size=(n_m, n_m)) + 1j * rng.normal(size=(n_m, n_m))
+        m[np.abs(np.subtract.outer(np.arange(n_m), np.arange(n_m))) % 2 == 1] = 0
+        x = rng.normal(size=dim_a * n_m * dim_b) + 1j * rng.normal(size=dim_a * n_m * dim_b)
+        p = D.Placement(dim_a, D.from_dense(m, 0.0), dim_b, 0, 0, "g")
+        assert p.compact() is None
+        got = D.apply_placed(p, D.StateVector(0, x), cmul_mode=cmul).amps
+        want = O.apply_placed(dim_a, O.from_dense(m), dim_b, x, cmul)
+        assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("n", [8, 12])
+def test_circuit_full_state(configs, cmul, n):
+    rec = configs["circuits"][str(n)]
+    ops = W.random_layered_ops(n, rec["layers"], rec["seed"])
+    c = D.Circuit(n, [D.GateOp(*o) for o in ops])
+    res = D.run(c, shots=1024, seed=0, span_limit=n, emit_state=True)
+    want = np.load(os.path.join(GOLDEN, f"circuit_n{n}_state.npy"))
+    assert np.array_equal(res.state, want)
+    assert res.counts == rec["counts"]
+    assert len(res.timings_ns["per_gate"]) == len(ops)
+
+
+def test_circuit_n20_vs_reference_digest_and_oracle(configs, cmul):
+    rec = configs["circuits"]["20"]
+    ops = W.random_layered_ops(20, rec["layers"], rec["seed"])
+    c = D.Circuit(20, [D.GateOp(*o) for o in ops])
+    st = D.run_gates(D.init_state(20), D.compile_circuit(c, span_limit=20), cmul_mode=cmul)
+    amps = st.amps
+    assert digest(amps) == rec["digest"]
+    idx = np.array(rec["sample_idx"])
+    assert np.array_equal(amps[idx], pairs_to_complex(rec["sample"]))
+    assert abs(st.norm() - 1.0) < 1e-10
+
+
+def test_fusion_case(configs, cmul):
+    rec = configs["circuits"]["fusion_case"]
+    c = D.Circuit(rec["n"], [D.GateOp(*o) for o in rec["ops"]])
+    for fusion in (False, True):
+        res = D.run(c, shots=512, seed=3, fusion=fusion, emit_state=True, span_limit=6)
+        want = pairs_to_complex(rec["runs"][str(fusion)]["state"])
+        assert rel_l2(res.state, want) < 1e-12
+        assert np.array_equal(res.state, want), fusion
+        assert len(res.timings_ns["per_gate"]) == rec["runs"][str(fusion)]["gates"]
+        assert res.counts == rec["runs"][str(fusion)]["counts"]
+
+
+def test_ghz_kats(kats, cmul):
+    for n, rec in kats["kats"]["ghz"].items():
+        n = int(n)
+        ops = [("h", (0,), ())] + [("cx", (i, i + 1), ()) for i in range(n - 1)]
+        res = D.run(D.Circuit(n, [D.GateOp(*o) for o in ops]), shots=1024, seed=0, emit_state=True)
+        assert digest(res.state) == rec["digest"]
+        assert res.counts == rec["counts"]
+    sim = kats["kernel_protocol"]["ghz4_simulate"]
+    res = D.run(D.Circuit(4, [D.GateOp(*o) for o in sim["ops"]]), shots=1024, seed=7, emit_state=True)
+    assert np.array_equal(res.state, pairs_to_complex(sim["result"]["state"]))
+    assert res.counts == sim["result"]["counts"] == {"0000": 534, "1111": 490}
+
+
+def test_config4_n22_slice(configs):
+    rec = configs["config4_n22"]
+    c4 = W.config4(22, seed=0)
+    assert digest(c4["x"]) == rec["x_digest"]
+    span = D.build_span_unitary(D.from_dense(c4["u4"], 0.0), c4["positions"], c4["span"])
+    a = D.kron_identity(c4["left"], span, c4["right"])
+    assert a.diag_indices() == rec["offsets"]
+    assert digest(values(a)) == rec["a_digest"]
+    y = D.spmv(a, c4["x"])
+    assert digest(y) == rec["y_digest"]
+
+
+# ---- errors, determinism, edge sizes ----------------------------------------------
+
+def test_error_contract():
+    with pytest.raises(D.ShapeError, match="not multiplyable"):
+        D.spmv(D.identity(4), np.ones(5))
+    with pytest.raises(D.ShapeError, match="not multiplyable"):
+        D.matmul(D.identity(4), D.identity(8))
+    with pytest.raises(D.ResourceError):
+        D.init_state(31)
+    with pytest.raises(D.ResourceError):
+        D.init_state(0)
+    p = D.Placement(2, D.from_dense(np.eye(4), 0.0), 2, 0, 1, "i")
+    with pytest.raises(D.ShapeError):
+        D.apply_placed(p, D.init_state(3))
+    with pytest.raises(ValueError):
+        D.run(D.Circuit(1, [D.GateOp("h", (0,))]), backend="gpu")
+
+
+def test_spmv_many_diagonals_and_extremes():
+    """nd beyond the unrolled paths (13..64 dynamic, >64 global table) and |d| = n-1."""
+    rng = np.random.default_rng(21)
+    for n, nd in ((97, 13), (200, 40), (300, 80), (1000, 130)):
+        offs = rng.choice(np.arange(-(n - 1), n), size=nd, replace=False)
+        offs[0], offs[1] = n - 1, -(n - 1)
+        diags = {}
+        for d in sorted(set(int(o) for o in offs)):
+            ln = n - abs(d)
+            diags[d] = (rng.normal(size=ln), rng.normal(size=ln))
+        om = O.omat_from_diags(n, diags)
+        a = D.DiaqMatrix(n)
+        for d, (r, i) in diags.items():
+            a.set_diag(d, r, i)
+        x = rng.normal(size=n) + 1j * rng.normal(size=n)
+        assert np.array_equal(D.spmv(a, x), O.spmv(om, x))
+
+
+def test_determinism_and_immutability(cmul):
+    rng = np.random.default_rng(2)
+    m = rng.normal(size=(48, 48)) + 1j * rng.normal(size=(48, 48))
+    m[np.abs(np.subtract.outer(np.arange(48), np.arange(48))) > 5] = 0
+    a = D.from_dense(m, 0.0)
+    assert D.matmul(a, a) == D.matmul(a, a)
+    x = rng.normal(size=48) + 1j * rng.normal(size=48)
+    assert np.array_equal(D.spmv(a, x), D.spmv(a, x))
+    p = D.compile_circuit(D.Circuit(10, [D.GateOp("cx", (3, 8))]), span_limit=10)[0]
+    xs = D.StateVector(10, rng.normal(size=1024) + 1j * rng.normal(size=1024))
+    before = xs.amps.copy()
+    base = D.apply_placed(p, xs, threads=1).amps
+    for workers in (2, 3, 8):
+        assert np.array_equal(D.apply_placed(p, xs, threads=workers).amps, base)
+    assert np.array_equal(xs.amps, before)
+    # lazily built span matrix agrees with the compact apply
+    want = O.apply_placed(p.dim_a, omat(p.m), p.dim_b, before, cmul)
+    assert np.array_equal(base, want)
