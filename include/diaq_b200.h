@@ -143,6 +143,13 @@ typedef struct {
 int diaq_run_gates(int n_bits, int ngates, const diaq_gate_t *gates, void *state, int cmul_mode,
                    void **events, void *stream);
 
+/* ---- timing (per-gate CUDA events, resolved after the loop) ---------------- */
+int diaq_timer_create(int n, void **events);
+int diaq_timer_record(void *event, void *stream);
+/* waits for events[n-1]; ms_out[i] = milliseconds from events[i] to events[i+1] */
+int diaq_timer_elapsed(int n, void **events, float *ms_out);
+int diaq_timer_destroy(int n, void **events);
+
 /* ---- state helpers ------------------------------------------------------ */
 /* |index> (reference init_state, sim.py:53-59) */
 int diaq_init_basis(int64_t n_amps, void *x, int64_t index, void *stream);

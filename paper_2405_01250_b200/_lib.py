@@ -78,6 +78,10 @@ _SIGS = {
     "diaq_run_gates": ([_INT, _INT, ctypes.POINTER(Gate), _P, _INT, _P, _P], _INT),
     "diaq_init_basis": ([_I64, _P, _I64, _P], _INT),
     "diaq_norm2": ([_I64, _P, _P, _P], _INT),
+    "diaq_timer_create": ([_INT, _P], _INT),
+    "diaq_timer_record": ([_P, _P], _INT),
+    "diaq_timer_elapsed": ([_INT, _P, _P], _INT),
+    "diaq_timer_destroy": ([_INT, _P], _INT),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -193,3 +197,30 @@ def layout(n: int, offs: np.ndarray) -> tuple[np.ndarray, int]:
     call("diaq_layout", int(n), len(offs), offs.ctypes.data if len(offs) else None,
          starts.ctypes.data if len(offs) else None, ctypes.addressof(total))
     return starts, int(total.value)
+
+
+class Timer:
+    """n CUDA events owned by the library (per-gate timing without host syncs)."""
+
+    def __init__(self, n: int):
+        self.n = int(n)
+        self.events = (ctypes.c_void_p * max(1, self.n))()
+        call("diaq_timer_create", self.n, self.events)
+
+    def record(self, i: int) -> None:
+        call("diaq_timer_record", self.events[i], stream_handle())
+
+    def slice_ptr(self, start: int) -> int:
+        return ctypes.addressof(self.events) + start * ctypes.sizeof(ctypes.c_void_p)
+
+    def elapsed_ms(self) -> np.ndarray:
+        out = np.zeros(max(1, self.n - 1), dtype=np.float32)
+        call("diaq_timer_elapsed", self.n, self.events, out.ctypes.data)
+        return out[: self.n - 1]
+
+    def __del__(self):
+        try:
+            if _lib is not None:
+                _lib.diaq_timer_destroy(self.n, self.events)
+        except Exception:
+            pass

@@ -73,3 +73,40 @@ extern "C" int diaq_layout(int64_t n, int64_t nd, const int64_t *offs, int64_t *
     *total = (cur + 7) & ~7ll;
     return DIAQ_OK;
 }
+
+// ---- per-gate timing events (reference run() per_gate timings, sim.py:193-199) ----
+extern "C" int diaq_timer_create(int n, void **events) {
+    if (n < 0 || (n > 0 && !events)) return set_error(DIAQ_ERR_VALUE, "diaq_timer_create: bad arguments");
+    for (int i = 0; i < n; ++i) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) {
+            for (int j = 0; j < i; ++j) cudaEventDestroy((cudaEvent_t)events[j]);
+            return set_error(DIAQ_ERR_CUDA, "cudaEventCreate: %s", cudaGetErrorString(cudaGetLastError()));
+        }
+        events[i] = (void *)e;
+    }
+    return DIAQ_OK;
+}
+
+// waits for events[n-1]; ms_out[i] = time between events[i] and events[i+1]
+extern "C" int diaq_timer_elapsed(int n, void **events, float *ms_out) {
+    if (n < 1 || !events || !ms_out) return set_error(DIAQ_ERR_VALUE, "diaq_timer_elapsed: bad arguments");
+    if (cudaEventSynchronize((cudaEvent_t)events[n - 1]) != cudaSuccess)
+        return set_error(DIAQ_ERR_CUDA, "cudaEventSynchronize: %s", cudaGetErrorString(cudaGetLastError()));
+    for (int i = 0; i + 1 < n; ++i)
+        if (cudaEventElapsedTime(&ms_out[i], (cudaEvent_t)events[i], (cudaEvent_t)events[i + 1]) != cudaSuccess)
+            return set_error(DIAQ_ERR_CUDA, "cudaEventElapsedTime: %s", cudaGetErrorString(cudaGetLastError()));
+    return DIAQ_OK;
+}
+
+extern "C" int diaq_timer_destroy(int n, void **events) {
+    for (int i = 0; i < n; ++i)
+        if (events[i]) cudaEventDestroy((cudaEvent_t)events[i]);
+    return DIAQ_OK;
+}
+
+extern "C" int diaq_timer_record(void *event, void *stream) {
+    if (cudaEventRecord((cudaEvent_t)event, (cudaStream_t)stream) != cudaSuccess)
+        return set_error(DIAQ_ERR_CUDA, "cudaEventRecord: %s", cudaGetErrorString(cudaGetLastError()));
+    return DIAQ_OK;
+}

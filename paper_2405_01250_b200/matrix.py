@@ -338,30 +338,43 @@ def multiply_diagonals(diag_a: Diagonal, diag_b: Diagonal, n_dim: int):
     return d_c, c.get(d_c)
 
 
-def _as_device_vector(x, n: int, what: str):
+def _as_device_vector(x, n: int):
+    """(device complex128 vector, kind) with kind in {"numpy", "cuda", "cpu_tensor"}."""
     t = L.torch()
     if isinstance(x, t.Tensor):
         if tuple(x.shape) != (n,):
             raise ShapeError(f"not multiplyable: {n}x{n} by vector of shape {tuple(x.shape)}")
-        return L.to_device_c128(x), True
+        return L.to_device_c128(x), ("cuda" if x.device.type == "cuda" else "cpu_tensor")
     x = np.asarray(x)
     if x.shape != (n,):
         raise ShapeError(f"not multiplyable: {n}x{n} by vector of shape {x.shape}")
-    return L.to_device_c128(x), False
+    return L.to_device_c128(x), "numpy"
 
 
-def spmv(a: DiaqMatrix, x) -> np.ndarray:
+def spmv(a: DiaqMatrix, x, out=None):
     """Sparse matrix-vector product A @ x (matrix.py:253-278).
 
-    Bitwise equal to the reference.  A host `x` returns a host complex128
-    array (reference behaviour); a CUDA tensor `x` returns a CUDA tensor.
+    Bitwise equal to the reference.  A host numpy `x` returns a host
+    complex128 array (reference behaviour); a CUDA tensor returns a CUDA
+    tensor.  `out` (extension): a complex128 torch tensor, on the device or in
+    (pinned) host memory, that receives y.
     """
     n = a.n_dim
-    xd, on_device = _as_device_vector(x, n, "spmv")
-    y = L.empty_c128(n)
+    xd, kind = _as_device_vector(x, n)
+    t = L.torch()
+    if out is not None and (not isinstance(out, t.Tensor) or tuple(out.shape) != (n,)
+                            or out.dtype != t.complex128):
+        raise ShapeError(f"out must be a complex128 tensor of shape ({n},)")
+    y = out if out is not None and out.device.type == "cuda" else L.empty_c128(n)
     st = a._struct()
     L.call("diaq_spmv", ctypes.byref(st), xd.data_ptr(), y.data_ptr(), L.stream_handle())
-    return y if on_device else y.cpu().numpy()
+    if out is not None:
+        if out is not y:
+            out.copy_(y)
+        return out
+    if kind == "numpy":
+        return y.cpu().numpy()
+    return y if kind == "cuda" else y.cpu()
 
 
 # -- metadata operations (host side; not on the hot path) ---------------------

@@ -232,17 +232,17 @@ class _GateProgram:
 
 
 def run_gates(state: StateVector, placements: list[Placement], cmul_mode: int | None = None,
-              events: list | None = None, inplace: bool = False) -> StateVector:
+              timer: "L.Timer | None" = None, inplace: bool = False) -> StateVector:
     """Apply placements in order on the device; each maximal run of compact
     gates goes through one native call (diaq_run_gates, in place).  The input
-    state is left untouched unless inplace=True."""
+    state is left untouched unless inplace=True.  `timer` (len(placements)+1
+    events) records the boundaries of every gate."""
     mode = CMUL_MODE if cmul_mode is None else cmul_mode
     n_bits = len(state).bit_length() - 1
     xd = state.device_amps
     if not inplace:
         xd = xd.clone()
     i = 0
-    ev_i = 0
     s = L.stream_handle()
     while i < len(placements):
         j = i
@@ -252,24 +252,18 @@ def run_gates(state: StateVector, placements: list[Placement], cmul_mode: int | 
             j += 1
         if comps:
             prog = _GateProgram(comps)
-            evs = None
-            if events is not None:
-                sub = events[ev_i: ev_i + prog.n + 1]
-                evs = (ctypes.c_void_p * len(sub))(*[e.cuda_event for e in sub])
-            L.call("diaq_run_gates", n_bits, prog.n, prog.arr, xd.data_ptr(), int(mode),
-                   evs, s)
-            ev_i += prog.n
+            evs = timer.slice_ptr(i) if timer is not None else None
+            L.call("diaq_run_gates", n_bits, prog.n, prog.arr, xd.data_ptr(), int(mode), evs, s)
             i = j
             continue
         p = placements[i]
         yd = L.empty_c128(xd.numel())
-        if events is not None:
-            events[ev_i].record()
+        if timer is not None:
+            timer.record(i)
         _apply_into(p, xd, yd, mode)
         xd = yd
-        if events is not None:
-            events[ev_i + 1].record()
-        ev_i += 1
+        if timer is not None:
+            timer.record(i + 1)
         i += 1
     return StateVector(state.n_qubits, xd)
 
@@ -292,28 +286,23 @@ def run(
     if backend not in BACKENDS:
         raise ValueError(f"backend must be one of {BACKENDS}, got '{backend}'")
     kwargs = {} if span_limit is None else {"span_limit": span_limit}
-    t = L.torch()
-
     t0 = time.perf_counter_ns()
     placements = fuse_pass(compile_circuit(circuit, **kwargs), enabled=fusion)
     t_compile = time.perf_counter_ns() - t0
 
     state = init_state(circuit.n_qubits)
-    events = [t.cuda.Event(enable_timing=True) for _ in range(len(placements) + 1)]
+    timer = L.Timer(len(placements) + 1)
     t0 = time.perf_counter_ns()
     if backend == "diaq":
-        state = run_gates(state, placements, events=events, inplace=True)
+        state = run_gates(state, placements, timer=timer, inplace=True)
     else:
-        events[0].record()
+        timer.record(0)
         for i, p in enumerate(placements):
             state = apply_dense(p, state)
-            events[i + 1].record()
-    events[-1].synchronize()
+            timer.record(i + 1)
+    ms = timer.elapsed_ms()  # one host sync after the whole loop
     t_apply = time.perf_counter_ns() - t0
-    per_gate = {
-        f"{i}:{p.name}": int(round(events[i].elapsed_time(events[i + 1]) * 1e6))
-        for i, p in enumerate(placements)
-    }
+    per_gate = {f"{i}:{p.name}": int(round(float(ms[i]) * 1e6)) for i, p in enumerate(placements)}
 
     t0 = time.perf_counter_ns()
     counts = measure_all_sample(state, shots, seed)
