@@ -21,16 +21,36 @@ import numpy as np
 
 
 def haar(rng: np.random.Generator, dim: int) -> np.ndarray:
+    """Haar unitary by modified Gram-Schmidt in plain Python arithmetic.
+
+    Same distribution as QR with the r_ii phase fix (MGS yields a positive
+    real diagonal of R), but no LAPACK/BLAS: every operation is a correctly
+    rounded IEEE op in a fixed order, so the gate is bit-identical on every
+    host (fixtures stay valid on any GPU box).
+    """
     z = rng.normal(size=(dim, dim)) + 1j * rng.normal(size=(dim, dim))
-    q, r = np.linalg.qr(z)
-    ph = np.diagonal(r) / np.abs(np.diagonal(r))
-    return np.ascontiguousarray(q * ph[None, :], dtype=np.complex128)
+    cols = [[complex(z[i, j]) for i in range(dim)] for j in range(dim)]
+    q = []
+    for v in cols:
+        v = list(v)
+        for u in q:
+            proj = sum((u[i].conjugate() * v[i] for i in range(dim)), 0j)
+            v = [v[i] - proj * u[i] for i in range(dim)]
+        nrm = math.sqrt(math.fsum(c.real * c.real + c.imag * c.imag for c in v))
+        q.append([c / nrm for c in v])
+    return np.ascontiguousarray(np.array(q, dtype=np.complex128).T)
 
 
 def random_state(rng: np.random.Generator, n_amps: int) -> np.ndarray:
-    x = rng.normal(size=n_amps) + 1j * rng.normal(size=n_amps)
-    x /= np.linalg.norm(x)
-    return x.astype(np.complex128)
+    """normal + 1j*normal, L2-normalised with an exactly rounded norm (math.fsum),
+    so x is bit-identical on every host (no BLAS reduction order)."""
+    re = rng.normal(size=n_amps)
+    im = rng.normal(size=n_amps)
+    nrm = math.sqrt(math.fsum(re * re) + math.fsum(im * im))
+    x = np.empty(n_amps, dtype=np.complex128)
+    x.real = re / nrm
+    x.imag = im / nrm
+    return x
 
 
 def rz(theta: float) -> np.ndarray:
