@@ -66,6 +66,11 @@ const char *diaq_last_error(void);               /* thread-local message */
 int diaq_device_count(int *count);
 uint64_t diaq_launch_count(void);                /* kernels launched by this library */
 void diaq_reset_launch_count(void);
+/* launch-geometry knobs (never change results): "spmv_raster" (0 strip-
+ * fastest, 1 column chunks), "spmv_chunk", "spmv_xpol" (0 normal, 1 L2
+ * evict_last for x), "spmv_ctas_per_sm" (0 = occupancy max),
+ * "gate_ctas_per_sm" */
+int diaq_tune(const char *key, int64_t value);
 
 /* ---- layout (host only) ----------------------------------------------
  * Row-aligned storage starts for a diagonal set; returns total arena
@@ -142,6 +147,23 @@ typedef struct {
  * (per-gate timings, resolved by the caller after the loop). */
 int diaq_run_gates(int n_bits, int ngates, const diaq_gate_t *gates, void *state, int cmul_mode,
                    void **events, void *stream);
+
+/* ---- sharded state ------------------------------------------
+ * The 2^n_bits state is split over P = 2^(n_bits-local_bits) ranks by its
+ * top bits; rank r holds indices [r*2^local_bits, (r+1)*2^local_bits).
+ * A gate's operands on bits >= local_bits are "global".  Relabel the
+ * operands by descending shift; the global ones form the top kg bits of the
+ * gate index.  Rank r produces only its own row block vr (its global operand
+ * bit values) and reads column block v from srcs[v] (v = values of the
+ * global operands, first = highest shift = most significant).
+ * diaq_shard_plan (host only) reports which blocks rank r reads; the caller
+ * exchanges the partner shards for those blocks, then calls
+ * diaq_apply_gate_sharded (srcs[v] may be NULL for unread blocks; y may
+ * alias srcs[vr], the rank's own shard). */
+int diaq_shard_plan(int n_bits, int local_bits, int k, const double *g_host, const int *shifts,
+                    int64_t rank, uint32_t *need_mask, int *n_global, uint32_t *own_block);
+int diaq_apply_gate_sharded(int n_bits, int local_bits, int k, const double *g_host, const int *shifts,
+                            int64_t rank, const void *const *srcs, void *y, int cmul_mode, void *stream);
 
 /* ---- timing (per-gate CUDA events, resolved after the loop) ---------------- */
 int diaq_timer_create(int n, void **events);

@@ -62,6 +62,7 @@ _SIGS = {
     "diaq_device_count": ([ctypes.POINTER(_INT)], _INT),
     "diaq_launch_count": ([], ctypes.c_uint64),
     "diaq_reset_launch_count": ([], None),
+    "diaq_tune": ([ctypes.c_char_p, _I64], _INT),
     "diaq_layout": ([_I64, _I64, _P, _P, _P], _INT),
     "diaq_kron_identity": ([_I64, _MP, _I64, _MP, _P], _INT),
     "diaq_span_plan": ([_INT, _P, _P, _INT, _P, _P], _INT),
@@ -78,6 +79,8 @@ _SIGS = {
     "diaq_run_gates": ([_INT, _INT, ctypes.POINTER(Gate), _P, _INT, _P, _P], _INT),
     "diaq_init_basis": ([_I64, _P, _I64, _P], _INT),
     "diaq_norm2": ([_I64, _P, _P, _P], _INT),
+    "diaq_shard_plan": ([_INT, _INT, _INT, _P, _P, _I64, _P, _P, _P], _INT),
+    "diaq_apply_gate_sharded": ([_INT, _INT, _INT, _P, _P, _I64, _P, _P, _INT, _P], _INT),
     "diaq_timer_create": ([_INT, _P], _INT),
     "diaq_timer_record": ([_P, _P], _INT),
     "diaq_timer_elapsed": ([_INT, _P, _P], _INT),
@@ -131,6 +134,11 @@ def check(rc: int, what: str) -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args), name)
+
+
+def tune(key: str, value: int) -> None:
+    """Set a launch-geometry knob of the library (results never depend on it)."""
+    call("diaq_tune", key.encode(), int(value))
 
 
 def launch_count() -> int:

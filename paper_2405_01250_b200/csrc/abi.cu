@@ -9,6 +9,8 @@
 namespace diaq {
 
 static thread_local std::string g_last_error;
+static Tuning g_tuning;
+Tuning &tuning() { return g_tuning; }
 static std::atomic<uint64_t> g_launches{0};
 
 int set_error(int code, const char *fmt, ...) {
@@ -34,6 +36,19 @@ int check_launch(const char *what) {
 using namespace diaq;
 
 extern "C" int diaq_version(void) { return 1; }
+
+extern "C" int diaq_tune(const char *key, int64_t value) {
+    if (!key) return set_error(DIAQ_ERR_VALUE, "diaq_tune: null key");
+    const std::string k(key);
+    Tuning &t = g_tuning;
+    if (k == "spmv_raster") t.spmv_raster = (int)value;
+    else if (k == "spmv_chunk") t.spmv_chunk = (int)(value < 1 ? 1 : value);
+    else if (k == "spmv_xpol") t.spmv_xpol = (int)value;
+    else if (k == "spmv_ctas_per_sm") t.spmv_ctas_per_sm = (int)value;
+    else if (k == "gate_ctas_per_sm") t.gate_ctas_per_sm = (int)(value < 1 ? 1 : value);
+    else return set_error(DIAQ_ERR_VALUE, "diaq_tune: unknown key %s", key);
+    return DIAQ_OK;
+}
 
 extern "C" const char *diaq_last_error(void) { return g_last_error.c_str(); }
 

@@ -64,6 +64,55 @@ __global__ void __launch_bounds__(kThreads) gate_kernel(const __grid_constant__ 
     }
 }
 
+// ---- sharded state: multi-source gate kernel ---------------
+// The state is split over its top log2(P) bits.  A gate's operands split
+// into KL local bits and KG global (rank) bits.  After relabelling by
+// descending shift the global operands are the top KG bits of the gate
+// index, so for this rank only the 2^KL rows of block `vr` (its own global
+// bit values) are produced, and column block v (global operand values v) is
+// read from src[v]: this rank's shard for v == vr, a received partner shard
+// otherwise.  Ascending relabelled column = ascending embedding in the full
+// index, so per-amplitude summation order equals the single-GPU kernel's and
+// the reference's.
+template <int KL, int KG>
+struct MultiParams {
+    double2 *y;
+    int64_t ngroups;
+    int sh_sorted[KL > 0 ? KL : 1];
+    int64_t emb[1 << KL];
+    const double2 *src[1 << KG];
+    uint32_t srcmask;
+    uint32_t nzmask[1 << KL];
+    double2 g[1 << KL][1 << (KL + KG)];
+};
+
+template <int KL, int KG, int MODE>
+__global__ void __launch_bounds__(kThreads) gate_kernel_multi(const __grid_constant__ MultiParams<KL, KG> p) {
+    constexpr int ML = 1 << KL;
+    constexpr int MG = 1 << KG;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < p.ngroups; gi += stride) {
+        const uint64_t base = insert_zero_bits<KL>((uint64_t)gi, p.sh_sorted);
+        double2 xs[MG][ML];
+#pragma unroll
+        for (int v = 0; v < MG; ++v)
+#pragma unroll
+            for (int c = 0; c < ML; ++c)
+                xs[v][c] = ((p.srcmask >> v) & 1u) ? ld_plain(p.src[v] + base + p.emb[c]) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int r = 0; r < ML; ++r) {
+            double2 acc = make_double2(0.0, 0.0);
+            const uint32_t nz = p.nzmask[r];
+#pragma unroll
+            for (int v = 0; v < MG; ++v)
+#pragma unroll
+                for (int c = 0; c < ML; ++c)
+                    if ((nz >> (v * ML + c)) & 1u) acc = cadd(acc, cmul<MODE>(p.g[r][v * ML + c], xs[v][c]));
+            st_plain(p.y + base + p.emb[r], acc);
+        }
+    }
+}
+
 struct PlacedDiag {
     const double2 *row0;  // m value for span row `row` is row0[row]
     int64_t lo, hi;       // valid span rows
@@ -203,7 +252,8 @@ static int launch_gate(int n_bits, const double *g, const int *shifts, const voi
     p.x = (const double2 *)x;
     p.y = (double2 *)y;
     const int64_t want = (p.ngroups + kThreads - 1) / kThreads;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * 8));
+    const int grid = (int)std::max<int64_t>(
+        1, std::min<int64_t>(want, (int64_t)sm_count() * tuning().gate_ctas_per_sm));
     if (cmul_mode == DIAQ_CMUL_FMA) gate_kernel<K, DIAQ_CMUL_FMA><<<grid, kThreads, 0, s>>>(p);
     else gate_kernel<K, DIAQ_CMUL_PLAIN><<<grid, kThreads, 0, s>>>(p);
     count_launch();
@@ -221,6 +271,102 @@ int apply_gate(int n_bits, int k, const double *g, const int *shifts, const void
         case 4: return launch_gate<4>(n_bits, g, shifts, x, y, cmul_mode, s);
         default: return launch_gate<5>(n_bits, g, shifts, x, y, cmul_mode, s);
     }
+}
+
+
+// Relabelled view of a gate for a sharded state: operands sorted by
+// descending global shift (global operands first).  For rank `rank` returns
+// the block value vr of its global operand bits and the mask of column blocks
+// its rows read (nonzero entries).
+struct ShardView {
+    int k, kl, kg;
+    int perm[kMaxGateK];     // relabelled position j -> original operand
+    int shift[kMaxGateK];    // shift of relabelled operand j (descending)
+    int orig[32];            // relabelled index -> original gate index
+    uint32_t vr;             // this rank's global-operand block value
+    uint32_t need;           // column blocks read by this rank's rows
+};
+
+static int shard_view(int n_bits, int local_bits, int k, const double *g, const int *shifts, int64_t rank,
+                      ShardView &v) {
+    if (k < 1 || k > kMaxGateK) return set_error(DIAQ_ERR_UNSUPPORTED, "gate width %d outside 1..5", k);
+    if (local_bits < 1 || local_bits > n_bits) return set_error(DIAQ_ERR_SHAPE, "local_bits %d invalid", local_bits);
+    for (int i = 0; i < k; ++i) {
+        if (shifts[i] < 0 || shifts[i] >= n_bits)
+            return set_error(DIAQ_ERR_SHAPE, "gate shift %d outside state of %d qubits", shifts[i], n_bits);
+        for (int j = 0; j < i; ++j)
+            if (shifts[j] == shifts[i]) return set_error(DIAQ_ERR_SHAPE, "repeated gate bit %d", shifts[i]);
+    }
+    v.k = k;
+    for (int i = 0; i < k; ++i) v.perm[i] = i;
+    std::sort(v.perm, v.perm + k, [&](int a, int b) { return shifts[a] > shifts[b]; });
+    v.kg = 0;
+    for (int j = 0; j < k; ++j) {
+        v.shift[j] = shifts[v.perm[j]];
+        if (v.shift[j] >= local_bits) ++v.kg;
+    }
+    v.kl = k - v.kg;
+    const int M = 1 << k;
+    for (int cp = 0; cp < M; ++cp) {
+        int c = 0;
+        for (int j = 0; j < k; ++j) c |= ((cp >> (k - 1 - j)) & 1) << (k - 1 - v.perm[j]);
+        v.orig[cp] = c;
+    }
+    v.vr = 0;
+    for (int j = 0; j < v.kg; ++j) v.vr |= (uint32_t)((rank >> (v.shift[j] - local_bits)) & 1) << (v.kg - 1 - j);
+    v.need = 0;
+    const int ML = 1 << v.kl;
+    for (int rl = 0; rl < ML; ++rl) {
+        const int rp = ((int)v.vr << v.kl) | rl;
+        for (int cp = 0; cp < M; ++cp) {
+            const double re = g[2 * (v.orig[rp] * M + v.orig[cp])], im = g[2 * (v.orig[rp] * M + v.orig[cp]) + 1];
+            if (re != 0.0 || im != 0.0) v.need |= 1u << (cp >> v.kl);
+        }
+    }
+    return DIAQ_OK;
+}
+
+template <int KL, int KG>
+static int launch_multi(const ShardView &v, int local_bits, const double *g, const void *const *srcs, void *y,
+                        int cmul_mode, cudaStream_t s) {
+    constexpr int ML = 1 << KL;
+    constexpr int M = 1 << (KL + KG);
+    MultiParams<KL, KG> p;
+    p.y = (double2 *)y;
+    p.ngroups = (int64_t)1 << (local_bits - KL);
+    int sl[kMaxGateK];
+    for (int j = 0; j < KL; ++j) sl[j] = v.shift[KG + j];
+    std::sort(sl, sl + KL);
+    for (int j = 0; j < KL; ++j) p.sh_sorted[j] = sl[j];
+    if (KL == 0) p.sh_sorted[0] = 0;
+    for (int cl = 0; cl < ML; ++cl) {
+        int64_t e = 0;
+        for (int j = 0; j < KL; ++j) e |= (int64_t)((cl >> (KL - 1 - j)) & 1) << v.shift[KG + j];
+        p.emb[cl] = e;
+    }
+    p.srcmask = v.need;
+    for (int b = 0; b < (1 << KG); ++b) {
+        p.src[b] = (const double2 *)srcs[b];
+        if (((v.need >> b) & 1u) && !srcs[b])
+            return set_error(DIAQ_ERR_VALUE, "sharded gate: source block %d is needed but missing", b);
+    }
+    for (int rl = 0; rl < ML; ++rl) {
+        const int rp = ((int)v.vr << KL) | rl;
+        uint32_t nz = 0;
+        for (int cp = 0; cp < M; ++cp) {
+            const double re = g[2 * (v.orig[rp] * M + v.orig[cp])], im = g[2 * (v.orig[rp] * M + v.orig[cp]) + 1];
+            p.g[rl][cp] = make_double2(re, im);
+            if (re != 0.0 || im != 0.0) nz |= 1u << cp;
+        }
+        p.nzmask[rl] = nz;
+    }
+    const int64_t want = (p.ngroups + kThreads - 1) / kThreads;
+    const int grid = (int)std::max<int64_t>(
+        1, std::min<int64_t>(want, (int64_t)sm_count() * tuning().gate_ctas_per_sm));
+    if (cmul_mode == DIAQ_CMUL_FMA) gate_kernel_multi<KL, KG, DIAQ_CMUL_FMA><<<grid, kThreads, 0, s>>>(p);
+    else gate_kernel_multi<KL, KG, DIAQ_CMUL_PLAIN><<<grid, kThreads, 0, s>>>(p);
+    count_launch();
+    return check_launch("gate_kernel_multi");
 }
 
 }  // namespace diaq
@@ -296,4 +442,33 @@ extern "C" int diaq_norm2(int64_t n_amps, const void *x, double *work_dev, void 
     norm2_final<<<1, 1024, 0, s>>>(work_dev + 1, nb, work_dev);
     count_launch(2);
     return check_launch("norm2");
+}
+
+extern "C" int diaq_shard_plan(int n_bits, int local_bits, int k, const double *g_host, const int *shifts,
+                               int64_t rank, uint32_t *need_mask, int *n_global, uint32_t *own_block) {
+    if (!g_host || !shifts || !need_mask) return set_error(DIAQ_ERR_VALUE, "diaq_shard_plan: null argument");
+    ShardView v;
+    const int rc = shard_view(n_bits, local_bits, k, g_host, shifts, rank, v);
+    if (rc) return rc;
+    *need_mask = v.need;
+    if (n_global) *n_global = v.kg;
+    if (own_block) *own_block = v.vr;
+    return DIAQ_OK;
+}
+
+extern "C" int diaq_apply_gate_sharded(int n_bits, int local_bits, int k, const double *g_host, const int *shifts,
+                                       int64_t rank, const void *const *srcs, void *y, int cmul_mode, void *stream) {
+    if (!g_host || !shifts || !srcs || !y) return set_error(DIAQ_ERR_VALUE, "diaq_apply_gate_sharded: null argument");
+    ShardView v;
+    int rc = shard_view(n_bits, local_bits, k, g_host, shifts, rank, v);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (v.kg == 0) return apply_gate(local_bits, k, g_host, shifts, srcs[0], y, cmul_mode, s);
+#define DIAQ_MULTI(KL_, KG_) \
+    if (v.kl == KL_ && v.kg == KG_) return launch_multi<KL_, KG_>(v, local_bits, g_host, srcs, y, cmul_mode, s);
+    DIAQ_MULTI(0, 1) DIAQ_MULTI(1, 1) DIAQ_MULTI(2, 1) DIAQ_MULTI(3, 1) DIAQ_MULTI(4, 1)
+    DIAQ_MULTI(0, 2) DIAQ_MULTI(1, 2) DIAQ_MULTI(2, 2) DIAQ_MULTI(3, 2)
+    DIAQ_MULTI(0, 3) DIAQ_MULTI(1, 3) DIAQ_MULTI(2, 3)
+#undef DIAQ_MULTI
+    return set_error(DIAQ_ERR_UNSUPPORTED, "sharded gate with %d local + %d global operands", v.kl, v.kg);
 }

@@ -112,6 +112,15 @@ __device__ __forceinline__ uint64_t insert_zero_bits(uint64_t g, const int *sh) 
 
 // ---- host-side error plumbing (defined in abi.cu) ------------------------
 namespace diaq {
+// launch-geometry knobs (diaq_tune); results never depend on them
+struct Tuning {
+    int spmv_raster = 1;       // 0: strips fastest per tile, 1: column chunks
+    int spmv_chunk = 8;        // strips per work item in raster 1
+    int spmv_xpol = 0;         // 0: x evict_normal, 1: x evict_last
+    int spmv_ctas_per_sm = 0;  // 0: occupancy maximum
+    int gate_ctas_per_sm = 32;
+};
+Tuning &tuning();
 int set_error(int code, const char *fmt, ...);
 void count_launch(int n = 1);
 int check_launch(const char *what);

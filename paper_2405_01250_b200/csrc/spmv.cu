@@ -36,23 +36,31 @@ template <int MAXD>
 struct SpmvParams {
     int64_t n;
     int64_t ntiles, stride_tiles, nstrips, nitems;
+    int64_t nchunks;   // raster 1: chunks of `chunk` strips per column
+    int raster, chunk;
     const double2 *x;
     double2 *y;
     int nd;
     SpmvDiag dg[MAXD];
 };
 
+template <int XPOL>
+__device__ __forceinline__ double2 ld_x(const double2 *p, uint64_t pol_last) {
+    if constexpr (XPOL == 1) return ld_reuse_hint(p, pol_last);
+    else return ld_reuse(p);
+}
+
 // one row: ascending-d accumulation with reference rounding
-template <int ND>
+template <int ND, int XPOL>
 __device__ __forceinline__ double2 spmv_row(const SpmvDiag *dg, int nd, int64_t r, const double2 *x,
-                                            uint64_t pol) {
+                                            uint64_t pol, uint64_t pol_last) {
     double2 v[ND > 0 ? ND : 1], xv[ND > 0 ? ND : 1];
 #pragma unroll
     for (int i = 0; i < ND; ++i) {
         const bool ok = (r >= dg[i].lo) & (r < dg[i].hi);
         if (ok) {
             v[i] = ld_stream(dg[i].row0 + r, pol);
-            xv[i] = ld_reuse(x + r + dg[i].off);
+            xv[i] = ld_x<XPOL>(x + r + dg[i].off, pol_last);
         } else {
             v[i] = make_double2(0.0, 0.0);
             xv[i] = make_double2(0.0, 0.0);
@@ -69,38 +77,56 @@ __device__ __forceinline__ double2 spmv_row(const SpmvDiag *dg, int nd, int64_t 
 }
 
 // runtime diagonal count (ND == 0): same order, loads not hoisted
+template <int XPOL>
 __device__ __forceinline__ double2 spmv_row_dyn(const SpmvDiag *dg, int nd, int64_t r,
-                                                const double2 *x, uint64_t pol) {
+                                                const double2 *x, uint64_t pol, uint64_t pol_last) {
     double2 acc = make_double2(0.0, 0.0);
 #pragma unroll 4
     for (int i = 0; i < nd; ++i) {
         if (r >= dg[i].lo && r < dg[i].hi) {
             const double2 v = ld_stream(dg[i].row0 + r, pol);
-            const double2 xv = ld_reuse(x + r + dg[i].off);
+            const double2 xv = ld_x<XPOL>(x + r + dg[i].off, pol_last);
             acc = cadd(acc, cmul_plain(v, xv));
         }
     }
     return acc;
 }
 
-template <int MAXD, int ND>
+// Work item -> tiles.  raster 0: item = (b, j) with the strip j fastest, one
+// tile per item.  raster 1: item = (b, chunk of strips) -- one CTA walks
+// `chunk` strips of column b, so the x tile of strip j is reused by the same
+// CTA for strips j-1, j, j+1 (L1/L2 hits) and HBM sees x about once.
+template <int MAXD, int ND, int XPOL>
 __global__ void __launch_bounds__(kThreads) spmv_kernel(const __grid_constant__ SpmvParams<MAXD> p) {
     const uint64_t pol = policy_evict_first();
+    const uint64_t pol_last = XPOL ? policy_evict_last() : 0ull;
     for (int64_t it = blockIdx.x; it < p.nitems; it += gridDim.x) {
-        const int64_t j = it % p.nstrips;
-        const int64_t b = it / p.nstrips;
-        const int64_t t = j * p.stride_tiles + b;
-        if (b >= p.stride_tiles || t >= p.ntiles) continue;
-        const int64_t r = t * kThreads + threadIdx.x;
-        if (r >= p.n) continue;
-        double2 acc;
-        if constexpr (ND > 0) acc = spmv_row<ND>(p.dg, p.nd, r, p.x, pol);
-        else acc = spmv_row_dyn(p.dg, p.nd, r, p.x, pol);
-        st_stream(p.y + r, acc);
+        int64_t b, j0, j1;
+        if (p.raster == 0) {
+            j0 = it % p.nstrips;
+            b = it / p.nstrips;
+            j1 = j0 + 1;
+        } else {
+            const int64_t jc = it % p.nchunks;
+            b = it / p.nchunks;
+            j0 = jc * p.chunk;
+            j1 = j0 + p.chunk < p.nstrips ? j0 + p.chunk : p.nstrips;
+        }
+        if (b >= p.stride_tiles) continue;
+        for (int64_t j = j0; j < j1; ++j) {
+            const int64_t t = j * p.stride_tiles + b;
+            if (t >= p.ntiles) break;
+            const int64_t r = t * kThreads + threadIdx.x;
+            if (r >= p.n) continue;
+            double2 acc;
+            if constexpr (ND > 0) acc = spmv_row<ND, XPOL>(p.dg, p.nd, r, p.x, pol, pol_last);
+            else acc = spmv_row_dyn<XPOL>(p.dg, p.nd, r, p.x, pol, pol_last);
+            st_stream(p.y + r, acc);
+        }
     }
 }
 
-// large diagonal counts: tables in global memory
+// large diagonal counts: tables in global memory, raster 0
 __global__ void __launch_bounds__(kThreads)
 spmv_kernel_global(int64_t n, int nd, const SpmvDiag *__restrict__ dg, const double2 *x, double2 *y,
                    int64_t ntiles, int64_t stride_tiles, int64_t nstrips, int64_t nitems) {
@@ -112,7 +138,7 @@ spmv_kernel_global(int64_t n, int nd, const SpmvDiag *__restrict__ dg, const dou
         if (b >= stride_tiles || t >= ntiles) continue;
         const int64_t r = t * kThreads + threadIdx.x;
         if (r >= n) continue;
-        double2 acc = spmv_row_dyn(dg, nd, r, x, pol);
+        double2 acc = spmv_row_dyn<0>(dg, nd, r, x, pol, 0ull);
         st_stream(y + r, acc);
     }
 }
@@ -142,7 +168,7 @@ void spmv_raster(int64_t n, int64_t nd, const int64_t *offs, int64_t *ntiles, in
     *nstrips = (nt + st - 1) / st;
 }
 
-static int grid_for(const void *func, int64_t items) {
+static int grid_for(const void *func, int64_t items, int ctas_per_sm = 0) {
     int dev = 0, sms = kSms, per_sm = 1;
     if (cudaGetDevice(&dev) == cudaSuccess)
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -150,17 +176,23 @@ static int grid_for(const void *func, int64_t items) {
         per_sm < 1)
         per_sm = 1;
     cudaGetLastError();
+    if (ctas_per_sm > 0 && ctas_per_sm < per_sm) per_sm = ctas_per_sm;
     const int64_t g = std::min<int64_t>(items, (int64_t)sms * per_sm);
     return (int)std::max<int64_t>(g, 1);
 }
 
-template <int ND>
-static int launch_param(const SpmvParams<kParamDiags> &p, cudaStream_t s) {
-    const void *f = (const void *)spmv_kernel<kParamDiags, ND>;
-    const int grid = grid_for(f, p.nitems);
-    spmv_kernel<kParamDiags, ND><<<grid, kThreads, 0, s>>>(p);
+template <int ND, int XPOL>
+static int launch_param_x(const SpmvParams<kParamDiags> &p, cudaStream_t s) {
+    const void *f = (const void *)spmv_kernel<kParamDiags, ND, XPOL>;
+    const int grid = grid_for(f, p.nitems, tuning().spmv_ctas_per_sm);
+    spmv_kernel<kParamDiags, ND, XPOL><<<grid, kThreads, 0, s>>>(p);
     count_launch();
     return check_launch("spmv_kernel");
+}
+
+template <int ND>
+static int launch_param(const SpmvParams<kParamDiags> &p, cudaStream_t s) {
+    return tuning().spmv_xpol ? launch_param_x<ND, 1>(p, s) : launch_param_x<ND, 0>(p, s);
 }
 
 }  // namespace diaq
@@ -188,7 +220,10 @@ extern "C" int diaq_spmv(const diaq_matrix_t *a, const void *x, void *y, void *s
         p.ntiles = ntiles;
         p.stride_tiles = stride;
         p.nstrips = nstrips;
-        p.nitems = stride * nstrips;
+        p.raster = tuning().spmv_raster ? 1 : 0;
+        p.chunk = tuning().spmv_chunk;
+        p.nchunks = (nstrips + p.chunk - 1) / p.chunk;
+        p.nitems = p.raster ? stride * p.nchunks : stride * nstrips;
         p.x = (const double2 *)x;
         p.y = (double2 *)y;
         p.nd = (int)a->nd;

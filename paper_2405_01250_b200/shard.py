@@ -1,0 +1,251 @@
+"""Sharded state vector over several GPUs (no reference counterpart).
+
+The 2^n state is split over P = 2^p ranks by its top p bits (reference
+qubits 0..p-1, since qubit 0 is the most significant bit): rank r owns
+indices [r*2^L, (r+1)*2^L), L = n - p.  For every gate:
+
+* all operands local (bits < L): no communication, the single-GPU kernel;
+* some operands global: diaq_shard_plan tells each rank which column blocks
+  its rows read.  Block-diagonal gates in the global bits (RZ/diagonal gates
+  on any qubit, CX with a global control) read only the rank's own block --
+  no communication.  Otherwise every rank sends its shard to the ranks that
+  read it and receives the partner shards it reads (NCCL send/recv over
+  NVLink/NVSwitch via torch.distributed, or any comm with the same
+  interface), then diaq_apply_gate_sharded combines own + partner blocks.
+
+The per-amplitude summation order equals the single-GPU path's, so a sharded
+run is bitwise equal to the unsharded one.  Norms are an all-reduce (sum)
+of local |x|^2.  Timing is by CUDA events, max over ranks.
+
+The host logic (plans, partner schedule, exchange) is independent of the
+device: `apply_fn` defaults to the CUDA kernel; CPU tests inject a numpy
+stand-in and run it over gloo with world_size 2 and 4.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib as L
+from .gates import Placement
+
+
+def gate_plan(n_bits: int, local_bits: int, g: np.ndarray, shifts, rank: int) -> tuple[int, int, int]:
+    """(need_mask, n_global, own_block) for `rank` (host-only C-ABI call)."""
+    gd = np.ascontiguousarray(g, dtype=np.complex128)
+    sh = np.ascontiguousarray(shifts, dtype=np.int32)
+    need = ctypes.c_uint32(0)
+    kg = ctypes.c_int(0)
+    vr = ctypes.c_uint32(0)
+    L.call("diaq_shard_plan", n_bits, local_bits, len(sh), gd.ctypes.data, sh.ctypes.data, int(rank),
+           ctypes.addressof(need), ctypes.addressof(kg), ctypes.addressof(vr))
+    return int(need.value), int(kg.value), int(vr.value)
+
+
+def global_shifts(shifts, local_bits: int) -> list[int]:
+    """Global operand shifts in block-index order (descending shift = MSB first)."""
+    return sorted((s for s in shifts if s >= local_bits), reverse=True)
+
+
+def block_rank(rank: int, block: int, gshifts: list[int], local_bits: int) -> int:
+    """Rank holding column block `block` for the rows of `rank`."""
+    kg = len(gshifts)
+    r = rank
+    for j, s in enumerate(gshifts):
+        bit = (block >> (kg - 1 - j)) & 1
+        pos = s - local_bits
+        r = (r & ~(1 << pos)) | (bit << pos)
+    return r
+
+
+def exchange_schedule(n_bits: int, local_bits: int, g, shifts, world: int):
+    """needs[r] = {block: source rank} every rank reads, for all ranks."""
+    gs = global_shifts(shifts, local_bits)
+    needs = []
+    for r in range(world):
+        mask, _, _ = gate_plan(n_bits, local_bits, g, shifts, r)
+        needs.append({b: block_rank(r, b, gs, local_bits) for b in range(1 << len(gs)) if (mask >> b) & 1})
+    return needs
+
+
+def _cuda_apply(n_bits, local_bits, g, shifts, rank, srcs, y, cmul_mode):
+    gd = np.ascontiguousarray(g, dtype=np.complex128)
+    sh = np.ascontiguousarray(shifts, dtype=np.int32)
+    arr = (ctypes.c_void_p * len(srcs))(*[(t.data_ptr() if t is not None else None) for t in srcs])
+    L.call("diaq_apply_gate_sharded", n_bits, local_bits, len(sh), gd.ctypes.data, sh.ctypes.data, int(rank),
+           arr, y.data_ptr(), int(cmul_mode), L.stream_handle())
+
+
+class TorchDistComm:
+    """torch.distributed transport (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def exchange(self, sends, recvs) -> None:
+        """sends: [(peer, tensor)], recvs: [(peer, tensor)] -- one batched group."""
+        import torch
+        re = torch.view_as_real  # complex128 travels as float64 pairs (gloo has no complex)
+        ops = [self.dist.P2POp(self.dist.isend, re(t), p, self.group) for p, t in sends]
+        ops += [self.dist.P2POp(self.dist.irecv, re(t), p, self.group) for p, t in recvs]
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def allreduce_sum(self, value: float, like) -> float:
+        import torch
+        t = torch.tensor([value], dtype=torch.float64, device=like.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        return float(t.item())
+
+    def gather(self, local):
+        import torch
+        lr = torch.view_as_real(local)
+        parts = [torch.empty_like(lr) for _ in range(self.world)] if self.rank == 0 else None
+        self.dist.gather(lr, parts, dst=0, group=self.group)
+        return torch.view_as_complex(torch.cat(parts)) if self.rank == 0 else None
+
+
+class ShardedState:
+    """This rank's 2^L amplitudes of a 2^n state split over `comm.world` ranks."""
+
+    def __init__(self, n_qubits: int, local, comm, apply_fn=None):
+        self.n_qubits = int(n_qubits)
+        self.comm = comm
+        world = comm.world
+        if world & (world - 1):
+            raise ValueError(f"world size {world} is not a power of two")
+        self.p = world.bit_length() - 1
+        self.local_bits = self.n_qubits - self.p
+        if self.local_bits < 1:
+            raise ValueError("more shards than amplitudes")
+        self.local = local
+        self.apply_fn = apply_fn or _cuda_apply
+        self.stats = {"gates": 0, "local": 0, "no_comm_global": 0, "exchanged": 0, "bytes_received": 0}
+        self._recv = {}
+
+    @classmethod
+    def basis(cls, n_qubits: int, comm, device=None, apply_fn=None) -> "ShardedState":
+        """|0...0> split over the ranks (reference init_state, sim.py:53-59)."""
+        import torch
+        world = comm.world
+        lb = n_qubits - (world.bit_length() - 1)
+        dev = device if device is not None else L.device()
+        local = torch.zeros(2**lb, dtype=torch.complex128, device=dev)
+        if comm.rank == 0:
+            local[0] = 1.0
+        return cls(n_qubits, local, comm, apply_fn)
+
+    def _recv_buffer(self, peer: int):
+        import torch
+        buf = self._recv.get(peer)
+        if buf is None or buf.numel() != self.local.numel():
+            buf = torch.empty_like(self.local)
+            self._recv[peer] = buf
+        return buf
+
+    def apply_gate(self, g: np.ndarray, shifts, cmul_mode: int) -> None:
+        """One compact gate (operand i on state bit shifts[i]) on the sharded state."""
+        n, lb, me = self.n_qubits, self.local_bits, self.comm.rank
+        self.stats["gates"] += 1
+        if all(s < lb for s in shifts):
+            self.stats["local"] += 1
+            self.apply_fn(n, lb, g, shifts, me, [self.local], self.local, cmul_mode)
+            return
+        needs = exchange_schedule(n, lb, g, shifts, self.comm.world)
+        sends = [(q, self.local) for q in range(self.comm.world) if q != me and me in needs[q].values()]
+        recvs = [(src, self._recv_buffer(src)) for src in sorted(set(needs[me].values())) if src != me]
+        if recvs or sends:
+            self.stats["exchanged"] += 1
+            self.stats["bytes_received"] += 16 * self.local.numel() * len(recvs)
+            self.comm.exchange(sends, recvs)
+        else:
+            self.stats["no_comm_global"] += 1
+        kg = len(global_shifts(shifts, lb))
+        srcs = [None] * (1 << kg)
+        for b, src in needs[me].items():
+            srcs[b] = self.local if src == me else self._recv[src]
+        self.apply_fn(n, lb, g, shifts, me, srcs, self.local, cmul_mode)
+
+    def apply_placements(self, placements: list[Placement], cmul_mode: int | None = None) -> None:
+        from . import sim
+        mode = sim.CMUL_MODE if cmul_mode is None else cmul_mode
+        for p in placements:
+            comp = p.compact()
+            if comp is None:
+                raise ValueError(f"sharded apply needs compact placements, got {p!r}")
+            g, shifts = comp
+            self.apply_gate(g, shifts, mode)
+
+    def norm(self) -> float:
+        """||psi|| over all ranks (all-reduce of local |x|^2)."""
+        if self.local.device.type == "cuda":
+            from .sim import norm2
+            local = norm2(self.local)
+        else:
+            local = float((self.local.abs() ** 2).sum().item())
+        return float(np.sqrt(self.comm.allreduce_sum(local, self.local)))
+
+    def gather(self):
+        """Full state on rank 0 (tests only: 2^n amplitudes)."""
+        return self.comm.gather(self.local)
+
+
+class EmulatedComm:
+    """P ranks driven by ONE process on one device (tests/benchmarks with fewer
+    GPUs than ranks).  Ranks run one after another per gate; the exchange
+    is a device copy of the partner's pre-gate shard, so nothing waits on
+    another kernel (no cross-rank spin)."""
+
+    def __init__(self, world: int):
+        self.world = world
+        self.rank = 0
+
+
+def run_emulated(n_qubits: int, world: int, placements: list[Placement], cmul_mode: int | None = None,
+                 device=None):
+    """Apply placements to |0..0> split over `world` emulated ranks on one
+    device; returns (list of local shards, stats).  Same plans and kernels as
+    the multi-process path."""
+    import torch
+
+    from . import sim
+    mode = sim.CMUL_MODE if cmul_mode is None else cmul_mode
+    comms = []
+    states = []
+    for r in range(world):
+        c = EmulatedComm(world)
+        c.rank = r
+        comms.append(c)
+        states.append(ShardedState.basis(n_qubits, c, device=device))
+    lb = states[0].local_bits
+    stats = {"gates": 0, "local": 0, "no_comm_global": 0, "exchanged": 0}
+    for p in placements:
+        g, shifts = p.compact()
+        stats["gates"] += 1
+        if all(s < lb for s in shifts):
+            stats["local"] += 1
+            for r in range(world):
+                _cuda_apply(n_qubits, lb, g, shifts, r, [states[r].local], states[r].local, mode)
+            continue
+        needs = exchange_schedule(n_qubits, lb, g, shifts, world)
+        crosses = any(src != r for r in range(world) for src in needs[r].values())
+        stats["exchanged" if crosses else "no_comm_global"] += 1
+        snap = {}
+        if crosses:  # partner data as it was before this gate
+            for r in range(world):
+                for src in needs[r].values():
+                    if src != r and src not in snap:
+                        snap[src] = states[src].local.clone()
+        kg = len(global_shifts(shifts, lb))
+        for r in range(world):
+            srcs = [None] * (1 << kg)
+            for b, src in needs[r].items():
+                srcs[b] = states[r].local if src == r else snap[src]
+            _cuda_apply(n_qubits, lb, g, shifts, r, srcs, states[r].local, mode)
+    return [s.local for s in states], stats

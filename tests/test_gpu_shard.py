@@ -1,0 +1,60 @@
+"""GPU: the sharded path (multi-source kernel + exchange plans) emulated on
+one device with P = 2, 4, 8 ranks, against the reference goldens (bitwise)
+and the unsharded run.  Multi-process host logic: tests/test_shard_cpu.py."""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_2405_01250_b200 as D
+from conftest import GOLDEN, digest
+from paper_2405_01250_b200 import _lib as L
+from paper_2405_01250_b200 import workloads as W
+from paper_2405_01250_b200.shard import run_emulated
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cmul(configs):
+    return L.CMUL_FMA if configs["meta"]["numpy_cmul"] == "fma" else L.CMUL_PLAIN
+
+
+def _full(shards):
+    import torch
+    return torch.cat(shards).cpu().numpy()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sharded_n12_matches_reference(configs, cmul, world):
+    rec = configs["circuits"]["12"]
+    ops = W.random_layered_ops(12, rec["layers"], rec["seed"])
+    pls = D.compile_circuit(D.Circuit(12, [D.GateOp(*o) for o in ops]), span_limit=12)
+    shards, stats = run_emulated(12, world, pls, cmul_mode=cmul)
+    want = np.load(os.path.join(GOLDEN, "circuit_n12_state.npy"))
+    assert np.array_equal(_full(shards), want)
+    assert stats["exchanged"] > 0
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sharded_n20_matches_reference_digest(configs, cmul, world):
+    rec = configs["circuits"]["20"]
+    ops = W.random_layered_ops(20, rec["layers"], rec["seed"])
+    pls = D.compile_circuit(D.Circuit(20, [D.GateOp(*o) for o in ops]), span_limit=20)
+    shards, stats = run_emulated(20, world, pls, cmul_mode=cmul)
+    assert digest(_full(shards)) == rec["digest"]
+
+
+def test_sharded_mixed_gates_match_unsharded(cmul):
+    n = 10
+    ops = W.random_layered_ops(n, 2, seed=9)
+    ops += [("ccx", (0, 1, 2), ()), ("ccx", (2, 0, 9), ()), ("ccx", (9, 8, 0), ()), ("swap", (0, 9), ()),
+            ("swap", (1, 0), ()), ("cz", (0, 1), ()), ("u3", (0,), (0.1, 0.2, 0.3)), ("h", (2,), ()),
+            ("cx", (2, 1), ()), ("y", (1,), ())]
+    pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
+    want = D.run_gates(D.init_state(n), pls, cmul_mode=cmul).amps
+    for world in (2, 4, 8):
+        shards, _ = run_emulated(n, world, pls, cmul_mode=cmul)
+        assert np.array_equal(_full(shards), want), world

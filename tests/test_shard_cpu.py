@@ -1,0 +1,168 @@
+"""Multi-process (gloo, world_size 2 and 4) tests of the sharded-state host logic.
+
+The ranks run the real planning/exchange code of paper_2405_01250_b200.shard
+(diaq_shard_plan from the C-ABI, partner schedule, batched send/recv); the
+per-rank arithmetic is a numpy stand-in of the CUDA multi-source kernel
+defined here (the device kernel itself is covered by tests/test_gpu_shard.py).
+The gathered state must equal the single-process oracle bitwise.
+"""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from oracle import oracle as O
+from paper_2405_01250_b200 import workloads as W
+
+
+def numpy_apply(n_bits, local_bits, g, shifts, rank, srcs, y, cmul_mode):
+    """CPU stand-in of diaq_apply_gate_sharded: rows of this rank, columns
+    gathered from the source blocks, summed in ascending embedding order."""
+    from paper_2405_01250_b200.shard import global_shifts
+    k = len(shifts)
+    g = np.asarray(g)
+    idx = (rank << local_bits) + np.arange(1 << local_bits, dtype=np.int64)
+    emb = [sum(((c >> (k - 1 - i)) & 1) << shifts[i] for i in range(k)) for c in range(1 << k)]
+    gate_mask = sum(1 << s for s in shifts)
+    rg = np.zeros_like(idx)
+    for i, s in enumerate(shifts):
+        rg |= ((idx >> s) & 1) << (k - 1 - i)
+    free = idx & ~gate_mask
+    gs = global_shifts(shifts, local_bits)
+    acc = np.zeros(len(idx), dtype=np.complex128)
+    xs = [None if t is None else t.numpy() for t in srcs]
+    for cg in sorted(range(1 << k), key=lambda c: emb[c]):
+        coef = g[rg, cg]
+        nz = coef != 0
+        if not nz.any():
+            continue
+        col = free | emb[cg]
+        block = np.zeros_like(idx)
+        for j, s in enumerate(gs):
+            block |= ((col >> s) & 1) << (len(gs) - 1 - j)
+        vals = np.zeros(len(idx), dtype=np.complex128)
+        for b in np.unique(block[nz]):
+            sel = nz & (block == b)
+            vals[sel] = xs[int(b)][col[sel] & ((1 << local_bits) - 1)]
+        term = coef * vals  # numpy complex multiply: the reference's rounding on this host
+        acc[nz] = acc[nz] + term[nz]
+    y.copy_(torch.from_numpy(acc))
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, n, ops, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2405_01250_b200 as D
+        from paper_2405_01250_b200.shard import ShardedState, TorchDistComm
+        comm = TorchDistComm()
+        st = ShardedState.basis(n, comm, device=torch.device("cpu"), apply_fn=numpy_apply)
+        pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
+        st.apply_placements(pls, cmul_mode=O.numpy_cmul_mode())
+        nrm = st.norm()
+        full = st.gather()
+        if rank == 0:
+            out_q.put((full.numpy(), nrm, st.stats))
+    finally:
+        dist.destroy_process_group()
+
+
+def run_world(world: int, n: int, ops):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, ops, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    import queue
+    import time
+    deadline = time.time() + 300
+    res = None
+    while res is None:
+        try:
+            res = q.get(timeout=2)
+        except queue.Empty:
+            if any(p.exitcode not in (None, 0) for p in procs) or time.time() > deadline:
+                for p in procs:
+                    p.kill()
+                raise AssertionError("a sharded worker failed") from None
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_random_layered_circuit_matches_oracle(world):
+    n = 8
+    ops = W.random_layered_ops(n, 3, seed=4)
+    ops += [("ccx", (0, 5, 1), ()), ("swap", (1, 6), ()), ("cz", (0, 1), ()), ("rz", (0,), (0.3,)),
+            ("u3", (1,), (0.1, 0.2, 0.3)), ("cx", (7, 0), ()), ("cx", (0, 7), ())]
+    full, nrm, stats = run_world(world, n, ops)
+    want = O.run_circuit(n, ops, cmul_mode=O.numpy_cmul_mode())
+    assert np.array_equal(full, want)
+    assert abs(nrm - 1.0) < 1e-12
+    assert stats["gates"] == len(ops)
+    assert stats["exchanged"] > 0 and stats["local"] > 0
+
+
+def test_exchange_schedule_rules():
+    """Cross-shard rules of SURVEY 8(e): diagonal gates and global controls
+    need no partner; a flip of global bit g needs rank r ^ (1 << (g-L))."""
+    from paper_2405_01250_b200 import gates as G
+    from paper_2405_01250_b200.shard import exchange_schedule
+    n, lb, world = 6, 4, 4
+    rx = G.GATE_DEFS["rx"][2](0.7)
+    rz = G.GATE_DEFS["rz"][2](0.7)
+    cx = G.GATE_DEFS["cx"][2]()
+    # RX on global bit 5 (reference qubit 0)
+    needs = exchange_schedule(n, lb, rx, [5], world)
+    for r in range(world):
+        assert sorted(needs[r].values()) == sorted({r, r ^ 2})
+    # RZ on a global bit: own block only
+    needs = exchange_schedule(n, lb, rz, [4], world)
+    assert all(list(nd.values()) == [r] for r, nd in enumerate(needs))
+    # CX with global control (bit 5) and local target (bit 0): no communication
+    needs = exchange_schedule(n, lb, cx, [5, 0], world)
+    assert all(list(nd.values()) == [r] for r, nd in enumerate(needs))
+    # CX with local control, global target (bit 4): partner r ^ 1
+    needs = exchange_schedule(n, lb, cx, [0, 4], world)
+    for r in range(world):
+        assert sorted(needs[r].values()) == sorted({r, r ^ 1})
+    # CX with both operands global: control=1 ranks read the target partner
+    needs = exchange_schedule(n, lb, cx, [5, 4], world)
+    for r in range(world):
+        want = {r} if not (r >> 1) & 1 else {r ^ 1}
+        assert set(needs[r].values()) == want
+
+
+def test_cross_shard_fraction_matches_survey():
+    """Counts quoted in SURVEY 8(e) for the config-5 generator (seed 0, 20 layers)."""
+    from paper_2405_01250_b200 import gates as G
+    from paper_2405_01250_b200.shard import exchange_schedule
+    for n, world, want in ((31, 2, 18), (32, 4, 44), (33, 8, 65)):
+        lb = n - (world.bit_length() - 1)
+        ops = W.random_layered_ops(n, 20, seed=0)
+        crosses = 0
+        for name, qubits, params in ops:
+            g = G.GATE_DEFS[name][2](*params)
+            shifts = [n - 1 - q for q in qubits]
+            if all(s < lb for s in shifts):
+                continue
+            needs = exchange_schedule(n, lb, g, shifts, world)
+            if any(src != r for r in range(world) for src in needs[r].values()):
+                crosses += 1
+        assert crosses == want, (n, world, crosses)
