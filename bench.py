@@ -318,6 +318,13 @@ def run_ours(args):
                "path": "paper_2405_01250_b200.spmv(a, pinned host x, out=pinned host y)"}
         del xh, yh
 
+    secondary = {}
+    if not args.no_secondary:
+        try:
+            secondary = secondary_workloads(args, D, L, W, torch)
+        except Exception as e:  # never lose the headline line
+            secondary = {"error": repr(e)}
+
     peak, peak_src = measured_peak()
     prof = profiled_traffic()
     kern_ms = statistics.mean(step_ms)
@@ -358,6 +365,7 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "gates": gates,
+        "secondary": secondary,
         "check": {"y_norm": y_norm, "unitary_norm_err": abs(y_norm - 1.0)},
         "step_ms_minmax": [round(min(step_ms), 4), round(max(step_ms), 4)],
     }
@@ -365,6 +373,64 @@ def run_ours(args):
     if dist is not None:
         dist.destroy_process_group()
     return 0
+
+
+def secondary_workloads(args, D, L, W, torch) -> dict:
+    """The other BASELINE configs (launch-bound sizes), device-timed."""
+    out = {}
+    s = torch.cuda.current_stream()
+
+    def dev_time(fn, reps):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(reps):
+            fn()
+        e1.record(s)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    # config 1: spmv n=14 (3 diagonals), latency-bound
+    c1 = W.config1(0)
+    a1 = D.kron_identity(c1["left"], D.from_dense(c1["u"], 0.0), c1["right"])
+    x1 = torch.from_numpy(c1["x"]).cuda()
+    ms = dev_time(lambda: D.spmv(a1, x1), 50)
+    out["config1_spmv_n14"] = {"us_per_spmv": round(ms * 1e3, 2),
+                               "GBs": round(alg_bytes(2**14, a1.diag_indices()) / ms / 1e6, 1)}
+    # config 2: spgemm n=12, sweep of 64 seeded pairs (products/s incl. plan + prune readback)
+    pairs = []
+    for seed in range(64):
+        p = W.config2(seed)
+        span = D.build_span_unitary(D.from_dense(p["u4"], 0.0), p["u4_positions"], p["u4_span"])
+        A = D.kron_identity(p["a_left"], span, p["a_right"])
+        B = D.matmul(D.kron_identity(p["b1_left"], D.from_dense(p["u2"], 0.0), p["b1_right"]),
+                     D.kron_identity(p["b0_left"], D.from_dense(W.rz(p["theta"]), 0.0), p["b0_right"]))
+        pairs.append((A, B))
+    for A, B in pairs[:3]:
+        D.matmul(A, B)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for A, B in pairs:
+        C = D.matmul(A, B)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / len(pairs)
+    out["config2_spgemm_n12"] = {"us_per_product": round(dt * 1e6, 1), "products_per_s": round(1 / dt, 1),
+                                 "c_diagonals": C.diag_count(), "note": "wall clock per matmul() call"}
+    # config 3: random layered circuit n=20, 40 layers, 1200 gates
+    ops = W.random_layered_ops(20, 40, seed=0)
+    pls = D.compile_circuit(D.Circuit(20, [D.GateOp(*o) for o in ops]), span_limit=20)
+    st = D.init_state(20)
+    ms = dev_time(lambda: D.run_gates(st, pls, inplace=True), 3)
+    t0 = time.perf_counter()
+    res = D.run(D.Circuit(20, [D.GateOp(*o) for o in ops]), shots=1024, seed=0, span_limit=20)
+    e2e_s = time.perf_counter() - t0
+    out["config3_circuit_n20"] = {"gates": len(pls), "ms_per_circuit": round(ms, 3),
+                                  "gates_per_s": round(len(pls) / ms * 1e3, 1),
+                                  "run_api_wall_s": round(e2e_s, 4),
+                                  "run_api_apply_ms": round(res.timings_ns["apply_total"] / 1e6, 3)}
+    return out
 
 
 def main():
@@ -376,6 +442,7 @@ def main():
     ap.add_argument("--n", type=int, default=N_QUBITS)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -1,0 +1,104 @@
+"""GPU parity at BASELINE.json's full sizes through size-independent properties.
+
+* config 4 at n=28 (38.45 GB of diagonals, built on the device): the matrix
+  is block diagonal with 64 copies of the n=22 parity matrix, so selected
+  2^22 blocks of y must equal the oracle's n=22 spmv bitwise; y keeps the
+  norm of x (the operator is unitary) to 1e-12.
+* gate application at n=28: a gate inside a 2^22 block equals the oracle's
+  n=22 placement bitwise; a CX is an exact permutation; G then G^dagger
+  returns x to 1e-13.
+* spgemm at n=20: bitwise against the oracle.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2405_01250_b200 as D
+from oracle import oracle as O
+from paper_2405_01250_b200 import _lib as L
+from paper_2405_01250_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    return t
+
+
+@pytest.fixture(scope="module")
+def cmul(configs):
+    return L.CMUL_FMA if configs["meta"]["numpy_cmul"] == "fma" else L.CMUL_PLAIN
+
+
+def test_config4_n28_blocks_and_norm(torch):
+    n = 28
+    c4 = W.config4(22, seed=0, with_x=False)
+    span = D.build_span_unitary(D.from_dense(c4["u4"], 0.0), c4["positions"], c4["span"])
+    a = D.kron_identity(2 ** (n - 22), span, c4["right"])
+    assert a.diag_indices() == [-(2**21) - 8, -(2**21), -(2**21) + 8, -8, 0, 8, 2**21 - 8, 2**21, 2**21 + 8]
+    g = torch.Generator(device="cuda")
+    g.manual_seed(77)
+    x = torch.randn(2**n, dtype=torch.complex128, device="cuda", generator=g)
+    x /= torch.linalg.vector_norm(x)
+    y = D.spmv(a, x)
+    assert abs(float(torch.linalg.vector_norm(y)) - 1.0) < 1e-12
+    a22 = O.kron_identity(1, O.span_unitary(c4["u4"], c4["positions"], c4["span"]), c4["right"])
+    blk = 2**22
+    for b in (0, 29, 63):
+        xb = x[b * blk:(b + 1) * blk].cpu().numpy()
+        yb = y[b * blk:(b + 1) * blk].cpu().numpy()
+        assert np.array_equal(yb, O.spmv(a22, xb)), b
+    del a, y
+
+
+def test_gate_apply_n28_properties(torch, cmul):
+    n = 28
+    g = torch.Generator(device="cuda")
+    g.manual_seed(78)
+    x = torch.randn(2**n, dtype=torch.complex128, device="cuda", generator=g)
+    x /= torch.linalg.vector_norm(x)
+    st = D.StateVector(n, x)
+    # RX on qubit 10 (bit 17) stays inside each 2^22 block
+    rx = D.compile_circuit(D.Circuit(n, [D.GateOp("rx", (10,), (0.9,))]))[0]
+    y = D.apply_placed(rx, st, cmul_mode=cmul).device_amps
+    blk = 2**22
+    m = O.from_dense(D.GATE_DEFS["rx"][2](0.9))
+    for b in (0, 41):
+        xb = x[b * blk:(b + 1) * blk].cpu().numpy()
+        want = O.apply_placed(2 ** (21 - 17), m, 2**17, xb, cmul)
+        assert np.array_equal(y[b * blk:(b + 1) * blk].cpu().numpy(), want)
+    # CX(3, 25): control bit 24, target bit 2 -> exact permutation
+    cx = D.compile_circuit(D.Circuit(n, [D.GateOp("cx", (3, 25))]), span_limit=n)[0]
+    y = D.apply_placed(cx, st, cmul_mode=cmul).device_amps
+    idx = torch.arange(2**n, device="cuda", dtype=torch.int64)
+    src = torch.where((idx >> 24) & 1 == 1, idx ^ 4, idx)
+    assert torch.equal(y, x[src])
+    del y, idx, src
+    # Haar 2-qubit gate on (0, 27), then its adjoint
+    u = W.haar(np.random.default_rng(3), 4)
+    fwd = D.Placement(1, None, 1, 0, 27, "u", gate=(u, [0, 27]))
+    back = D.Placement(1, None, 1, 0, 27, "u+", gate=(u.conj().T, [0, 27]))
+    y = D.apply_placed(fwd, st, cmul_mode=cmul)
+    assert abs(y.norm() - 1.0) < 1e-12
+    z = D.apply_placed(back, y, cmul_mode=cmul).device_amps
+    assert float(torch.linalg.vector_norm(z - x)) < 1e-13
+
+
+def test_spgemm_n20_bitwise():
+    rng = np.random.default_rng(4)
+    u4 = W.haar(rng, 4)
+    u2 = W.haar(rng, 2)
+    A = D.kron_identity(2**3, D.build_span_unitary(D.from_dense(u4, 0.0), [0, 9], 10), 2**7)
+    B = D.kron_identity(2**11, D.from_dense(u2, 0.0), 2**8)
+    C = D.matmul(A, B)
+    oa = O.kron_identity(2**3, O.span_unitary(u4, [0, 9], 10), 2**7)
+    ob = O.kron_identity(2**11, O.from_dense(u2), 2**8)
+    oc = O.matmul(oa, ob)
+    assert C.diag_indices() == oc.offs.tolist()
+    for d in oc.offs.tolist()[:: max(1, len(oc.offs) // 7)]:
+        r, i = oc.diag(d)
+        got = C.get(d)
+        assert np.array_equal(got.re, r) and np.array_equal(got.im, i), d
