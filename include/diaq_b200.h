@@ -106,6 +106,12 @@ int diaq_to_dense(const diaq_matrix_t *a, void *dense, void *stream);
 /* ---- spmv (reference matrix.py:253-278) -------------------------------
  * y = A x, bitwise equal to the reference (ascending d, no FMA). */
 int diaq_spmv(const diaq_matrix_t *a, const void *x, void *y, void *stream);
+/* y_host = A x_host with the H2D of x, the spmv and the D2H of y pipelined
+ * in chunks of chunk_rows rows over three streams (host buffers should be
+ * pinned).  x_dev / y_dev are n-element device scratch vectors.  Returns
+ * when y_host is complete; bitwise equal to diaq_spmv. */
+int diaq_spmv_host(const diaq_matrix_t *a, const void *x_host, void *y_host, void *x_dev, void *y_dev,
+                   int64_t chunk_rows, void *stream);
 
 /* ---- spgemm (reference matrix.py:173-250) -----------------------------
  * plan (host): candidate result offsets (sorted), nc <= nda*ndb. */
@@ -171,6 +177,16 @@ int diaq_timer_record(void *event, void *stream);
 /* waits for events[n-1]; ms_out[i] = milliseconds from events[i] to events[i+1] */
 int diaq_timer_elapsed(int n, void **events, float *ms_out);
 int diaq_timer_destroy(int n, void **events);
+
+/* Same result as diaq_run_gates (bitwise), but consecutive gates whose
+ * mixing operand bits fit in a tile of 2^tile_bits amplitudes (low bits
+ * included) are applied in ONE pass over HBM through shared memory.
+ * Operands a gate does not mix (controls, diagonal gates) may lie outside
+ * the tile.  tile_bits <= 0 picks the default (11); *npasses (optional)
+ * receives the number of HBM passes.  events: as diaq_run_gates (a pass's
+ * time is attributed to its first gate). */
+int diaq_run_gates_fused(int n_bits, int ngates, const diaq_gate_t *gates, void *state, int cmul_mode,
+                         int tile_bits, void **events, int *npasses, void *stream);
 
 /* ---- state helpers ------------------------------------------------------ */
 /* |index> (reference init_state, sim.py:53-59) */

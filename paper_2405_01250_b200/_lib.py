@@ -71,12 +71,14 @@ _SIGS = {
     "diaq_from_dense_fill": ([_P, _MP, _P], _INT),
     "diaq_to_dense": ([_MP, _P, _P], _INT),
     "diaq_spmv": ([_MP, _P, _P, _P], _INT),
+    "diaq_spmv_host": ([_MP, _P, _P, _P, _P, _I64, _P], _INT),
     "diaq_spgemm_plan": ([_I64, _I64, _P, _I64, _P, _P, _P], _INT),
     "diaq_spgemm_workspace": ([_I64, _I64, _I64], _I64),
     "diaq_spgemm": ([_MP, _MP, _MP, _P, ctypes.c_double, _P, _I64, _P], _INT),
     "diaq_apply_placed": ([_I64, _MP, _I64, _P, _P, _INT, _P], _INT),
     "diaq_apply_gate": ([_INT, _INT, _P, _P, _P, _P, _INT, _P], _INT),
     "diaq_run_gates": ([_INT, _INT, ctypes.POINTER(Gate), _P, _INT, _P, _P], _INT),
+    "diaq_run_gates_fused": ([_INT, _INT, ctypes.POINTER(Gate), _P, _INT, _INT, _P, _P, _P], _INT),
     "diaq_init_basis": ([_I64, _P, _I64, _P], _INT),
     "diaq_norm2": ([_I64, _P, _P, _P], _INT),
     "diaq_shard_plan": ([_INT, _INT, _INT, _P, _P, _I64, _P, _P, _P], _INT),

@@ -21,6 +21,7 @@
 //     back to back and x comes from HBM about once.
 #include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 
@@ -35,6 +36,7 @@ struct SpmvDiag {
 template <int MAXD>
 struct SpmvParams {
     int64_t n;
+    int64_t r0, rend;  // rows [r0, rend) of y are produced
     int64_t ntiles, stride_tiles, nstrips, nitems;
     int64_t nchunks;   // raster 1: chunks of `chunk` strips per column
     int raster, chunk;
@@ -116,8 +118,8 @@ __global__ void __launch_bounds__(kThreads) spmv_kernel(const __grid_constant__ 
         for (int64_t j = j0; j < j1; ++j) {
             const int64_t t = j * p.stride_tiles + b;
             if (t >= p.ntiles) break;
-            const int64_t r = t * kThreads + threadIdx.x;
-            if (r >= p.n) continue;
+            const int64_t r = p.r0 + t * kThreads + threadIdx.x;
+            if (r >= p.rend) continue;
             double2 acc;
             if constexpr (ND > 0) acc = spmv_row<ND, XPOL>(p.dg, p.nd, r, p.x, pol, pol_last);
             else acc = spmv_row_dyn<XPOL>(p.dg, p.nd, r, p.x, pol, pol_last);
@@ -128,16 +130,16 @@ __global__ void __launch_bounds__(kThreads) spmv_kernel(const __grid_constant__ 
 
 // large diagonal counts: tables in global memory, raster 0
 __global__ void __launch_bounds__(kThreads)
-spmv_kernel_global(int64_t n, int nd, const SpmvDiag *__restrict__ dg, const double2 *x, double2 *y,
-                   int64_t ntiles, int64_t stride_tiles, int64_t nstrips, int64_t nitems) {
+spmv_kernel_global(int64_t r0, int64_t rend, int nd, const SpmvDiag *__restrict__ dg, const double2 *x,
+                   double2 *y, int64_t ntiles, int64_t stride_tiles, int64_t nstrips, int64_t nitems) {
     const uint64_t pol = policy_evict_first();
     for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
         const int64_t j = it % nstrips;
         const int64_t b = it / nstrips;
         const int64_t t = j * stride_tiles + b;
         if (b >= stride_tiles || t >= ntiles) continue;
-        const int64_t r = t * kThreads + threadIdx.x;
-        if (r >= n) continue;
+        const int64_t r = r0 + t * kThreads + threadIdx.x;
+        if (r >= rend) continue;
         double2 acc = spmv_row_dyn<0>(dg, nd, r, x, pol, 0ull);
         st_stream(y + r, acc);
     }
@@ -199,24 +201,24 @@ static int launch_param(const SpmvParams<kParamDiags> &p, cudaStream_t s) {
 
 using namespace diaq;
 
-extern "C" int diaq_spmv(const diaq_matrix_t *a, const void *x, void *y, void *stream) {
-    if (!a || !x || !y) return set_error(DIAQ_ERR_VALUE, "diaq_spmv: null argument");
-    cudaStream_t s = (cudaStream_t)stream;
+// y rows [r0, r0 + nrows) of y = A x (whole x and matrix addressable)
+static int spmv_rows(const diaq_matrix_t *a, const void *x, void *y, int64_t r0, int64_t nrows, cudaStream_t s) {
     const int64_t n = a->n;
-    if (n < 1) return set_error(DIAQ_ERR_SHAPE, "diaq_spmv: n_dim must be >= 1");
+    if (nrows <= 0) return DIAQ_OK;
     if (a->nd == 0) {
         // no stored diagonals: y = 0 (reference returns zeros)
-        if (cudaMemsetAsync(y, 0, (size_t)n * 16, s) != cudaSuccess)
-            return set_error(DIAQ_ERR_CUDA, "diaq_spmv: memset failed: %s",
-                             cudaGetErrorString(cudaGetLastError()));
+        if (cudaMemsetAsync((double2 *)y + r0, 0, (size_t)nrows * 16, s) != cudaSuccess)
+            return set_error(DIAQ_ERR_CUDA, "diaq_spmv: memset failed: %s", cudaGetErrorString(cudaGetLastError()));
         return DIAQ_OK;
     }
     int64_t ntiles, stride, nstrips;
-    spmv_raster(n, a->nd, a->offs, &ntiles, &stride, &nstrips);
+    spmv_raster(nrows, a->nd, a->offs, &ntiles, &stride, &nstrips);
     const double2 *vals = (const double2 *)a->vals;
     if (a->nd <= kParamDiags) {
         SpmvParams<kParamDiags> p;
         p.n = n;
+        p.r0 = r0;
+        p.rend = r0 + nrows;
         p.ntiles = ntiles;
         p.stride_tiles = stride;
         p.nstrips = nstrips;
@@ -268,13 +270,87 @@ extern "C" int diaq_spmv(const diaq_matrix_t *a, const void *x, void *y, void *s
     }
     cudaMemcpyAsync(dtab, h, bytes, cudaMemcpyHostToDevice, s);
     const int grid = grid_for((const void *)spmv_kernel_global, stride * nstrips);
-    spmv_kernel_global<<<grid, kThreads, 0, s>>>(n, (int)a->nd, dtab, (const double2 *)x,
-                                                 (double2 *)y, ntiles, stride, nstrips,
-                                                 stride * nstrips);
+    spmv_kernel_global<<<grid, kThreads, 0, s>>>(r0, r0 + nrows, (int)a->nd, dtab, (const double2 *)x, (double2 *)y,
+                                                 ntiles, stride, nstrips, stride * nstrips);
     count_launch();
     const int rc = check_launch("spmv_kernel_global");
     cudaFreeAsync(dtab, s);
     cudaStreamSynchronize(s);  // host table lifetime
     free(h);
+    return rc;
+}
+
+extern "C" int diaq_spmv(const diaq_matrix_t *a, const void *x, void *y, void *stream) {
+    if (!a || !x || !y) return set_error(DIAQ_ERR_VALUE, "diaq_spmv: null argument");
+    if (a->n < 1) return set_error(DIAQ_ERR_SHAPE, "diaq_spmv: n_dim must be >= 1");
+    return spmv_rows(a, x, y, 0, a->n, (cudaStream_t)stream);
+}
+
+// Host-buffer spmv with copies and compute overlapped chunk by chunk: x
+// chunks go up on one stream, each y chunk is computed as soon as the x
+// window it reads (rows [r + d_min, r + d_max]) is resident, and goes down on
+// a third stream -- so H2D and D2H share the PCIe link full-duplex instead
+// of running back to back.  Synchronous: returns when y_host is complete.
+extern "C" int diaq_spmv_host(const diaq_matrix_t *a, const void *x_host, void *y_host, void *x_dev, void *y_dev,
+                              int64_t chunk_rows, void *stream) {
+    if (!a || !x_host || !y_host || !x_dev || !y_dev) return set_error(DIAQ_ERR_VALUE, "diaq_spmv_host: null argument");
+    const int64_t n = a->n;
+    if (n < 1) return set_error(DIAQ_ERR_SHAPE, "diaq_spmv_host: n_dim must be >= 1");
+    if (chunk_rows <= 0) chunk_rows = (int64_t)1 << 22;
+    cudaStream_t s = (cudaStream_t)stream;
+    static thread_local cudaStream_t up = nullptr, down = nullptr;
+    if (!up && (cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking) != cudaSuccess ||
+                cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking) != cudaSuccess))
+        return set_error(DIAQ_ERR_CUDA, "diaq_spmv_host: stream create failed");
+    int64_t dmin = 0, dmax = 0;
+    for (int64_t i = 0; i < a->nd; ++i) {
+        dmin = std::min(dmin, a->offs[i]);
+        dmax = std::max(dmax, a->offs[i]);
+    }
+    const int64_t nchunks = (n + chunk_rows - 1) / chunk_rows;
+    std::vector<cudaEvent_t> xev((size_t)nchunks), yev((size_t)nchunks);
+    for (auto *v : {&xev, &yev})
+        for (auto &e : *v)
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+                return set_error(DIAQ_ERR_CUDA, "diaq_spmv_host: event create failed");
+    cudaEvent_t start;
+    cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+    cudaEventRecord(start, s);  // x_dev / y_dev may still be in use by earlier work on s
+    cudaStreamWaitEvent(up, start, 0);
+    cudaStreamWaitEvent(down, start, 0);
+    int rc = DIAQ_OK;
+    int64_t next_y = 0;
+    for (int64_t j = 0; j < nchunks && rc == DIAQ_OK; ++j) {
+        const int64_t r = j * chunk_rows, cnt = std::min(chunk_rows, n - r);
+        if (cudaMemcpyAsync((double2 *)x_dev + r, (const double2 *)x_host + r, (size_t)cnt * 16,
+                            cudaMemcpyHostToDevice, up) != cudaSuccess) {
+            rc = set_error(DIAQ_ERR_CUDA, "diaq_spmv_host: H2D failed");
+            break;
+        }
+        cudaEventRecord(xev[(size_t)j], up);
+        const int64_t have = r + cnt;  // x rows [0, have) resident
+        while (next_y < nchunks) {
+            const int64_t yr = next_y * chunk_rows, ycnt = std::min(chunk_rows, n - yr);
+            if (std::min(n, yr + ycnt + dmax) > have && have < n) break;
+            cudaStreamWaitEvent(s, xev[(size_t)j], 0);
+            rc = spmv_rows(a, x_dev, y_dev, yr, ycnt, s);
+            if (rc) break;
+            cudaEventRecord(yev[(size_t)next_y], s);
+            cudaStreamWaitEvent(down, yev[(size_t)next_y], 0);
+            if (cudaMemcpyAsync((double2 *)y_host + yr, (const double2 *)y_dev + yr, (size_t)ycnt * 16,
+                                cudaMemcpyDeviceToHost, down) != cudaSuccess) {
+                rc = set_error(DIAQ_ERR_CUDA, "diaq_spmv_host: D2H failed");
+                break;
+            }
+            ++next_y;
+        }
+    }
+    (void)dmin;
+    if (cudaStreamSynchronize(down) != cudaSuccess && rc == DIAQ_OK)
+        rc = set_error(DIAQ_ERR_CUDA, "diaq_spmv_host: %s", cudaGetErrorString(cudaGetLastError()));
+    cudaStreamSynchronize(s);
+    for (auto *v : {&xev, &yev})
+        for (auto &e : *v) cudaEventDestroy(e);
+    cudaEventDestroy(start);
     return rc;
 }

@@ -351,20 +351,46 @@ def _as_device_vector(x, n: int):
     return L.to_device_c128(x), "numpy"
 
 
+HOST_PIPELINE_MIN = 1 << 21  # rows; above this host vectors take the pipelined path
+HOST_CHUNK_ROWS = 1 << 22
+
+
 def spmv(a: DiaqMatrix, x, out=None):
     """Sparse matrix-vector product A @ x (matrix.py:253-278).
 
     Bitwise equal to the reference.  A host numpy `x` returns a host
     complex128 array (reference behaviour); a CUDA tensor returns a CUDA
     tensor.  `out` (extension): a complex128 torch tensor, on the device or in
-    (pinned) host memory, that receives y.
+    (pinned) host memory, that receives y.  Large host vectors go through
+    diaq_spmv_host, which overlaps the H2D of x, the kernel and the D2H of y
+    chunk by chunk.
     """
     n = a.n_dim
-    xd, kind = _as_device_vector(x, n)
     t = L.torch()
     if out is not None and (not isinstance(out, t.Tensor) or tuple(out.shape) != (n,)
                             or out.dtype != t.complex128):
         raise ShapeError(f"out must be a complex128 tensor of shape ({n},)")
+    on_host = not (isinstance(x, t.Tensor) and x.device.type == "cuda")
+    if on_host and n >= HOST_PIPELINE_MIN and (out is None or out.device.type == "cpu"):
+        if isinstance(x, t.Tensor):
+            if tuple(x.shape) != (n,):
+                raise ShapeError(f"not multiplyable: {n}x{n} by vector of shape {tuple(x.shape)}")
+            xh = x.contiguous() if x.dtype == t.complex128 else x.to(t.complex128).contiguous()
+        else:
+            xa = np.asarray(x)
+            if xa.shape != (n,):
+                raise ShapeError(f"not multiplyable: {n}x{n} by vector of shape {xa.shape}")
+            xh = t.from_numpy(np.ascontiguousarray(xa, dtype=np.complex128))
+        yh = out if out is not None else t.empty(n, dtype=t.complex128, pin_memory=True)
+        xd = L.empty_c128(n)
+        yd = L.empty_c128(n)
+        st = a._struct()
+        L.call("diaq_spmv_host", ctypes.byref(st), xh.data_ptr(), yh.data_ptr(), xd.data_ptr(), yd.data_ptr(),
+               HOST_CHUNK_ROWS, L.stream_handle())
+        if out is not None:
+            return out
+        return yh.numpy() if not isinstance(x, t.Tensor) else yh
+    xd, kind = _as_device_vector(x, n)
     y = out if out is not None and out.device.type == "cuda" else L.empty_c128(n)
     st = a._struct()
     L.call("diaq_spmv", ctypes.byref(st), xd.data_ptr(), y.data_ptr(), L.stream_handle())

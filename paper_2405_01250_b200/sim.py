@@ -50,6 +50,10 @@ def _probe_numpy_cmul() -> int:
 # rounding of the gate-apply complex multiply; defaults to this host's numpy
 CMUL_MODE = _probe_numpy_cmul()
 
+# shared-memory tile of the fused multi-gate passes (diaq_run_gates_fused);
+# 0 applies every gate as its own HBM sweep.  Results are identical.
+FUSE_TILE_BITS = 11
+
 
 class StateVector:
     """2^n complex128 amplitudes, resident on the device.
@@ -232,7 +236,8 @@ class _GateProgram:
 
 
 def run_gates(state: StateVector, placements: list[Placement], cmul_mode: int | None = None,
-              timer: "L.Timer | None" = None, inplace: bool = False) -> StateVector:
+              timer: "L.Timer | None" = None, inplace: bool = False,
+              tile_bits: int | None = None) -> StateVector:
     """Apply placements in order on the device; each maximal run of compact
     gates goes through one native call (diaq_run_gates, in place).  The input
     state is left untouched unless inplace=True.  `timer` (len(placements)+1
@@ -253,7 +258,12 @@ def run_gates(state: StateVector, placements: list[Placement], cmul_mode: int | 
         if comps:
             prog = _GateProgram(comps)
             evs = timer.slice_ptr(i) if timer is not None else None
-            L.call("diaq_run_gates", n_bits, prog.n, prog.arr, xd.data_ptr(), int(mode), evs, s)
+            tb = FUSE_TILE_BITS if tile_bits is None else tile_bits
+            if tb > 0:
+                L.call("diaq_run_gates_fused", n_bits, prog.n, prog.arr, xd.data_ptr(), int(mode), int(tb), evs,
+                       None, s)
+            else:
+                L.call("diaq_run_gates", n_bits, prog.n, prog.arr, xd.data_ptr(), int(mode), evs, s)
             i = j
             continue
         p = placements[i]

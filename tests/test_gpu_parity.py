@@ -359,3 +359,42 @@ def test_determinism_and_immutability(cmul):
     # lazily built span matrix agrees with the compact apply
     want = O.apply_placed(p.dim_a, omat(p.m), p.dim_b, before, cmul)
     assert np.array_equal(base, want)
+
+
+def test_fused_passes_match_unfused(cmul):
+    """Shared-memory multi-gate passes are bitwise equal to gate-by-gate sweeps."""
+    rng = np.random.default_rng(8)
+    for n in (3, 8, 11, 14, 20):
+        ops = W.random_layered_ops(n, 3, seed=n)
+        for _ in range(12):
+            q = [int(v) for v in rng.choice(n, size=3, replace=False)]
+            ops += [("ccx", tuple(q), ()), ("swap", (q[0], q[1]), ()), ("cz", (q[1], q[2]), ()),
+                    ("u3", (q[2],), (0.1, 0.7, 1.3)), ("h", (q[0],), ()), ("t", (q[1],), ())]
+        pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
+        u = W.haar(rng, 4)
+        a, b = (int(v) for v in rng.choice(n, size=2, replace=False))
+        lo, hi = min(a, b), max(a, b)
+        pls.append(D.Placement(2**lo, None, 2 ** (n - 1 - hi), lo, hi, "haar",
+                               gate=(u, [a - lo, b - lo])))
+        x0 = D.StateVector(n, W.random_state(rng, 2**n))
+        want = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=0).amps
+        for tb in (6, 8, 11, 12):
+            got = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=tb).amps
+            assert np.array_equal(got, want), (n, tb)
+
+
+def test_spmv_host_pipeline_chunks(monkeypatch):
+    """Pipelined host spmv (chunked H2D / kernel / D2H) is bitwise the device spmv."""
+    import torch
+    c4 = W.config4(22, seed=0, with_x=False)
+    span = D.build_span_unitary(D.from_dense(c4["u4"], 0.0), c4["positions"], c4["span"])
+    a = D.kron_identity(1, span, c4["right"])
+    x = W.random_state(np.random.default_rng(6), 2**22)
+    want = D.spmv(a, torch.from_numpy(x).cuda()).cpu().numpy()
+    for chunk in (300007, 2**20, 2**23):
+        monkeypatch.setattr(D.matrix, "HOST_CHUNK_ROWS", chunk)
+        assert np.array_equal(D.spmv(a, x), want), chunk
+        xh = torch.from_numpy(x).pin_memory()
+        yh = torch.empty(2**22, dtype=torch.complex128).pin_memory()
+        assert D.spmv(a, xh, out=yh) is yh
+        assert np.array_equal(yh.numpy(), want), chunk
