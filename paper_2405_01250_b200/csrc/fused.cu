@@ -103,17 +103,54 @@ __device__ __forceinline__ void apply_in_tile(double2 *tile, int T, const FusedG
     }
 }
 
+constexpr int kMaxPassGates = 64;   // gate records staged in shared memory per pass
+constexpr int kBatch = 8;  // tile elements per thread per load/store batch
+
+// Tile element e = tid + kThreads*k.  Its state offset is
+// (e & lowmask) + hi_off[e >> lowbits]: the low tile bits are the low state
+// bits (contiguous), the rest come from a per-CTA table built once.
 template <int MODE, int MAXKIN>
-__global__ void __launch_bounds__(kThreads) fused_pass_kernel(const __grid_constant__ PassParams p) {
+__global__ void __launch_bounds__(kThreads, MAXKIN >= 3 ? 2 : 4) fused_pass_kernel(const __grid_constant__ PassParams p) {
     extern __shared__ double2 tile[];
+    __shared__ uint64_t hi_off[1 << kMaxTileBits >> 3];
+    __shared__ FusedGate sg[kMaxPassGates];
     const int T = p.tbits;
     const uint32_t tsize = 1u << T;
+    int lowbits = 0;
+    while (lowbits < T && p.tb[lowbits] == lowbits) ++lowbits;
+    if (lowbits > 8) lowbits = 8;  // e >> 8 indexes the table; kThreads == 256
+    const uint32_t lowmask = (1u << lowbits) - 1u;
+    for (uint32_t h = threadIdx.x; h < (tsize >> lowbits); h += blockDim.x) {
+        uint64_t off = 0;
+        for (int j = lowbits; j < T; ++j) off |= (uint64_t)((h >> (j - lowbits)) & 1u) << p.tb[j];
+        hi_off[h] = off;
+    }
+    const int ng = p.g1 - p.g0;
+    const bool staged = ng <= kMaxPassGates;
+    if (staged)
+        for (int i = threadIdx.x; i < ng * (int)(sizeof(FusedGate) / 4); i += blockDim.x)
+            reinterpret_cast<int *>(sg)[i] = reinterpret_cast<const int *>(p.gates + p.g0)[i];
+    __syncthreads();
+    const int per_thread = (int)(tsize >= kThreads ? tsize / kThreads : 1);
     for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
         const uint64_t base = insert_zero_bits_dyn((uint64_t)t, p.tb, T);
-        for (uint32_t e = threadIdx.x; e < tsize; e += blockDim.x) tile[e] = ld_plain(p.x + base + spread_tile(e, p.tb, T));
+        for (int k0 = 0; k0 < per_thread; k0 += kBatch) {
+            double2 v[kBatch];
+#pragma unroll
+            for (int k = 0; k < kBatch; ++k) {
+                const uint32_t e = threadIdx.x + (uint32_t)(k0 + k) * kThreads;
+                if (k0 + k < per_thread && e < tsize)
+                    v[k] = ld_reuse(p.x + base + (e & lowmask) + hi_off[e >> lowbits]);
+            }
+#pragma unroll
+            for (int k = 0; k < kBatch; ++k) {
+                const uint32_t e = threadIdx.x + (uint32_t)(k0 + k) * kThreads;
+                if (k0 + k < per_thread && e < tsize) tile[e] = v[k];
+            }
+        }
         __syncthreads();
-        for (int gi = p.g0; gi < p.g1; ++gi) {
-            const FusedGate &G = p.gates[gi];
+        for (int gi = 0; gi < ng; ++gi) {
+            const FusedGate &G = staged ? sg[gi] : p.gates[p.g0 + gi];
             switch (G.kin) {
                 case 0: {  // diagonal in every operand: element-wise
                     for (uint32_t e = threadIdx.x; e < tsize; e += blockDim.x) {
@@ -131,7 +168,10 @@ __global__ void __launch_bounds__(kThreads) fused_pass_kernel(const __grid_const
             }
             __syncthreads();
         }
-        for (uint32_t e = threadIdx.x; e < tsize; e += blockDim.x) st_plain(p.x + base + spread_tile(e, p.tb, T), tile[e]);
+        for (int k = 0; k < per_thread; ++k) {
+            const uint32_t e = threadIdx.x + (uint32_t)k * kThreads;
+            if (e < tsize) st_stream(p.x + base + (e & lowmask) + hi_off[e >> lowbits], tile[e]);
+        }
         __syncthreads();
     }
 }
