@@ -1,20 +1,28 @@
-// fused.cu -- multi-gate passes over shared-memory tiles (sm_100a).
+// fused.cu -- multi-gate passes: register-tiled, shared-memory staged (sm_100a).
 //
 // The run loop (reference sim.py:193-199) applies gates one at a time; on the
-// GPU each gate is a full 32*2^n-byte sweep of HBM.  A pass instead loads a
-// tile of 2^T amplitudes -- every index that varies only in a chosen set B
-// of T state bits (B always contains the low bits, so a tile row is a
-// contiguous 128-byte run) -- into shared memory, applies a run of
-// consecutive gates whose MIXING operand bits all lie in B, and writes the
-// tile back: one HBM sweep for the whole run.
+// GPU each gate alone is a full 32*2^n-byte sweep of HBM.  A pass instead
+// moves a tile of 2^T amplitudes -- every index that varies only in a set B
+// of T state bits (B contains the low bits, so tile rows are contiguous
+// 128-byte runs) -- through the SM once and applies a run of consecutive
+// gates whose MIXING operand bits all lie in B:
+//
+//   HBM --(coalesced)--> smem tile --> registers: phase 1 gates --> smem -->
+//   registers: phase 2 gates --> ... --> smem --(coalesced)--> HBM
+//
+// Each thread holds 2^R amplitudes in registers (R = T - 8, 256 threads).  A
+// phase picks R tile bits as "register bits" and applies every consecutive
+// gate whose mixing bits are among them entirely in registers; shared memory
+// is touched once per phase, not once per gate.  The smem tile is XOR-
+// swizzled so any lane<->bit mapping stays (nearly) bank-conflict free.
 //
 // Parity is unchanged: every gate is still applied on its own, in circuit
 // order, with the gate kernel's arithmetic (relabelled ascending-embedding
 // column order, numpy complex-multiply rounding, sequential adds from +0,
-// exactly-zero entries skipped).  Operands a gate does not mix (controls,
-// diagonal gates such as RZ/CZ) need not lie in B: within a group those bits
-// are fixed, so they only select which sub-block of the gate applies
-// (exactly the sharded-state argument, apply.cu).
+// exactly-zero entries skipped).  Operands a gate does not mix (controls;
+// diagonal gates such as RZ/CZ) may lie anywhere: within a register group
+// those bits are fixed, so they only select which sub-block of the gate
+// applies (the same argument as the sharded kernel, apply.cu).
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -24,36 +32,57 @@
 namespace diaq {
 
 constexpr int kMaxTileBits = 12;
-constexpr int kMaxFusedK = 4;      // operands per gate on this path
-constexpr int kLowBits = 3;        // tile rows are 2^3 amplitudes = 128 B
+constexpr int kThreadBits = 8;      // 256 threads
+constexpr int kLowBits = 3;         // tile rows are 2^3 amplitudes = 128 B
+constexpr int kMaxRegKin = 1;       // mixing operands applied in registers (wider: own pass)
+constexpr int kMaxSel = 4;          // selector (non-mixing) operands
+constexpr int kMaxPassGates = 96;   // gate records staged in smem per pass
+constexpr int kMaxPhases = 32;
 
-struct FusedGate {
-    int kin, kout;                 // mixing operands (in the tile), block-selector operands
-    int tsorted[kMaxFusedK];       // ascending tile positions of the mixing operands
-    int emb[1 << kMaxFusedK];      // tile offset of relabelled mixing index c
-    int osel[kMaxFusedK];          // selector j: 1 = bit from tile index, 0 = bit from tile base
-    int opos[kMaxFusedK];          // tile position or state shift of selector j
-    int coef_off;                  // coef[coef_off + (b << 2kin) + r * 2^kin + c]
-    int nz_off;                    // nz[nz_off + (b << kin) + r]
+static_assert(kThreads == (1 << kThreadBits), "thread layout");
+
+struct RegGate {
+    int kin;                  // 0, 1 or 2 mixing operands
+    int rb[kMaxRegKin];       // register bits of the mixing operands, descending (relabelled order)
+    int kout;                 // selector operands
+    int osel[kMaxSel];        // 0: bit `opos` of the tile base; 1: thread bit at tile position opos;
+                              // 2: register bit opos (varies between register groups)
+    int opos[kMaxSel];
+    int rsel;                 // any osel == 2
+    int coef_off;             // coef[coef_off + (b << 2kin) + r * 2^kin + c]   (pass-relative)
+    int nz_off;               // nz[nz_off + (b << kin) + r]
+    int cls_off;              // cls[cls_off + b]: 0 general, 1 identity (skip), 2 swap (kin 1)
+    // fast-path classification (host): 0 generic, 1 dense 1-qubit (no selector),
+    // 2 diagonal with one selector, 3 selector-controlled swap (CX-like)
+    int op;
+    int swap_when;            // op 3: selector value whose block is the swap
+    int mpos;                 // generic phases: tile position of the mixing bit
 };
 
-struct PassParams {
+struct Phase {
+    int g0, g1;               // gates [g0, g1) of the pass (pass-relative)
+    int generic;              // 1: gates applied in shared memory (no register bits)
+    int rpos[4];              // tile positions of the register bits, ascending (R entries)
+    int tpos[kMaxTileBits];   // tile positions of the thread bits, ascending (T - R entries)
+};
+
+struct TileParams {
     double2 *x;
     int64_t ntiles;
-    int tbits;                     // T
-    int tb[kMaxTileBits];          // ascending state bits of the tile
-    int g0, g1;                    // gates [g0, g1) of the program
-    const FusedGate *gates;
-    const double2 *coef;
+    int tbits;                // T
+    int tb[kMaxTileBits];     // ascending state bits of the tile
+    int nphases;
+    const Phase *phases;      // device
+    int ngates;
+    const RegGate *gates;     // device (pass-relative order)
+    const double2 *coef;      // this pass's tables, staged into shared memory
     const uint32_t *nz;
+    const uint32_t *cls;
+    int ncoef, nnz, ncls;
 };
 
-__device__ __forceinline__ uint64_t spread_tile(uint32_t e, const int *tb, int T) {
-    uint64_t out = 0;
-#pragma unroll
-    for (int j = 0; j < kMaxTileBits; ++j)
-        if (j < T) out |= (uint64_t)((e >> j) & 1u) << tb[j];
-    return out;
+__device__ __forceinline__ uint32_t swz(uint32_t e) {
+    return e ^ (((e >> 3) ^ (e >> 6) ^ (e >> 9)) & 7u);
 }
 
 __device__ __forceinline__ uint64_t insert_zero_bits_dyn(uint64_t g, const int *sh, int k) {
@@ -64,113 +93,230 @@ __device__ __forceinline__ uint64_t insert_zero_bits_dyn(uint64_t g, const int *
     return g;
 }
 
-__device__ __forceinline__ uint32_t block_of(const FusedGate &G, uint32_t te, uint64_t base) {
-    uint32_t b = 0;
-    for (int j = 0; j < G.kout; ++j) {
-        const uint32_t bit = G.osel[j] ? (te >> G.opos[j]) & 1u : (uint32_t)((base >> G.opos[j]) & 1ull);
-        b |= bit << (G.kout - 1 - j);
-    }
-    return b;
+template <int R>
+__device__ __forceinline__ uint32_t reg_spread(int j, const int *rpos) {
+    uint32_t e = 0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) e |= (uint32_t)((j >> i) & 1) << rpos[i];
+    return e;
 }
 
-template <int KIN, int MODE>
-__device__ __forceinline__ void apply_in_tile(double2 *tile, int T, const FusedGate &G, uint64_t base,
-                                              const double2 *__restrict__ coef, const uint32_t *__restrict__ nz) {
-    constexpr int M = 1 << KIN;
-    const uint32_t ngroups = 1u << (T - KIN);
+// ---- fast paths (R = 3 register bits) --------------------------------------
+
+template <int B1, int MODE>
+__device__ __forceinline__ void dense1(double2 (&v)[8], const double2 *c, uint32_t n0, uint32_t n1) {
+    const double2 c00 = c[0], c01 = c[1], c10 = c[2], c11 = c[3];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        const int j0 = ((g >> B1) << (B1 + 1)) | (g & ((1 << B1) - 1));
+        const int j1 = j0 | (1 << B1);
+        const double2 x0 = v[j0], x1 = v[j1];
+        double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+        if (n0 & 1u) a0 = cadd(a0, cmul<MODE>(c00, x0));
+        if (n0 & 2u) a0 = cadd(a0, cmul<MODE>(c01, x1));
+        if (n1 & 1u) a1 = cadd(a1, cmul<MODE>(c10, x0));
+        if (n1 & 2u) a1 = cadd(a1, cmul<MODE>(c11, x1));
+        v[j0] = a0;
+        v[j1] = a1;
+    }
+}
+
+template <int RB, int MODE>
+__device__ __forceinline__ void diag_reg(double2 (&v)[8], double2 d0, double2 d1, uint32_t z0, uint32_t z1) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const bool hi = (j >> RB) & 1;
+        const double2 d = hi ? d1 : d0;
+        const bool nz = hi ? (z1 & 1u) : (z0 & 1u);
+        v[j] = nz ? cadd(make_double2(0.0, 0.0), cmul<MODE>(d, v[j])) : make_double2(0.0, 0.0);
+    }
+}
+
+template <int B1>
+__device__ __forceinline__ void swap_all(double2 (&v)[8]) {
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        const int j0 = ((g >> B1) << (B1 + 1)) | (g & ((1 << B1) - 1));
+        const int j1 = j0 | (1 << B1);
+        const double2 t = v[j0];
+        v[j0] = v[j1];
+        v[j1] = t;
+    }
+}
+
+template <int RC, int B1>
+__device__ __forceinline__ void swap_ctrl(double2 (&v)[8], int when) {
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        const int j0 = ((g >> B1) << (B1 + 1)) | (g & ((1 << B1) - 1));
+        const int j1 = j0 | (1 << B1);
+        if (((j0 >> RC) & 1) == when) {
+            const double2 t = v[j0];
+            v[j0] = v[j1];
+            v[j1] = t;
+        }
+    }
+}
+
+template <int R, int MODE>
+__device__ __forceinline__ void dispatch_gate(double2 (&v)[1 << R], const RegGate &G, uint32_t tpart, uint64_t base,
+                                              const double2 *sc, const uint32_t *snz, const uint32_t *scls) {
+    // if-chains, not switches: a jump table would force v[] into local memory
+    (void)scls;
+    static_assert(R == 3, "register fast paths are written for 8 amplitudes per thread");
+    {
+        if (G.op == 1) {
+            const double2 *c = sc + G.coef_off;
+            const uint32_t n0 = snz[G.nz_off], n1 = snz[G.nz_off + 1];
+            const int b1 = G.rb[0];
+            if (b1 == 0) dense1<0, MODE>(v, c, n0, n1);
+            else if (b1 == 1) dense1<1, MODE>(v, c, n0, n1);
+            else dense1<2, MODE>(v, c, n0, n1);
+            return;
+        }
+        if (G.op == 2) {
+            const double2 d0 = sc[G.coef_off], d1 = sc[G.coef_off + 1];
+            const uint32_t z0 = snz[G.nz_off], z1 = snz[G.nz_off + 1];
+            if (G.osel[0] == 2) {
+                const int rb = G.opos[0];
+                if (rb == 0) diag_reg<0, MODE>(v, d0, d1, z0, z1);
+                else if (rb == 1) diag_reg<1, MODE>(v, d0, d1, z0, z1);
+                else diag_reg<2, MODE>(v, d0, d1, z0, z1);
+            } else {
+                const uint32_t b = G.osel[0] == 0 ? (uint32_t)((base >> G.opos[0]) & 1ull) : (tpart >> G.opos[0]) & 1u;
+                const double2 d = b ? d1 : d0;
+                const bool nz = b ? (z1 & 1u) : (z0 & 1u);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    v[j] = nz ? cadd(make_double2(0.0, 0.0), cmul<MODE>(d, v[j])) : make_double2(0.0, 0.0);
+            }
+            return;
+        }
+        if (G.op == 3) {
+            const int b1 = G.rb[0];
+            if (G.osel[0] == 2) {
+                const int rc = G.opos[0];
+                const int code = rc * 4 + b1;
+                if (code == 0 * 4 + 1) swap_ctrl<0, 1>(v, G.swap_when);
+                else if (code == 0 * 4 + 2) swap_ctrl<0, 2>(v, G.swap_when);
+                else if (code == 1 * 4 + 0) swap_ctrl<1, 0>(v, G.swap_when);
+                else if (code == 1 * 4 + 2) swap_ctrl<1, 2>(v, G.swap_when);
+                else if (code == 2 * 4 + 0) swap_ctrl<2, 0>(v, G.swap_when);
+                else swap_ctrl<2, 1>(v, G.swap_when);
+            } else {
+                const uint32_t b = G.osel[0] == 0 ? (uint32_t)((base >> G.opos[0]) & 1ull) : (tpart >> G.opos[0]) & 1u;
+                if ((int)b == G.swap_when) {
+                    if (b1 == 0) swap_all<0>(v);
+                    else if (b1 == 1) swap_all<1>(v);
+                    else swap_all<2>(v);
+                }
+            }
+            return;
+        }
+    }
+}
+
+// Generic gate (any selectors, <= 1 mixing bit) applied in the shared-memory
+// tile: the cold path for gates the register fast paths do not cover.
+template <int MODE>
+__device__ __forceinline__ void smem_gate(double2 *tile, int T, const RegGate &G, uint64_t base, const double2 *sc,
+                                          const uint32_t *snz) {
+    const int kin = G.kin;
+    const uint32_t ngroups = 1u << (T - kin);
     for (uint32_t grp = threadIdx.x; grp < ngroups; grp += blockDim.x) {
-        uint32_t tbase = grp;
-#pragma unroll
-        for (int i = 0; i < KIN; ++i) {
-            const uint32_t low = tbase & ((1u << G.tsorted[i]) - 1u);
-            tbase = ((tbase >> G.tsorted[i]) << (G.tsorted[i] + 1)) | low;
+        uint32_t e0 = grp;
+        if (kin) e0 = ((e0 >> G.mpos) << (G.mpos + 1)) | (e0 & ((1u << G.mpos) - 1u));
+        uint32_t b = 0;
+        for (int s = 0; s < G.kout; ++s) {
+            const uint32_t bit = G.osel[s] ? (e0 >> G.opos[s]) & 1u : (uint32_t)((base >> G.opos[s]) & 1ull);
+            b |= bit << (G.kout - 1 - s);
         }
-        const uint32_t b = block_of(G, tbase, base);
-        const double2 *cb = coef + G.coef_off + ((int)b << (2 * KIN));
-        const uint32_t *nb = nz + G.nz_off + ((int)b << KIN);
-        double2 xs[M];
-#pragma unroll
-        for (int c = 0; c < M; ++c) xs[c] = tile[tbase + G.emb[c]];
-#pragma unroll
-        for (int r = 0; r < M; ++r) {
-            double2 acc = make_double2(0.0, 0.0);
-            const uint32_t m = nb[r];
-#pragma unroll
-            for (int c = 0; c < M; ++c)
-                if ((m >> c) & 1u) acc = cadd(acc, cmul<MODE>(cb[r * M + c], xs[c]));
-            tile[tbase + G.emb[r]] = acc;
+        const double2 *c = sc + G.coef_off + ((int)b << (2 * kin));
+        const uint32_t *nz = snz + G.nz_off + ((int)b << kin);
+        if (kin == 0) {
+            const uint32_t i0 = swz(e0);
+            tile[i0] = (nz[0] & 1u) ? cadd(make_double2(0.0, 0.0), cmul<MODE>(c[0], tile[i0])) : make_double2(0.0, 0.0);
+        } else {
+            const uint32_t i0 = swz(e0), i1 = swz(e0 | (1u << G.mpos));
+            const double2 x0 = tile[i0], x1 = tile[i1];
+            double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+            if (nz[0] & 1u) a0 = cadd(a0, cmul<MODE>(c[0], x0));
+            if (nz[0] & 2u) a0 = cadd(a0, cmul<MODE>(c[1], x1));
+            if (nz[1] & 1u) a1 = cadd(a1, cmul<MODE>(c[2], x0));
+            if (nz[1] & 2u) a1 = cadd(a1, cmul<MODE>(c[3], x1));
+            tile[i0] = a0;
+            tile[i1] = a1;
         }
     }
 }
 
-constexpr int kMaxPassGates = 64;   // gate records staged in shared memory per pass
-constexpr int kBatch = 8;  // tile elements per thread per load/store batch
-
-// Tile element e = tid + kThreads*k.  Its state offset is
-// (e & lowmask) + hi_off[e >> lowbits]: the low tile bits are the low state
-// bits (contiguous), the rest come from a per-CTA table built once.
-template <int MODE, int MAXKIN>
-__global__ void __launch_bounds__(kThreads, MAXKIN >= 3 ? 2 : 4) fused_pass_kernel(const __grid_constant__ PassParams p) {
+template <int R, int MODE>
+__global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(const __grid_constant__ TileParams p) {
     extern __shared__ double2 tile[];
-    __shared__ uint64_t hi_off[1 << kMaxTileBits >> 3];
-    __shared__ FusedGate sg[kMaxPassGates];
+    __shared__ uint64_t hi_off[(1 << kMaxTileBits) >> kLowBits];
+    __shared__ Phase sph[kMaxPhases];
+    __shared__ RegGate sg[kMaxPassGates];
+    constexpr int NR = 1 << R;
     const int T = p.tbits;
     const uint32_t tsize = 1u << T;
-    int lowbits = 0;
-    while (lowbits < T && p.tb[lowbits] == lowbits) ++lowbits;
-    if (lowbits > 8) lowbits = 8;  // e >> 8 indexes the table; kThreads == 256
-    const uint32_t lowmask = (1u << lowbits) - 1u;
-    for (uint32_t h = threadIdx.x; h < (tsize >> lowbits); h += blockDim.x) {
+    double2 *sc = tile + tsize;
+    uint32_t *snz = reinterpret_cast<uint32_t *>(sc + p.ncoef);
+    uint32_t *scls = snz + p.nnz;
+    for (int i = threadIdx.x; i < p.ncoef; i += blockDim.x) sc[i] = p.coef[i];
+    for (int i = threadIdx.x; i < p.nnz; i += blockDim.x) snz[i] = p.nz[i];
+    for (int i = threadIdx.x; i < p.ncls; i += blockDim.x) scls[i] = p.cls[i];
+    // tile element e -> state offset: low kLowBits tile bits are state bits 0..2
+    for (uint32_t h = threadIdx.x; h < (tsize >> kLowBits); h += blockDim.x) {
         uint64_t off = 0;
-        for (int j = lowbits; j < T; ++j) off |= (uint64_t)((h >> (j - lowbits)) & 1u) << p.tb[j];
+        for (int j = kLowBits; j < T; ++j) off |= (uint64_t)((h >> (j - kLowBits)) & 1u) << p.tb[j];
         hi_off[h] = off;
     }
-    const int ng = p.g1 - p.g0;
-    const bool staged = ng <= kMaxPassGates;
-    if (staged)
-        for (int i = threadIdx.x; i < ng * (int)(sizeof(FusedGate) / 4); i += blockDim.x)
-            reinterpret_cast<int *>(sg)[i] = reinterpret_cast<const int *>(p.gates + p.g0)[i];
+    for (int i = threadIdx.x; i < p.nphases * (int)(sizeof(Phase) / 4); i += blockDim.x)
+        reinterpret_cast<int *>(sph)[i] = reinterpret_cast<const int *>(p.phases)[i];
+    for (int i = threadIdx.x; i < p.ngates * (int)(sizeof(RegGate) / 4); i += blockDim.x)
+        reinterpret_cast<int *>(sg)[i] = reinterpret_cast<const int *>(p.gates)[i];
     __syncthreads();
-    const int per_thread = (int)(tsize >= kThreads ? tsize / kThreads : 1);
+    constexpr uint32_t lowmask = (1u << kLowBits) - 1u;
+    const int per_thread = (int)(tsize >> kThreadBits);
     for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
         const uint64_t base = insert_zero_bits_dyn((uint64_t)t, p.tb, T);
-        for (int k0 = 0; k0 < per_thread; k0 += kBatch) {
-            double2 v[kBatch];
+        // HBM -> smem, coalesced (consecutive e are consecutive state indices in runs of 8)
+        for (int k0 = 0; k0 < per_thread; k0 += 4) {
+            double2 w[4];
 #pragma unroll
-            for (int k = 0; k < kBatch; ++k) {
+            for (int k = 0; k < 4; ++k) {
                 const uint32_t e = threadIdx.x + (uint32_t)(k0 + k) * kThreads;
-                if (k0 + k < per_thread && e < tsize)
-                    v[k] = ld_reuse(p.x + base + (e & lowmask) + hi_off[e >> lowbits]);
+                if (k0 + k < per_thread) w[k] = ld_reuse(p.x + base + (e & lowmask) + hi_off[e >> kLowBits]);
             }
 #pragma unroll
-            for (int k = 0; k < kBatch; ++k) {
+            for (int k = 0; k < 4; ++k) {
                 const uint32_t e = threadIdx.x + (uint32_t)(k0 + k) * kThreads;
-                if (k0 + k < per_thread && e < tsize) tile[e] = v[k];
+                if (k0 + k < per_thread) tile[swz(e)] = w[k];
             }
         }
         __syncthreads();
-        for (int gi = 0; gi < ng; ++gi) {
-            const FusedGate &G = staged ? sg[gi] : p.gates[p.g0 + gi];
-            switch (G.kin) {
-                case 0: {  // diagonal in every operand: element-wise
-                    for (uint32_t e = threadIdx.x; e < tsize; e += blockDim.x) {
-                        const uint32_t b = block_of(G, e, base);
-                        double2 acc = make_double2(0.0, 0.0);
-                        if (p.nz[G.nz_off + b] & 1u) acc = cadd(acc, cmul<MODE>(p.coef[G.coef_off + b], tile[e]));
-                        tile[e] = acc;
-                    }
-                    break;
+        for (int ph_i = 0; ph_i < p.nphases; ++ph_i) {
+            const Phase &ph = sph[ph_i];
+            if (ph.generic) {
+                for (int gi = ph.g0; gi < ph.g1; ++gi) {
+                    smem_gate<MODE>(tile, T, sg[gi], base, sc, snz);
+                    __syncthreads();
                 }
-                case 1: apply_in_tile<1, MODE>(tile, T, G, base, p.coef, p.nz); break;
-                case 2: if constexpr (MAXKIN >= 2) apply_in_tile<2, MODE>(tile, T, G, base, p.coef, p.nz); break;
-                case 3: if constexpr (MAXKIN >= 3) apply_in_tile<3, MODE>(tile, T, G, base, p.coef, p.nz); break;
-                default: if constexpr (MAXKIN >= 4) apply_in_tile<4, MODE>(tile, T, G, base, p.coef, p.nz); break;
+                continue;
             }
+            uint32_t tpart = 0;
+            for (int i = 0; i < T - R; ++i) tpart |= ((threadIdx.x >> i) & 1u) << ph.tpos[i];
+            double2 v[NR];
+#pragma unroll
+            for (int j = 0; j < NR; ++j) v[j] = tile[swz(tpart | reg_spread<R>(j, ph.rpos))];
+            for (int gi = ph.g0; gi < ph.g1; ++gi) dispatch_gate<R, MODE>(v, sg[gi], tpart, base, sc, snz, scls);
+#pragma unroll
+            for (int j = 0; j < NR; ++j) tile[swz(tpart | reg_spread<R>(j, ph.rpos))] = v[j];
             __syncthreads();
         }
         for (int k = 0; k < per_thread; ++k) {
             const uint32_t e = threadIdx.x + (uint32_t)k * kThreads;
-            if (e < tsize) st_stream(p.x + base + (e & lowmask) + hi_off[e >> lowbits], tile[e]);
+            st_stream(p.x + base + (e & lowmask) + hi_off[e >> kLowBits], tile[swz(e)]);
         }
         __syncthreads();
     }
@@ -194,117 +340,234 @@ static uint32_t mixing_mask(int k, const double *g) {
     return mix;
 }
 
-struct Program {
-    std::vector<FusedGate> gates;
+struct Packed {
     std::vector<double2> coef;
     std::vector<uint32_t> nz;
-    struct Pass {
-        int g0, g1;
-        int maxkin = 1;
-        std::vector<int> bits;  // ascending state bits of the tile
-        std::vector<int> members;  // indices into the caller's gate list
-    };
-    std::vector<Pass> passes;
+    std::vector<uint32_t> cls;
 };
 
-static int pack_gate(const diaq_gate_t &gt, const std::vector<int> &bits, Program &pr) {
-    const int k = gt.k;
-    const int M = 1 << k;
+struct PassPlan {
+    std::vector<int> bits;        // ascending state bits of the tile (empty: standalone gate)
+    std::vector<int> members;     // caller gate indices, in order
+    std::vector<Phase> phases;
+    std::vector<RegGate> gates;   // pass-relative
+    Packed pk;                    // pass-relative coefficient tables
+};
+
+static int tile_pos(const std::vector<int> &bits, int shift) {
+    for (size_t j = 0; j < bits.size(); ++j)
+        if (bits[j] == shift) return (int)j;
+    return -1;
+}
+
+static int pack_reg_gate(const diaq_gate_t &gt, const std::vector<int> &bits, const Phase &ph, int R, Packed &pk,
+                         RegGate &G) {
+    const int k = gt.k, M = 1 << k;
     const uint32_t mix = mixing_mask(k, gt.g);
-    std::vector<int> mops, sops;  // mixing / selector operands
+    std::vector<int> mops, sops;
     for (int i = 0; i < k; ++i) ((mix >> i) & 1u ? mops : sops).push_back(i);
     std::sort(mops.begin(), mops.end(), [&](int a, int b) { return gt.shifts[a] > gt.shifts[b]; });
     std::sort(sops.begin(), sops.end(), [&](int a, int b) { return gt.shifts[a] > gt.shifts[b]; });
-    FusedGate G;
     memset(&G, 0, sizeof(G));
     G.kin = (int)mops.size();
     G.kout = (int)sops.size();
-    if (G.kin > kMaxFusedK || G.kout > kMaxFusedK) return set_error(DIAQ_ERR_UNSUPPORTED, "fused gate too wide");
-    auto tpos = [&](int shift) {
-        for (size_t j = 0; j < bits.size(); ++j)
-            if (bits[j] == shift) return (int)j;
-        return -1;
-    };
-    std::vector<int> tp;
+    if (G.kin > kMaxRegKin || G.kout > kMaxSel) return set_error(DIAQ_ERR_UNSUPPORTED, "fused gate too wide");
     for (int j = 0; j < G.kin; ++j) {
-        const int p = tpos(gt.shifts[mops[j]]);
-        if (p < 0) return set_error(DIAQ_ERR_VALUE, "fused pass: mixing bit outside the tile");
-        tp.push_back(p);
+        const int tp = tile_pos(bits, gt.shifts[mops[j]]);
+        int rb = -1;
+        for (int i = 0; i < R; ++i)
+            if (ph.rpos[i] == tp) rb = i;
+        if (tp < 0 || rb < 0) return set_error(DIAQ_ERR_VALUE, "fused pass: mixing bit outside the phase registers");
+        G.rb[j] = rb;  // descending shift -> descending register bit
     }
-    std::vector<int> ts = tp;
-    std::sort(ts.begin(), ts.end());
-    for (int j = 0; j < G.kin; ++j) G.tsorted[j] = ts[j];
-    const int MI = 1 << G.kin;
-    for (int c = 0; c < MI; ++c) {
-        int e = 0;
-        for (int j = 0; j < G.kin; ++j) e |= ((c >> (G.kin - 1 - j)) & 1) << tp[j];
-        G.emb[c] = e;
-    }
+    G.rsel = 0;
     for (int j = 0; j < G.kout; ++j) {
         const int s = gt.shifts[sops[j]];
-        const int p = tpos(s);
-        G.osel[j] = p >= 0 ? 1 : 0;
-        G.opos[j] = p >= 0 ? p : s;
+        const int tp = tile_pos(bits, s);
+        if (tp < 0) {
+            G.osel[j] = 0;
+            G.opos[j] = s;
+            continue;
+        }
+        int rb = -1;
+        for (int i = 0; i < R; ++i)
+            if (ph.rpos[i] == tp) rb = i;
+        if (rb >= 0) {
+            G.osel[j] = 2;
+            G.opos[j] = rb;
+            G.rsel = 1;
+        } else {
+            G.osel[j] = 1;
+            G.opos[j] = tp;
+        }
     }
-    // original gate index from (selector value b, mixing value c)
     auto orig = [&](int b, int c) {
         int o = 0;
         for (int j = 0; j < G.kin; ++j) o |= ((c >> (G.kin - 1 - j)) & 1) << (k - 1 - mops[j]);
         for (int j = 0; j < G.kout; ++j) o |= ((b >> (G.kout - 1 - j)) & 1) << (k - 1 - sops[j]);
         return o;
     };
-    G.coef_off = (int)pr.coef.size();
-    G.nz_off = (int)pr.nz.size();
-    for (int b = 0; b < (1 << G.kout); ++b)
+    const int MI = 1 << G.kin;
+    G.coef_off = (int)pk.coef.size();
+    G.nz_off = (int)pk.nz.size();
+    G.cls_off = (int)pk.cls.size();
+    for (int b = 0; b < (1 << G.kout); ++b) {
+        bool ident = true, swap = (MI == 2);
         for (int r = 0; r < MI; ++r) {
             uint32_t m = 0;
             for (int c = 0; c < MI; ++c) {
                 const int o_r = orig(b, r), o_c = orig(b, c);
                 const double re = gt.g[2 * (o_r * M + o_c)], im = gt.g[2 * (o_r * M + o_c) + 1];
-                pr.coef.push_back(make_double2(re, im));
+                pk.coef.push_back(make_double2(re, im));
                 if (re != 0.0 || im != 0.0) m |= 1u << c;
+                const bool one = (re == 1.0 && im == 0.0), zero = (re == 0.0 && im == 0.0);
+                if (r == c ? !one : !zero) ident = false;
+                if (r != c ? !one : !zero) swap = false;
             }
-            pr.nz.push_back(m);
+            pk.nz.push_back(m);
         }
-    pr.gates.push_back(G);
+        pk.cls.push_back(ident ? 1u : (swap ? 2u : 0u));
+    }
+    G.op = 0;
+    if (G.kin == 1 && G.kout == 0) G.op = 1;
+    else if (G.kin == 0 && G.kout == 1) G.op = 2;
+    else if (G.kin == 1 && G.kout == 1) {
+        const uint32_t c0 = pk.cls[G.cls_off], c1 = pk.cls[G.cls_off + 1];
+        if (c0 == 1 && c1 == 2) { G.op = 3; G.swap_when = 1; }
+        else if (c0 == 2 && c1 == 1) { G.op = 3; G.swap_when = 0; }
+    }
     return DIAQ_OK;
 }
 
-// Greedy left-to-right: extend the current pass while the union of mixing
-// bits (plus the low bits) fits in T; gates wider than kMaxFusedK or whose
-// mixing bits alone exceed T become single-gate passes (tile empty: bits
-// left empty, applied by gate_kernel).
-static int schedule(int n_bits, int ngates, const diaq_gate_t *gates, int T, Program &pr) {
+// gates the register fast paths handle: dense 1-qubit, 1-selector diagonal,
+// 1-selector controlled swap (classification by pack_reg_gate on a dummy phase)
+static bool fast_op(const diaq_gate_t &gt) {
+    const uint32_t mix = mixing_mask(gt.k, gt.g);
+    int kin = 0;
+    for (int i = 0; i < gt.k; ++i) kin += (mix >> i) & 1u;
+    const int kout = gt.k - kin;
+    if (kin > 1 || kout > 1) return false;
+    if (kin == 1 && kout == 0) return true;
+    if (kin == 0 && kout == 1) return true;
+    // kin == 1 && kout == 1: blocks must be {identity, swap}
+    std::vector<int> bits;
+    for (int b = 0; b < 64; ++b) bits.push_back(b);
+    Phase ph;
+    memset(&ph, 0, sizeof(ph));
+    int mshift = -1;
+    for (int i = 0; i < gt.k; ++i)
+        if ((mix >> i) & 1u) mshift = gt.shifts[i];
+    ph.rpos[0] = mshift;
+    ph.rpos[1] = 62;
+    ph.rpos[2] = 63;
+    Packed pk;
+    RegGate G;
+    if (pack_reg_gate(gt, bits, ph, 3, pk, G) != DIAQ_OK) return false;
+    return G.op == 3;
+}
+
+static int pack_smem_gate(const diaq_gate_t &gt, const std::vector<int> &bits, Packed &pk, RegGate &G) {
+    Phase ph;
+    memset(&ph, 0, sizeof(ph));
+    for (int i = 0; i < 4; ++i) ph.rpos[i] = -100;  // no register bits: selectors are tile or base bits
+    const uint32_t mix = mixing_mask(gt.k, gt.g);
+    int mshift = -1;
+    for (int i = 0; i < gt.k; ++i)
+        if ((mix >> i) & 1u) mshift = gt.shifts[i];
+    // pack_reg_gate needs the mixing bit among the registers: give it one fake register
+    if (mshift >= 0) ph.rpos[0] = tile_pos(bits, mshift);
+    const int rc = pack_reg_gate(gt, bits, ph, 1, pk, G);
+    if (rc) return rc;
+    G.mpos = mshift >= 0 ? tile_pos(bits, mshift) : 0;
+    for (int s = 0; s < G.kout; ++s)
+        if (G.osel[s] == 2) return set_error(DIAQ_ERR_VALUE, "smem gate selector on a register bit");
+    G.op = 0;
+    return DIAQ_OK;
+}
+
+// Greedy, order preserving: a pass grows while the union of mixing bits
+// (plus the low bits) fits in T; within a pass a phase grows while the
+// union of its gates' mixing bits fits in R registers.  Gates that cannot
+// be applied in registers (more than 2 mixing or 4 selector operands)
+// become standalone single-gate passes (gate_kernel).
+static int schedule(int n_bits, int ngates, const diaq_gate_t *gates, int T, int R, std::vector<PassPlan> &plan) {
     const int low = std::min(kLowBits, n_bits);
-    std::vector<int> cur_members;
+    std::vector<int> members;
     std::vector<char> inb(64, 0);
     int nb = 0;
     auto reset = [&]() {
         std::fill(inb.begin(), inb.end(), 0);
         nb = 0;
         for (int b = 0; b < low; ++b) { inb[b] = 1; ++nb; }
-        cur_members.clear();
+        members.clear();
     };
     auto flush = [&]() -> int {
-        if (cur_members.empty()) return DIAQ_OK;
-        Program::Pass ps;
-        std::vector<int> bits;
+        if (members.empty()) return DIAQ_OK;
+        PassPlan ps;
         for (int b = 0; b < 64; ++b)
-            if (inb[b]) bits.push_back(b);
-        // pad the tile to exactly T bits with the lowest unused bits
-        for (int b = 0; (int)bits.size() < T && b < n_bits; ++b)
-            if (!inb[b]) { bits.push_back(b); }
-        std::sort(bits.begin(), bits.end());
-        ps.bits = bits;
-        ps.members = cur_members;
-        ps.g0 = (int)pr.gates.size();
-        for (int gi : cur_members) {
-            const int rc = pack_gate(gates[gi], bits, pr);
-            if (rc) return rc;
-            ps.maxkin = std::max(ps.maxkin, pr.gates.back().kin);
+            if (inb[b]) ps.bits.push_back(b);
+        for (int b = 0; (int)ps.bits.size() < T && b < n_bits; ++b)
+            if (!inb[b]) ps.bits.push_back(b);
+        std::sort(ps.bits.begin(), ps.bits.end());
+        ps.members = members;
+        size_t i = 0;
+        while (i < members.size()) {
+            if (!fast_op(gates[members[i]])) {  // cold path: its own shared-memory phase
+                Phase ph;
+                memset(&ph, 0, sizeof(ph));
+                ph.generic = 1;
+                ph.g0 = (int)ps.gates.size();
+                RegGate G;
+                const int rc = pack_smem_gate(gates[members[i]], ps.bits, ps.pk, G);
+                if (rc) return rc;
+                ps.gates.push_back(G);
+                ph.g1 = (int)ps.gates.size();
+                ps.phases.push_back(ph);
+                ++i;
+                continue;
+            }
+            std::vector<int> used;  // tile positions of mixing bits in this phase
+            size_t j = i;
+            while (j < members.size()) {
+                const diaq_gate_t &gt = gates[members[j]];
+                if (!fast_op(gt)) break;
+                const uint32_t mix = mixing_mask(gt.k, gt.g);
+                std::vector<int> add;
+                for (int o = 0; o < gt.k; ++o)
+                    if ((mix >> o) & 1u) {
+                        const int tp = tile_pos(ps.bits, gt.shifts[o]);
+                        if (std::find(used.begin(), used.end(), tp) == used.end() &&
+                            std::find(add.begin(), add.end(), tp) == add.end())
+                            add.push_back(tp);
+                    }
+                if ((int)(used.size() + add.size()) > R) break;
+                used.insert(used.end(), add.begin(), add.end());
+                ++j;
+            }
+            Phase ph;
+            memset(&ph, 0, sizeof(ph));
+            std::vector<int> rp = used;
+            for (int tp = 0; (int)rp.size() < R; ++tp)
+                if (std::find(rp.begin(), rp.end(), tp) == rp.end()) rp.push_back(tp);
+            std::sort(rp.begin(), rp.end());
+            for (int q = 0; q < R; ++q) ph.rpos[q] = rp[q];
+            int tq = 0;
+            for (int tp = 0; tp < (int)ps.bits.size(); ++tp)
+                if (std::find(rp.begin(), rp.end(), tp) == rp.end()) ph.tpos[tq++] = tp;
+            ph.g0 = (int)ps.gates.size();
+            for (size_t q = i; q < j; ++q) {
+                RegGate G;
+                const int rc = pack_reg_gate(gates[members[q]], ps.bits, ph, R, ps.pk, G);
+                if (rc) return rc;
+                ps.gates.push_back(G);
+            }
+            ph.g1 = (int)ps.gates.size();
+            ps.phases.push_back(ph);
+            i = j;
         }
-        ps.g1 = (int)pr.gates.size();
-        pr.passes.push_back(ps);
+        if ((int)ps.phases.size() > kMaxPhases || (int)ps.gates.size() > kMaxPassGates)
+            return set_error(DIAQ_ERR_VALUE, "fused pass too long");
+        plan.push_back(ps);
         return DIAQ_OK;
     };
     reset();
@@ -319,17 +582,17 @@ static int schedule(int n_bits, int ngates, const diaq_gate_t *gates, int T, Pro
             if ((mix >> j) & 1u) { ++kin; add += inb[gt.shifts[j]] ? 0 : 1; }
             else ++kout;
         }
-        if (kin > kMaxFusedK || kout > kMaxFusedK) {  // too wide for the tile path: its own pass
+        if (kin > kMaxRegKin || kin > R || kout > kMaxSel) {  // standalone pass
             int rc = flush();
             if (rc) return rc;
             reset();
-            Program::Pass ps;
-            ps.g0 = ps.g1 = -1;
+            PassPlan ps;
             ps.members = {i};
-            pr.passes.push_back(ps);
+            plan.push_back(ps);
             continue;
         }
-        if (nb + add > T) {
+        // phases per pass are bounded too: a pass can need up to one phase per gate
+        if (nb + add > T || (int)members.size() >= std::min(kMaxPassGates, kMaxPhases)) {
             int rc = flush();
             if (rc) return rc;
             reset();
@@ -339,7 +602,7 @@ static int schedule(int n_bits, int ngates, const diaq_gate_t *gates, int T, Pro
         }
         for (int j = 0; j < gt.k; ++j)
             if (((mix >> j) & 1u) && !inb[gt.shifts[j]]) { inb[gt.shifts[j]] = 1; ++nb; }
-        cur_members.push_back(i);
+        members.push_back(i);
     }
     return flush();
 }
@@ -354,6 +617,12 @@ static int sm_count_f() {
     return sms;
 }
 
+template <int R>
+static const void *tile_kernel_ptr(int cmul_mode) {
+    return cmul_mode == DIAQ_CMUL_FMA ? (const void *)tile_pass_kernel<R, DIAQ_CMUL_FMA>
+                                      : (const void *)tile_pass_kernel<R, DIAQ_CMUL_PLAIN>;
+}
+
 }  // namespace diaq
 
 using namespace diaq;
@@ -363,83 +632,100 @@ extern "C" int diaq_run_gates_fused(int n_bits, int ngates, const diaq_gate_t *g
     if (ngates < 0 || (ngates > 0 && !gates) || !state)
         return set_error(DIAQ_ERR_VALUE, "diaq_run_gates_fused: bad arguments");
     cudaStream_t s = (cudaStream_t)stream;
-    int T = tile_bits <= 0 ? 11 : tile_bits;
-    T = std::min(std::min(T, kMaxTileBits), n_bits);
-    Program pr;
-    int rc = schedule(n_bits, ngates, gates, T, pr);
-    if (rc) return rc;
-    if (npasses) *npasses = (int)pr.passes.size();
-    FusedGate *dg = nullptr;
-    double2 *dc = nullptr;
-    uint32_t *dn = nullptr;
-    const size_t gb = sizeof(FusedGate) * std::max<size_t>(1, pr.gates.size());
-    const size_t cb = sizeof(double2) * std::max<size_t>(1, pr.coef.size());
-    const size_t nbytes = sizeof(uint32_t) * std::max<size_t>(1, pr.nz.size());
-    if (cudaMallocAsync((void **)&dg, gb, s) != cudaSuccess || cudaMallocAsync((void **)&dc, cb, s) != cudaSuccess ||
-        cudaMallocAsync((void **)&dn, nbytes, s) != cudaSuccess)
-        return set_error(DIAQ_ERR_CUDA, "diaq_run_gates_fused: program alloc failed");
-    if (!pr.gates.empty()) {
-        cudaMemcpyAsync(dg, pr.gates.data(), sizeof(FusedGate) * pr.gates.size(), cudaMemcpyHostToDevice, s);
-        cudaMemcpyAsync(dc, pr.coef.data(), sizeof(double2) * pr.coef.size(), cudaMemcpyHostToDevice, s);
-        cudaMemcpyAsync(dn, pr.nz.data(), sizeof(uint32_t) * pr.nz.size(), cudaMemcpyHostToDevice, s);
+    (void)tile_bits;
+    const int T = kThreadBits + 3;  // R = 3 register bits x 256 threads (tile_bits > 0 selects this path)
+    const bool tiled = n_bits >= T;
+    const int R = T - kThreadBits;
+    std::vector<PassPlan> plan;
+    int rc = DIAQ_OK;
+    if (tiled) {
+        rc = schedule(n_bits, ngates, gates, T, R, plan);
+        if (rc) return rc;
+    } else {  // state smaller than a tile: gate by gate
+        for (int i = 0; i < ngates; ++i) {
+            PassPlan ps;
+            ps.members = {i};
+            plan.push_back(ps);
+        }
     }
-    const size_t smem_max = sizeof(double2) << kMaxTileBits;
+    if (npasses) *npasses = (int)plan.size();
+    // one device buffer: per pass [phases | gates | coef | nz | cls], 16-byte aligned
+    struct Off { size_t ph, g, coef, nz, cls; };
+    std::vector<Off> off(plan.size());
+    size_t cur = 0;
+    auto al = [](size_t v) { return (v + 15) & ~(size_t)15; };
+    for (size_t i = 0; i < plan.size(); ++i) {
+        const PassPlan &ps = plan[i];
+        off[i].ph = cur; cur = al(cur + sizeof(Phase) * ps.phases.size());
+        off[i].g = cur; cur = al(cur + sizeof(RegGate) * ps.gates.size());
+        off[i].coef = cur; cur = al(cur + sizeof(double2) * ps.pk.coef.size());
+        off[i].nz = cur; cur = al(cur + sizeof(uint32_t) * ps.pk.nz.size());
+        off[i].cls = cur; cur = al(cur + sizeof(uint32_t) * ps.pk.cls.size());
+    }
+    const size_t bytes = cur + 16;
+    std::vector<char> host(bytes, 0);
+    for (size_t i = 0; i < plan.size(); ++i) {
+        const PassPlan &ps = plan[i];
+        if (!ps.phases.empty()) memcpy(&host[off[i].ph], ps.phases.data(), sizeof(Phase) * ps.phases.size());
+        if (!ps.gates.empty()) memcpy(&host[off[i].g], ps.gates.data(), sizeof(RegGate) * ps.gates.size());
+        if (!ps.pk.coef.empty()) memcpy(&host[off[i].coef], ps.pk.coef.data(), sizeof(double2) * ps.pk.coef.size());
+        if (!ps.pk.nz.empty()) memcpy(&host[off[i].nz], ps.pk.nz.data(), sizeof(uint32_t) * ps.pk.nz.size());
+        if (!ps.pk.cls.empty()) memcpy(&host[off[i].cls], ps.pk.cls.data(), sizeof(uint32_t) * ps.pk.cls.size());
+    }
+    char *dbuf = nullptr;
+    if (tiled && !plan.empty()) {
+        if (cudaMallocAsync((void **)&dbuf, bytes, s) != cudaSuccess)
+            return set_error(DIAQ_ERR_CUDA, "diaq_run_gates_fused: program alloc failed");
+        cudaMemcpyAsync(dbuf, host.data(), bytes, cudaMemcpyHostToDevice, s);
+    }
+    const size_t smem_max = (sizeof(double2) << kMaxTileBits) + 48 * 1024;
     static bool attr_set = false;
     if (!attr_set) {
-#define DIAQ_SMEM_ATTR(M_, K_) \
-    cudaFuncSetAttribute(fused_pass_kernel<M_, K_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
-        DIAQ_SMEM_ATTR(DIAQ_CMUL_FMA, 1) DIAQ_SMEM_ATTR(DIAQ_CMUL_FMA, 2) DIAQ_SMEM_ATTR(DIAQ_CMUL_FMA, 3)
-        DIAQ_SMEM_ATTR(DIAQ_CMUL_FMA, 4) DIAQ_SMEM_ATTR(DIAQ_CMUL_PLAIN, 1) DIAQ_SMEM_ATTR(DIAQ_CMUL_PLAIN, 2)
-        DIAQ_SMEM_ATTR(DIAQ_CMUL_PLAIN, 3) DIAQ_SMEM_ATTR(DIAQ_CMUL_PLAIN, 4)
-#undef DIAQ_SMEM_ATTR
+        cudaFuncSetAttribute(tile_pass_kernel<3, DIAQ_CMUL_FMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+        cudaFuncSetAttribute(tile_pass_kernel<3, DIAQ_CMUL_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
         attr_set = true;
     }
-    int gate_idx = 0;
     if (events && cudaEventRecord((cudaEvent_t)events[0], s) != cudaSuccess)
         return set_error(DIAQ_ERR_CUDA, "diaq_run_gates_fused: event record failed");
-    for (size_t pi = 0; pi < pr.passes.size() && rc == DIAQ_OK; ++pi) {
-        const Program::Pass &ps = pr.passes[pi];
-        if (ps.g0 < 0 || ps.members.size() == 1) {
+    for (size_t pi = 0; pi < plan.size() && rc == DIAQ_OK; ++pi) {
+        const PassPlan &ps = plan[pi];
+        if (ps.bits.empty() || ps.members.size() == 1) {
             const diaq_gate_t &gt = gates[ps.members[0]];
             rc = apply_gate(n_bits, gt.k, gt.g, gt.shifts, state, state, cmul_mode, s);
         } else {
-            PassParams p;
+            TileParams p;
             p.x = (double2 *)state;
             p.tbits = (int)ps.bits.size();
             for (int j = 0; j < p.tbits; ++j) p.tb[j] = ps.bits[j];
             p.ntiles = (int64_t)1 << (n_bits - p.tbits);
-            p.g0 = ps.g0;
-            p.g1 = ps.g1;
-            p.gates = dg;
-            p.coef = dc;
-            p.nz = dn;
-            const size_t smem = sizeof(double2) << p.tbits;
-            const int mk = std::min(4, std::max(1, ps.maxkin));
-            const bool fma = cmul_mode == DIAQ_CMUL_FMA;
-            const void *f = nullptr;
-            switch (mk) {
-                case 1: f = fma ? (const void *)fused_pass_kernel<DIAQ_CMUL_FMA, 1> : (const void *)fused_pass_kernel<DIAQ_CMUL_PLAIN, 1>; break;
-                case 2: f = fma ? (const void *)fused_pass_kernel<DIAQ_CMUL_FMA, 2> : (const void *)fused_pass_kernel<DIAQ_CMUL_PLAIN, 2>; break;
-                case 3: f = fma ? (const void *)fused_pass_kernel<DIAQ_CMUL_FMA, 3> : (const void *)fused_pass_kernel<DIAQ_CMUL_PLAIN, 3>; break;
-                default: f = fma ? (const void *)fused_pass_kernel<DIAQ_CMUL_FMA, 4> : (const void *)fused_pass_kernel<DIAQ_CMUL_PLAIN, 4>; break;
-            }
+            p.nphases = (int)ps.phases.size();
+            p.phases = (const Phase *)(dbuf + off[pi].ph);
+            p.ngates = (int)ps.gates.size();
+            p.gates = (const RegGate *)(dbuf + off[pi].g);
+            p.coef = (const double2 *)(dbuf + off[pi].coef);
+            p.nz = (const uint32_t *)(dbuf + off[pi].nz);
+            p.cls = (const uint32_t *)(dbuf + off[pi].cls);
+            p.ncoef = (int)ps.pk.coef.size();
+            p.nnz = (int)ps.pk.nz.size();
+            p.ncls = (int)ps.pk.cls.size();
+            const size_t smem = (sizeof(double2) << p.tbits) + sizeof(double2) * p.ncoef +
+                                sizeof(uint32_t) * (p.nnz + p.ncls);
+            if (smem > smem_max) return set_error(DIAQ_ERR_VALUE, "fused pass tables exceed shared memory");
+            const void *f = tile_kernel_ptr<3>(cmul_mode);
             int per_sm = 1;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kThreads, smem);
-            const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(p.ntiles, (int64_t)sm_count_f() * std::max(1, per_sm)));
+            const int64_t grid =
+                std::max<int64_t>(1, std::min<int64_t>(p.ntiles, (int64_t)sm_count_f() * std::max(1, per_sm)));
             void *args[] = {(void *)&p};
             cudaLaunchKernel(f, dim3((unsigned)grid), dim3(kThreads), args, smem, s);
             count_launch();
-            rc = check_launch("fused_pass_kernel");
+            rc = check_launch("tile_pass_kernel");
         }
-        gate_idx += (int)ps.members.size();
         // events[i]..events[i+1] bracket gate i; a fused pass's time lands on
         // its first gate, the others record zero-length intervals
         if (events && rc == DIAQ_OK)
             for (int gi : ps.members) cudaEventRecord((cudaEvent_t)events[gi + 1], s);
     }
-    cudaFreeAsync(dg, s);
-    cudaFreeAsync(dc, s);
-    cudaFreeAsync(dn, s);
-    (void)gate_idx;
+    if (dbuf) cudaFreeAsync(dbuf, s);
     return rc;
 }
