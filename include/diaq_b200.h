@@ -171,6 +171,13 @@ int diaq_shard_plan(int n_bits, int local_bits, int k, const double *g_host, con
 int diaq_apply_gate_sharded(int n_bits, int local_bits, int k, const double *g_host, const int *shifts,
                             int64_t rank, const void *const *srcs, void *y, int cmul_mode, void *stream);
 
+/* ---- sampling (reference measure_all_sample, sim.py:142-161) -------------
+ * hits[k] = min(#{i : cdf_i <= u_k}, N-1) with cdf = sequential float64
+ * cumsum of round(|x_i|^2, 12), reproduced exactly (binade-segmented exact
+ * integer scans); *norm2_out = sum |x_i|^2.  u_host: `shots` uniforms. */
+int diaq_sample_hits(int64_t n_amps, const void *x, const double *u_host, int64_t shots, int64_t *hits_host,
+                     double *norm2_out, void *stream);
+
 /* ---- timing (per-gate CUDA events, resolved after the loop) ---------------- */
 int diaq_timer_create(int n, void **events);
 int diaq_timer_record(void *event, void *stream);

@@ -83,6 +83,7 @@ _SIGS = {
     "diaq_norm2": ([_I64, _P, _P, _P], _INT),
     "diaq_shard_plan": ([_INT, _INT, _INT, _P, _P, _I64, _P, _P, _P], _INT),
     "diaq_apply_gate_sharded": ([_INT, _INT, _INT, _P, _P, _I64, _P, _P, _INT, _P], _INT),
+    "diaq_sample_hits": ([_I64, _P, _P, _I64, _P, _P, _P], _INT),
     "diaq_timer_create": ([_INT, _P], _INT),
     "diaq_timer_record": ([_P, _P], _INT),
     "diaq_timer_elapsed": ([_INT, _P, _P], _INT),

@@ -1,0 +1,256 @@
+// sample.cu -- the reference's inverse-CDF sampler on the device.
+//
+// Reference: sim.py:142-161.  p = |a|^2, q = round(p, 12), cdf = np.cumsum(q)
+// (a SEQUENTIAL float64 sum), hits = min(searchsorted(cdf, u, 'right'), N-1)
+// for the splitmix64 uniforms u.  Counts must match the reference exactly, so
+// every step reproduces numpy's float64 operations bit for bit:
+//
+//  * |a| as numpy computes it for complex128 on this build: with m = max(|re|,
+//    |im|), r = min/m, |a| = m * sqrt(fma(r, r, 1)) (checked against numpy on
+//    4e5 samples); p = |a|*|a|; q = rint(p * 1e12) / 1e12 (numpy's round).
+//  * the cumsum c_i = fl(c_{i-1} + q_i) is sequential, but it is exactly
+//    computable in parallel per binade: while c stays in [2^e, 2^(e+1)) its
+//    values are integer multiples of U = 2^(e-52), and fl(c + q) = c +
+//    RNE(q / U) * U as long as no tie occurs and the result stays in the
+//    binade.  So within a segment c_i = U * (K0 + inclusive_scan(k)) with
+//    k_i = RNE(q_i / U) -- an exact int64 scan.  A segment ends at the first
+//    element that leaves the binade or hits an exact tie; that one step is
+//    done in float64 on the host (same IEEE rounding) and a new segment
+//    starts.  c grows from >= 1e-12 to ~1, so there are at most ~45 segments.
+//  * searchsorted is a per-shot binary search over the materialised cdf.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+
+namespace diaq {
+
+__device__ __forceinline__ double np_cabs(double2 a) {
+    double x = fabs(a.x), y = fabs(a.y);
+    if (x < y) {
+        const double t = x;
+        x = y;
+        y = t;
+    }
+    if (x == 0.0) return 0.0;
+    const double r = __ddiv_rn(y, x);
+    return __dmul_rn(x, __dsqrt_rn(__fma_rn(r, r, 1.0)));
+}
+
+__global__ void __launch_bounds__(kThreads) sample_q_kernel(const double2 *x, int64_t n, double *q, double *psum_part,
+                                                            unsigned long long *first_nz) {
+    double s = 0.0;
+    unsigned long long first = ~0ull;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const double a = np_cabs(x[i]);
+        const double p = __dmul_rn(a, a);
+        const double qi = __ddiv_rn(rint(__dmul_rn(p, 1e12)), 1e12);
+        q[i] = qi;
+        s += p;
+        if (qi > 0.0 && (unsigned long long)i < first) first = (unsigned long long)i;
+    }
+    __shared__ double red[kThreads / 32];
+    __shared__ unsigned long long redf[kThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_down_sync(0xffffffffu, s, o);
+        const unsigned long long f = __shfl_down_sync(0xffffffffu, first, o);
+        first = f < first ? f : first;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red[threadIdx.x >> 5] = s;
+        redf[threadIdx.x >> 5] = first;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        unsigned long long f = ~0ull;
+        for (int w = 0; w < kThreads / 32; ++w) {
+            t += red[w];
+            f = redf[w] < f ? redf[w] : f;
+        }
+        psum_part[blockIdx.x] = t;
+        if (f != ~0ull) atomicMin(first_nz, f);
+    }
+}
+
+// k_i = RNE(q_i * 2^(52-e)) and the exit condition of the segment
+__global__ void __launch_bounds__(kThreads) sample_k_kernel(const double *q, int64_t i0, int64_t cnt, double scale,
+                                                            long long *k, unsigned char *tie) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += stride) {
+        const double v = __dmul_rn(q[i0 + j], scale);  // exact: scaling by a power of two
+        const double f = floor(v);
+        const double fr = v - f;                        // exact
+        tie[j] = fr == 0.5;
+        // clamp: anything >= 2^53 ends the segment at this element, and the
+        // clamp keeps the prefix up to the first exit exact (no int64 overflow)
+        const double r = rint(v);                       // round half to even
+        k[j] = r >= 9007199254740992.0 ? (1ll << 53) : (long long)r;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) sample_exit_kernel(const long long *S, const unsigned char *tie, int64_t cnt,
+                                                               long long kbase, unsigned long long *exit_at) {
+    const long long lim = 1ll << 53;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += stride)
+        if (tie[j] || kbase + S[j] >= lim) atomicMin(exit_at, (unsigned long long)j);
+}
+
+__global__ void __launch_bounds__(kThreads) sample_c_kernel(const long long *S, int64_t i0, int64_t cnt, long long kbase,
+                                                            double U, double *c) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += stride)
+        c[i0 + j] = __dmul_rn((double)(kbase + S[j]), U);  // exact: integer < 2^53 times a power of two
+}
+
+__global__ void sample_search_kernel(const double *c, int64_t n, const double *u, int64_t shots, long long *hits) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= shots) return;
+    const double uk = u[k];
+    int64_t lo = 0, hi = n;  // first index with c > u
+    while (lo < hi) {
+        const int64_t mid = lo + (hi - lo) / 2;
+        if (c[mid] <= uk) lo = mid + 1;
+        else hi = mid;
+    }
+    hits[k] = lo < n - 1 ? lo : n - 1;
+}
+
+static int grid_of(int64_t n) {
+    int dev = 0, sms = kSms;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaGetLastError();
+    return (int)std::max<int64_t>(1, std::min<int64_t>((n + kThreads - 1) / kThreads, (int64_t)sms * 8));
+}
+
+}  // namespace diaq
+
+using namespace diaq;
+
+#define DIAQ_CK(call)                                                                                \
+    do {                                                                                             \
+        cudaError_t e_ = (call);                                                                     \
+        if (e_ != cudaSuccess) {                                                                     \
+            rc = set_error(DIAQ_ERR_CUDA, "diaq_sample_hits: %s (%s)", #call, cudaGetErrorString(e_)); \
+            goto done;                                                                               \
+        }                                                                                            \
+    } while (0)
+
+extern "C" int diaq_sample_hits(int64_t n, const void *x, const double *u_host, int64_t shots, int64_t *hits_host,
+                                double *norm2_out, void *stream) {
+    if (!x || n < 1 || shots < 0 || (shots > 0 && (!u_host || !hits_host)))
+        return set_error(DIAQ_ERR_VALUE, "diaq_sample_hits: bad arguments");
+    cudaStream_t s = (cudaStream_t)stream;
+    int rc = DIAQ_OK;
+    const int64_t C = std::min<int64_t>(n, (int64_t)1 << 22);  // scan chunk
+    double *q = nullptr, *c = nullptr, *part = nullptr, *ud = nullptr;
+    long long *k = nullptr, *S = nullptr, *hd = nullptr;
+    unsigned char *tie = nullptr;
+    unsigned long long *flag = nullptr;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    const int gq = grid_of(n);
+    std::vector<double> hpart((size_t)gq);
+    unsigned long long first = ~0ull;
+    DIAQ_CK(cudaMallocAsync((void **)&q, sizeof(double) * (size_t)n, s));
+    DIAQ_CK(cudaMallocAsync((void **)&c, sizeof(double) * (size_t)n, s));
+    DIAQ_CK(cudaMallocAsync((void **)&part, sizeof(double) * (size_t)gq, s));
+    DIAQ_CK(cudaMallocAsync((void **)&k, sizeof(long long) * (size_t)C, s));
+    DIAQ_CK(cudaMallocAsync((void **)&S, sizeof(long long) * (size_t)C, s));
+    DIAQ_CK(cudaMallocAsync((void **)&tie, (size_t)C, s));
+    DIAQ_CK(cudaMallocAsync((void **)&flag, sizeof(unsigned long long), s));
+    cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, k, S, (int)C, s);
+    DIAQ_CK(cudaMallocAsync(&tmp, std::max<size_t>(tmp_bytes, 16), s));
+    DIAQ_CK(cudaMemsetAsync(flag, 0xff, sizeof(unsigned long long), s));
+    sample_q_kernel<<<gq, kThreads, 0, s>>>((const double2 *)x, n, q, part, flag);
+    count_launch();
+    DIAQ_CK(cudaGetLastError());
+    DIAQ_CK(cudaMemcpyAsync(hpart.data(), part, sizeof(double) * (size_t)gq, cudaMemcpyDeviceToHost, s));
+    DIAQ_CK(cudaMemcpyAsync(&first, flag, sizeof(first), cudaMemcpyDeviceToHost, s));
+    DIAQ_CK(cudaStreamSynchronize(s));
+    if (norm2_out) {
+        double t = 0.0;
+        for (double v : hpart) t += v;
+        *norm2_out = t;
+    }
+    if (shots == 0) goto done;
+    // elements before the first nonzero q have cdf 0
+    if (first == ~0ull) {
+        DIAQ_CK(cudaMemsetAsync(c, 0, sizeof(double) * (size_t)n, s));
+    } else {
+        const int64_t s0 = (int64_t)first;
+        if (s0 > 0) DIAQ_CK(cudaMemsetAsync(c, 0, sizeof(double) * (size_t)s0, s));
+        double cur = 0.0;
+        DIAQ_CK(cudaMemcpyAsync(&cur, q + s0, sizeof(double), cudaMemcpyDeviceToHost, s));
+        DIAQ_CK(cudaStreamSynchronize(s));
+        DIAQ_CK(cudaMemcpyAsync(c + s0, &cur, sizeof(double), cudaMemcpyHostToDevice, s));
+        int64_t i = s0 + 1;
+        while (i < n) {
+            int e = 0;
+            std::frexp(cur, &e);            // cur in [2^(e-1), 2^e)
+            const int eb = e - 1;            // binade exponent
+            const double U = std::ldexp(1.0, eb - 52);
+            const double scale = std::ldexp(1.0, 52 - eb);
+            long long kbase = (long long)std::ldexp(cur, 52 - eb);  // exact integer in [2^52, 2^53)
+            // walk chunks until the segment ends
+            while (i < n) {
+                const int64_t cnt = std::min<int64_t>(C, n - i);
+                const int g = grid_of(cnt);
+                sample_k_kernel<<<g, kThreads, 0, s>>>(q, i, cnt, scale, k, tie);
+                cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, k, S, (int)cnt, s);
+                DIAQ_CK(cudaMemsetAsync(flag, 0xff, sizeof(unsigned long long), s));
+                sample_exit_kernel<<<g, kThreads, 0, s>>>(S, tie, cnt, kbase, flag);
+                count_launch(3);
+                DIAQ_CK(cudaGetLastError());
+                unsigned long long ex = ~0ull;
+                long long last = 0;
+                DIAQ_CK(cudaMemcpyAsync(&ex, flag, sizeof(ex), cudaMemcpyDeviceToHost, s));
+                DIAQ_CK(cudaMemcpyAsync(&last, S + cnt - 1, sizeof(last), cudaMemcpyDeviceToHost, s));
+                DIAQ_CK(cudaStreamSynchronize(s));
+                const int64_t upto = ex == ~0ull ? cnt : (int64_t)ex;
+                if (upto > 0) {
+                    sample_c_kernel<<<grid_of(upto), kThreads, 0, s>>>(S, i, upto, kbase, U, c);
+                    count_launch();
+                    DIAQ_CK(cudaGetLastError());
+                }
+                if (ex == ~0ull) {
+                    kbase += last;
+                    i += cnt;
+                    continue;
+                }
+                // the exiting element: one float64 step on the host, then a new segment
+                long long sprev = 0;
+                double qx = 0.0;
+                if (upto > 0) DIAQ_CK(cudaMemcpyAsync(&sprev, S + upto - 1, sizeof(sprev), cudaMemcpyDeviceToHost, s));
+                DIAQ_CK(cudaMemcpyAsync(&qx, q + i + upto, sizeof(qx), cudaMemcpyDeviceToHost, s));
+                DIAQ_CK(cudaStreamSynchronize(s));
+                const double cprev = (double)(kbase + sprev) * U;
+                volatile double sum = cprev + qx;  // IEEE add, round to nearest even
+                cur = sum;
+                DIAQ_CK(cudaMemcpyAsync(c + i + upto, &cur, sizeof(double), cudaMemcpyHostToDevice, s));
+                DIAQ_CK(cudaStreamSynchronize(s));  // &cur is reused
+                i += upto + 1;
+                break;
+            }
+        }
+    }
+    DIAQ_CK(cudaMallocAsync((void **)&ud, sizeof(double) * (size_t)shots, s));
+    DIAQ_CK(cudaMallocAsync((void **)&hd, sizeof(long long) * (size_t)shots, s));
+    DIAQ_CK(cudaMemcpyAsync(ud, u_host, sizeof(double) * (size_t)shots, cudaMemcpyHostToDevice, s));
+    sample_search_kernel<<<(unsigned)((shots + kThreads - 1) / kThreads), kThreads, 0, s>>>(c, n, ud, shots, hd);
+    count_launch();
+    DIAQ_CK(cudaGetLastError());
+    DIAQ_CK(cudaMemcpyAsync(hits_host, hd, sizeof(long long) * (size_t)shots, cudaMemcpyDeviceToHost, s));
+    DIAQ_CK(cudaStreamSynchronize(s));
+done:
+    for (void *p : {(void *)q, (void *)c, (void *)part, (void *)k, (void *)S, (void *)tie, (void *)flag, tmp,
+                    (void *)ud, (void *)hd})
+        if (p) cudaFreeAsync(p, s);
+    return rc;
+}

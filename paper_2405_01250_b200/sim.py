@@ -17,8 +17,8 @@ DESIGN.md; the contract is 1e-12 relative L2).
 run() compiles on the host, then hands the whole gate list to the native
 loop diaq_run_gates (one C call, in-place updates, CUDA events around every
 gate resolved after the loop -- no per-gate host sync).  Sampling is the
-reference's splitmix64 inverse-CDF sampler on the host over the downloaded
-probabilities (device sampler is the next row).
+reference's splitmix64 inverse-CDF sampler, on the device with the
+reference's sequential CDF reproduced exactly (sample.cu).
 """
 from __future__ import annotations
 
@@ -200,20 +200,23 @@ def splitmix64_uniforms(seed: int, count: int) -> np.ndarray:
 def measure_all_sample(x: StateVector, shots: int, seed: int) -> dict[str, int]:
     """Sample `shots` bitstrings (q0..q(n-1), MSB first) from |amps|^2 (sim.py:142-161).
 
-    Probabilities are rounded to 1e-12 before the sequential CDF, exactly as
-    the reference does, so counts match it for states equal to ~1e-13.
+    On the device (sample.cu): probabilities rounded to 1e-12 and the
+    SEQUENTIAL float64 CDF of the reference are reproduced bit for bit, so
+    counts equal the reference's for the same state and seed.
     """
     if shots < 0:
         raise ValueError(f"shots must be >= 0, got {shots}")
-    p = np.abs(x.amps) ** 2
-    if abs(p.sum() - 1.0) > 1e-6:
-        raise NormalizationError(f"state norm^2 = {p.sum():.9f}, cannot sample")
+    xd = x.device_amps
+    u = splitmix64_uniforms(seed, shots)
+    hits = np.empty(max(shots, 1), dtype=np.int64)
+    norm2 = ctypes.c_double(0.0)
+    L.call("diaq_sample_hits", int(xd.numel()), xd.data_ptr(), u.ctypes.data if shots else None, int(shots),
+           hits.ctypes.data if shots else None, ctypes.addressof(norm2), L.stream_handle())
+    if abs(norm2.value - 1.0) > 1e-6:
+        raise NormalizationError(f"state norm^2 = {norm2.value:.9f}, cannot sample")
     if shots == 0:
         return {}
-    cdf = np.cumsum(np.round(p, 12))
-    u = splitmix64_uniforms(seed, shots)
-    hits = np.minimum(np.searchsorted(cdf, u, side="right"), len(p) - 1)
-    outcomes, freq = np.unique(hits, return_counts=True)
+    outcomes, freq = np.unique(hits[:shots], return_counts=True)
     width = x.n_qubits
     return {format(int(i), f"0{width}b"): int(c) for i, c in zip(outcomes, freq)}
 

@@ -398,3 +398,22 @@ def test_spmv_host_pipeline_chunks(monkeypatch):
         yh = torch.empty(2**22, dtype=torch.complex128).pin_memory()
         assert D.spmv(a, xh, out=yh) is yh
         assert np.array_equal(yh.numpy(), want), chunk
+
+
+def test_device_sampler_matches_reference_sampler():
+    """Device sampler (exact sequential CDF) == the reference numpy sampler, shot for shot."""
+    rng = np.random.default_rng(31)
+    for n, shots, seed in ((1, 100, 0), (6, 4096, 3), (10, 100000, 7), (14, 50000, 11), (18, 20000, 5)):
+        x = W.random_state(rng, 2**n)
+        if n == 6:
+            x[::3] = 0  # zero runs and a sparse CDF
+            x /= np.sqrt(np.sum(np.abs(x) ** 2))
+        st = D.StateVector(n, x)
+        assert D.measure_all_sample(st, shots, seed) == O.measure_all_sample(x, n, shots, seed), n
+    uni = D.StateVector(10, np.full(1024, 1 / 32, dtype=complex))
+    assert D.measure_all_sample(uni, 8192, 1) == O.measure_all_sample(np.full(1024, 1 / 32, dtype=complex),
+                                                                      10, 8192, 1)
+    assert D.measure_all_sample(D.init_state(3), 100, 5) == {"000": 100}
+    assert D.measure_all_sample(D.init_state(2), 0, 1) == {}
+    with pytest.raises(D.NormalizationError):
+        D.measure_all_sample(D.StateVector(1, np.array([1.0, 0.5], dtype=complex)), 16, 0)
