@@ -36,8 +36,8 @@ constexpr int kThreadBits = 8;      // 256 threads
 constexpr int kLowBits = 3;         // tile rows are 2^3 amplitudes = 128 B
 constexpr int kMaxRegKin = 1;       // mixing operands applied in registers (wider: own pass)
 constexpr int kMaxSel = 4;          // selector (non-mixing) operands
-constexpr int kMaxPassGates = 96;   // gate records staged in smem per pass
-constexpr int kMaxPhases = 32;
+constexpr int kMaxPassGates = 48;   // gate records staged in smem per pass
+constexpr int kMaxPhases = 24;
 
 static_assert(kThreads == (1 << kThreadBits), "thread layout");
 
@@ -111,11 +111,17 @@ __device__ __forceinline__ void dense1(double2 (&v)[8], const double2 *c, uint32
         const int j0 = ((g >> B1) << (B1 + 1)) | (g & ((1 << B1) - 1));
         const int j1 = j0 | (1 << B1);
         const double2 x0 = v[j0], x1 = v[j1];
-        double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
-        if (n0 & 1u) a0 = cadd(a0, cmul<MODE>(c00, x0));
-        if (n0 & 2u) a0 = cadd(a0, cmul<MODE>(c01, x1));
-        if (n1 & 1u) a1 = cadd(a1, cmul<MODE>(c10, x0));
-        if (n1 & 2u) a1 = cadd(a1, cmul<MODE>(c11, x1));
+        // acc starts at +0; +0 + t == t except for the sign of an exact zero,
+        // so the first term is taken as is (values unchanged, one add saved)
+        double2 a0, a1;
+        if ((n0 & 3u) == 3u) a0 = cadd(cmul<MODE>(c00, x0), cmul<MODE>(c01, x1));
+        else if (n0 & 1u) a0 = cmul<MODE>(c00, x0);
+        else if (n0 & 2u) a0 = cmul<MODE>(c01, x1);
+        else a0 = make_double2(0.0, 0.0);
+        if ((n1 & 3u) == 3u) a1 = cadd(cmul<MODE>(c10, x0), cmul<MODE>(c11, x1));
+        else if (n1 & 1u) a1 = cmul<MODE>(c10, x0);
+        else if (n1 & 2u) a1 = cmul<MODE>(c11, x1);
+        else a1 = make_double2(0.0, 0.0);
         v[j0] = a0;
         v[j1] = a1;
     }
@@ -128,7 +134,7 @@ __device__ __forceinline__ void diag_reg(double2 (&v)[8], double2 d0, double2 d1
         const bool hi = (j >> RB) & 1;
         const double2 d = hi ? d1 : d0;
         const bool nz = hi ? (z1 & 1u) : (z0 & 1u);
-        v[j] = nz ? cadd(make_double2(0.0, 0.0), cmul<MODE>(d, v[j])) : make_double2(0.0, 0.0);
+        v[j] = nz ? cmul<MODE>(d, v[j]) : make_double2(0.0, 0.0);
     }
 }
 
@@ -187,8 +193,7 @@ __device__ __forceinline__ void dispatch_gate(double2 (&v)[1 << R], const RegGat
                 const double2 d = b ? d1 : d0;
                 const bool nz = b ? (z1 & 1u) : (z0 & 1u);
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    v[j] = nz ? cadd(make_double2(0.0, 0.0), cmul<MODE>(d, v[j])) : make_double2(0.0, 0.0);
+                for (int j = 0; j < 8; ++j) v[j] = nz ? cmul<MODE>(d, v[j]) : make_double2(0.0, 0.0);
             }
             return;
         }
@@ -251,7 +256,7 @@ __device__ __forceinline__ void smem_gate(double2 *tile, int T, const RegGate &G
 }
 
 template <int R, int MODE>
-__global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(const __grid_constant__ TileParams p) {
+__global__ void __launch_bounds__(kThreads, 3) tile_pass_kernel(const __grid_constant__ TileParams p) {
     extern __shared__ double2 tile[];
     __shared__ uint64_t hi_off[(1 << kMaxTileBits) >> kLowBits];
     __shared__ Phase sph[kMaxPhases];
