@@ -170,6 +170,11 @@ int diaq_shard_plan(int n_bits, int local_bits, int k, const double *g_host, con
                     int64_t rank, uint32_t *need_mask, int *n_global, uint32_t *own_block);
 int diaq_apply_gate_sharded(int n_bits, int local_bits, int k, const double *g_host, const int *shifts,
                             int64_t rank, const void *const *srcs, void *y, int cmul_mode, void *stream);
+/* diaq_run_gates_fused on one rank's shard for a run of gates that need no
+ * partner data (every mixing operand local; selectors may be global bits,
+ * read from `rank`).  Shifts are in the full n_bits index space. */
+int diaq_run_gates_local(int n_bits, int local_bits, int64_t rank, int ngates, const diaq_gate_t *gates,
+                         void *shard, int cmul_mode, int tile_bits, void **events, int *npasses, void *stream);
 
 /* ---- sampling (reference measure_all_sample, sim.py:142-161) -------------
  * hits[k] = min(#{i : cdf_i <= u_k}, N-1) with cdf = sequential float64

@@ -444,6 +444,27 @@ extern "C" int diaq_norm2(int64_t n_amps, const void *x, double *work_dev, void 
     return check_launch("norm2");
 }
 
+namespace diaq {
+// a gate that reads only this rank's own block (no partner data needed)
+int apply_gate_sharded_own(int n_bits, int local_bits, int k, const double *g, const int *shifts, int64_t rank,
+                           void *shard, int cmul_mode, cudaStream_t s) {
+    ShardView v;
+    int rc = shard_view(n_bits, local_bits, k, g, shifts, rank, v);
+    if (rc) return rc;
+    if (v.kg == 0) return apply_gate(local_bits, k, g, shifts, shard, shard, cmul_mode, s);
+    if (v.need != (1u << v.vr)) return set_error(DIAQ_ERR_VALUE, "gate needs partner shards (need mask %u)", v.need);
+    const void *srcs[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    srcs[v.vr] = shard;
+#define DIAQ_MULTI(KL_, KG_) \
+    if (v.kl == KL_ && v.kg == KG_) return launch_multi<KL_, KG_>(v, local_bits, g, srcs, shard, cmul_mode, s);
+    DIAQ_MULTI(0, 1) DIAQ_MULTI(1, 1) DIAQ_MULTI(2, 1) DIAQ_MULTI(3, 1) DIAQ_MULTI(4, 1)
+    DIAQ_MULTI(0, 2) DIAQ_MULTI(1, 2) DIAQ_MULTI(2, 2) DIAQ_MULTI(3, 2)
+    DIAQ_MULTI(0, 3) DIAQ_MULTI(1, 3) DIAQ_MULTI(2, 3)
+#undef DIAQ_MULTI
+    return set_error(DIAQ_ERR_UNSUPPORTED, "sharded gate with %d local + %d global operands", v.kl, v.kg);
+}
+}  // namespace diaq
+
 extern "C" int diaq_shard_plan(int n_bits, int local_bits, int k, const double *g_host, const int *shifts,
                                int64_t rank, uint32_t *need_mask, int *n_global, uint32_t *own_block) {
     if (!g_host || !shifts || !need_mask) return set_error(DIAQ_ERR_VALUE, "diaq_shard_plan: null argument");

@@ -79,6 +79,7 @@ struct TileParams {
     const uint32_t *nz;
     const uint32_t *cls;
     int ncoef, nnz, ncls;
+    uint64_t gbase;           // sharded state: rank bits (rank << local_bits) for selector lookups
 };
 
 __device__ __forceinline__ uint32_t swz(uint32_t e) {
@@ -285,6 +286,7 @@ __global__ void __launch_bounds__(kThreads, 3) tile_pass_kernel(const __grid_con
     const int per_thread = (int)(tsize >> kThreadBits);
     for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
         const uint64_t base = insert_zero_bits_dyn((uint64_t)t, p.tb, T);
+        const uint64_t sbase = base | p.gbase;  // full-state index bits for selectors
         // HBM -> smem, coalesced (consecutive e are consecutive state indices in runs of 8)
         for (int k0 = 0; k0 < per_thread; k0 += 4) {
             double2 w[4];
@@ -304,7 +306,7 @@ __global__ void __launch_bounds__(kThreads, 3) tile_pass_kernel(const __grid_con
             const Phase &ph = sph[ph_i];
             if (ph.generic) {
                 for (int gi = ph.g0; gi < ph.g1; ++gi) {
-                    smem_gate<MODE>(tile, T, sg[gi], base, sc, snz);
+                    smem_gate<MODE>(tile, T, sg[gi], sbase, sc, snz);
                     __syncthreads();
                 }
                 continue;
@@ -314,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 3) tile_pass_kernel(const __grid_con
             double2 v[NR];
 #pragma unroll
             for (int j = 0; j < NR; ++j) v[j] = tile[swz(tpart | reg_spread<R>(j, ph.rpos))];
-            for (int gi = ph.g0; gi < ph.g1; ++gi) dispatch_gate<R, MODE>(v, sg[gi], tpart, base, sc, snz, scls);
+            for (int gi = ph.g0; gi < ph.g1; ++gi) dispatch_gate<R, MODE>(v, sg[gi], tpart, sbase, sc, snz, scls);
 #pragma unroll
             for (int j = 0; j < NR; ++j) tile[swz(tpart | reg_spread<R>(j, ph.rpos))] = v[j];
             __syncthreads();
@@ -495,7 +497,8 @@ static int pack_smem_gate(const diaq_gate_t &gt, const std::vector<int> &bits, P
 // union of its gates' mixing bits fits in R registers.  Gates that cannot
 // be applied in registers (more than 2 mixing or 4 selector operands)
 // become standalone single-gate passes (gate_kernel).
-static int schedule(int n_bits, int ngates, const diaq_gate_t *gates, int T, int R, std::vector<PassPlan> &plan) {
+static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gates, int T, int R,
+                    std::vector<PassPlan> &plan) {
     const int low = std::min(kLowBits, n_bits);
     std::vector<int> members;
     std::vector<char> inb(64, 0);
@@ -582,10 +585,16 @@ static int schedule(int n_bits, int ngates, const diaq_gate_t *gates, int T, int
         const uint32_t mix = mixing_mask(gt.k, gt.g);
         int kin = 0, kout = 0, add = 0;
         for (int j = 0; j < gt.k; ++j) {
-            if (gt.shifts[j] < 0 || gt.shifts[j] >= n_bits)
-                return set_error(DIAQ_ERR_SHAPE, "gate shift %d outside state of %d qubits", gt.shifts[j], n_bits);
-            if ((mix >> j) & 1u) { ++kin; add += inb[gt.shifts[j]] ? 0 : 1; }
-            else ++kout;
+            if (gt.shifts[j] < 0 || gt.shifts[j] >= n_total)
+                return set_error(DIAQ_ERR_SHAPE, "gate shift %d outside state of %d qubits", gt.shifts[j], n_total);
+            if ((mix >> j) & 1u) {
+                if (gt.shifts[j] >= n_bits)
+                    return set_error(DIAQ_ERR_VALUE, "gate mixes global bit %d: it needs the partner shard", gt.shifts[j]);
+                ++kin;
+                add += inb[gt.shifts[j]] ? 0 : 1;
+            } else {
+                ++kout;
+            }
         }
         if (kin > kMaxRegKin || kin > R || kout > kMaxSel) {  // standalone pass
             int rc = flush();
@@ -614,6 +623,8 @@ static int schedule(int n_bits, int ngates, const diaq_gate_t *gates, int T, int
 
 int apply_gate(int n_bits, int k, const double *g, const int *shifts, const void *x, void *y, int cmul_mode,
                cudaStream_t s);
+int apply_gate_sharded_own(int n_bits, int local_bits, int k, const double *g, const int *shifts, int64_t rank,
+                           void *shard, int cmul_mode, cudaStream_t s);
 
 static int sm_count_f() {
     int dev = 0, sms = kSms;
@@ -632,10 +643,11 @@ static const void *tile_kernel_ptr(int cmul_mode) {
 
 using namespace diaq;
 
-extern "C" int diaq_run_gates_fused(int n_bits, int ngates, const diaq_gate_t *gates, void *state, int cmul_mode,
-                                    int tile_bits, void **events, int *npasses, void *stream) {
+static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const diaq_gate_t *gates, void *state,
+                     int cmul_mode, int tile_bits, void **events, int *npasses, void *stream) {
     if (ngates < 0 || (ngates > 0 && !gates) || !state)
         return set_error(DIAQ_ERR_VALUE, "diaq_run_gates_fused: bad arguments");
+    const bool sharded = n_total > n_bits;
     cudaStream_t s = (cudaStream_t)stream;
     (void)tile_bits;
     const int T = kThreadBits + 3;  // R = 3 register bits x 256 threads (tile_bits > 0 selects this path)
@@ -644,9 +656,9 @@ extern "C" int diaq_run_gates_fused(int n_bits, int ngates, const diaq_gate_t *g
     std::vector<PassPlan> plan;
     int rc = DIAQ_OK;
     if (tiled) {
-        rc = schedule(n_bits, ngates, gates, T, R, plan);
+        rc = schedule(n_bits, n_total, ngates, gates, T, R, plan);
         if (rc) return rc;
-    } else {  // state smaller than a tile: gate by gate
+    } else {  // state smaller than a tile: gate by gate (standalone path below)
         for (int i = 0; i < ngates; ++i) {
             PassPlan ps;
             ps.members = {i};
@@ -696,7 +708,8 @@ extern "C" int diaq_run_gates_fused(int n_bits, int ngates, const diaq_gate_t *g
         const PassPlan &ps = plan[pi];
         if (ps.bits.empty() || ps.members.size() == 1) {
             const diaq_gate_t &gt = gates[ps.members[0]];
-            rc = apply_gate(n_bits, gt.k, gt.g, gt.shifts, state, state, cmul_mode, s);
+            if (sharded) rc = apply_gate_sharded_own(n_total, n_bits, gt.k, gt.g, gt.shifts, rank, state, cmul_mode, s);
+            else rc = apply_gate(n_bits, gt.k, gt.g, gt.shifts, state, state, cmul_mode, s);
         } else {
             TileParams p;
             p.x = (double2 *)state;
@@ -713,6 +726,7 @@ extern "C" int diaq_run_gates_fused(int n_bits, int ngates, const diaq_gate_t *g
             p.ncoef = (int)ps.pk.coef.size();
             p.nnz = (int)ps.pk.nz.size();
             p.ncls = (int)ps.pk.cls.size();
+            p.gbase = sharded ? ((uint64_t)rank << n_bits) : 0ull;
             const size_t smem = (sizeof(double2) << p.tbits) + sizeof(double2) * p.ncoef +
                                 sizeof(uint32_t) * (p.nnz + p.ncls);
             if (smem > smem_max) return set_error(DIAQ_ERR_VALUE, "fused pass tables exceed shared memory");
@@ -733,4 +747,16 @@ extern "C" int diaq_run_gates_fused(int n_bits, int ngates, const diaq_gate_t *g
     }
     if (dbuf) cudaFreeAsync(dbuf, s);
     return rc;
+}
+
+extern "C" int diaq_run_gates_fused(int n_bits, int ngates, const diaq_gate_t *gates, void *state, int cmul_mode,
+                                    int tile_bits, void **events, int *npasses, void *stream) {
+    return run_fused(n_bits, n_bits, 0, ngates, gates, state, cmul_mode, tile_bits, events, npasses, stream);
+}
+
+extern "C" int diaq_run_gates_local(int n_bits, int local_bits, int64_t rank, int ngates, const diaq_gate_t *gates,
+                                    void *shard, int cmul_mode, int tile_bits, void **events, int *npasses,
+                                    void *stream) {
+    if (local_bits < 1 || local_bits > n_bits) return set_error(DIAQ_ERR_SHAPE, "local_bits %d invalid", local_bits);
+    return run_fused(n_bits, local_bits, rank, ngates, gates, shard, cmul_mode, tile_bits, events, npasses, stream);
 }

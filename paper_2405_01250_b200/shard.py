@@ -172,15 +172,49 @@ class ShardedState:
             srcs[b] = self.local if src == me else self._recv[src]
         self.apply_fn(n, lb, g, shifts, me, srcs, self.local, cmul_mode)
 
+    def _needs_exchange(self, g, shifts) -> bool:
+        lb = self.local_bits
+        if all(s < lb for s in shifts):
+            return False
+        needs = exchange_schedule(self.n_qubits, lb, g, shifts, self.comm.world)
+        return any(src != r for r, nd in enumerate(needs) for src in nd.values())
+
     def apply_placements(self, placements: list[Placement], cmul_mode: int | None = None) -> None:
+        """Apply gates in order.  On the GPU every maximal run of gates that
+        needs no partner data (the same decision on every rank) goes through
+        one fused native call (diaq_run_gates_local: shared-memory multi-gate
+        passes, global-bit controls read from the rank index); cross-shard
+        gates exchange and use the multi-source kernel."""
         from . import sim
         mode = sim.CMUL_MODE if cmul_mode is None else cmul_mode
+        comps = []
         for p in placements:
             comp = p.compact()
             if comp is None:
                 raise ValueError(f"sharded apply needs compact placements, got {p!r}")
-            g, shifts = comp
+            comps.append(comp)
+        if self.apply_fn is not _cuda_apply or sim.FUSE_TILE_BITS <= 0:
+            for g, shifts in comps:
+                self.apply_gate(g, shifts, mode)
+            return
+        i = 0
+        while i < len(comps):
+            j = i
+            while j < len(comps) and not self._needs_exchange(*comps[j]):
+                j += 1
+            if j > i:
+                run = comps[i:j]
+                prog = sim._GateProgram(run)
+                L.call("diaq_run_gates_local", self.n_qubits, self.local_bits, self.comm.rank, prog.n, prog.arr,
+                       self.local.data_ptr(), int(mode), int(sim.FUSE_TILE_BITS), None, None, L.stream_handle())
+                self.stats["gates"] += len(run)
+                self.stats["local"] += sum(all(s < self.local_bits for s in sh) for _, sh in run)
+                self.stats["no_comm_global"] += sum(not all(s < self.local_bits for s in sh) for _, sh in run)
+                i = j
+                continue
+            g, shifts = comps[i]
             self.apply_gate(g, shifts, mode)
+            i += 1
 
     def norm(self) -> float:
         """||psi|| over all ranks (all-reduce of local |x|^2)."""
@@ -225,19 +259,43 @@ def run_emulated(n_qubits: int, world: int, placements: list[Placement], cmul_mo
         states.append(ShardedState.basis(n_qubits, c, device=device))
     lb = states[0].local_bits
     stats = {"gates": 0, "local": 0, "no_comm_global": 0, "exchanged": 0}
-    for p in placements:
-        g, shifts = p.compact()
-        stats["gates"] += 1
+    comps = [p.compact() for p in placements]
+    fuse = sim.FUSE_TILE_BITS > 0
+
+    def crosses(g, shifts):
         if all(s < lb for s in shifts):
+            return False, None
+        needs = exchange_schedule(n_qubits, lb, g, shifts, world)
+        return any(src != r for r in range(world) for src in needs[r].values()), needs
+
+    i = 0
+    while i < len(comps):
+        if fuse:
+            j = i
+            while j < len(comps) and not crosses(*comps[j])[0]:
+                j += 1
+            if j > i:
+                prog = sim._GateProgram(comps[i:j])
+                for r in range(world):
+                    L.call("diaq_run_gates_local", n_qubits, lb, r, prog.n, prog.arr, states[r].local.data_ptr(),
+                           int(mode), int(sim.FUSE_TILE_BITS), None, None, L.stream_handle())
+                for g, shifts in comps[i:j]:
+                    stats["gates"] += 1
+                    stats["local" if all(s < lb for s in shifts) else "no_comm_global"] += 1
+                i = j
+                continue
+        g, shifts = comps[i]
+        stats["gates"] += 1
+        cross, needs = crosses(g, shifts)
+        if needs is None:
             stats["local"] += 1
             for r in range(world):
                 _cuda_apply(n_qubits, lb, g, shifts, r, [states[r].local], states[r].local, mode)
+            i += 1
             continue
-        needs = exchange_schedule(n_qubits, lb, g, shifts, world)
-        crosses = any(src != r for r in range(world) for src in needs[r].values())
-        stats["exchanged" if crosses else "no_comm_global"] += 1
+        stats["exchanged" if cross else "no_comm_global"] += 1
         snap = {}
-        if crosses:  # partner data as it was before this gate
+        if cross:  # partner data as it was before this gate
             for r in range(world):
                 for src in needs[r].values():
                     if src != r and src not in snap:
@@ -248,4 +306,5 @@ def run_emulated(n_qubits: int, world: int, placements: list[Placement], cmul_mo
             for b, src in needs[r].items():
                 srcs[b] = states[r].local if src == r else snap[src]
             _cuda_apply(n_qubits, lb, g, shifts, r, srcs, states[r].local, mode)
+        i += 1
     return [s.local for s in states], stats

@@ -22,6 +22,14 @@ def cmul(configs):
     return L.CMUL_FMA if configs["meta"]["numpy_cmul"] == "fma" else L.CMUL_PLAIN
 
 
+@pytest.fixture(params=[0, 11], ids=["gate-by-gate", "fused"], autouse=True)
+def fuse_mode(request):
+    old = D.sim.FUSE_TILE_BITS
+    D.sim.FUSE_TILE_BITS = request.param
+    yield request.param
+    D.sim.FUSE_TILE_BITS = old
+
+
 def _full(shards):
     import torch
     return torch.cat(shards).cpu().numpy()
