@@ -61,6 +61,42 @@ spgemm_kernel(const double2 *__restrict__ av, const double2 *__restrict__ bv, do
     }
 }
 
+// small plans travel in the kernel parameters (no H2D copy, no stream sync)
+constexpr int kParamCands = 128;
+constexpr int kParamPairs = 512;
+
+struct SgParamPlan {
+    SgCand cands[kParamCands];
+    SgPair pairs[kParamPairs];
+};
+
+__global__ void __launch_bounds__(kThreads)
+spgemm_kernel_param(const double2 *__restrict__ av, const double2 *__restrict__ bv, double2 *cv,
+                    const __grid_constant__ SgParamPlan plan, uint8_t *keep, double prune_eps) {
+    const SgCand &cd = plan.cands[blockIdx.y];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t len_round = (cd.len + 31) & ~31ll;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < len_round; k += stride) {
+        const bool live = k < cd.len;
+        double2 acc = make_double2(0.0, 0.0);
+        if (live) {
+            const int64_t i = cd.row_lo + k;
+            for (int q = cd.pbeg; q < cd.pend; ++q) {
+                const SgPair &pr = plan.pairs[q];
+                if (i >= pr.lo && i < pr.hi) {
+                    const double2 a = ld_reuse(av + pr.a_row0 + i);
+                    const double2 b = ld_reuse(bv + pr.b_row0 + i);
+                    acc = cadd(acc, cmul_plain(a, b));
+                }
+            }
+            st_stream(cv + cd.c_row0 + cd.row_lo + k, acc);
+        }
+        const bool big = live && (fabs(acc.x) + fabs(acc.y) > prune_eps);
+        const unsigned any = __ballot_sync(0xffffffffu, big);
+        if (any && (threadIdx.x & 31) == 0) keep[blockIdx.y] = 1;
+    }
+}
+
 struct Plan {
     std::vector<int64_t> offc;
     std::vector<std::vector<std::pair<int64_t, int64_t>>> pairs;  // (ia, ib) per candidate
@@ -150,6 +186,22 @@ extern "C" int diaq_spgemm(const diaq_matrix_t *a, const diaq_matrix_t *b, diaq_
         cd.pend = (int32_t)hp.size();
         maxlen = std::max(maxlen, cd.len);
     }
+    int dev = 0, sms = kSms;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaMemsetAsync(keep_dev, 0, (size_t)c->nd, s) != cudaSuccess)
+        return set_error(DIAQ_ERR_CUDA, "diaq_spgemm: memset failed");
+    const int64_t want = (maxlen + kThreads - 1) / kThreads;
+    const int64_t cap = std::max<int64_t>(1, (int64_t)sms * 8 / (int64_t)hc.size());
+    if ((int)hc.size() <= kParamCands && (int)hp.size() <= kParamPairs) {
+        static thread_local SgParamPlan pp;  // host staging of the by-value kernel argument
+        std::copy(hc.begin(), hc.end(), pp.cands);
+        std::copy(hp.begin(), hp.end(), pp.pairs);
+        dim3 grid((unsigned)std::max<int64_t>(1, std::min(want, cap)), (unsigned)hc.size());
+        spgemm_kernel_param<<<grid, kThreads, 0, s>>>((const double2 *)a->vals, (const double2 *)b->vals,
+                                                       (double2 *)c->vals, pp, keep_dev, prune_eps);
+        count_launch();
+        return check_launch("spgemm_kernel_param");
+    }
     const size_t need = sizeof(SgPair) * hp.size() + sizeof(SgCand) * hc.size();
     if (!workspace || workspace_bytes < (int64_t)need)
         return set_error(DIAQ_ERR_VALUE, "diaq_spgemm: workspace too small (%zu bytes needed)", need);
@@ -159,12 +211,6 @@ extern "C" int diaq_spgemm(const diaq_matrix_t *a, const diaq_matrix_t *b, diaq_
     if (cudaMemcpyAsync(dcands, hc.data(), sizeof(SgCand) * hc.size(), cudaMemcpyHostToDevice, s) != cudaSuccess ||
         cudaMemcpyAsync(dpairs, hp.data(), sizeof(SgPair) * hp.size(), cudaMemcpyHostToDevice, s) != cudaSuccess)
         return set_error(DIAQ_ERR_CUDA, "diaq_spgemm: plan upload failed");
-    if (cudaMemsetAsync(keep_dev, 0, (size_t)c->nd, s) != cudaSuccess)
-        return set_error(DIAQ_ERR_CUDA, "diaq_spgemm: memset failed");
-    int dev = 0, sms = kSms;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t want = (maxlen + kThreads - 1) / kThreads;
-    const int64_t cap = std::max<int64_t>(1, (int64_t)sms * 8 / (int64_t)hc.size());
     for (int64_t base = 0; base < (int64_t)hc.size(); base += 65535) {
         const int cnt = (int)std::min<int64_t>(65535, (int64_t)hc.size() - base);
         dim3 grid((unsigned)std::max<int64_t>(1, std::min(want, cap)), cnt);
