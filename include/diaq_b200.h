@@ -117,7 +117,9 @@ int diaq_spmv_host(const diaq_matrix_t *a, const void *x_host, void *y_host, voi
  * plan (host): candidate result offsets (sorted), nc <= nda*ndb. */
 int diaq_spgemm_plan(int64_t n, int64_t nda, const int64_t *offa, int64_t ndb, const int64_t *offb,
                      int64_t *offc, int64_t *nc);
-/* device workspace bytes needed by diaq_spgemm for these operands */
+/* device workspace bytes needed by diaq_spgemm for these operands (plans with
+ * <= 128 candidates and <= 512 pairs travel in the kernel parameters; the
+ * workspace may then be NULL) */
 int64_t diaq_spgemm_workspace(int64_t nda, int64_t ndb, int64_t nc);
 /* multiply into the candidate layout `c` and flag keep_dev[i] = 1 iff
  * candidate i has an element with |re|+|im| > prune_eps (matrix.py:246-249) */

@@ -287,13 +287,16 @@ def _spgemm(a: DiaqMatrix, b: DiaqMatrix, prune_eps: float):
     if len(offc) == 0:
         return offc, np.zeros(0, np.uint8), cvals, starts
     keep = t.empty(len(offc), dtype=t.uint8, device=cvals.device)
-    ws_bytes = int(L.load().diaq_spgemm_workspace(len(da.offs), len(db.offs), len(offc)))
-    ws = t.empty(ws_bytes, dtype=t.uint8, device=cvals.device)
+    if len(offc) <= 128 and len(da.offs) * len(db.offs) <= 512:
+        ws, ws_bytes = None, 0  # the plan travels in the kernel parameters
+    else:
+        ws_bytes = int(L.load().diaq_spgemm_workspace(len(da.offs), len(db.offs), len(offc)))
+        ws = t.empty(ws_bytes, dtype=t.uint8, device=cvals.device)
     sa = L.mat_struct(n, da.offs, da.starts, da.vals)
     sb = L.mat_struct(n, db.offs, db.starts, db.vals)
     sc = L.mat_struct(n, offc, starts, cvals)
     L.call("diaq_spgemm", ctypes.byref(sa), ctypes.byref(sb), ctypes.byref(sc), keep.data_ptr(),
-           float(prune_eps), ws.data_ptr(), ws_bytes, L.stream_handle())
+           float(prune_eps), ws.data_ptr() if ws is not None else None, ws_bytes, L.stream_handle())
     return offc, keep.cpu().numpy(), cvals, starts
 
 

@@ -417,3 +417,18 @@ def test_device_sampler_matches_reference_sampler():
     assert D.measure_all_sample(D.init_state(2), 0, 1) == {}
     with pytest.raises(D.NormalizationError):
         D.measure_all_sample(D.StateVector(1, np.array([1.0, 0.5], dtype=complex)), 16, 0)
+
+
+def test_spgemm_large_plan_and_offsets():
+    """Plans beyond the by-value limit (>512 pairs) use the device-table kernel; bitwise."""
+    rng = np.random.default_rng(17)
+    for n, band in ((48, 24), (64, 40)):
+        m1 = rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))
+        m2 = rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))
+        mask = np.abs(np.subtract.outer(np.arange(n), np.arange(n))) > band
+        m1[mask] = 0
+        m2[mask] = 0
+        c = D.matmul(D.from_dense(m1, 0.0), D.from_dense(m2, 0.0))
+        oc = O.matmul(O.from_dense(m1), O.from_dense(m2))
+        assert c.diag_indices() == oc.offs.tolist()
+        assert np.array_equal(values(c), np.concatenate([r + 1j * i for r, i in (oc.diag(d) for d in oc.offs)]))
