@@ -500,6 +500,8 @@ static int pack_smem_gate(const diaq_gate_t &gt, const std::vector<int> &bits, P
 static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gates, int T, int R,
                     std::vector<PassPlan> &plan) {
     const int low = std::min(kLowBits, n_bits);
+    std::vector<char> fast((size_t)ngates);  // register fast-path classification, once per gate
+    for (int i = 0; i < ngates; ++i) fast[(size_t)i] = (gates[i].k >= 1 && gates[i].k <= 5) ? fast_op(gates[i]) : 0;
     std::vector<int> members;
     std::vector<char> inb(64, 0);
     int nb = 0;
@@ -520,7 +522,7 @@ static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gate
         ps.members = members;
         size_t i = 0;
         while (i < members.size()) {
-            if (!fast_op(gates[members[i]])) {  // cold path: its own shared-memory phase
+            if (!fast[(size_t)members[i]]) {  // cold path: its own shared-memory phase
                 Phase ph;
                 memset(&ph, 0, sizeof(ph));
                 ph.generic = 1;
@@ -538,7 +540,7 @@ static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gate
             size_t j = i;
             while (j < members.size()) {
                 const diaq_gate_t &gt = gates[members[j]];
-                if (!fast_op(gt)) break;
+                if (!fast[(size_t)members[j]]) break;
                 const uint32_t mix = mixing_mask(gt.k, gt.g);
                 std::vector<int> add;
                 for (int o = 0; o < gt.k; ++o)
