@@ -104,11 +104,11 @@ __device__ __forceinline__ uint32_t reg_spread(int j, const int *rpos) {
 
 // ---- fast paths (R = 3 register bits) --------------------------------------
 
-template <int B1, int MODE>
-__device__ __forceinline__ void dense1(double2 (&v)[8], const double2 *c, uint32_t n0, uint32_t n1) {
+template <int R, int B1, int MODE>
+__device__ __forceinline__ void dense1(double2 (&v)[1 << R], const double2 *c, uint32_t n0, uint32_t n1) {
     const double2 c00 = c[0], c01 = c[1], c10 = c[2], c11 = c[3];
 #pragma unroll
-    for (int g = 0; g < 4; ++g) {
+    for (int g = 0; g < (1 << (R - 1)); ++g) {
         const int j0 = ((g >> B1) << (B1 + 1)) | (g & ((1 << B1) - 1));
         const int j1 = j0 | (1 << B1);
         const double2 x0 = v[j0], x1 = v[j1];
@@ -128,10 +128,10 @@ __device__ __forceinline__ void dense1(double2 (&v)[8], const double2 *c, uint32
     }
 }
 
-template <int RB, int MODE>
-__device__ __forceinline__ void diag_reg(double2 (&v)[8], double2 d0, double2 d1, uint32_t z0, uint32_t z1) {
+template <int R, int RB, int MODE>
+__device__ __forceinline__ void diag_reg(double2 (&v)[1 << R], double2 d0, double2 d1, uint32_t z0, uint32_t z1) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < (1 << R); ++j) {
         const bool hi = (j >> RB) & 1;
         const double2 d = hi ? d1 : d0;
         const bool nz = hi ? (z1 & 1u) : (z0 & 1u);
@@ -139,10 +139,10 @@ __device__ __forceinline__ void diag_reg(double2 (&v)[8], double2 d0, double2 d1
     }
 }
 
-template <int B1>
-__device__ __forceinline__ void swap_all(double2 (&v)[8]) {
+template <int R, int B1>
+__device__ __forceinline__ void swap_all(double2 (&v)[1 << R]) {
 #pragma unroll
-    for (int g = 0; g < 4; ++g) {
+    for (int g = 0; g < (1 << (R - 1)); ++g) {
         const int j0 = ((g >> B1) << (B1 + 1)) | (g & ((1 << B1) - 1));
         const int j1 = j0 | (1 << B1);
         const double2 t = v[j0];
@@ -151,10 +151,10 @@ __device__ __forceinline__ void swap_all(double2 (&v)[8]) {
     }
 }
 
-template <int RC, int B1>
-__device__ __forceinline__ void swap_ctrl(double2 (&v)[8], int when) {
+template <int R, int RC, int B1>
+__device__ __forceinline__ void swap_ctrl(double2 (&v)[1 << R], int when) {
 #pragma unroll
-    for (int g = 0; g < 4; ++g) {
+    for (int g = 0; g < (1 << (R - 1)); ++g) {
         const int j0 = ((g >> B1) << (B1 + 1)) | (g & ((1 << B1) - 1));
         const int j1 = j0 | (1 << B1);
         if (((j0 >> RC) & 1) == when) {
@@ -165,60 +165,57 @@ __device__ __forceinline__ void swap_ctrl(double2 (&v)[8], int when) {
     }
 }
 
+// compile-time dispatch of a runtime register bit b in [0, R)
+#define DIAQ_RB_DISPATCH(R_, b_, CALL)                              \
+    do {                                                            \
+        if ((b_) == 0) { constexpr int RB_ = 0; CALL; }             \
+        else if ((b_) == 1) { constexpr int RB_ = 1; CALL; }        \
+        else if ((R_) == 3 || (b_) == 2) { constexpr int RB_ = 2; CALL; } \
+        else { constexpr int RB_ = (R_) >= 4 ? 3 : 2; CALL; }       \
+    } while (0)
+
+template <int R, int RC, int MODE>
+__device__ __forceinline__ void swap_ctrl_b1(double2 (&v)[1 << R], int b1, int when) {
+    if (b1 == 0) { if constexpr (RC != 0) swap_ctrl<R, RC, 0>(v, when); }
+    else if (b1 == 1) { if constexpr (RC != 1) swap_ctrl<R, RC, 1>(v, when); }
+    else if (R == 3 || b1 == 2) { if constexpr (RC != 2) swap_ctrl<R, RC, 2>(v, when); }
+    else { if constexpr (R >= 4 && RC != 3) swap_ctrl<R, RC, (R >= 4 ? 3 : 2)>(v, when); }
+}
+
 template <int R, int MODE>
 __device__ __forceinline__ void dispatch_gate(double2 (&v)[1 << R], const RegGate &G, uint32_t tpart, uint64_t base,
                                               const double2 *sc, const uint32_t *snz, const uint32_t *scls) {
     // if-chains, not switches: a jump table would force v[] into local memory
     (void)scls;
-    static_assert(R == 3, "register fast paths are written for 8 amplitudes per thread");
-    {
-        if (G.op == 1) {
-            const double2 *c = sc + G.coef_off;
-            const uint32_t n0 = snz[G.nz_off], n1 = snz[G.nz_off + 1];
-            const int b1 = G.rb[0];
-            if (b1 == 0) dense1<0, MODE>(v, c, n0, n1);
-            else if (b1 == 1) dense1<1, MODE>(v, c, n0, n1);
-            else dense1<2, MODE>(v, c, n0, n1);
-            return;
-        }
-        if (G.op == 2) {
-            const double2 d0 = sc[G.coef_off], d1 = sc[G.coef_off + 1];
-            const uint32_t z0 = snz[G.nz_off], z1 = snz[G.nz_off + 1];
-            if (G.osel[0] == 2) {
-                const int rb = G.opos[0];
-                if (rb == 0) diag_reg<0, MODE>(v, d0, d1, z0, z1);
-                else if (rb == 1) diag_reg<1, MODE>(v, d0, d1, z0, z1);
-                else diag_reg<2, MODE>(v, d0, d1, z0, z1);
-            } else {
-                const uint32_t b = G.osel[0] == 0 ? (uint32_t)((base >> G.opos[0]) & 1ull) : (tpart >> G.opos[0]) & 1u;
-                const double2 d = b ? d1 : d0;
-                const bool nz = b ? (z1 & 1u) : (z0 & 1u);
+    static_assert(R == 3 || R == 4, "register fast paths cover 8 or 16 amplitudes per thread");
+    if (G.op == 1) {
+        const double2 *c = sc + G.coef_off;
+        const uint32_t n0 = snz[G.nz_off], n1 = snz[G.nz_off + 1];
+        DIAQ_RB_DISPATCH(R, G.rb[0], (dense1<R, RB_, MODE>(v, c, n0, n1)));
+        return;
+    }
+    if (G.op == 2) {
+        const double2 d0 = sc[G.coef_off], d1 = sc[G.coef_off + 1];
+        const uint32_t z0 = snz[G.nz_off], z1 = snz[G.nz_off + 1];
+        if (G.osel[0] == 2) {
+            DIAQ_RB_DISPATCH(R, G.opos[0], (diag_reg<R, RB_, MODE>(v, d0, d1, z0, z1)));
+        } else {
+            const uint32_t b = G.osel[0] == 0 ? (uint32_t)((base >> G.opos[0]) & 1ull) : (tpart >> G.opos[0]) & 1u;
+            const double2 d = b ? d1 : d0;
+            const bool nz = b ? (z1 & 1u) : (z0 & 1u);
 #pragma unroll
-                for (int j = 0; j < 8; ++j) v[j] = nz ? cmul<MODE>(d, v[j]) : make_double2(0.0, 0.0);
-            }
-            return;
+            for (int j = 0; j < (1 << R); ++j) v[j] = nz ? cmul<MODE>(d, v[j]) : make_double2(0.0, 0.0);
         }
-        if (G.op == 3) {
-            const int b1 = G.rb[0];
-            if (G.osel[0] == 2) {
-                const int rc = G.opos[0];
-                const int code = rc * 4 + b1;
-                if (code == 0 * 4 + 1) swap_ctrl<0, 1>(v, G.swap_when);
-                else if (code == 0 * 4 + 2) swap_ctrl<0, 2>(v, G.swap_when);
-                else if (code == 1 * 4 + 0) swap_ctrl<1, 0>(v, G.swap_when);
-                else if (code == 1 * 4 + 2) swap_ctrl<1, 2>(v, G.swap_when);
-                else if (code == 2 * 4 + 0) swap_ctrl<2, 0>(v, G.swap_when);
-                else swap_ctrl<2, 1>(v, G.swap_when);
-            } else {
-                const uint32_t b = G.osel[0] == 0 ? (uint32_t)((base >> G.opos[0]) & 1ull) : (tpart >> G.opos[0]) & 1u;
-                if ((int)b == G.swap_when) {
-                    if (b1 == 0) swap_all<0>(v);
-                    else if (b1 == 1) swap_all<1>(v);
-                    else swap_all<2>(v);
-                }
-            }
-            return;
+        return;
+    }
+    if (G.op == 3) {
+        if (G.osel[0] == 2) {
+            DIAQ_RB_DISPATCH(R, G.opos[0], (swap_ctrl_b1<R, RB_, MODE>(v, G.rb[0], G.swap_when)));
+        } else {
+            const uint32_t b = G.osel[0] == 0 ? (uint32_t)((base >> G.opos[0]) & 1ull) : (tpart >> G.opos[0]) & 1u;
+            if ((int)b == G.swap_when) DIAQ_RB_DISPATCH(R, G.rb[0], (swap_all<R, RB_>(v)));
         }
+        return;
     }
 }
 
@@ -257,7 +254,7 @@ __device__ __forceinline__ void smem_gate(double2 *tile, int T, const RegGate &G
 }
 
 template <int R, int MODE>
-__global__ void __launch_bounds__(kThreads, 3) tile_pass_kernel(const __grid_constant__ TileParams p) {
+__global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(const __grid_constant__ TileParams p) {
     extern __shared__ double2 tile[];
     __shared__ uint64_t hi_off[(1 << kMaxTileBits) >> kLowBits];
     __shared__ Phase sph[kMaxPhases];
@@ -651,8 +648,8 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
         return set_error(DIAQ_ERR_VALUE, "diaq_run_gates_fused: bad arguments");
     const bool sharded = n_total > n_bits;
     cudaStream_t s = (cudaStream_t)stream;
-    (void)tile_bits;
-    const int T = kThreadBits + 3;  // R = 3 register bits x 256 threads (tile_bits > 0 selects this path)
+    // tile_bits 12 -> 16 amplitudes per thread (R = 4), else 8 (R = 3); 256 threads
+    const int T = tile_bits >= kThreadBits + 4 ? kThreadBits + 4 : kThreadBits + 3;
     const bool tiled = n_bits >= T;
     const int R = T - kThreadBits;
     std::vector<PassPlan> plan;
@@ -702,6 +699,8 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
     if (!attr_set) {
         cudaFuncSetAttribute(tile_pass_kernel<3, DIAQ_CMUL_FMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
         cudaFuncSetAttribute(tile_pass_kernel<3, DIAQ_CMUL_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+        cudaFuncSetAttribute(tile_pass_kernel<4, DIAQ_CMUL_FMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+        cudaFuncSetAttribute(tile_pass_kernel<4, DIAQ_CMUL_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
         attr_set = true;
     }
     if (events && cudaEventRecord((cudaEvent_t)events[0], s) != cudaSuccess)
@@ -732,7 +731,7 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
             const size_t smem = (sizeof(double2) << p.tbits) + sizeof(double2) * p.ncoef +
                                 sizeof(uint32_t) * (p.nnz + p.ncls);
             if (smem > smem_max) return set_error(DIAQ_ERR_VALUE, "fused pass tables exceed shared memory");
-            const void *f = tile_kernel_ptr<3>(cmul_mode);
+            const void *f = R >= 4 ? tile_kernel_ptr<4>(cmul_mode) : tile_kernel_ptr<3>(cmul_mode);
             int per_sm = 1;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kThreads, smem);
             const int64_t grid =
