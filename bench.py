@@ -283,25 +283,34 @@ def run_ours(args):
     gate_bytes = 32 * N  # per GPU per gate (each rank's 2^n amplitudes read + written)
 
     # ---- e2e through the public API with pinned host buffers
+    # (failures are caught per rank, then every rank joins the same collective)
     e2e = None
     if not args.no_e2e:
-        xh = torch.empty(N, dtype=torch.complex128, pin_memory=True)
-        xh.copy_(x)
-        yh = torch.empty(N, dtype=torch.complex128, pin_memory=True)
-        torch.cuda.synchronize()
-        e_steps = max(1, min(args.steps, 5))
-        D.spmv(a, xh, out=yh)  # warm-up (allocator)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(e_steps):
-            D.spmv(a, xh, out=yh)
-        torch.cuda.synchronize()
-        e_s = max_over_ranks(dist, (time.perf_counter() - t0) / e_steps, dev)
-        e2e = {"value": round(nbytes * world / e_s / 1e9, 3), "unit": "GB/s",
-               "h2d_bytes_per_step": 16 * N, "d2h_bytes_per_step": 16 * N,
-               "ms_per_step": round(1e3 * e_s, 3),
-               "path": "paper_2405_01250_b200.spmv(a, pinned host x, out=pinned host y)"}
-        del xh, yh
+        e_local, e_err = float("inf"), None
+        try:
+            xh = torch.empty(N, dtype=torch.complex128, pin_memory=True)
+            xh.copy_(x)
+            yh = torch.empty(N, dtype=torch.complex128, pin_memory=True)
+            torch.cuda.synchronize()
+            e_steps = max(1, min(args.steps, 5))
+            D.spmv(a, xh, out=yh)  # warm-up (allocator)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(e_steps):
+                D.spmv(a, xh, out=yh)
+            torch.cuda.synchronize()
+            e_local = (time.perf_counter() - t0) / e_steps
+            del xh, yh
+        except Exception as ex:  # pinned-memory limits etc.: report, do not hang the other ranks
+            e_err = repr(ex)
+        e_s = max_over_ranks(dist, e_local, dev)
+        if e_s == float("inf"):
+            e2e = {"error": e_err or "e2e failed on another rank"}
+        else:
+            e2e = {"value": round(nbytes * world / e_s / 1e9, 3), "unit": "GB/s",
+                   "h2d_bytes_per_step": 16 * N, "d2h_bytes_per_step": 16 * N,
+                   "ms_per_step": round(1e3 * e_s, 3),
+                   "path": "paper_2405_01250_b200.spmv(a, pinned host x, out=pinned host y)"}
 
     secondary = {}
     if not args.no_secondary:
