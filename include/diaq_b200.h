@@ -103,6 +103,12 @@ int diaq_from_dense_fill(const void *dense, diaq_matrix_t *out, void *stream);
 /* to_dense (reference matrix.py:156-167) into a zeroed device n x n buffer */
 int diaq_to_dense(const diaq_matrix_t *a, void *dense, void *stream);
 
+/* ---- accounting (reference nnz matrix.py:393-400, memory.py:29-46) --------
+ * entries with |re|+|im| > eps, and (optional, NULL to skip) the number of
+ * distinct 2x2 blocks holding such an entry (BSR model).  Synchronous. */
+int diaq_count_nonzero(const diaq_matrix_t *a, double eps, int64_t *nnz_out, int64_t *bsr_blocks_out,
+                       void *stream);
+
 /* ---- spmv (reference matrix.py:253-278) -------------------------------
  * y = A x, bitwise equal to the reference (ascending d, no FMA). */
 int diaq_spmv(const diaq_matrix_t *a, const void *x, void *y, void *stream);

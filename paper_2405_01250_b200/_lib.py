@@ -71,6 +71,7 @@ _SIGS = {
     "diaq_from_dense_fill": ([_P, _MP, _P], _INT),
     "diaq_to_dense": ([_MP, _P, _P], _INT),
     "diaq_spmv": ([_MP, _P, _P, _P], _INT),
+    "diaq_count_nonzero": ([_MP, ctypes.c_double, _P, _P, _P], _INT),
     "diaq_spmv_host": ([_MP, _P, _P, _P, _P, _I64, _P], _INT),
     "diaq_spgemm_plan": ([_I64, _I64, _P, _I64, _P, _P, _P], _INT),
     "diaq_spgemm_workspace": ([_I64, _I64, _I64], _I64),

@@ -308,3 +308,119 @@ extern "C" int diaq_to_dense(const diaq_matrix_t *a, void *dense, void *stream) 
     if (!dense || !a) return set_error(DIAQ_ERR_VALUE, "diaq_to_dense: null argument");
     return gather_launch(dense, const_cast<diaq_matrix_t *>(a), true, (cudaStream_t)stream);
 }
+
+// ---- accounting on the device (reference nnz matrix.py:393-400, memory.py:29-46) ----
+
+struct CountDiag {
+    const double2 *vals;  // k = 0
+    int64_t len, d;
+};
+
+__global__ void __launch_bounds__(kThreads)
+count_nonzero_kernel(const CountDiag *__restrict__ dg, double eps, unsigned long long *count) {
+    const CountDiag g = dg[blockIdx.y];
+    unsigned long long c = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < g.len; k += stride) {
+        const double2 v = g.vals[k];
+        c += (fabs(v.x) + fabs(v.y) > eps) ? 1ull : 0ull;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+// 2x2 blocks holding a nonzero: one bit per block, then a popcount
+__global__ void __launch_bounds__(kThreads)
+bsr_mark_kernel(const CountDiag *__restrict__ dg, double eps, int64_t nb, unsigned int *bitmap) {
+    const CountDiag g = dg[blockIdx.y];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < g.len; k += stride) {
+        const double2 v = g.vals[k];
+        if (fabs(v.x) + fabs(v.y) > eps) {
+            const int64_t row = k - (g.d < 0 ? g.d : 0), col = row + g.d;
+            const int64_t blk = (row >> 1) * nb + (col >> 1);
+            atomicOr(bitmap + (blk >> 5), 1u << (blk & 31));
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) popcount_kernel(const unsigned int *bitmap, int64_t words,
+                                                            unsigned long long *count) {
+    unsigned long long c = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += stride) c += __popc(bitmap[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+static int count_common(const diaq_matrix_t *a, double eps, int64_t *nnz_out, int64_t *bsr_out, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (nnz_out) *nnz_out = 0;
+    if (bsr_out) *bsr_out = 0;
+    if (a->nd == 0) return DIAQ_OK;
+    std::vector<CountDiag> h((size_t)a->nd);
+    int64_t maxlen = 0;
+    for (int64_t i = 0; i < a->nd; ++i) {
+        const int64_t d = a->offs[i];
+        h[i].vals = (const double2 *)a->vals + a->starts[i];
+        h[i].len = a->n - (d < 0 ? -d : d);
+        h[i].d = d;
+        maxlen = std::max(maxlen, h[i].len);
+    }
+    CountDiag *dt = upload_table(h, s);
+    if (!dt) return set_error(DIAQ_ERR_CUDA, "count table upload failed");
+    unsigned long long *cnt = nullptr;
+    unsigned int *bitmap = nullptr;
+    const int64_t nb = (a->n + 1) / 2;
+    const int64_t words = (nb * nb + 31) / 32;
+    int rc = DIAQ_OK;
+    unsigned long long hc[2] = {0, 0};
+    if (cudaMallocAsync((void **)&cnt, 2 * sizeof(unsigned long long), s) != cudaSuccess) {
+        cudaFreeAsync(dt, s);
+        return set_error(DIAQ_ERR_CUDA, "count alloc failed");
+    }
+    cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), s);
+    for (int64_t base = 0; base < a->nd; base += 65535) {
+        const int cntd = (int)std::min<int64_t>(65535, a->nd - base);
+        dim3 grid(grid_x(maxlen, cntd), cntd);
+        if (nnz_out) {
+            count_nonzero_kernel<<<grid, kThreads, 0, s>>>(dt + base, eps, cnt);
+            count_launch();
+        }
+    }
+    if (bsr_out) {
+        if (cudaMallocAsync((void **)&bitmap, sizeof(unsigned int) * (size_t)words, s) != cudaSuccess) {
+            rc = set_error(DIAQ_ERR_RESOURCE, "bsr bitmap of %lld words does not fit", (long long)words);
+        } else {
+            cudaMemsetAsync(bitmap, 0, sizeof(unsigned int) * (size_t)words, s);
+            for (int64_t base = 0; base < a->nd; base += 65535) {
+                const int cntd = (int)std::min<int64_t>(65535, a->nd - base);
+                dim3 grid(grid_x(maxlen, cntd), cntd);
+                bsr_mark_kernel<<<grid, kThreads, 0, s>>>(dt + base, eps, nb, bitmap);
+                count_launch();
+            }
+            popcount_kernel<<<grid_x(words, 1), kThreads, 0, s>>>(bitmap, words, cnt + 1);
+            count_launch();
+        }
+    }
+    if (rc == DIAQ_OK) rc = check_launch("count kernels");
+    if (rc == DIAQ_OK) {
+        cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, s);
+        if (cudaStreamSynchronize(s) != cudaSuccess)
+            rc = set_error(DIAQ_ERR_CUDA, "count sync: %s", cudaGetErrorString(cudaGetLastError()));
+    }
+    if (bitmap) cudaFreeAsync(bitmap, s);
+    cudaFreeAsync(cnt, s);
+    cudaFreeAsync(dt, s);
+    if (nnz_out) *nnz_out = (int64_t)hc[0];
+    if (bsr_out) *bsr_out = (int64_t)hc[1];
+    return rc;
+}
+
+extern "C" int diaq_count_nonzero(const diaq_matrix_t *a, double eps, int64_t *nnz_out, int64_t *bsr_blocks_out,
+                                  void *stream) {
+    if (!a || eps < 0) return set_error(DIAQ_ERR_VALUE, "diaq_count_nonzero: bad arguments");
+    return count_common(a, eps, nnz_out, bsr_blocks_out, stream);
+}

@@ -503,13 +503,11 @@ def kron_identity(left_dim: int, m: DiaqMatrix, right_dim: int) -> DiaqMatrix:
 
 
 def nnz(a: DiaqMatrix, eps: float = 1e-15) -> int:
-    """Stored entries with |re| + |im| > eps (matrix.py:393-400)."""
+    """Stored entries with |re| + |im| > eps (matrix.py:393-400), counted on the device."""
     if eps < 0:
         raise ValueError("eps must be >= 0")
-    total = 0
-    for diag in a.diagonals():
-        total += int(np.count_nonzero(np.abs(diag.re) + np.abs(diag.im) > eps))
-    return total
+    from .memory import device_counts
+    return device_counts(a, eps)[0]
 
 
 def sparsity(a: DiaqMatrix, eps: float = 1e-15) -> float:

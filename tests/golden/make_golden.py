@@ -291,9 +291,29 @@ def main() -> int:
              "y_digest": digest(y4), "y_norm": float(np.linalg.norm(y4)),
              "sample_idx": idx.tolist(), "y_sample": [[v.real, v.imag] for v in y4[idx]],
              "ref_spmv_s": t_spmv, "u4": [[[v.real, v.imag] for v in row] for row in c4["u4"]]}
+    # ---- analysis / memory models (reference analysis.py, memory.py)
+    def recs(rs):
+        return [[r.timestep, r.gate_name, r.sparsity, r.diag_count, r.nnz, r.memory_map()] for r in rs]
+
+    ghz10 = R.Circuit(10, [R.GateOp("h", (0,))] + [R.GateOp("cx", (i, i + 1)) for i in range(9)])
+    rl6_ops = W.random_layered_ops(6, 2, seed=2)
+    rl6 = R.Circuit(6, [R.GateOp(*o) for o in rl6_ops])
+    analysis = {
+        "ghz10_chain": recs(R.chain_product_analysis(ghz10)),
+        "ghz10_timestep": recs(R.timestep_analysis(ghz10)),
+        "rl6_ops": ops_to_json(rl6_ops),
+        "rl6_chain_left": recs(R.chain_product_analysis(rl6, span_limit=6)),
+        "rl6_chain_right": recs(R.chain_product_analysis(rl6, span_limit=6, order="right")),
+        "rl6_timestep_eps": recs(R.timestep_analysis(rl6, eps=1e-3, span_limit=6)),
+        "memory": {
+            "corner": R.estimate_map(R.from_dense(corner, 0.0)),
+            "cx": R.estimate_map(R.from_dense(cx, 0.0)),
+            "kron_h": R.estimate_map(kh),
+        },
+    }
     with open(os.path.join(HERE, "configs.json"), "w") as f:
-        json.dump({"meta": meta, "config2_sweep": sweep, "circuits": circuits, "config4_n22": c4rec},
-                  f)
+        json.dump({"meta": meta, "config2_sweep": sweep, "circuits": circuits, "config4_n22": c4rec,
+                   "analysis": analysis}, f)
     print(f"goldens written in {time.time() - t_start:.1f}s")
     return 0
 

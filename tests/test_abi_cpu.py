@@ -147,3 +147,11 @@ def test_compute_fails_loudly_without_device():
         init_state(3)
     with pytest.raises(L.DeviceError):
         from_dense(np.eye(2))
+
+
+def test_analysis_guard_without_device():
+    from paper_2405_01250_b200 import Circuit, GateOp, ResourceError, chain_product_analysis
+    with pytest.raises(ResourceError):
+        chain_product_analysis(Circuit(15, [GateOp("h", (0,))]))
+    with pytest.raises(ValueError):
+        chain_product_analysis(Circuit(2, [GateOp("h", (0,))]), order="middle")
