@@ -124,8 +124,11 @@ class DiaqMatrix:
             for i, d in enumerate(dv.offs.tolist()):
                 s = int(dv.starts[i])
                 seg = arena[s:s + self.n_dim - abs(d)]
-                host[d] = Diagonal(d, np.ascontiguousarray(seg.real, dtype=self.dtype),
-                                   np.ascontiguousarray(seg.imag, dtype=self.dtype))
+                re = np.ascontiguousarray(seg.real, dtype=self.dtype)
+                im = np.ascontiguousarray(seg.imag, dtype=self.dtype)
+                re.flags.writeable = False  # snapshots of the device arena: edit via set_diag
+                im.flags.writeable = False
+                host[d] = Diagonal(d, re, im)
             self._host = host
         return self._host
 

@@ -80,8 +80,11 @@ class StateVector:
 
     @property
     def amps(self) -> np.ndarray:
+        """Host view of the amplitudes.  For a device-resident state this is a
+        read-only snapshot (writing to it could not reach the device copy)."""
         if self._host is None:
             self._host = self._dev.cpu().numpy()
+            self._host.flags.writeable = False
         return self._host
 
     def __len__(self) -> int:
