@@ -1,0 +1,122 @@
+"""API-completeness checks of the drop-in surface (reference test_matrix.py /
+test_sim.py / test_gates.py behaviours) on the device-backed objects."""
+from __future__ import annotations
+
+import json
+import math
+
+import numpy as np
+import pytest
+
+import paper_2405_01250_b200 as D
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+CORNER = np.array([[1, 0, 0, 2], [0, 3, 0, 0], [0, 0, 4, 0], [5, 0, 0, 6]], dtype=complex)
+
+
+def banded(rng, n, k):
+    m = rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))
+    m[np.abs(np.subtract.outer(np.arange(n), np.arange(n))) > k] = 0
+    return m
+
+
+def test_transpose_adjoint_add_scale(rng):
+    for n in (1, 5, 12):
+        m = banded(rng, n, 2)
+        a = D.from_dense(m, 0.0)
+        assert np.array_equal(D.to_dense(D.transpose(a)), m.T)
+        assert D.transpose(D.transpose(a)) == a
+        assert np.array_equal(D.to_dense(D.adjoint(a)), m.conj().T)
+        m2 = banded(rng, n, 1)
+        b = D.from_dense(m2, 0.0)
+        assert np.abs(D.to_dense(D.add(a, b)) - (m + m2)).max() < 1e-14
+        assert D.add(a, D.DiaqMatrix(n)) == a
+        s = D.scale(a, 0.5 - 2j)
+        assert np.abs(D.to_dense(s) - (0.5 - 2j) * m).max() < 1e-14
+    with pytest.raises(D.ShapeError):
+        D.add(D.identity(4), D.identity(2))
+    h = D.from_dense(np.array([[1, 1], [1, -1]]) / np.sqrt(2), 0.0)
+    assert D.adjoint(h) == h
+
+
+def test_kron_and_json(rng):
+    for na, nb in ((2, 3), (3, 4), (4, 4), (5, 2)):
+        ma, mb = banded(rng, na, 1), banded(rng, nb, 1)
+        k = D.kron(D.from_dense(ma, 0.0), D.from_dense(mb, 0.0))
+        assert np.abs(D.to_dense(k) - np.kron(ma, mb)).max() < 1e-14
+    a = D.from_dense(banded(rng, 8, 3), 0.0)
+    b = D.from_json(D.to_json(a))
+    assert a == b
+    blob = json.loads(D.to_json(a))
+    assert blob["n"] == 8 and all(len(p) == 2 for dg in blob["diags"].values() for p in dg)
+
+
+def test_mutation_semantics():
+    a = D.from_dense(CORNER, 0.0)          # device-built
+    with pytest.raises(ValueError):
+        a.get(0).re[0] = 9.0               # host snapshots of device data are read-only
+    a.set_diag(1, [7.0, 8.0, 9.0])         # edits go through set_diag (copied, like the reference)
+    assert a.diag_indices() == [-3, 0, 1, 3]
+    y = D.spmv(a, np.ones(4))
+    assert np.array_equal(y, O.spmv(O.from_dense(D.to_dense(a)), np.ones(4, dtype=complex)))
+    a.drop(-3)
+    assert a.diag_indices() == [0, 1, 3]
+    c = a.copy()
+    c.set_diag(0, [0.0] * 4)
+    assert a.get(0).re.tolist() == [1.0, 3.0, 4.0, 6.0]   # copies are independent
+    st = D.init_state(2)
+    with pytest.raises(ValueError):
+        st.amps[0] = 0.0
+
+
+def test_single_precision_matrices(rng):
+    m = banded(rng, 16, 2)
+    a = D.from_dense(m, 0.0, dtype=np.float32)
+    assert a.get(0).re.dtype == np.float32
+    x = rng.normal(size=16) + 1j * rng.normal(size=16)
+    # the reference's float32 diagonals are upcast exactly by numpy inside spmv
+    m32 = m.real.astype(np.float32).astype(np.float64) + 1j * m.imag.astype(np.float32).astype(np.float64)
+    assert np.array_equal(D.spmv(a, x), O.spmv(O.from_dense(m32), x))
+    with pytest.raises(D.UnsupportedFeatureError):
+        D.matmul(a, a)
+
+
+def test_dense_backend_and_fusion_agree():
+    ops = [("h", (0,), ()), ("cx", (0, 3), ()), ("rz", (3,), (0.4,)), ("ccx", (1, 3, 0), ()),
+           ("swap", (2, 0), ()), ("u3", (1,), (0.3, 0.2, 0.1))]
+    c = D.Circuit(4, [D.GateOp(*o) for o in ops])
+    diaq = D.run(c, shots=0, emit_state=True, span_limit=4)
+    dense = D.run(c, backend="dense", shots=0, emit_state=True, span_limit=4)
+    fused = D.run(c, shots=0, emit_state=True, span_limit=4, fusion=True)
+    assert np.abs(diaq.state - dense.state).max() < 1e-12
+    assert np.abs(diaq.state - fused.state).max() < 1e-12
+    assert set(diaq.timings_ns) >= {"compile", "apply_total", "sample", "total", "per_gate"}
+    assert len(diaq.timings_ns["per_gate"]) == len(ops)
+
+
+def test_placement_edge_bits_and_reversed_operands():
+    """Gates on the lowest/highest bits and operand orders reversed against the
+    embedding, bitwise against the oracle's materialised span matrices."""
+    n = 9
+    ops = [("cx", (8, 0), ()), ("cx", (0, 8), ()), ("ccx", (8, 4, 0), ()), ("swap", (8, 7), ()),
+           ("h", (8,), ()), ("rx", (0,), (1.1,)), ("cz", (5, 1), ())]
+    x = np.random.default_rng(4).normal(size=2**n) + 0j
+    x /= np.linalg.norm(x)
+    mode = D.sim.CMUL_MODE
+    for name, q, p in ops:
+        pl = D.compile_circuit(D.Circuit(n, [D.GateOp(name, q, p)]), span_limit=n)[0]
+        got = D.apply_placed(pl, D.StateVector(n, x)).amps
+        (da, om, db, _, _), = O.compile_ops(n, [(name, q, p)])
+        assert np.array_equal(got, O.apply_placed(da, om, db, x, mode)), (name, q)
+
+
+def test_init_state_and_norm():
+    s = D.init_state(3)
+    assert np.array_equal(s.amps, [1, 0, 0, 0, 0, 0, 0, 0]) and s.norm() == 1.0
+    big = D.init_state(31, max_qubits=31)  # the guard is a parameter, as in the reference
+    assert big.norm() == 1.0
+    del big
+    x = np.full(8, 1 / math.sqrt(8), dtype=complex)
+    assert abs(D.StateVector(3, x).norm() - 1.0) < 1e-15
