@@ -118,6 +118,7 @@ struct Tuning {
     int spmv_chunk = 8;        // strips per work item in raster 1
     int spmv_xpol = 0;         // 0: x evict_normal, 1: x evict_last
     int spmv_ctas_per_sm = 0;  // 0: occupancy maximum
+    int spmv_banded = 1;       // stage banded x windows in shared memory
     int gate_ctas_per_sm = 32;
 };
 Tuning &tuning();

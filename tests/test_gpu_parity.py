@@ -432,3 +432,24 @@ def test_spgemm_large_plan_and_offsets():
         oc = O.matmul(O.from_dense(m1), O.from_dense(m2))
         assert c.diag_indices() == oc.offs.tolist()
         assert np.array_equal(values(c), np.concatenate([r + 1j * i for r, i in (oc.diag(d) for d in oc.offs)]))
+
+
+def test_spmv_banded_staging_is_bitwise():
+    """The shared-memory banded spmv path equals the direct path bitwise."""
+    import torch
+    rng = np.random.default_rng(23)
+    for n, offs in ((4096, [-40, -32, 0, 8, 24]), (1 << 16, [-(1 << 12) - 8, -(1 << 12), 0, 3, (1 << 12) + 5]),
+                    (1000, [-999, 0, 999]), (777, [-5, -4, 0, 1, 2, 60, 61])):
+        a = D.DiaqMatrix(n)
+        for d in offs:
+            ln = n - abs(d)
+            a.set_diag(d, rng.normal(size=ln), rng.normal(size=ln))
+        x = torch.from_numpy(rng.normal(size=n) + 1j * rng.normal(size=n)).cuda()
+        L.tune("spmv_banded", 1)
+        y1 = D.spmv(a, x).cpu().numpy()
+        L.tune("spmv_banded", 0)
+        y0 = D.spmv(a, x).cpu().numpy()
+        L.tune("spmv_banded", 1)
+        assert np.array_equal(y0, y1), offs
+        om = O.omat_from_diags(n, {dg.index: (dg.re, dg.im) for dg in a.diagonals()})
+        assert np.array_equal(y1, O.spmv(om, x.cpu().numpy()))
