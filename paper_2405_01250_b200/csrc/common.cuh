@@ -119,6 +119,7 @@ struct Tuning {
     int spmv_xpol = 0;         // 0: x evict_normal, 1: x evict_last
     int spmv_ctas_per_sm = 0;  // 0: occupancy maximum
     int spmv_banded = 1;       // stage banded x windows in shared memory
+    int spmv_strips = 1;       // strip raster for far offsets (0: plain row order)
     int gate_ctas_per_sm = 32;
 };
 Tuning &tuning();

@@ -213,7 +213,7 @@ void spmv_raster(int64_t n, int64_t nd, const int64_t *offs, int64_t *ntiles, in
         if (a > far_rows && (s == 0 || a < s)) s = a;
     }
     *ntiles = nt;
-    if (s == 0) {
+    if (s == 0 || !tuning().spmv_strips) {
         *stride = nt;
         *nstrips = 1;
         return;

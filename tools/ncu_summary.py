@@ -85,7 +85,7 @@ def main():
     for name, recs in full.items():
         for rec in recs:
             tot = rec.get("dram__bytes_read.sum", 0) + rec.get("dram__bytes_write.sum", 0)
-            if "spmv_kernel" in rec["kernel"]:
+            if "spmv" in rec["kernel"]:
                 summ["spmv_dram_bytes_per_launch"] = tot
                 summ["spmv_source"] = f"profiles/{args.tag}_ncu_full.json ({name})"
             elif "gate_kernel" in rec["kernel"] or "tile_pass_kernel" in rec["kernel"]:

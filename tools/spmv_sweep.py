@@ -46,10 +46,11 @@ def main():
     fn = lambda: L.call("diaq_spmv", ctypes.byref(st), x.data_ptr(), y.data_ptr(), s)
     ref = None
     res = []
-    for raster, chunk, xpol, ctas in itertools.chain(
-            [(0, 1, 0, 0), (0, 1, 1, 0)],
-            itertools.product([1], [2, 4, 8, 16, 32], [0, 1], [0]),
-            itertools.product([1], [8], [0], [2, 4, 6])):
+    for banded, strips, raster, chunk, xpol, ctas in (
+            (1, 1, 0, 1, 0, 0), (1, 0, 0, 1, 0, 0), (0, 1, 0, 1, 0, 0), (0, 0, 0, 1, 0, 0),
+            (1, 1, 0, 1, 0, 6), (0, 1, 1, 8, 0, 0)):
+        L.tune("spmv_banded", banded)
+        L.tune("spmv_strips", strips)
         L.tune("spmv_raster", raster)
         L.tune("spmv_chunk", chunk)
         L.tune("spmv_xpol", xpol)
@@ -58,7 +59,7 @@ def main():
         if ref is None:
             ref = y.clone()
         same = bool(torch.equal(ref, y))
-        rec = {"raster": raster, "chunk": chunk, "xpol": xpol, "ctas_per_sm": ctas, "ms": round(ms, 4),
+        rec = {"banded": banded, "strips": strips, "raster": raster, "chunk": chunk, "xpol": xpol, "ctas_per_sm": ctas, "ms": round(ms, 4),
                "GBs": round(nbytes / ms / 1e6, 1), "bitwise_same": same}
         print(json.dumps(rec), flush=True)
         res.append(rec)
