@@ -182,6 +182,164 @@ __global__ void __launch_bounds__(kThreads) spmv_banded_kernel(const __grid_cons
     }
 }
 
+// ---- TMA bulk-copy pipeline (banded matrices) --------------------------------
+// A single elected thread streams each tile's inputs into shared memory with
+// cp.async.bulk (one contiguous copy per diagonal segment and per x band
+// window, completion counted on an mbarrier), double-buffered so the copies
+// of tile k+1 overlap the arithmetic of tile k.  The loads need no registers,
+// so memory-level parallelism no longer trades against occupancy.
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+constexpr int kTmaMaxStages = 4;
+
+// stage layout in dynamic shared memory: ND diagonal segments of 256
+// elements, then nbands x windows of 256 + 2h elements
+struct TmaLayout {
+    int ndiag, nbands, w;       // w = 256 + 2h
+    uint32_t stage_elems;       // double2 elements per stage
+};
+
+// issue the copies of the tile at rows [r0, r0 + 256) into stage buffer `sb`
+template <int ND>
+__device__ __forceinline__ void tma_issue(const SpmvParams<kParamDiags> &p, double2 *sb, int w, int64_t r0,
+                                          uint64_t *bar, uint64_t pol_first, uint64_t pol_x) {
+    uint32_t total = 0;
+    const int h = p.halo;
+    for (int i = 0; i < ND; ++i) {
+        const int64_t a = r0 > p.dg[i].lo ? r0 : p.dg[i].lo;
+        const int64_t b = r0 + kThreads < p.dg[i].hi ? r0 + kThreads : p.dg[i].hi;
+        if (a < b) total += (uint32_t)(b - a) * 16u;
+    }
+    for (int bd = 0; bd < p.nbands; ++bd) {
+        const int64_t lo = r0 + p.center[bd] - h, hi = r0 + kThreads + p.center[bd] + h;
+        const int64_t a = lo > 0 ? lo : 0, b = hi < p.n ? hi : p.n;
+        if (a < b) total += (uint32_t)(b - a) * 16u;
+    }
+    mbar_expect_tx(bar, total);
+    for (int i = 0; i < ND; ++i) {
+        const int64_t a = r0 > p.dg[i].lo ? r0 : p.dg[i].lo;
+        const int64_t b = r0 + kThreads < p.dg[i].hi ? r0 + kThreads : p.dg[i].hi;
+        if (a < b) bulk_g2s(sb + i * kThreads + (a - r0), p.dg[i].row0 + a, (uint32_t)(b - a) * 16u, bar, pol_first);
+    }
+    double2 *xb = sb + ND * kThreads;
+    for (int bd = 0; bd < p.nbands; ++bd) {
+        const int64_t lo = r0 + p.center[bd] - h, hi = r0 + kThreads + p.center[bd] + h;
+        const int64_t a = lo > 0 ? lo : 0, b = hi < p.n ? hi : p.n;
+        if (a < b) bulk_g2s(xb + bd * w + (a - lo), p.x + a, (uint32_t)(b - a) * 16u, bar, pol_x);
+    }
+}
+
+template <int ND>
+__global__ void __launch_bounds__(kThreads) spmv_tma_kernel(const __grid_constant__ SpmvParams<kParamDiags> p,
+                                                            int nstages) {
+    extern __shared__ __align__(128) double2 smem_stage[];
+    __shared__ __align__(8) uint64_t bars[kTmaMaxStages];
+    const int h = p.halo;
+    const int w = kThreads + 2 * h;
+    const uint32_t stage_elems = (uint32_t)(ND * kThreads + p.nbands * w);
+    uint64_t pol_first = 0, pol_x = 0;
+    if (threadIdx.x == 0) {
+        pol_first = policy_evict_first();
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_x));
+        for (int s = 0; s < nstages; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto tile_of = [&](int64_t it, int64_t &r0) -> bool {
+        const int64_t j = it % p.nstrips, b = it / p.nstrips;
+        const int64_t t = j * p.stride_tiles + b;
+        if (b >= p.stride_tiles || t >= p.ntiles) return false;
+        r0 = p.r0 + t * kThreads;
+        return true;
+    };
+    auto next_valid = [&](int64_t it, int64_t &r0) -> int64_t {
+        while (it < p.nitems && !tile_of(it, r0)) it += gridDim.x;
+        return it;
+    };
+    // ring of in-flight tiles: the producer (thread 0) keeps nstages-1 ahead
+    int64_t q_it[kTmaMaxStages], q_r0[kTmaMaxStages];
+    int64_t scratch = 0;
+    int64_t fetch_it = next_valid(blockIdx.x, scratch);
+    int issued = 0;
+    for (; issued < nstages && fetch_it < p.nitems; ++issued) {
+        q_it[issued] = fetch_it;
+        tile_of(fetch_it, q_r0[issued]);
+        if (threadIdx.x == 0) tma_issue<ND>(p, smem_stage + issued * stage_elems, w, q_r0[issued], &bars[issued],
+                                            pol_first, pol_x);
+        fetch_it = next_valid(fetch_it + gridDim.x, scratch);
+    }
+    uint32_t parity = 0;
+    for (int k = 0; k < issued || fetch_it < p.nitems; ++k) {
+        const int slot = k % nstages;
+        if (k >= issued) break;
+        mbar_wait(&bars[slot], parity);
+        const double2 *sb = smem_stage + slot * stage_elems;
+        const double2 *xb = sb + ND * kThreads;
+        const int64_t r0 = q_r0[slot];
+        const int64_t r = r0 + threadIdx.x;
+        if (r < p.rend) {
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int i = 0; i < ND; ++i) {
+                if ((r >= p.dg[i].lo) & (r < p.dg[i].hi)) {
+                    const double2 v = sb[i * kThreads + threadIdx.x];
+                    const double2 xv = xb[p.dg[i].band * w + threadIdx.x + h + p.dg[i].resid];
+                    acc = cadd(acc, cmul_plain(v, xv));
+                }
+            }
+            st_stream(p.y + r, acc);
+        }
+        __syncthreads();  // slot fully consumed before it is refilled
+        if (fetch_it < p.nitems) {
+            int64_t r0n = 0;
+            tile_of(fetch_it, r0n);
+            q_r0[slot] = r0n;
+            q_it[slot] = fetch_it;
+            if (threadIdx.x == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                tma_issue<ND>(p, smem_stage + slot * stage_elems, w, r0n, &bars[slot], pol_first, pol_x);
+            }
+            ++issued;
+            int64_t dummy = 0;
+            fetch_it = next_valid(fetch_it + gridDim.x, dummy);
+        }
+        if (slot == nstages - 1) parity ^= 1u;
+    }
+    (void)q_it;
+}
+
 // large diagonal counts: tables in global memory, raster 0
 __global__ void __launch_bounds__(kThreads)
 spmv_kernel_global(int64_t r0, int64_t rend, int nd, const SpmvDiag *__restrict__ dg, const double2 *x,
@@ -249,6 +407,25 @@ static int launch_param_x(const SpmvParams<kParamDiags> &p, cudaStream_t s) {
 template <int ND>
 static int launch_param(const SpmvParams<kParamDiags> &p, cudaStream_t s) {
     if constexpr (ND > 0) {
+        if (p.nbands > 0 && tuning().spmv_tma) {
+            const void *f = (const void *)spmv_tma_kernel<ND>;
+            SpmvParams<kParamDiags> q = p;
+            q.raster = 0;
+            q.nitems = q.stride_tiles * q.nstrips;
+            const int nstages = std::max(2, std::min(kTmaMaxStages, tuning().spmv_tma_stages));
+            const size_t stage_bytes = 16 * (size_t)(ND * kThreads + q.nbands * (kThreads + 2 * q.halo));
+            const size_t smem = stage_bytes * (size_t)nstages;
+            cudaFuncSetAttribute(spmv_tma_kernel<ND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            int per_sm = 1, dev = 0, sms = kSms;
+            if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kThreads, smem);
+            cudaGetLastError();
+            if (tuning().spmv_ctas_per_sm > 0) per_sm = std::min(per_sm, tuning().spmv_ctas_per_sm);
+            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(q.nitems, (int64_t)sms * std::max(1, per_sm)));
+            spmv_tma_kernel<ND><<<grid, kThreads, smem, s>>>(q, nstages);
+            count_launch();
+            return check_launch("spmv_tma_kernel");
+        }
         if (p.nbands > 0) {
             const void *f = (const void *)spmv_banded_kernel<ND>;
             SpmvParams<kParamDiags> q = p;
