@@ -120,7 +120,7 @@ struct Tuning {
     int spmv_ctas_per_sm = 0;  // 0: occupancy maximum
     int spmv_banded = 1;       // stage banded x windows in shared memory
     int spmv_strips = 1;       // strip raster for far offsets (0: plain row order)
-    int spmv_tma = 1;          // banded path through the TMA bulk-copy pipeline
+    int spmv_tma = 0;          // banded path through the TMA bulk-copy pipeline (opt-in: measured slower)
     int spmv_tma_stages = 4;   // tiles in flight per CTA
     int gate_ctas_per_sm = 32;
 };

@@ -453,3 +453,21 @@ def test_spmv_banded_staging_is_bitwise():
         assert np.array_equal(y0, y1), offs
         om = O.omat_from_diags(n, {dg.index: (dg.re, dg.im) for dg in a.diagonals()})
         assert np.array_equal(y1, O.spmv(om, x.cpu().numpy()))
+
+
+def test_spmv_tma_pipeline_is_bitwise():
+    """Opt-in TMA bulk-copy spmv (cp.async.bulk + mbarrier ring) equals the default path."""
+    import torch
+    c4 = W.config4(22, seed=0, with_x=False)
+    span = D.build_span_unitary(D.from_dense(c4["u4"], 0.0), c4["positions"], c4["span"])
+    a = D.kron_identity(1, span, c4["right"])
+    x = torch.from_numpy(W.random_state(np.random.default_rng(9), 2**22)).cuda()
+    want = D.spmv(a, x).cpu().numpy()
+    try:
+        L.tune("spmv_tma", 1)
+        for stages in (2, 3, 4):
+            L.tune("spmv_tma_stages", stages)
+            assert np.array_equal(D.spmv(a, x).cpu().numpy(), want), stages
+    finally:
+        L.tune("spmv_tma", 0)
+        L.tune("spmv_tma_stages", 4)
