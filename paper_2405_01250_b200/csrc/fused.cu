@@ -38,6 +38,7 @@ constexpr int kMaxRegKin = 1;       // mixing operands applied in registers (wid
 constexpr int kMaxSel = 4;          // selector (non-mixing) operands
 constexpr int kMaxPassGates = 48;   // gate records staged in smem per pass
 constexpr int kMaxPhases = 24;
+constexpr int kPrePhases = 4;       // phases whose register slots are precomputed per CTA
 
 static_assert(kThreads == (1 << kThreadBits), "thread layout");
 
@@ -259,6 +260,10 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
     __shared__ uint64_t hi_off[(1 << kMaxTileBits) >> kLowBits];
     __shared__ Phase sph[kMaxPhases];
     __shared__ RegGate sg[kMaxPassGates];
+    // per-(phase, thread) smem slots of the thread's registers and its thread-bit
+    // pattern, computed once per CTA instead of once per tile
+    __shared__ uint16_t s_off[kPrePhases][1 << R][kThreads];
+    __shared__ uint32_t s_tpart[kPrePhases][kThreads];
     constexpr int NR = 1 << R;
     const int T = p.tbits;
     const uint32_t tsize = 1u << T;
@@ -281,6 +286,16 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
     __syncthreads();
     constexpr uint32_t lowmask = (1u << kLowBits) - 1u;
     const int per_thread = (int)(tsize >> kThreadBits);
+    const int npre = p.nphases < kPrePhases ? p.nphases : kPrePhases;
+    for (int ph_i = 0; ph_i < npre; ++ph_i) {
+        const Phase &ph = sph[ph_i];
+        uint32_t tpart = 0;
+        for (int i = 0; i < T - R; ++i) tpart |= ((threadIdx.x >> i) & 1u) << ph.tpos[i];
+        s_tpart[ph_i][threadIdx.x] = tpart;
+#pragma unroll
+        for (int j = 0; j < NR; ++j) s_off[ph_i][j][threadIdx.x] = (uint16_t)swz(tpart | reg_spread<R>(j, ph.rpos));
+    }
+    __syncthreads();
     for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
         const uint64_t base = insert_zero_bits_dyn((uint64_t)t, p.tb, T);
         const uint64_t sbase = base | p.gbase;  // full-state index bits for selectors
@@ -308,14 +323,26 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
                 }
                 continue;
             }
-            uint32_t tpart = 0;
-            for (int i = 0; i < T - R; ++i) tpart |= ((threadIdx.x >> i) & 1u) << ph.tpos[i];
             double2 v[NR];
+            uint32_t tpart;
+            if (ph_i < kPrePhases) {
+                tpart = s_tpart[ph_i][threadIdx.x];
 #pragma unroll
-            for (int j = 0; j < NR; ++j) v[j] = tile[swz(tpart | reg_spread<R>(j, ph.rpos))];
+                for (int j = 0; j < NR; ++j) v[j] = tile[s_off[ph_i][j][threadIdx.x]];
+            } else {
+                tpart = 0;
+                for (int i = 0; i < T - R; ++i) tpart |= ((threadIdx.x >> i) & 1u) << ph.tpos[i];
+#pragma unroll
+                for (int j = 0; j < NR; ++j) v[j] = tile[swz(tpart | reg_spread<R>(j, ph.rpos))];
+            }
             for (int gi = ph.g0; gi < ph.g1; ++gi) dispatch_gate<R, MODE>(v, sg[gi], tpart, sbase, sc, snz, scls);
+            if (ph_i < kPrePhases) {
 #pragma unroll
-            for (int j = 0; j < NR; ++j) tile[swz(tpart | reg_spread<R>(j, ph.rpos))] = v[j];
+                for (int j = 0; j < NR; ++j) tile[s_off[ph_i][j][threadIdx.x]] = v[j];
+            } else {
+#pragma unroll
+                for (int j = 0; j < NR; ++j) tile[swz(tpart | reg_spread<R>(j, ph.rpos))] = v[j];
+            }
             __syncthreads();
         }
         for (int k = 0; k < per_thread; ++k) {
