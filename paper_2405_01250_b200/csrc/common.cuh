@@ -122,6 +122,7 @@ struct Tuning {
     int spmv_strips = 1;       // strip raster for far offsets (0: plain row order)
     int spmv_tma = 0;          // banded path through the TMA bulk-copy pipeline (opt-in: measured slower)
     int spmv_tma_stages = 4;   // tiles in flight per CTA
+    int spmv_async = 1;        // banded path through cp.async (LDGSTS) staging (default: fastest)
     int gate_ctas_per_sm = 32;
 };
 Tuning &tuning();

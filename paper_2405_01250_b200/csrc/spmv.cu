@@ -182,16 +182,70 @@ __global__ void __launch_bounds__(kThreads) spmv_banded_kernel(const __grid_cons
     }
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// ---- cp.async variant (banded matrices) --------------------------------------
+// Every diagonal value of the tile is copied global -> shared with
+// cp.async (LDGSTS: no register is held while the load is in flight), so all
+// ND loads of a row are outstanding at once at full occupancy (128-thread
+// CTAs, 16 per SM), instead of the ~3 that fit in registers.
+constexpr int kAsyncThreads = 128;
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "l"(pol)
+                 : "memory");
+}
+
+template <int ND>
+__global__ void __launch_bounds__(kAsyncThreads) spmv_async_kernel(const __grid_constant__ SpmvParams<kParamDiags> p) {
+    __shared__ __align__(16) double2 sd[ND > 0 ? ND : 1][kAsyncThreads];
+    __shared__ __align__(16) double2 xs[kMaxBands][kAsyncThreads + 2 * kMaxHalo];
+    const uint64_t pol = policy_evict_first();
+    uint64_t polx;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(polx));
+    const int h = p.halo;
+    const int w = kAsyncThreads + 2 * h;
+    for (int64_t it = blockIdx.x; it < p.nitems; it += gridDim.x) {
+        const int64_t j = it % p.nstrips;
+        const int64_t b = it / p.nstrips;
+        const int64_t t = j * p.stride_tiles + b;
+        if (b >= p.stride_tiles || t >= p.ntiles) continue;  // uniform over the CTA
+        const int64_t r0t = p.r0 + t * kAsyncThreads;
+        const int64_t r = r0t + threadIdx.x;
+#pragma unroll
+        for (int i = 0; i < ND; ++i)
+            if (r < p.rend && r >= p.dg[i].lo && r < p.dg[i].hi) cp_async16(&sd[i][threadIdx.x], p.dg[i].row0 + r, pol);
+        for (int bd = 0; bd < p.nbands; ++bd) {
+            const int64_t base = r0t + p.center[bd] - h;
+            for (int i = threadIdx.x; i < w; i += kAsyncThreads) {
+                const int64_t idx = base + i;
+                if (idx >= 0 && idx < p.n) cp_async16(&xs[bd][i], p.x + idx, polx);
+            }
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        if (r < p.rend) {
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int i = 0; i < ND; ++i) {
+                if ((r >= p.dg[i].lo) & (r < p.dg[i].hi))
+                    acc = cadd(acc, cmul_plain(sd[i][threadIdx.x], xs[p.dg[i].band][threadIdx.x + h + p.dg[i].resid]));
+            }
+            st_stream(p.y + r, acc);
+        }
+        __syncthreads();
+    }
+}
+
 // ---- TMA bulk-copy pipeline (banded matrices) --------------------------------
 // A single elected thread streams each tile's inputs into shared memory with
 // cp.async.bulk (one contiguous copy per diagonal segment and per x band
 // window, completion counted on an mbarrier), double-buffered so the copies
 // of tile k+1 overlap the arithmetic of tile k.  The loads need no registers,
 // so memory-level parallelism no longer trades against occupancy.
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
 
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -407,6 +461,27 @@ static int launch_param_x(const SpmvParams<kParamDiags> &p, cudaStream_t s) {
 template <int ND>
 static int launch_param(const SpmvParams<kParamDiags> &p, cudaStream_t s) {
     if constexpr (ND > 0) {
+        if (p.nbands > 0 && tuning().spmv_async) {
+            const void *f = (const void *)spmv_async_kernel<ND>;
+            SpmvParams<kParamDiags> q = p;
+            const int64_t nrows = q.rend - q.r0;
+            const int64_t nt = (nrows + kAsyncThreads - 1) / kAsyncThreads;
+            const int64_t scale = kThreads / kAsyncThreads;  // strip stride in 128-row tiles
+            q.ntiles = nt;
+            q.stride_tiles = q.nstrips > 1 ? q.stride_tiles * scale : nt;
+            q.nstrips = (nt + q.stride_tiles - 1) / q.stride_tiles;
+            q.raster = 0;
+            q.nitems = q.stride_tiles * q.nstrips;
+            int per_sm = 1, dev = 0, sms = kSms;
+            if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kAsyncThreads, 0);
+            cudaGetLastError();
+            if (tuning().spmv_ctas_per_sm > 0) per_sm = std::min(per_sm, tuning().spmv_ctas_per_sm);
+            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(q.nitems, (int64_t)sms * std::max(1, per_sm)));
+            spmv_async_kernel<ND><<<grid, kAsyncThreads, 0, s>>>(q);
+            count_launch();
+            return check_launch("spmv_async_kernel");
+        }
         if (p.nbands > 0 && tuning().spmv_tma) {
             const void *f = (const void *)spmv_tma_kernel<ND>;
             SpmvParams<kParamDiags> q = p;

@@ -447,10 +447,13 @@ def test_spmv_banded_staging_is_bitwise():
         x = torch.from_numpy(rng.normal(size=n) + 1j * rng.normal(size=n)).cuda()
         L.tune("spmv_banded", 1)
         y1 = D.spmv(a, x).cpu().numpy()
+        L.tune("spmv_async", 0)
+        y2 = D.spmv(a, x).cpu().numpy()
+        L.tune("spmv_async", 1)
         L.tune("spmv_banded", 0)
         y0 = D.spmv(a, x).cpu().numpy()
         L.tune("spmv_banded", 1)
-        assert np.array_equal(y0, y1), offs
+        assert np.array_equal(y0, y1) and np.array_equal(y0, y2), offs
         om = O.omat_from_diags(n, {dg.index: (dg.re, dg.im) for dg in a.diagonals()})
         assert np.array_equal(y1, O.spmv(om, x.cpu().numpy()))
 

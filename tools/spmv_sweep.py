@@ -46,9 +46,10 @@ def main():
     fn = lambda: L.call("diaq_spmv", ctypes.byref(st), x.data_ptr(), y.data_ptr(), s)
     ref = None
     res = []
-    for tma, stages, banded, strips, raster, chunk, xpol, ctas in (
-            (0, 2, 1, 1, 0, 1, 0, 0), (1, 2, 1, 1, 0, 1, 0, 0), (1, 3, 1, 1, 0, 1, 0, 0), (1, 4, 1, 1, 0, 1, 0, 0),
-            (1, 4, 1, 1, 0, 1, 0, 1), (1, 4, 1, 0, 0, 1, 0, 0)):
+    for asy, tma, stages, banded, strips, raster, chunk, xpol, ctas in (
+            (0, 0, 2, 1, 1, 0, 1, 0, 0), (1, 0, 2, 1, 1, 0, 1, 0, 0), (1, 0, 2, 1, 1, 0, 1, 0, 12),
+            (1, 0, 2, 1, 0, 0, 1, 0, 0)):
+        L.tune("spmv_async", asy)
         L.tune("spmv_tma", tma)
         L.tune("spmv_tma_stages", stages)
         L.tune("spmv_banded", banded)
@@ -61,7 +62,7 @@ def main():
         if ref is None:
             ref = y.clone()
         same = bool(torch.equal(ref, y))
-        rec = {"tma": tma, "stages": stages, "banded": banded, "strips": strips, "raster": raster, "chunk": chunk, "xpol": xpol, "ctas_per_sm": ctas, "ms": round(ms, 4),
+        rec = {"async": asy, "tma": tma, "stages": stages, "banded": banded, "strips": strips, "raster": raster, "chunk": chunk, "xpol": xpol, "ctas_per_sm": ctas, "ms": round(ms, 4),
                "GBs": round(nbytes / ms / 1e6, 1), "bitwise_same": same}
         print(json.dumps(rec), flush=True)
         res.append(rec)
