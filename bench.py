@@ -326,7 +326,7 @@ def run_ours(args):
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": peak_src,
                 "traffic": prof.get("spmv_dram_bytes_per_launch"),
-                "alg_bytes_per_launch": nbytes, "kernel": "diaq::spmv_kernel<64,9>",
+                "alg_bytes_per_launch": nbytes, "kernel": "diaq::spmv_async_kernel<9> (cp.async-staged banded spmv)",
                 "frac_of_8TBs_spec": round(achieved / 8000.0, 4)}
     gates_scale = 1 if (world > 1 and args.sharded_gates) else world
     gates = {"gates_per_s": round(gates_scale * n_gates / (g_ms * 1e-3), 2), "ms_per_gate": round(ms_per_gate, 4),
