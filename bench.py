@@ -479,6 +479,22 @@ def secondary_workloads(args, D, L, W, torch) -> dict:
     t0 = time.perf_counter()
     res = D.run(D.Circuit(20, [D.GateOp(*o) for o in ops]), shots=1024, seed=0, span_limit=20)
     e2e_s = time.perf_counter() - t0
+    # config 5 shape on one GPU: a 2^29-amplitude state split into 2 emulated
+    # shards (same plans and kernels as the NCCL path; the exchange is a
+    # device copy here), one random layer drawn over all 29 qubits
+    from paper_2405_01250_b200.shard import run_emulated
+    ops5 = W.random_layered_ops(29, 1, seed=0)
+    pls5 = D.compile_circuit(D.Circuit(29, [D.GateOp(*o) for o in ops5]), span_limit=29)
+    run_emulated(29, 2, pls5)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    shards, st5 = run_emulated(29, 2, pls5)
+    torch.cuda.synchronize()
+    dt5 = time.perf_counter() - t0
+    out["config5_sharded_emulated_n29_p2"] = {"gates": len(pls5), "s_per_layer": round(dt5, 4),
+                                             "gates_per_s": round(len(pls5) / dt5, 1), "stats": st5,
+                                             "note": "2 shards on one GPU; exchange = device copy (NVLink unmeasured)"}
+    del shards
     out["config3_circuit_n20"] = {"gates": len(pls), "ms_per_circuit": round(ms, 3),
                                   "gates_per_s": round(len(pls) / ms * 1e3, 1),
                                   "run_api_wall_s": round(e2e_s, 4),
