@@ -69,6 +69,12 @@ __device__ __forceinline__ void st_stream(double2 *p, double2 v) {
     asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
 
+// 256-bit streaming store of two adjacent elements (p must be 32-byte aligned)
+__device__ __forceinline__ void st_stream2(double2 *p, double2 a, double2 b) {
+    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y)
+                 : "memory");
+}
+
 __device__ __forceinline__ void st_plain(double2 *p, double2 v) {
     asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }

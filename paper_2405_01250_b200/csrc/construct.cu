@@ -35,21 +35,33 @@ struct KronParams {
     KronDiag dg[kParamDiags];
 };
 
+__device__ __forceinline__ double2 kron_value(const KronParams &p, const KronDiag &dg, int64_t k) {
+    int64_t pos, src;
+    if (p.pow2) {
+        pos = k & (p.block - 1);
+        src = pos >> p.right_shift;
+    } else {
+        pos = k % p.block;
+        src = pos / p.right;
+    }
+    return pos < dg.run ? ld_reuse(dg.src + src) : make_double2(0.0, 0.0);
+}
+
+// Two adjacent output elements per thread and iteration, written with one
+// 256-bit store; an element left over at either end of a diagonal (odd
+// arena start / odd remaining length) is written singly by one thread.
 __global__ void __launch_bounds__(kThreads) kron_identity_kernel(const __grid_constant__ KronParams p) {
     const KronDiag &dg = p.dg[blockIdx.y];
+    const int64_t k0 = ((uintptr_t)dg.dst & 31) ? 1 : 0;
+    const int64_t pairs = dg.len > k0 ? (dg.len - k0) >> 1 : 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < dg.len; k += stride) {
-        int64_t pos, src;
-        if (p.pow2) {
-            pos = k & (p.block - 1);
-            src = pos >> p.right_shift;
-        } else {
-            pos = k % p.block;
-            src = pos / p.right;
-        }
-        double2 v = make_double2(0.0, 0.0);
-        if (pos < dg.run) v = ld_reuse(dg.src + src);
-        st_stream(dg.dst + k, v);
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < pairs; j += stride) {
+        const int64_t k = k0 + 2 * j;
+        st_stream2(dg.dst + k, kron_value(p, dg, k), kron_value(p, dg, k + 1));
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && dg.len > 0) {
+        if (k0) st_stream(dg.dst, kron_value(p, dg, 0));
+        if (k0 + 2 * pairs < dg.len) st_stream(dg.dst + dg.len - 1, kron_value(p, dg, dg.len - 1));
     }
 }
 
@@ -188,7 +200,7 @@ extern "C" int diaq_kron_identity(int64_t left, const diaq_matrix_t *m, int64_t 
             p.dg[j].run = (m->n - (d < 0 ? -d : d)) * right;
             maxlen = std::max(maxlen, p.dg[j].len);
         }
-        dim3 grid(grid_x(maxlen, cnt), cnt);
+        dim3 grid(grid_x((maxlen + 1) / 2, cnt), cnt);
         kron_identity_kernel<<<grid, kThreads, 0, s>>>(p);
         count_launch();
         const int rc = check_launch("kron_identity_kernel");
