@@ -33,6 +33,8 @@ struct KronParams {
     int block_shift, right_shift;
     int nd;
     KronDiag dg[kParamDiags];
+    int64_t beg[kParamDiags];  // arena offset of each output diagonal from dg[0].dst (flat mode)
+    int64_t end;               // beg[nd-1] + dg[nd-1].len
 };
 
 __device__ __forceinline__ double2 kron_value(const KronParams &p, const KronDiag &dg, int64_t k) {
@@ -62,6 +64,114 @@ __global__ void __launch_bounds__(kThreads) kron_identity_kernel(const __grid_co
     if (blockIdx.x == 0 && threadIdx.x == 0 && dg.len > 0) {
         if (k0) st_stream(dg.dst, kron_value(p, dg, 0));
         if (k0 + 2 * pairs < dg.len) st_stream(dg.dst + dg.len - 1, kron_value(p, dg, dg.len - 1));
+    }
+}
+
+// Arena-linear variant: the batch's output diagonals are one contiguous
+// arena range (gaps only the < 8-element alignment padding of diaq_layout,
+// which receives zeros), written front to back as a single 256-bit store
+// stream like a fill -- no per-diagonal grid rows competing for DRAM pages.
+// A thread's pairs advance monotonically, so it keeps the current
+// diagonal's fields in registers and re-reads the table only on crossing a
+// diagonal boundary (a pair straddling one takes the generic lookup).
+__device__ __forceinline__ double2 kron_flat_value(const KronParams &p, int i, int64_t e) {
+    const int64_t k = e - p.beg[i];
+    if (k < 0 || k >= p.dg[i].len) return make_double2(0.0, 0.0);
+    return kron_value(p, p.dg[i], k);
+}
+
+__device__ __forceinline__ int kron_flat_find(const KronParams &p, int64_t e) {
+    int i = 0;
+    while (i + 1 < p.nd && e >= p.beg[i + 1]) ++i;
+    return i;
+}
+
+template <bool kPow2>
+struct KronCursor {
+    const double2 *src;
+    int64_t lo, hi;  // [lo, hi): arena range of the cached diagonal's elements
+    int64_t run, block, right;
+    int block_shift, right_shift;
+    uint64_t pol;  // L2 evict_last: the source diagonal is re-read once per left block, between
+                   // which a whole block of output streams through L2 and would evict it
+
+    __device__ __forceinline__ void load(const KronParams &p, int i) {
+        src = p.dg[i].src;
+        lo = p.beg[i];
+        hi = lo + p.dg[i].len;
+        run = p.dg[i].run;
+        block = p.block;
+        right = p.right;
+        block_shift = p.block_shift;
+        right_shift = p.right_shift;
+    }
+    __device__ __forceinline__ double2 at(int64_t k) const {
+        int64_t pos, idx;
+        if (kPow2) {
+            pos = k & (block - 1);
+            idx = pos >> right_shift;
+        } else {
+            pos = k % block;
+            idx = pos / right;
+        }
+        return pos < run ? ld_reuse_hint(src + idx, pol) : make_double2(0.0, 0.0);
+    }
+    // elements k and k+1; one load when both read the same source element
+    // (right >= 2 and the pair inside one run of R), the common case
+    __device__ __forceinline__ void at2(int64_t k, double2 &a, double2 &b) const {
+        int64_t pos, idx;
+        if (kPow2) {
+            pos = k & (block - 1);
+            idx = pos >> right_shift;
+        } else {
+            pos = k % block;
+            idx = pos / right;
+        }
+        const int64_t pos1 = pos + 1 == block ? 0 : pos + 1;
+        const int64_t idx1 = kPow2 ? (pos1 >> right_shift) : pos1 / right;
+        a = pos < run ? ld_reuse_hint(src + idx, pol) : make_double2(0.0, 0.0);
+        if (idx1 == idx && pos1 < run) b = a;
+        else b = pos1 < run ? ld_reuse_hint(src + idx1, pol) : make_double2(0.0, 0.0);
+    }
+};
+
+template <bool kPow2>
+__global__ void __launch_bounds__(kThreads) kron_identity_flat_kernel(const __grid_constant__ KronParams p) {
+    double2 *base = p.dg[0].dst;
+    const int64_t first = ((uintptr_t)base & 31) ? 1 : 0;
+    const int64_t pairs = p.end > first ? (p.end - first) >> 1 : 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= pairs) return;
+    int i = kron_flat_find(p, first + 2 * j);
+    KronCursor<kPow2> c;
+    c.pol = policy_evict_last();
+    c.load(p, i);
+    constexpr int U = 4;  // pairs in flight per thread (all loads issued before the stores)
+    for (; j < pairs; j += U * stride) {
+        double2 v[2 * U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t e = first + 2 * (j + u * stride);
+            if (j + u * stride >= pairs) break;
+            if (e >= c.hi && i + 1 < p.nd && e >= p.beg[i + 1]) {
+                i = kron_flat_find(p, e);
+                c.load(p, i);
+            }
+            if (e >= c.lo && e + 1 < c.hi) {
+                c.at2(e - c.lo, v[2 * u], v[2 * u + 1]);
+            } else {  // padding or a diagonal boundary inside the pair
+                v[2 * u] = kron_flat_value(p, kron_flat_find(p, e), e);
+                v[2 * u + 1] = kron_flat_value(p, kron_flat_find(p, e + 1), e + 1);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (j + u * stride < pairs) st_stream2(base + first + 2 * (j + u * stride), v[2 * u], v[2 * u + 1]);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (first && p.end > 0) st_stream(base, kron_flat_value(p, 0, 0));
+        if (first + 2 * pairs < p.end) st_stream(base + p.end - 1, kron_flat_value(p, p.nd - 1, p.end - 1));
     }
 }
 
@@ -189,6 +299,7 @@ extern "C" int diaq_kron_identity(int64_t left, const diaq_matrix_t *m, int64_t 
         p.right_shift = p.pow2 ? log2i(right) : 0;
         p.nd = cnt;
         int64_t maxlen = 0;
+        bool flat = tuning().kron_flat != 0;
         for (int j = 0; j < cnt; ++j) {
             const int64_t i = base + j;
             const int64_t d = m->offs[i];
@@ -199,9 +310,27 @@ extern "C" int diaq_kron_identity(int64_t left, const diaq_matrix_t *m, int64_t 
             p.dg[j].len = out->n - (dout < 0 ? -dout : dout);
             p.dg[j].run = (m->n - (d < 0 ? -d : d)) * right;
             maxlen = std::max(maxlen, p.dg[j].len);
+            p.beg[j] = p.dg[j].dst - p.dg[0].dst;
+            if (j > 0) {
+                const int64_t gap = p.beg[j] - (p.beg[j - 1] + p.dg[j - 1].len);
+                if (gap < 0 || gap >= 8) flat = false;  // not a diaq_layout arena: keep to the diagonals
+            }
         }
-        dim3 grid(grid_x((maxlen + 1) / 2, cnt), cnt);
-        kron_identity_kernel<<<grid, kThreads, 0, s>>>(p);
+        p.end = p.beg[cnt - 1] + p.dg[cnt - 1].len;
+        if (flat) {
+            int dev = 0, sms = kSms;
+            if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaGetLastError();
+            const int64_t want = (p.end / 2 + kThreads - 1) / kThreads;
+            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * tuning().kron_ctas_per_sm));
+            if (p.pow2)
+                kron_identity_flat_kernel<true><<<grid, kThreads, 0, s>>>(p);
+            else
+                kron_identity_flat_kernel<false><<<grid, kThreads, 0, s>>>(p);
+        } else {
+            dim3 grid(grid_x((maxlen + 1) / 2, cnt), cnt);
+            kron_identity_kernel<<<grid, kThreads, 0, s>>>(p);
+        }
         count_launch();
         const int rc = check_launch("kron_identity_kernel");
         if (rc) return rc;

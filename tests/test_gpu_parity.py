@@ -129,6 +129,33 @@ def test_kron_identity_patterns(kats):
         assert np.array_equal(D.to_dense(got), want.to_dense())
 
 
+def banded(rng, n, k):
+    m = rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))
+    m[np.abs(np.subtract.outer(np.arange(n), np.arange(n))) > k] = 0
+    return m
+
+
+@pytest.mark.parametrize("flat", [1, 0])
+def test_kron_identity_store_paths(flat):
+    """Arena-linear (default) and per-diagonal kron_identity kernels, odd and
+    power-of-two shapes, ragged diagonal lengths, against the oracle."""
+    from paper_2405_01250_b200 import _lib as L
+    rng = np.random.default_rng(11)
+    L.tune("kron_flat", flat)
+    try:
+        for nm, left, right, band in ((37, 3, 5, 6), (16, 64, 8, 3), (5, 1, 1, 4), (33, 7, 1, 32), (64, 2, 32, 9)):
+            m = banded(rng, nm, band)
+            m[np.abs(rng.normal(size=m.shape)) > 1.5] = 0   # holes inside kept diagonals
+            want = O.kron_identity(left, O.from_dense(m), right)
+            got = D.kron_identity(left, D.from_dense(m, 0.0), right)
+            assert got.diag_indices() == want.offs.tolist()
+            for d in got.diag_indices():
+                wre, wim = want.diag(d)
+                assert np.array_equal(got.get(d).re, wre) and np.array_equal(got.get(d).im, wim), (nm, d)
+    finally:
+        L.tune("kron_flat", 1)
+
+
 def test_span_embeddings(kats):
     for case in kats["kats"]["span"]:
         g = D.from_dense(dense_from_pairs(case["g"]), 0.0)

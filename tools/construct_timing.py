@@ -33,13 +33,23 @@ def main():
     u = D.from_dense(c4["u4"], 0.0)
     span = D.build_span_unitary(u, c4["positions"], c4["span"])
     out = {}
-    ms = timed(lambda: D.kron_identity(2 ** (n - 22), span, c4["right"]))
     a = D.kron_identity(2 ** (n - 22), span, c4["right"])
     stored = sum(2 ** n - abs(d) for d in a.diag_indices()) * 16
-    out["kron_identity"] = {"n": n, "ms": round(ms, 3), "bytes": stored, "GB_s": round(stored / ms / 1e6, 1)}
     del a
+    for flat, ctas in ((0, 8), (1, 32)):
+        L.tune("kron_flat", flat)
+        L.tune("kron_ctas_per_sm", ctas)
+        ms = timed(lambda: D.kron_identity(2 ** (n - 22), span, c4["right"]))
+        out[f"kron_identity_flat{flat}_c{ctas}"] = {"n": n, "ms": round(ms, 3), "bytes": stored,
+                                                    "GB_s": round(stored / ms / 1e6, 1)}
+    L.tune("kron_flat", 1)
+    L.tune("kron_ctas_per_sm", 8)
     ms = timed(lambda: D.build_span_unitary(u, c4["positions"], c4["span"]))
     out["build_span_unitary_19"] = {"ms": round(ms, 4)}
+    buf = torch.empty(2 ** 31, dtype=torch.complex128, device="cuda")  # 34 GB
+    ms = timed(lambda: buf.zero_())
+    out["torch_zero_34GB"] = {"ms": round(ms, 3), "GB_s": round(buf.numel() * 16 / ms / 1e6, 1)}
+    del buf
     print(json.dumps(out))
 
 
