@@ -69,6 +69,18 @@ __device__ __forceinline__ void st_stream(double2 *p, double2 v) {
     asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// global -> shared 16-byte copy through L2 only (LDGSTS); no register is
+// held while it is in flight
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "l"(pol)
+                 : "memory");
+}
+
 // 256-bit streaming store of two adjacent elements (p must be 32-byte aligned)
 __device__ __forceinline__ void st_stream2(double2 *p, double2 a, double2 b) {
     asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y)
@@ -130,6 +142,7 @@ struct Tuning {
     int spmv_tma_stages = 4;   // tiles in flight per CTA
     int spmv_async = 1;        // banded path through cp.async (LDGSTS) staging (default: fastest)
     int gate_ctas_per_sm = 32;
+    int fused_dbuf = 1;        // fused passes: double-buffered tile (prefetch the next one)
     int kron_flat = 1;         // kron_identity as one arena-linear store stream
     int kron_ctas_per_sm = 32;  // CTAs per SM launched (4 resident; later ones refill)
 };

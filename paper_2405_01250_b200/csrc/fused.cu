@@ -81,6 +81,7 @@ struct TileParams {
     const uint32_t *cls;
     int ncoef, nnz, ncls;
     uint64_t gbase;           // sharded state: rank bits (rank << local_bits) for selector lookups
+    int nbuf;                 // 2: the next tile is prefetched (cp.async) while this one computes
 };
 
 __device__ __forceinline__ uint32_t swz(uint32_t e) {
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
     constexpr int NR = 1 << R;
     const int T = p.tbits;
     const uint32_t tsize = 1u << T;
-    double2 *sc = tile + tsize;
+    double2 *sc = tile + tsize * p.nbuf;
     uint32_t *snz = reinterpret_cast<uint32_t *>(sc + p.ncoef);
     uint32_t *scls = snz + p.nnz;
     for (int i = threadIdx.x; i < p.ncoef; i += blockDim.x) sc[i] = p.coef[i];
@@ -295,30 +296,38 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
 #pragma unroll
         for (int j = 0; j < NR; ++j) s_off[ph_i][j][threadIdx.x] = (uint16_t)swz(tpart | reg_spread<R>(j, ph.rpos));
     }
+    // HBM -> smem with cp.async, coalesced (consecutive e are consecutive
+    // state indices in runs of 8); every element of the tile in flight at once
+    const uint64_t pol = policy_evict_first();
+    auto fetch = [&](int64_t tt, double2 *buf) {
+        const uint64_t b = insert_zero_bits_dyn((uint64_t)tt, p.tb, T);
+        for (int k = 0; k < per_thread; ++k) {
+            const uint32_t e = threadIdx.x + (uint32_t)k * kThreads;
+            cp_async16(buf + swz(e), p.x + b + (e & lowmask) + hi_off[e >> kLowBits], pol);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
     __syncthreads();
+    int cur = 0;
+    if ((int64_t)blockIdx.x < p.ntiles) fetch(blockIdx.x, tile);
     for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
         const uint64_t base = insert_zero_bits_dyn((uint64_t)t, p.tb, T);
         const uint64_t sbase = base | p.gbase;  // full-state index bits for selectors
-        // HBM -> smem, coalesced (consecutive e are consecutive state indices in runs of 8)
-        for (int k0 = 0; k0 < per_thread; k0 += 4) {
-            double2 w[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t e = threadIdx.x + (uint32_t)(k0 + k) * kThreads;
-                if (k0 + k < per_thread) w[k] = ld_reuse(p.x + base + (e & lowmask) + hi_off[e >> kLowBits]);
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t e = threadIdx.x + (uint32_t)(k0 + k) * kThreads;
-                if (k0 + k < per_thread) tile[swz(e)] = w[k];
-            }
+        double2 *tl = tile + (uint32_t)cur * tsize;
+        const int64_t tn = t + gridDim.x;
+        if (p.nbuf == 2 && tn < p.ntiles) {
+            // the other buffer was drained by the previous tile's store loop
+            fetch(tn, tile + (uint32_t)(cur ^ 1) * tsize);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
         __syncthreads();
         for (int ph_i = 0; ph_i < p.nphases; ++ph_i) {
             const Phase &ph = sph[ph_i];
             if (ph.generic) {
                 for (int gi = ph.g0; gi < ph.g1; ++gi) {
-                    smem_gate<MODE>(tile, T, sg[gi], sbase, sc, snz);
+                    smem_gate<MODE>(tl, T, sg[gi], sbase, sc, snz);
                     __syncthreads();
                 }
                 continue;
@@ -328,28 +337,30 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
             if (ph_i < kPrePhases) {
                 tpart = s_tpart[ph_i][threadIdx.x];
 #pragma unroll
-                for (int j = 0; j < NR; ++j) v[j] = tile[s_off[ph_i][j][threadIdx.x]];
+                for (int j = 0; j < NR; ++j) v[j] = tl[s_off[ph_i][j][threadIdx.x]];
             } else {
                 tpart = 0;
                 for (int i = 0; i < T - R; ++i) tpart |= ((threadIdx.x >> i) & 1u) << ph.tpos[i];
 #pragma unroll
-                for (int j = 0; j < NR; ++j) v[j] = tile[swz(tpart | reg_spread<R>(j, ph.rpos))];
+                for (int j = 0; j < NR; ++j) v[j] = tl[swz(tpart | reg_spread<R>(j, ph.rpos))];
             }
             for (int gi = ph.g0; gi < ph.g1; ++gi) dispatch_gate<R, MODE>(v, sg[gi], tpart, sbase, sc, snz, scls);
             if (ph_i < kPrePhases) {
 #pragma unroll
-                for (int j = 0; j < NR; ++j) tile[s_off[ph_i][j][threadIdx.x]] = v[j];
+                for (int j = 0; j < NR; ++j) tl[s_off[ph_i][j][threadIdx.x]] = v[j];
             } else {
 #pragma unroll
-                for (int j = 0; j < NR; ++j) tile[swz(tpart | reg_spread<R>(j, ph.rpos))] = v[j];
+                for (int j = 0; j < NR; ++j) tl[swz(tpart | reg_spread<R>(j, ph.rpos))] = v[j];
             }
             __syncthreads();
         }
         for (int k = 0; k < per_thread; ++k) {
             const uint32_t e = threadIdx.x + (uint32_t)k * kThreads;
-            st_stream(p.x + base + (e & lowmask) + hi_off[e >> kLowBits], tile[swz(e)]);
+            st_stream(p.x + base + (e & lowmask) + hi_off[e >> kLowBits], tl[swz(e)]);
         }
         __syncthreads();
+        if (p.nbuf == 2) cur ^= 1;
+        else if (tn < p.ntiles) fetch(tn, tile);  // single buffer: refill as soon as it is drained
     }
 }
 
@@ -721,7 +732,7 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
             return set_error(DIAQ_ERR_CUDA, "diaq_run_gates_fused: program alloc failed");
         cudaMemcpyAsync(dbuf, host.data(), bytes, cudaMemcpyHostToDevice, s);
     }
-    const size_t smem_max = (sizeof(double2) << kMaxTileBits) + 48 * 1024;
+    const size_t smem_max = (2 * sizeof(double2) << kMaxTileBits) + 48 * 1024;
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(tile_pass_kernel<3, DIAQ_CMUL_FMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
@@ -755,11 +766,22 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
             p.nnz = (int)ps.pk.nz.size();
             p.ncls = (int)ps.pk.cls.size();
             p.gbase = sharded ? ((uint64_t)rank << n_bits) : 0ull;
-            const size_t smem = (sizeof(double2) << p.tbits) + sizeof(double2) * p.ncoef +
-                                sizeof(uint32_t) * (p.nnz + p.ncls);
-            if (smem > smem_max) return set_error(DIAQ_ERR_VALUE, "fused pass tables exceed shared memory");
+            const size_t tables = sizeof(double2) * p.ncoef + sizeof(uint32_t) * (p.nnz + p.ncls);
             const void *f = R >= 4 ? tile_kernel_ptr<4>(cmul_mode) : tile_kernel_ptr<3>(cmul_mode);
+            // double-buffer the tile when that still leaves >= 2 CTAs per SM
             int per_sm = 1;
+            p.nbuf = 1;
+            size_t smem = (sizeof(double2) << p.tbits) + tables;
+            if (tuning().fused_dbuf) {
+                const size_t smem2 = (2 * sizeof(double2) << p.tbits) + tables;
+                int per_sm2 = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, f, kThreads, smem2);
+                if (per_sm2 >= 2 && smem2 <= smem_max) {
+                    p.nbuf = 2;
+                    smem = smem2;
+                }
+            }
+            if (smem > smem_max) return set_error(DIAQ_ERR_VALUE, "fused pass tables exceed shared memory");
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kThreads, smem);
             const int64_t grid =
                 std::max<int64_t>(1, std::min<int64_t>(p.ntiles, (int64_t)sm_count_f() * std::max(1, per_sm)));

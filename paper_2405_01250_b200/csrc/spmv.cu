@@ -182,9 +182,6 @@ __global__ void __launch_bounds__(kThreads) spmv_banded_kernel(const __grid_cons
     }
 }
 
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
 
 // ---- cp.async variant (banded matrices) --------------------------------------
 // Every diagonal value of the tile is copied global -> shared with
@@ -193,11 +190,6 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
 // CTAs, 16 per SM), instead of the ~3 that fit in registers.
 constexpr int kAsyncThreads = 128;
 
-__device__ __forceinline__ void cp_async16(void *dst, const void *src, uint64_t pol) {
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
-                 "l"(pol)
-                 : "memory");
-}
 
 template <int ND>
 __global__ void __launch_bounds__(kAsyncThreads) spmv_async_kernel(const __grid_constant__ SpmvParams<kParamDiags> p) {

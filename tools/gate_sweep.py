@@ -15,7 +15,13 @@ from paper_2405_01250_b200.sim import _GateProgram
 
 
 def main():
-    for n, layers in ((28, 1), (20, 40)):
+    # usage: gate_sweep.py [key=value ...] -- diaq_tune settings; GATE_SWEEP_TILES="0,11" picks tile sizes
+    for kv in sys.argv[1:]:
+        k, v = kv.split("=")
+        L.tune(k, int(v))
+    tiles = [int(t) for t in os.environ.get("GATE_SWEEP_TILES", "0,8,9,10,11,12").split(",")]
+    sizes = ((28, 1), (20, 40)) if not os.environ.get("GATE_SWEEP_N28_ONLY") else ((28, 1),)
+    for n, layers in sizes:
         ops = W.random_layered_ops(n, layers, seed=0)
         pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
         prog = _GateProgram([p.compact() for p in pls])
@@ -23,7 +29,7 @@ def main():
         x[0] = 1
         s = torch.cuda.current_stream().cuda_stream
         ref = None
-        for tb in (0, 8, 9, 10, 11, 12):
+        for tb in tiles:
             npass = ctypes.c_int(0)
 
             def go():
@@ -49,7 +55,7 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / reps
-            print(json.dumps({"n": n, "gates": prog.n, "tile_bits": tb, "passes": npass.value if tb else prog.n,
+            print(json.dumps({"tune": sys.argv[1:], "n": n, "gates": prog.n, "tile_bits": tb, "passes": npass.value if tb else prog.n,
                               "ms": round(ms, 3), "gates_per_s": round(prog.n / ms * 1e3, 1),
                               "ms_per_pass": round(ms / max(1, npass.value if tb else prog.n), 4),
                               "first_run_bitwise_same_as_unfused": same}), flush=True)
