@@ -142,7 +142,6 @@ struct Tuning {
     int spmv_tma_stages = 4;   // tiles in flight per CTA
     int spmv_async = 1;        // banded path through cp.async (LDGSTS) staging (default: fastest)
     int gate_ctas_per_sm = 32;
-    int fused_dbuf = 1;        // fused passes: double-buffered tile (prefetch the next one)
     int kron_flat = 1;         // kron_identity as one arena-linear store stream
     int kron_ctas_per_sm = 32;  // CTAs per SM launched (4 resident; later ones refill)
 };

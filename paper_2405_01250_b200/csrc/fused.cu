@@ -81,8 +81,15 @@ struct TileParams {
     const uint32_t *cls;
     int ncoef, nnz, ncls;
     uint64_t gbase;           // sharded state: rank bits (rank << local_bits) for selector lookups
-    int nbuf;                 // 2: the next tile is prefetched (cp.async) while this one computes
+    uint64_t tmask;           // state bits of the tile
+    uint64_t gstep;           // gridDim.x deposited into the non-tile bits (tile base stride)
 };
+
+// base of tile t + gridDim.x from the base of tile t: add in the number
+// system of the non-tile bits (tile bits forced to 1 carry straight through)
+__device__ __forceinline__ uint64_t next_base(uint64_t base, const TileParams &p) {
+    return ((base | p.tmask) + p.gstep) & ~p.tmask;
+}
 
 __device__ __forceinline__ uint32_t swz(uint32_t e) {
     return e ^ (((e >> 3) ^ (e >> 6) ^ (e >> 9)) & 7u);
@@ -268,7 +275,7 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
     constexpr int NR = 1 << R;
     const int T = p.tbits;
     const uint32_t tsize = 1u << T;
-    double2 *sc = tile + tsize * p.nbuf;
+    double2 *sc = tile + tsize;
     uint32_t *snz = reinterpret_cast<uint32_t *>(sc + p.ncoef);
     uint32_t *scls = snz + p.nnz;
     for (int i = threadIdx.x; i < p.ncoef; i += blockDim.x) sc[i] = p.coef[i];
@@ -299,8 +306,7 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
     // HBM -> smem with cp.async, coalesced (consecutive e are consecutive
     // state indices in runs of 8); every element of the tile in flight at once
     const uint64_t pol = policy_evict_first();
-    auto fetch = [&](int64_t tt, double2 *buf) {
-        const uint64_t b = insert_zero_bits_dyn((uint64_t)tt, p.tb, T);
+    auto fetch = [&](uint64_t b, double2 *buf) {
         for (int k = 0; k < per_thread; ++k) {
             const uint32_t e = threadIdx.x + (uint32_t)k * kThreads;
             cp_async16(buf + swz(e), p.x + b + (e & lowmask) + hi_off[e >> kLowBits], pol);
@@ -308,20 +314,14 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     __syncthreads();
-    int cur = 0;
-    if ((int64_t)blockIdx.x < p.ntiles) fetch(blockIdx.x, tile);
+    // (a second tile buffer to prefetch into was measured slower: it costs a
+    // resident CTA per SM, and the pass is issue-bound, not latency-bound)
+    uint64_t base = insert_zero_bits_dyn((uint64_t)blockIdx.x, p.tb, T);
+    if ((int64_t)blockIdx.x < p.ntiles) fetch(base, tile);
+    double2 *tl = tile;
     for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-        const uint64_t base = insert_zero_bits_dyn((uint64_t)t, p.tb, T);
         const uint64_t sbase = base | p.gbase;  // full-state index bits for selectors
-        double2 *tl = tile + (uint32_t)cur * tsize;
-        const int64_t tn = t + gridDim.x;
-        if (p.nbuf == 2 && tn < p.ntiles) {
-            // the other buffer was drained by the previous tile's store loop
-            fetch(tn, tile + (uint32_t)(cur ^ 1) * tsize);
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-        } else {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncthreads();
         for (int ph_i = 0; ph_i < p.nphases; ++ph_i) {
             const Phase &ph = sph[ph_i];
@@ -359,8 +359,8 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
             st_stream(p.x + base + (e & lowmask) + hi_off[e >> kLowBits], tl[swz(e)]);
         }
         __syncthreads();
-        if (p.nbuf == 2) cur ^= 1;
-        else if (tn < p.ntiles) fetch(tn, tile);  // single buffer: refill as soon as it is drained
+        base = next_base(base, p);
+        if (t + gridDim.x < p.ntiles) fetch(base, tile);  // refill as soon as the tile is drained
     }
 }
 
@@ -732,7 +732,7 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
             return set_error(DIAQ_ERR_CUDA, "diaq_run_gates_fused: program alloc failed");
         cudaMemcpyAsync(dbuf, host.data(), bytes, cudaMemcpyHostToDevice, s);
     }
-    const size_t smem_max = (2 * sizeof(double2) << kMaxTileBits) + 48 * 1024;
+    const size_t smem_max = (sizeof(double2) << kMaxTileBits) + 48 * 1024;
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(tile_pass_kernel<3, DIAQ_CMUL_FMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
@@ -768,23 +768,17 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
             p.gbase = sharded ? ((uint64_t)rank << n_bits) : 0ull;
             const size_t tables = sizeof(double2) * p.ncoef + sizeof(uint32_t) * (p.nnz + p.ncls);
             const void *f = R >= 4 ? tile_kernel_ptr<4>(cmul_mode) : tile_kernel_ptr<3>(cmul_mode);
-            // double-buffer the tile when that still leaves >= 2 CTAs per SM
             int per_sm = 1;
-            p.nbuf = 1;
-            size_t smem = (sizeof(double2) << p.tbits) + tables;
-            if (tuning().fused_dbuf) {
-                const size_t smem2 = (2 * sizeof(double2) << p.tbits) + tables;
-                int per_sm2 = 0;
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, f, kThreads, smem2);
-                if (per_sm2 >= 2 && smem2 <= smem_max) {
-                    p.nbuf = 2;
-                    smem = smem2;
-                }
-            }
+            const size_t smem = (sizeof(double2) << p.tbits) + tables;
             if (smem > smem_max) return set_error(DIAQ_ERR_VALUE, "fused pass tables exceed shared memory");
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kThreads, smem);
             const int64_t grid =
                 std::max<int64_t>(1, std::min<int64_t>(p.ntiles, (int64_t)sm_count_f() * std::max(1, per_sm)));
+            p.tmask = 0;
+            for (int j = 0; j < p.tbits; ++j) p.tmask |= 1ull << p.tb[j];
+            p.gstep = 0;  // deposit grid into the non-tile bits, low to high
+            for (int b = 0, k = 0; b < 64 && ((uint64_t)grid >> k) != 0; ++b)
+                if (!((p.tmask >> b) & 1ull)) p.gstep |= (((uint64_t)grid >> k++) & 1ull) << b;
             void *args[] = {(void *)&p};
             cudaLaunchKernel(f, dim3((unsigned)grid), dim3(kThreads), args, smem, s);
             count_launch();
