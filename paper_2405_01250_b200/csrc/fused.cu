@@ -38,7 +38,8 @@ constexpr int kMaxRegKin = 1;       // mixing operands applied in registers (wid
 constexpr int kMaxSel = 4;          // selector (non-mixing) operands
 constexpr int kMaxPassGates = 48;   // gate records staged in smem per pass
 constexpr int kMaxPhases = 24;
-constexpr int kPrePhases = 4;       // phases whose register slots are precomputed per CTA
+constexpr int kPrePhases = 4;       // phases whose register slots are precomputed per CTA (R = 3; 3 at R = 4,
+                                    // within the 48 KB of static shared memory)
 
 static_assert(kThreads == (1 << kThreadBits), "thread layout");
 
@@ -60,11 +61,42 @@ struct RegGate {
     int mpos;                 // generic phases: tile position of the mixing bit
 };
 
+// Affine relabelling of tile indices, f -> A f ^ c ^ (XOR of b_i over the set
+// full-state bits bbit_i): how a run of permutation gates (X, CX, SWAP, any
+// gate whose matrix is a 0/1 permutation affine in the index bits) moves
+// amplitudes.  Such runs are not executed: they are folded into the smem
+// slot each amplitude is written to (phase store / tile load).
+constexpr int kMaxPermBase = 8;
+
+struct Affine {
+    int on;
+    int nb;
+    uint32_t c;
+    uint32_t a[kMaxTileBits];    // image of tile bit j
+    int bbit[kMaxPermBase];
+    uint32_t b[kMaxPermBase];
+};
+
+__device__ __forceinline__ uint32_t aff_lin(const Affine &m, uint32_t f, int T) {
+    uint32_t r = 0;
+    for (int j = 0; j < T; ++j)
+        if ((f >> j) & 1u) r ^= m.a[j];
+    return r;
+}
+
+__device__ __forceinline__ uint32_t aff_const(const Affine &m, uint64_t sbase) {
+    uint32_t r = m.c;
+    for (int i = 0; i < m.nb; ++i)
+        if ((sbase >> m.bbit[i]) & 1ull) r ^= m.b[i];
+    return r;
+}
+
 struct Phase {
     int g0, g1;               // gates [g0, g1) of the pass (pass-relative)
     int generic;              // 1: gates applied in shared memory (no register bits)
     int rpos[4];              // tile positions of the register bits, ascending (R entries)
     int tpos[kMaxTileBits];   // tile positions of the thread bits, ascending (T - R entries)
+    Affine post;              // permutation run after the phase's gates, applied by its store
 };
 
 struct TileParams {
@@ -81,6 +113,7 @@ struct TileParams {
     const uint32_t *cls;
     int ncoef, nnz, ncls;
     uint64_t gbase;           // sharded state: rank bits (rank << local_bits) for selector lookups
+    Affine pre;               // permutation run opening the pass, applied by the tile load
     uint64_t tmask;           // state bits of the tile
     uint64_t gstep;           // gridDim.x deposited into the non-tile bits (tile base stride)
 };
@@ -270,8 +303,14 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
     __shared__ RegGate sg[kMaxPassGates];
     // per-(phase, thread) smem slots of the thread's registers and its thread-bit
     // pattern, computed once per CTA instead of once per tile
-    __shared__ uint16_t s_off[kPrePhases][1 << R][kThreads];
-    __shared__ uint32_t s_tpart[kPrePhases][kThreads];
+    constexpr int kPre = R >= 4 ? kPrePhases - 1 : kPrePhases;
+    __shared__ uint16_t s_off[kPre][1 << R][kThreads];
+    __shared__ uint32_t s_tpart[kPre][kThreads];
+    // folded permutations: swizzled images of the thread part / register part
+    __shared__ uint16_t s_pt[kPre][kThreads];
+    __shared__ uint16_t s_pj[kPre][1 << R];
+    __shared__ uint16_t s_lt[kThreads];
+    __shared__ uint16_t s_lk[1 << (kMaxTileBits - kThreadBits)];
     constexpr int NR = 1 << R;
     const int T = p.tbits;
     const uint32_t tsize = 1u << T;
@@ -294,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
     __syncthreads();
     constexpr uint32_t lowmask = (1u << kLowBits) - 1u;
     const int per_thread = (int)(tsize >> kThreadBits);
-    const int npre = p.nphases < kPrePhases ? p.nphases : kPrePhases;
+    const int npre = p.nphases < kPre ? p.nphases : kPre;
     for (int ph_i = 0; ph_i < npre; ++ph_i) {
         const Phase &ph = sph[ph_i];
         uint32_t tpart = 0;
@@ -302,14 +341,30 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
         s_tpart[ph_i][threadIdx.x] = tpart;
 #pragma unroll
         for (int j = 0; j < NR; ++j) s_off[ph_i][j][threadIdx.x] = (uint16_t)swz(tpart | reg_spread<R>(j, ph.rpos));
+        if (ph.post.on) {  // swz is linear over GF(2): slot = swz(A tpart) ^ swz(A spread(j)) ^ swz(const)
+            s_pt[ph_i][threadIdx.x] = (uint16_t)swz(aff_lin(ph.post, tpart, T));
+            if (threadIdx.x < NR) s_pj[ph_i][threadIdx.x] = (uint16_t)swz(aff_lin(ph.post, reg_spread<R>(threadIdx.x, ph.rpos), T));
+        }
+    }
+    if (p.pre.on) {
+        s_lt[threadIdx.x] = (uint16_t)swz(aff_lin(p.pre, threadIdx.x, T));
+        if (threadIdx.x < (tsize >> kThreadBits)) s_lk[threadIdx.x] = (uint16_t)swz(aff_lin(p.pre, threadIdx.x << kThreadBits, T));
     }
     // HBM -> smem with cp.async, coalesced (consecutive e are consecutive
     // state indices in runs of 8); every element of the tile in flight at once
     const uint64_t pol = policy_evict_first();
     auto fetch = [&](uint64_t b, double2 *buf) {
-        for (int k = 0; k < per_thread; ++k) {
-            const uint32_t e = threadIdx.x + (uint32_t)k * kThreads;
-            cp_async16(buf + swz(e), p.x + b + (e & lowmask) + hi_off[e >> kLowBits], pol);
+        if (p.pre.on) {  // element e lands in the slot of its relabelled index
+            const uint32_t lt = s_lt[threadIdx.x] ^ swz(aff_const(p.pre, b | p.gbase));
+            for (int k = 0; k < per_thread; ++k) {
+                const uint32_t e = threadIdx.x + (uint32_t)k * kThreads;
+                cp_async16(buf + (lt ^ s_lk[k]), p.x + b + (e & lowmask) + hi_off[e >> kLowBits], pol);
+            }
+        } else {
+            for (int k = 0; k < per_thread; ++k) {
+                const uint32_t e = threadIdx.x + (uint32_t)k * kThreads;
+                cp_async16(buf + swz(e), p.x + b + (e & lowmask) + hi_off[e >> kLowBits], pol);
+            }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
@@ -334,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
             }
             double2 v[NR];
             uint32_t tpart;
-            if (ph_i < kPrePhases) {
+            if (ph_i < kPre) {
                 tpart = s_tpart[ph_i][threadIdx.x];
 #pragma unroll
                 for (int j = 0; j < NR; ++j) v[j] = tl[s_off[ph_i][j][threadIdx.x]];
@@ -345,7 +400,18 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
                 for (int j = 0; j < NR; ++j) v[j] = tl[swz(tpart | reg_spread<R>(j, ph.rpos))];
             }
             for (int gi = ph.g0; gi < ph.g1; ++gi) dispatch_gate<R, MODE>(v, sg[gi], tpart, sbase, sc, snz, scls);
-            if (ph_i < kPrePhases) {
+            if (ph.post.on) {
+                __syncthreads();  // relabelled slots belong to other threads' registers: all reads first
+                const uint32_t bc = aff_const(ph.post, sbase);
+                if (ph_i < kPre) {
+                    const uint32_t pt = s_pt[ph_i][threadIdx.x] ^ swz(bc);
+#pragma unroll
+                    for (int j = 0; j < NR; ++j) tl[pt ^ s_pj[ph_i][j]] = v[j];
+                } else {
+#pragma unroll
+                    for (int j = 0; j < NR; ++j) tl[swz(aff_lin(ph.post, tpart | reg_spread<R>(j, ph.rpos), T) ^ bc)] = v[j];
+                }
+            } else if (ph_i < kPre) {
 #pragma unroll
                 for (int j = 0; j < NR; ++j) tl[s_off[ph_i][j][threadIdx.x]] = v[j];
             } else {
@@ -394,6 +460,7 @@ struct PassPlan {
     std::vector<Phase> phases;
     std::vector<RegGate> gates;   // pass-relative
     Packed pk;                    // pass-relative coefficient tables
+    Affine pre;                   // permutation run opening the pass (pre.on = 0: none)
 };
 
 static int tile_pos(const std::vector<int> &bits, int shift) {
@@ -401,6 +468,121 @@ static int tile_pos(const std::vector<int> &bits, int shift) {
         if (bits[j] == shift) return (int)j;
     return -1;
 }
+
+// A gate whose matrix is a 0/1 permutation (entries exactly 1+0i or 0) that
+// is affine over GF(2) in the gate-index bits: old index x moves to new
+// index q(x) = XOR_{m: x_m} col[m] ^ d.  (X, CX in either orientation,
+// SWAP, X on several operands, ...; CCX/CSWAP are not affine.)
+struct PermGate {
+    bool ok = false;
+    uint32_t col[8] = {0};
+    uint32_t d = 0;
+};
+
+static PermGate perm_affine(const diaq_gate_t &gt) {
+    PermGate pg;
+    const int k = gt.k, M = 1 << k;
+    if (k < 1 || k > 8) return pg;
+    std::vector<int> q(M, -1);
+    for (int r = 0; r < M; ++r) {
+        int c1 = -1;
+        for (int c = 0; c < M; ++c) {
+            const double re = gt.g[2 * (r * M + c)], im = gt.g[2 * (r * M + c) + 1];
+            if (re == 1.0 && im == 0.0) {
+                if (c1 >= 0) return pg;
+                c1 = c;
+            } else if (!(re == 0.0 && im == 0.0)) {
+                return pg;
+            }
+        }
+        if (c1 < 0 || q[c1] >= 0) return pg;
+        q[c1] = r;  // new[r] = old[c1]: old index c1 moves to r
+    }
+    pg.d = (uint32_t)q[0];
+    for (int m = 0; m < k; ++m) pg.col[m] = (uint32_t)q[1 << m] ^ pg.d;
+    for (int x = 0; x < M; ++x) {
+        uint32_t y = pg.d;
+        for (int m = 0; m < k; ++m)
+            if ((x >> m) & 1) y ^= pg.col[m];
+        if (y != (uint32_t)q[x]) return pg;
+    }
+    pg.ok = true;
+    return pg;
+}
+
+// Host form of an Affine map while a run of permutation gates is folded:
+// row[o] is tile output bit o as a GF(2) combination of tile input bits
+// (bits 0..T-1), base (non-tile) state bits (T + i, state bit base[i]) and
+// the constant (bit 63).
+struct HostAffine {
+    int T = 0;
+    bool on = false;
+    std::vector<uint64_t> row;
+    std::vector<int> base;
+
+    void init(int t) {
+        T = t;
+        on = false;
+        row.assign(t, 0);
+        for (int o = 0; o < t; ++o) row[o] = 1ull << o;
+        base.clear();
+    }
+    // this <- q o this for one permutation gate; false if the map would need
+    // more than kMaxPermBase base bits
+    bool fold(const diaq_gate_t &gt, const PermGate &pg, const std::vector<int> &bits) {
+        const int k = gt.k;
+        std::vector<uint64_t> in(k), out(k);
+        std::vector<int> tp(k);
+        for (int i = 0; i < k; ++i) {
+            tp[i] = tile_pos(bits, gt.shifts[i]);
+            if (tp[i] >= 0) {
+                in[i] = row[tp[i]];
+            } else {
+                int idx = -1;
+                for (size_t b = 0; b < base.size(); ++b)
+                    if (base[b] == gt.shifts[i]) idx = (int)b;
+                if (idx < 0) {
+                    if ((int)base.size() >= kMaxPermBase) return false;
+                    idx = (int)base.size();
+                    base.push_back(gt.shifts[i]);
+                }
+                in[i] = 1ull << (T + idx);
+            }
+        }
+        // operand i is gate-index bit k-1-i
+        for (int i = 0; i < k; ++i) {
+            const int gb = k - 1 - i;
+            uint64_t e = ((pg.d >> gb) & 1u) ? (1ull << 63) : 0ull;
+            for (int m = 0; m < k; ++m)
+                if ((pg.col[m] >> gb) & 1u) e ^= in[k - 1 - m];
+            out[i] = e;
+        }
+        for (int i = 0; i < k; ++i) {
+            if (tp[i] >= 0) continue;
+            if (out[i] != in[i]) return false;  // a bit outside the tile cannot move (mixing bits are in the tile)
+        }
+        for (int i = 0; i < k; ++i)
+            if (tp[i] >= 0) row[tp[i]] = out[i];
+        on = true;
+        return true;
+    }
+    Affine pack() const {
+        Affine a;
+        memset(&a, 0, sizeof(a));
+        a.on = on ? 1 : 0;
+        if (!on) return a;
+        for (int o = 0; o < T; ++o) {
+            for (int j = 0; j < T; ++j)
+                if ((row[o] >> j) & 1ull) a.a[j] |= 1u << o;
+            for (size_t b = 0; b < base.size(); ++b)
+                if ((row[o] >> (T + b)) & 1ull) a.b[b] |= 1u << o;
+            if ((row[o] >> 63) & 1ull) a.c |= 1u << o;
+        }
+        a.nb = (int)base.size();
+        for (size_t b = 0; b < base.size(); ++b) a.bbit[b] = base[b];
+        return a;
+    }
+};
 
 static int pack_reg_gate(const diaq_gate_t &gt, const std::vector<int> &bits, const Phase &ph, int R, Packed &pk,
                          RegGate &G) {
@@ -536,15 +718,21 @@ static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gate
                     std::vector<PassPlan> &plan) {
     const int low = std::min(kLowBits, n_bits);
     std::vector<char> fast((size_t)ngates);  // register fast-path classification, once per gate
-    for (int i = 0; i < ngates; ++i) fast[(size_t)i] = (gates[i].k >= 1 && gates[i].k <= 5) ? fast_op(gates[i]) : 0;
+    std::vector<PermGate> perm((size_t)ngates);
+    for (int i = 0; i < ngates; ++i) {
+        fast[(size_t)i] = (gates[i].k >= 1 && gates[i].k <= 5) ? fast_op(gates[i]) : 0;
+        if (tuning().fused_perm && gates[i].k >= 1 && gates[i].k <= 5) perm[(size_t)i] = perm_affine(gates[i]);
+    }
     std::vector<int> members;
     std::vector<char> inb(64, 0);
+    std::vector<int> pbase;  // non-mixing operand bits of the pass's permutation gates (fold bound)
     int nb = 0;
     auto reset = [&]() {
         std::fill(inb.begin(), inb.end(), 0);
         nb = 0;
         for (int b = 0; b < low; ++b) { inb[b] = 1; ++nb; }
         members.clear();
+        pbase.clear();
     };
     auto flush = [&]() -> int {
         if (members.empty()) return DIAQ_OK;
@@ -555,43 +743,86 @@ static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gate
             if (!inb[b]) ps.bits.push_back(b);
         std::sort(ps.bits.begin(), ps.bits.end());
         ps.members = members;
-        size_t i = 0;
-        while (i < members.size()) {
-            if (!fast[(size_t)members[i]]) {  // cold path: its own shared-memory phase
-                Phase ph;
-                memset(&ph, 0, sizeof(ph));
-                ph.generic = 1;
-                ph.g0 = (int)ps.gates.size();
-                RegGate G;
-                const int rc = pack_smem_gate(gates[members[i]], ps.bits, ps.pk, G);
-                if (rc) return rc;
-                ps.gates.push_back(G);
-                ph.g1 = (int)ps.gates.size();
-                ps.phases.push_back(ph);
-                ++i;
+        // 1. phase specs: register phases (<= R mixing bits), generic smem
+        //    phases, and permutation runs folded into the previous phase's
+        //    store (or the tile load when the pass opens with one)
+        struct Spec {
+            int generic = 0;
+            std::vector<int> mem;
+            std::vector<int> used;
+            HostAffine post;
+        };
+        std::vector<Spec> specs;
+        HostAffine pre;
+        pre.init((int)ps.bits.size());
+        bool open = false;
+        for (size_t i = 0; i < members.size(); ++i) {
+            const int gi = members[i];
+            const diaq_gate_t &gt = gates[gi];
+            if (perm[(size_t)gi].ok) {
+                HostAffine *tgt;
+                if (specs.empty()) {
+                    tgt = &pre;
+                } else if (!specs.back().generic) {
+                    tgt = &specs.back().post;
+                } else {  // after a shared-memory phase: an empty register phase carries it
+                    Spec sp;
+                    sp.post.init((int)ps.bits.size());
+                    specs.push_back(sp);
+                    tgt = &specs.back().post;
+                }
+                open = false;
+                if (!tgt->fold(gt, perm[(size_t)gi], ps.bits))
+                    return set_error(DIAQ_ERR_VALUE, "fused pass: permutation fold overflow");
                 continue;
             }
-            std::vector<int> used;  // tile positions of mixing bits in this phase
-            size_t j = i;
-            while (j < members.size()) {
-                const diaq_gate_t &gt = gates[members[j]];
-                if (!fast[(size_t)members[j]]) break;
+            if (fast[(size_t)gi]) {
                 const uint32_t mix = mixing_mask(gt.k, gt.g);
                 std::vector<int> add;
                 for (int o = 0; o < gt.k; ++o)
                     if ((mix >> o) & 1u) {
                         const int tp = tile_pos(ps.bits, gt.shifts[o]);
-                        if (std::find(used.begin(), used.end(), tp) == used.end() &&
+                        if ((!open || std::find(specs.back().used.begin(), specs.back().used.end(), tp) ==
+                                          specs.back().used.end()) &&
                             std::find(add.begin(), add.end(), tp) == add.end())
                             add.push_back(tp);
                     }
-                if ((int)(used.size() + add.size()) > R) break;
-                used.insert(used.end(), add.begin(), add.end());
-                ++j;
+                if (open && (int)(specs.back().used.size() + add.size()) <= R) {
+                    specs.back().mem.push_back(gi);
+                    specs.back().used.insert(specs.back().used.end(), add.begin(), add.end());
+                } else {
+                    Spec sp;
+                    sp.mem = {gi};
+                    sp.used = add;
+                    sp.post.init((int)ps.bits.size());
+                    specs.push_back(sp);
+                    open = true;
+                }
+                continue;
             }
+            Spec sp;  // cold path: its own shared-memory phase
+            sp.generic = 1;
+            sp.mem = {gi};
+            specs.push_back(sp);
+            open = false;
+        }
+        ps.pre = pre.pack();
+        // 2. pack
+        for (const Spec &sp : specs) {
             Phase ph;
             memset(&ph, 0, sizeof(ph));
-            std::vector<int> rp = used;
+            if (sp.generic) {
+                ph.generic = 1;
+                ph.g0 = (int)ps.gates.size();
+                RegGate G;
+                const int rc = pack_smem_gate(gates[sp.mem[0]], ps.bits, ps.pk, G);
+                if (rc) return rc;
+                ps.gates.push_back(G);
+                ph.g1 = (int)ps.gates.size();
+                ps.phases.push_back(ph);
+                continue;
+            }
+            std::vector<int> rp = sp.used;
             for (int tp = 0; (int)rp.size() < R; ++tp)
                 if (std::find(rp.begin(), rp.end(), tp) == rp.end()) rp.push_back(tp);
             std::sort(rp.begin(), rp.end());
@@ -600,15 +831,15 @@ static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gate
             for (int tp = 0; tp < (int)ps.bits.size(); ++tp)
                 if (std::find(rp.begin(), rp.end(), tp) == rp.end()) ph.tpos[tq++] = tp;
             ph.g0 = (int)ps.gates.size();
-            for (size_t q = i; q < j; ++q) {
+            for (int gi : sp.mem) {
                 RegGate G;
-                const int rc = pack_reg_gate(gates[members[q]], ps.bits, ph, R, ps.pk, G);
+                const int rc = pack_reg_gate(gates[gi], ps.bits, ph, R, ps.pk, G);
                 if (rc) return rc;
                 ps.gates.push_back(G);
             }
             ph.g1 = (int)ps.gates.size();
+            ph.post = sp.post.pack();
             ps.phases.push_back(ph);
-            i = j;
         }
         if ((int)ps.phases.size() > kMaxPhases || (int)ps.gates.size() > kMaxPassGates)
             return set_error(DIAQ_ERR_VALUE, "fused pass too long");
@@ -633,7 +864,8 @@ static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gate
                 ++kout;
             }
         }
-        if (kin > kMaxRegKin || kin > R || kout > kMaxSel) {  // standalone pass
+        const bool pg = perm[(size_t)i].ok;
+        if (pg ? (kin > T - low) : (kin > kMaxRegKin || kin > R || kout > kMaxSel)) {  // standalone pass
             int rc = flush();
             if (rc) return rc;
             reset();
@@ -642,8 +874,15 @@ static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gate
             plan.push_back(ps);
             continue;
         }
+        // non-mixing operands of permutation gates may end up outside the tile;
+        // the folded maps carry at most kMaxPermBase of them
+        int padd = 0;
+        if (pg)
+            for (int j = 0; j < gt.k; ++j)
+                if (!((mix >> j) & 1u) && std::find(pbase.begin(), pbase.end(), gt.shifts[j]) == pbase.end()) ++padd;
         // phases per pass are bounded too: a pass can need up to one phase per gate
-        if (nb + add > T || (int)members.size() >= std::min(kMaxPassGates, kMaxPhases)) {
+        if (nb + add > T || (int)members.size() >= std::min(kMaxPassGates, kMaxPhases) ||
+            (int)pbase.size() + padd > kMaxPermBase) {
             int rc = flush();
             if (rc) return rc;
             reset();
@@ -653,6 +892,10 @@ static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gate
         }
         for (int j = 0; j < gt.k; ++j)
             if (((mix >> j) & 1u) && !inb[gt.shifts[j]]) { inb[gt.shifts[j]] = 1; ++nb; }
+        if (pg)
+            for (int j = 0; j < gt.k; ++j)
+                if (!((mix >> j) & 1u) && std::find(pbase.begin(), pbase.end(), gt.shifts[j]) == pbase.end())
+                    pbase.push_back(gt.shifts[j]);
         members.push_back(i);
     }
     return flush();
@@ -766,6 +1009,7 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
             p.nnz = (int)ps.pk.nz.size();
             p.ncls = (int)ps.pk.cls.size();
             p.gbase = sharded ? ((uint64_t)rank << n_bits) : 0ull;
+            p.pre = ps.pre;
             const size_t tables = sizeof(double2) * p.ncoef + sizeof(uint32_t) * (p.nnz + p.ncls);
             const void *f = R >= 4 ? tile_kernel_ptr<4>(cmul_mode) : tile_kernel_ptr<3>(cmul_mode);
             int per_sm = 1;

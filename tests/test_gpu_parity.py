@@ -410,6 +410,56 @@ def test_fused_passes_match_unfused(cmul):
             assert np.array_equal(got, want), (n, tb)
 
 
+def _perm_gate(q):
+    """0/1 matrix moving old index c to new index q[c]."""
+    m = np.zeros((len(q), len(q)), dtype=complex)
+    for c, r in enumerate(q):
+        m[r, c] = 1.0
+    return m
+
+
+@pytest.mark.parametrize("fold", [1, 0], ids=["folded", "executed"])
+def test_fused_permutation_runs(cmul, fold):
+    """X / CX / SWAP runs (and any 2-qubit 0/1 permutation) folded into the
+    passes' shared-memory addressing: runs opening a pass, closing a phase,
+    after a shared-memory phase, with controls inside and outside the tile
+    (more than the fold bound, forcing a new pass), against gate-by-gate."""
+    from paper_2405_01250_b200 import _lib as L
+    rng = np.random.default_rng(21)
+    L.tune("fused_perm", fold)
+    try:
+        for n in (9, 12, 16, 20):
+            ops = [("cx", (int(n - 1 - i), int(i % 3)), ()) for i in range(min(n - 3, 12))]  # high controls
+            ops += [("x", (0,), ()), ("swap", (1, n - 1), ())]
+            ops += W.random_layered_ops(n, 2, seed=n)
+            for _ in range(10):
+                q = [int(v) for v in rng.choice(n, size=3, replace=False)]
+                ops += [("cz", (q[0], q[1]), ()), ("cx", (q[1], q[2]), ()), ("x", (q[2],), ()),
+                        ("ry", (q[0],), (0.3,)), ("cx", (q[2], q[0]), ()), ("swap", (q[0], q[2]), ()),
+                        ("ccx", (q[0], q[1], q[2]), ()), ("cx", (q[0], q[1]), ())]
+            pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
+            for cyc in ([1, 3, 0, 2], [2, 0, 3, 1], [3, 2, 1, 0]):
+                a, b = (int(v) for v in rng.choice(n, size=2, replace=False))
+                lo, hi = min(a, b), max(a, b)
+                pls.append(D.Placement(2**lo, None, 2 ** (n - 1 - hi), lo, hi, "perm",
+                                       gate=(_perm_gate(cyc), [a - lo, b - lo])))
+            x0 = D.StateVector(n, W.random_state(rng, 2**n))
+            want = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=0).amps
+            for tb in (8, 11, 12):
+                got = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=tb).amps
+                assert np.array_equal(got, want), (n, tb)
+        # a pure permutation circuit is a relabelling: exact values, any order of runs
+        n = 18
+        ops = [("cx", (int(a), int(b)), ()) for a, b in rng.integers(0, n, size=(60, 2)) if a != b]
+        ops += [("x", (int(q),), ()) for q in rng.integers(0, n, size=10)]
+        pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
+        x0 = D.StateVector(n, W.random_state(rng, 2**n))
+        want = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=0).amps
+        assert np.array_equal(D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=11).amps, want)
+    finally:
+        L.tune("fused_perm", 1)
+
+
 def test_spmv_host_pipeline_chunks(monkeypatch):
     """Pipelined host spmv (chunked H2D / kernel / D2H) is bitwise the device spmv."""
     import torch
