@@ -55,9 +55,8 @@ struct RegGate {
     int nz_off;               // nz[nz_off + (b << kin) + r]
     int cls_off;              // cls[cls_off + b]: 0 general, 1 identity (skip), 2 swap (kin 1)
     // fast-path classification (host): 0 generic, 1 dense 1-qubit (no selector),
-    // 2 diagonal with one selector, 3 selector-controlled swap (CX-like)
+    // 2 diagonal with one selector
     int op;
-    int swap_when;            // op 3: selector value whose block is the swap
     int mpos;                 // generic phases: tile position of the mixing bit
 };
 
@@ -181,31 +180,7 @@ __device__ __forceinline__ void diag_reg(double2 (&v)[1 << R], double2 d0, doubl
     }
 }
 
-template <int R, int B1>
-__device__ __forceinline__ void swap_all(double2 (&v)[1 << R]) {
-#pragma unroll
-    for (int g = 0; g < (1 << (R - 1)); ++g) {
-        const int j0 = ((g >> B1) << (B1 + 1)) | (g & ((1 << B1) - 1));
-        const int j1 = j0 | (1 << B1);
-        const double2 t = v[j0];
-        v[j0] = v[j1];
-        v[j1] = t;
-    }
-}
 
-template <int R, int RC, int B1>
-__device__ __forceinline__ void swap_ctrl(double2 (&v)[1 << R], int when) {
-#pragma unroll
-    for (int g = 0; g < (1 << (R - 1)); ++g) {
-        const int j0 = ((g >> B1) << (B1 + 1)) | (g & ((1 << B1) - 1));
-        const int j1 = j0 | (1 << B1);
-        if (((j0 >> RC) & 1) == when) {
-            const double2 t = v[j0];
-            v[j0] = v[j1];
-            v[j1] = t;
-        }
-    }
-}
 
 // compile-time dispatch of a runtime register bit b in [0, R)
 #define DIAQ_RB_DISPATCH(R_, b_, CALL)                              \
@@ -216,16 +191,18 @@ __device__ __forceinline__ void swap_ctrl(double2 (&v)[1 << R], int when) {
         else { constexpr int RB_ = (R_) >= 4 ? 3 : 2; CALL; }       \
     } while (0)
 
-template <int R, int RC, int MODE>
-__device__ __forceinline__ void swap_ctrl_b1(double2 (&v)[1 << R], int b1, int when) {
-    if (b1 == 0) { if constexpr (RC != 0) swap_ctrl<R, RC, 0>(v, when); }
-    else if (b1 == 1) { if constexpr (RC != 1) swap_ctrl<R, RC, 1>(v, when); }
-    else if (R == 3 || b1 == 2) { if constexpr (RC != 2) swap_ctrl<R, RC, 2>(v, when); }
-    else { if constexpr (R >= 4 && RC != 3) swap_ctrl<R, RC, (R >= 4 ? 3 : 2)>(v, when); }
+
+// the tile's full-state base lives in shared memory and is re-read where a
+// selector needs it (an asm load: not hoisted into a register held across
+// the gate loop, where it would push the fast paths into spills)
+__device__ __forceinline__ uint64_t ld_base(const uint64_t *s) {
+    uint64_t v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(smem_u32(s)));
+    return v;
 }
 
 template <int R, int MODE>
-__device__ __forceinline__ void dispatch_gate(double2 (&v)[1 << R], const RegGate &G, uint32_t tpart, uint64_t base,
+__device__ __forceinline__ void dispatch_gate(double2 (&v)[1 << R], const RegGate &G, uint32_t tpart, const uint64_t *sbase_p,
                                               const double2 *sc, const uint32_t *snz, const uint32_t *scls) {
     // if-chains, not switches: a jump table would force v[] into local memory
     (void)scls;
@@ -242,20 +219,11 @@ __device__ __forceinline__ void dispatch_gate(double2 (&v)[1 << R], const RegGat
         if (G.osel[0] == 2) {
             DIAQ_RB_DISPATCH(R, G.opos[0], (diag_reg<R, RB_, MODE>(v, d0, d1, z0, z1)));
         } else {
-            const uint32_t b = G.osel[0] == 0 ? (uint32_t)((base >> G.opos[0]) & 1ull) : (tpart >> G.opos[0]) & 1u;
+            const uint32_t b = G.osel[0] == 0 ? (uint32_t)((ld_base(sbase_p) >> G.opos[0]) & 1ull) : (tpart >> G.opos[0]) & 1u;
             const double2 d = b ? d1 : d0;
             const bool nz = b ? (z1 & 1u) : (z0 & 1u);
 #pragma unroll
             for (int j = 0; j < (1 << R); ++j) v[j] = nz ? cmul<MODE>(d, v[j]) : make_double2(0.0, 0.0);
-        }
-        return;
-    }
-    if (G.op == 3) {
-        if (G.osel[0] == 2) {
-            DIAQ_RB_DISPATCH(R, G.opos[0], (swap_ctrl_b1<R, RB_, MODE>(v, G.rb[0], G.swap_when)));
-        } else {
-            const uint32_t b = G.osel[0] == 0 ? (uint32_t)((base >> G.opos[0]) & 1ull) : (tpart >> G.opos[0]) & 1u;
-            if ((int)b == G.swap_when) DIAQ_RB_DISPATCH(R, G.rb[0], (swap_all<R, RB_>(v)));
         }
         return;
     }
@@ -311,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
     __shared__ uint16_t s_pj[kPre][1 << R];
     __shared__ uint16_t s_lt[kThreads];
     __shared__ uint16_t s_lk[1 << (kMaxTileBits - kThreadBits)];
+    __shared__ uint64_t s_sbase;  // current tile's base | rank bits (selector lookups)
     constexpr int NR = 1 << R;
     const int T = p.tbits;
     const uint32_t tsize = 1u << T;
@@ -352,8 +321,8 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
     }
     // HBM -> smem with cp.async, coalesced (consecutive e are consecutive
     // state indices in runs of 8); every element of the tile in flight at once
-    const uint64_t pol = policy_evict_first();
     auto fetch = [&](uint64_t b, double2 *buf) {
+        const uint64_t pol = policy_evict_first();
         if (p.pre.on) {  // element e lands in the slot of its relabelled index
             const uint32_t lt = s_lt[threadIdx.x] ^ swz(aff_const(p.pre, b | p.gbase));
             for (int k = 0; k < per_thread; ++k) {
@@ -375,14 +344,14 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
     if ((int64_t)blockIdx.x < p.ntiles) fetch(base, tile);
     double2 *tl = tile;
     for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-        const uint64_t sbase = base | p.gbase;  // full-state index bits for selectors
+        if (threadIdx.x == 0) s_sbase = base | p.gbase;  // full-state index bits for selectors
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncthreads();
         for (int ph_i = 0; ph_i < p.nphases; ++ph_i) {
             const Phase &ph = sph[ph_i];
             if (ph.generic) {
                 for (int gi = ph.g0; gi < ph.g1; ++gi) {
-                    smem_gate<MODE>(tl, T, sg[gi], sbase, sc, snz);
+                    smem_gate<MODE>(tl, T, sg[gi], ld_base(&s_sbase), sc, snz);
                     __syncthreads();
                 }
                 continue;
@@ -399,10 +368,10 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
 #pragma unroll
                 for (int j = 0; j < NR; ++j) v[j] = tl[swz(tpart | reg_spread<R>(j, ph.rpos))];
             }
-            for (int gi = ph.g0; gi < ph.g1; ++gi) dispatch_gate<R, MODE>(v, sg[gi], tpart, sbase, sc, snz, scls);
+            for (int gi = ph.g0; gi < ph.g1; ++gi) dispatch_gate<R, MODE>(v, sg[gi], tpart, &s_sbase, sc, snz, scls);
             if (ph.post.on) {
                 __syncthreads();  // relabelled slots belong to other threads' registers: all reads first
-                const uint32_t bc = aff_const(ph.post, sbase);
+                const uint32_t bc = aff_const(ph.post, ld_base(&s_sbase));
                 if (ph_i < kPre) {
                     const uint32_t pt = s_pt[ph_i][threadIdx.x] ^ swz(bc);
 #pragma unroll
@@ -655,16 +624,12 @@ static int pack_reg_gate(const diaq_gate_t &gt, const std::vector<int> &bits, co
     G.op = 0;
     if (G.kin == 1 && G.kout == 0) G.op = 1;
     else if (G.kin == 0 && G.kout == 1) G.op = 2;
-    else if (G.kin == 1 && G.kout == 1) {
-        const uint32_t c0 = pk.cls[G.cls_off], c1 = pk.cls[G.cls_off + 1];
-        if (c0 == 1 && c1 == 2) { G.op = 3; G.swap_when = 1; }
-        else if (c0 == 2 && c1 == 1) { G.op = 3; G.swap_when = 0; }
-    }
     return DIAQ_OK;
 }
 
-// gates the register fast paths handle: dense 1-qubit, 1-selector diagonal,
-// 1-selector controlled swap (classification by pack_reg_gate on a dummy phase)
+// gates the register fast paths handle: dense 1-qubit and 1-selector
+// diagonal.  (Controlled swaps -- CX -- are permutations: folded into the
+// pass addressing, see HostAffine; the shared-memory path takes the rest.)
 static bool fast_op(const diaq_gate_t &gt) {
     const uint32_t mix = mixing_mask(gt.k, gt.g);
     int kin = 0;
@@ -673,21 +638,7 @@ static bool fast_op(const diaq_gate_t &gt) {
     if (kin > 1 || kout > 1) return false;
     if (kin == 1 && kout == 0) return true;
     if (kin == 0 && kout == 1) return true;
-    // kin == 1 && kout == 1: blocks must be {identity, swap}
-    std::vector<int> bits;
-    for (int b = 0; b < 64; ++b) bits.push_back(b);
-    Phase ph;
-    memset(&ph, 0, sizeof(ph));
-    int mshift = -1;
-    for (int i = 0; i < gt.k; ++i)
-        if ((mix >> i) & 1u) mshift = gt.shifts[i];
-    ph.rpos[0] = mshift;
-    ph.rpos[1] = 62;
-    ph.rpos[2] = 63;
-    Packed pk;
-    RegGate G;
-    if (pack_reg_gate(gt, bits, ph, 3, pk, G) != DIAQ_OK) return false;
-    return G.op == 3;
+    return false;
 }
 
 static int pack_smem_gate(const diaq_gate_t &gt, const std::vector<int> &bits, Packed &pk, RegGate &G) {
