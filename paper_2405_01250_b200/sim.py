@@ -52,7 +52,7 @@ CMUL_MODE = _probe_numpy_cmul()
 
 # shared-memory tile of the fused multi-gate passes (diaq_run_gates_fused);
 # 0 applies every gate as its own HBM sweep.  Results are identical.
-FUSE_TILE_BITS = 11
+FUSE_TILE_BITS = 12
 
 
 class StateVector:
@@ -227,18 +227,42 @@ def measure_all_sample(x: StateVector, shots: int, seed: int) -> dict[str, int]:
 # -- driver ----------------------------------------------------------------------
 
 
+_GATE_DTYPE = np.dtype({"names": ["k", "shifts", "g"], "formats": ["<i4", ("<i4", 5), "<u8"],
+                        "offsets": [0, 4, 24], "itemsize": 32})  # diaq_gate_t
+
+
 class _GateProgram:
-    """Compact gates packed for diaq_run_gates (keeps host buffers alive)."""
+    """Compact gates packed for diaq_run_gates (keeps host buffers alive).
+    Packed with numpy into the diaq_gate_t layout; the last program is
+    cached per run of Placement objects (held, so their ids stay theirs)."""
+
+    _last: tuple | None = None
 
     def __init__(self, comps):
-        self.mats = [np.ascontiguousarray(g, dtype=np.complex128) for g, _ in comps]
-        self.arr = (L.Gate * max(1, len(comps)))()
-        for i, ((_, shifts), g) in enumerate(zip(comps, self.mats)):
-            self.arr[i].k = len(shifts)
-            for j, s in enumerate(shifts):
-                self.arr[i].shifts[j] = int(s)
-            self.arr[i].g = g.ctypes.data
-        self.n = len(comps)
+        n = len(comps)
+        self.buf = np.zeros(max(1, n), dtype=_GATE_DTYPE)
+        if n:
+            # every gate matrix in one contiguous host block; g = base + offset
+            self.mats = np.concatenate([g for g, _ in comps], axis=None).astype(np.complex128, copy=False)
+            sizes = np.fromiter((g.size for g, _ in comps), dtype=np.int64, count=n)
+            offs = np.zeros(n, dtype=np.int64)
+            np.cumsum(sizes[:-1], out=offs[1:])
+            pad = (0, 0, 0, 0, 0)
+            self.buf["k"][:n] = [len(sh) for _, sh in comps]
+            self.buf["shifts"][:n] = [tuple(sh) + pad[len(sh):] for _, sh in comps]
+            self.buf["g"][:n] = self.mats.ctypes.data + 16 * offs
+        self.arr = self.buf.ctypes.data_as(ctypes.POINTER(L.Gate))
+        self.n = n
+
+    @classmethod
+    def for_placements(cls, pls):
+        key = tuple(id(p) for p in pls)
+        last = cls._last
+        if last is not None and last[0] == key:
+            return last[2]
+        prog = cls([p.compact() for p in pls])
+        cls._last = (key, list(pls), prog)
+        return prog
 
 
 def run_gates(state: StateVector, placements: list[Placement], cmul_mode: int | None = None,
@@ -257,12 +281,10 @@ def run_gates(state: StateVector, placements: list[Placement], cmul_mode: int | 
     s = L.stream_handle()
     while i < len(placements):
         j = i
-        comps = []
         while j < len(placements) and placements[j].compact() is not None:
-            comps.append(placements[j].compact())
             j += 1
-        if comps:
-            prog = _GateProgram(comps)
+        if j > i:
+            prog = _GateProgram.for_placements(placements[i:j])
             evs = timer.slice_ptr(i) if timer is not None else None
             tb = FUSE_TILE_BITS if tile_bits is None else tile_bits
             if tb > 0:

@@ -22,7 +22,7 @@ def cmul(configs):
     return L.CMUL_FMA if configs["meta"]["numpy_cmul"] == "fma" else L.CMUL_PLAIN
 
 
-@pytest.fixture(params=[0, 11], ids=["gate-by-gate", "fused"], autouse=True)
+@pytest.fixture(params=[0, 11, 12], ids=["gate-by-gate", "fused11", "fused12"], autouse=True)
 def fuse_mode(request):
     old = D.sim.FUSE_TILE_BITS
     D.sim.FUSE_TILE_BITS = request.param
