@@ -208,6 +208,13 @@ int diaq_timer_destroy(int n, void **events);
 int diaq_run_gates_fused(int n_bits, int ngates, const diaq_gate_t *gates, void *state, int cmul_mode,
                          int tile_bits, void **events, int *npasses, void *stream);
 
+/* Host-only view of the fused schedule (no device work): stats[0] HBM
+ * passes, [1] of them single-gate (gate kernel), [2] register/smem phases
+ * in the tiled passes, [3] permutation gates folded into pass addressing,
+ * [4] shared-memory (generic) phases.  local_bits < n_bits: one rank's
+ * shard, as diaq_run_gates_local. */
+int diaq_fused_plan(int n_bits, int local_bits, int ngates, const diaq_gate_t *gates, int tile_bits, int *stats);
+
 /* ---- state helpers ------------------------------------------------------ */
 /* |index> (reference init_state, sim.py:53-59) */
 int diaq_init_basis(int64_t n_amps, void *x, int64_t index, void *stream);

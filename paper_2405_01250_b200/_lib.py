@@ -80,6 +80,7 @@ _SIGS = {
     "diaq_apply_gate": ([_INT, _INT, _P, _P, _P, _P, _INT, _P], _INT),
     "diaq_run_gates": ([_INT, _INT, ctypes.POINTER(Gate), _P, _INT, _P, _P], _INT),
     "diaq_run_gates_fused": ([_INT, _INT, ctypes.POINTER(Gate), _P, _INT, _INT, _P, _P, _P], _INT),
+    "diaq_fused_plan": ([_INT, _INT, _INT, ctypes.POINTER(Gate), _INT, _P], _INT),
     "diaq_init_basis": ([_I64, _P, _I64, _P], _INT),
     "diaq_norm2": ([_I64, _P, _P, _P], _INT),
     "diaq_run_gates_local": ([_INT, _INT, _I64, _INT, ctypes.POINTER(Gate), _P, _INT, _INT, _P, _P, _P], _INT),

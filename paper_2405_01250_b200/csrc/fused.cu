@@ -25,6 +25,7 @@
 // applies (the same argument as the sharded kernel, apply.cu).
 #include <algorithm>
 #include <cstring>
+#include <memory>
 #include <vector>
 
 #include "common.cuh"
@@ -169,6 +170,21 @@ __device__ __forceinline__ void dense1(double2 (&v)[1 << R], const double2 *c, u
     }
 }
 
+// all four entries nonzero (RX, RY, H, U3 ...): branch-free, so the
+// compiler interleaves the 2^R independent multiply-add chains
+template <int R, int B1, int MODE>
+__device__ __forceinline__ void dense1_full(double2 (&v)[1 << R], const double2 *c) {
+    const double2 c00 = c[0], c01 = c[1], c10 = c[2], c11 = c[3];
+#pragma unroll
+    for (int g = 0; g < (1 << (R - 1)); ++g) {
+        const int j0 = ((g >> B1) << (B1 + 1)) | (g & ((1 << B1) - 1));
+        const int j1 = j0 | (1 << B1);
+        const double2 x0 = v[j0], x1 = v[j1];
+        v[j0] = cadd(cmul<MODE>(c00, x0), cmul<MODE>(c01, x1));
+        v[j1] = cadd(cmul<MODE>(c10, x0), cmul<MODE>(c11, x1));
+    }
+}
+
 template <int R, int RB, int MODE>
 __device__ __forceinline__ void diag_reg(double2 (&v)[1 << R], double2 d0, double2 d1, uint32_t z0, uint32_t z1) {
 #pragma unroll
@@ -210,7 +226,8 @@ __device__ __forceinline__ void dispatch_gate(double2 (&v)[1 << R], const RegGat
     if (G.op == 1) {
         const double2 *c = sc + G.coef_off;
         const uint32_t n0 = snz[G.nz_off], n1 = snz[G.nz_off + 1];
-        DIAQ_RB_DISPATCH(R, G.rb[0], (dense1<R, RB_, MODE>(v, c, n0, n1)));
+        if ((n0 & n1 & 3u) == 3u) DIAQ_RB_DISPATCH(R, G.rb[0], (dense1_full<R, RB_, MODE>(v, c)));
+        else DIAQ_RB_DISPATCH(R, G.rb[0], (dense1<R, RB_, MODE>(v, c, n0, n1)));
         return;
     }
     if (G.op == 2) {
@@ -857,10 +874,28 @@ int apply_gate(int n_bits, int k, const double *g, const int *shifts, const void
 int apply_gate_sharded_own(int n_bits, int local_bits, int k, const double *g, const int *shifts, int64_t rank,
                            void *shard, int cmul_mode, cudaStream_t s);
 
+// resident CTAs per SM for (kernel, dynamic smem), and the SM count: asked
+// of the runtime once per process (each query costs microseconds per pass)
+static int occupancy(const void *f, size_t smem) {
+    thread_local std::vector<std::pair<std::pair<const void *, size_t>, int>> memo;
+    for (const auto &m : memo)
+        if (m.first.first == f && m.first.second == smem) return m.second;
+    int per_sm = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kThreads, smem) != cudaSuccess) {
+        cudaGetLastError();
+        per_sm = 1;
+    }
+    memo.push_back({{f, smem}, per_sm});
+    return per_sm;
+}
+
 static int sm_count_f() {
+    thread_local int cached = 0;
+    if (cached) return cached;
     int dev = 0, sms = kSms;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaGetLastError();
+    cached = sms;
     return sms;
 }
 
@@ -874,32 +909,80 @@ static const void *tile_kernel_ptr(int cmul_mode) {
 
 using namespace diaq;
 
-static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const diaq_gate_t *gates, void *state,
-                     int cmul_mode, int tile_bits, void **events, int *npasses, void *stream) {
-    if (ngates < 0 || (ngates > 0 && !gates) || !state)
-        return set_error(DIAQ_ERR_VALUE, "diaq_run_gates_fused: bad arguments");
-    const bool sharded = n_total > n_bits;
-    cudaStream_t s = (cudaStream_t)stream;
-    // tile_bits 12 -> 16 amplitudes per thread (R = 4), else 8 (R = 3); 256 threads
-    const int T = tile_bits >= kThreadBits + 4 ? kThreadBits + 4 : kThreadBits + 3;
-    const bool tiled = n_bits >= T;
-    const int R = T - kThreadBits;
+// A scheduled and packed gate program.  Scheduling 10^3 gates costs about a
+// millisecond of host time -- as much as the passes themselves at n = 20 --
+// so the last few programs are kept per thread, keyed by the exact gate data,
+// together with their device copy (uploaded once per device: a per-call
+// pageable upload would stall the host behind the stream's queued passes).
+struct Program {
+    struct Off { size_t ph, g, coef, nz, cls; };
+    std::vector<char> key;
     std::vector<PassPlan> plan;
-    int rc = DIAQ_OK;
-    if (tiled) {
-        rc = schedule(n_bits, n_total, ngates, gates, T, R, plan);
-        if (rc) return rc;
-    } else {  // state smaller than a tile: gate by gate (standalone path below)
+    std::vector<Off> off;
+    std::vector<char> host;  // per pass [phases | gates | coef | nz | cls], 16-byte aligned
+    mutable std::vector<std::pair<int, char *>> dev;
+
+    const char *device_copy(int &rc) const {
+        int d = 0;
+        cudaGetDevice(&d);
+        for (const auto &e : dev)
+            if (e.first == d) return e.second;
+        char *p = nullptr;
+        if (cudaMalloc((void **)&p, host.size()) != cudaSuccess ||
+            cudaMemcpy(p, host.data(), host.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaGetLastError();
+            if (p) cudaFree(p);
+            rc = set_error(DIAQ_ERR_CUDA, "diaq_run_gates_fused: program upload failed");
+            return nullptr;
+        }
+        dev.push_back({d, p});
+        return p;
+    }
+    ~Program() {  // evicted: passes still queued may read the copy
+        int cur = 0;
+        const bool have = cudaGetDevice(&cur) == cudaSuccess;
+        for (const auto &e : dev) {
+            if (cudaSetDevice(e.first) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess) cudaFree(e.second);
+        }
+        if (have) cudaSetDevice(cur);
+        cudaGetLastError();
+    }
+};
+
+static std::vector<char> program_key(int n_total, int n_bits, int T, int ngates, const diaq_gate_t *gates) {
+    std::vector<char> key;
+    auto put = [&](const void *p, size_t n) {
+        const char *c = (const char *)p;
+        key.insert(key.end(), c, c + n);
+    };
+    const int head[5] = {n_total, n_bits, T, ngates, tuning().fused_perm};
+    put(head, sizeof(head));
+    for (int i = 0; i < ngates; ++i) {
+        const diaq_gate_t &gt = gates[i];
+        put(&gt.k, sizeof(int));
+        if (gt.k < 1 || gt.k > 5) continue;  // rejected by schedule()
+        put(gt.shifts, sizeof(int) * gt.k);
+        put(gt.g, sizeof(double) * 2 * ((size_t)1 << (2 * gt.k)));
+    }
+    return key;
+}
+
+static std::shared_ptr<const Program> build_program(int n_total, int n_bits, int T, int ngates, const diaq_gate_t *gates,
+                                                    int &rc) {
+    auto prog = std::make_shared<Program>();
+    std::vector<PassPlan> &plan = prog->plan;
+    if (n_bits >= T) {
+        rc = schedule(n_bits, n_total, ngates, gates, T, T - kThreadBits, plan);
+        if (rc) return nullptr;
+    } else {  // state smaller than a tile: gate by gate (standalone path)
         for (int i = 0; i < ngates; ++i) {
             PassPlan ps;
             ps.members = {i};
             plan.push_back(ps);
         }
     }
-    if (npasses) *npasses = (int)plan.size();
-    // one device buffer: per pass [phases | gates | coef | nz | cls], 16-byte aligned
-    struct Off { size_t ph, g, coef, nz, cls; };
-    std::vector<Off> off(plan.size());
+    std::vector<Program::Off> &off = prog->off;
+    off.resize(plan.size());
     size_t cur = 0;
     auto al = [](size_t v) { return (v + 15) & ~(size_t)15; };
     for (size_t i = 0; i < plan.size(); ++i) {
@@ -910,8 +993,8 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
         off[i].nz = cur; cur = al(cur + sizeof(uint32_t) * ps.pk.nz.size());
         off[i].cls = cur; cur = al(cur + sizeof(uint32_t) * ps.pk.cls.size());
     }
-    const size_t bytes = cur + 16;
-    std::vector<char> host(bytes, 0);
+    std::vector<char> &host = prog->host;
+    host.assign(cur + 16, 0);
     for (size_t i = 0; i < plan.size(); ++i) {
         const PassPlan &ps = plan[i];
         if (!ps.phases.empty()) memcpy(&host[off[i].ph], ps.phases.data(), sizeof(Phase) * ps.phases.size());
@@ -920,11 +1003,51 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
         if (!ps.pk.nz.empty()) memcpy(&host[off[i].nz], ps.pk.nz.data(), sizeof(uint32_t) * ps.pk.nz.size());
         if (!ps.pk.cls.empty()) memcpy(&host[off[i].cls], ps.pk.cls.data(), sizeof(uint32_t) * ps.pk.cls.size());
     }
-    char *dbuf = nullptr;
+    rc = DIAQ_OK;
+    return prog;
+}
+
+static std::shared_ptr<const Program> cached_program(int n_total, int n_bits, int T, int ngates,
+                                                     const diaq_gate_t *gates, int &rc) {
+    constexpr size_t kKeep = 4;
+    thread_local std::vector<std::shared_ptr<const Program>> cache;  // most recent first
+    std::vector<char> key = program_key(n_total, n_bits, T, ngates, gates);
+    for (size_t i = 0; i < cache.size(); ++i)
+        if (cache[i]->key == key) {
+            std::shared_ptr<const Program> hit = cache[i];
+            cache.erase(cache.begin() + (long)i);
+            cache.insert(cache.begin(), hit);
+            rc = DIAQ_OK;
+            return hit;
+        }
+    std::shared_ptr<const Program> prog = build_program(n_total, n_bits, T, ngates, gates, rc);
+    if (!prog) return nullptr;
+    const_cast<Program &>(*prog).key = std::move(key);
+    cache.insert(cache.begin(), prog);
+    if (cache.size() > kKeep) cache.pop_back();
+    return prog;
+}
+
+static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const diaq_gate_t *gates, void *state,
+                     int cmul_mode, int tile_bits, void **events, int *npasses, void *stream) {
+    if (ngates < 0 || (ngates > 0 && !gates) || !state)
+        return set_error(DIAQ_ERR_VALUE, "diaq_run_gates_fused: bad arguments");
+    const bool sharded = n_total > n_bits;
+    cudaStream_t s = (cudaStream_t)stream;
+    // tile_bits 12 -> 16 amplitudes per thread (R = 4), else 8 (R = 3); 256 threads
+    const int T = tile_bits >= kThreadBits + 4 ? kThreadBits + 4 : kThreadBits + 3;
+    const bool tiled = n_bits >= T;
+    const int R = T - kThreadBits;
+    int rc = DIAQ_OK;
+    std::shared_ptr<const Program> prog = cached_program(n_total, n_bits, T, ngates, gates, rc);
+    if (!prog) return rc;
+    const std::vector<PassPlan> &plan = prog->plan;
+    const std::vector<Program::Off> &off = prog->off;
+    if (npasses) *npasses = (int)plan.size();
+    const char *dbuf = nullptr;
     if (tiled && !plan.empty()) {
-        if (cudaMallocAsync((void **)&dbuf, bytes, s) != cudaSuccess)
-            return set_error(DIAQ_ERR_CUDA, "diaq_run_gates_fused: program alloc failed");
-        cudaMemcpyAsync(dbuf, host.data(), bytes, cudaMemcpyHostToDevice, s);
+        dbuf = prog->device_copy(rc);
+        if (!dbuf) return rc;
     }
     const size_t smem_max = (sizeof(double2) << kMaxTileBits) + 48 * 1024;
     static bool attr_set = false;
@@ -966,7 +1089,7 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
             int per_sm = 1;
             const size_t smem = (sizeof(double2) << p.tbits) + tables;
             if (smem > smem_max) return set_error(DIAQ_ERR_VALUE, "fused pass tables exceed shared memory");
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kThreads, smem);
+            per_sm = occupancy(f, smem);
             const int64_t grid =
                 std::max<int64_t>(1, std::min<int64_t>(p.ntiles, (int64_t)sm_count_f() * std::max(1, per_sm)));
             p.tmask = 0;
@@ -984,13 +1107,38 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
         if (events && rc == DIAQ_OK)
             for (int gi : ps.members) cudaEventRecord((cudaEvent_t)events[gi + 1], s);
     }
-    if (dbuf) cudaFreeAsync(dbuf, s);
     return rc;
 }
 
 extern "C" int diaq_run_gates_fused(int n_bits, int ngates, const diaq_gate_t *gates, void *state, int cmul_mode,
                                     int tile_bits, void **events, int *npasses, void *stream) {
     return run_fused(n_bits, n_bits, 0, ngates, gates, state, cmul_mode, tile_bits, events, npasses, stream);
+}
+
+extern "C" int diaq_fused_plan(int n_bits, int local_bits, int ngates, const diaq_gate_t *gates, int tile_bits,
+                               int *stats) {
+    if (ngates < 0 || (ngates > 0 && !gates) || !stats) return set_error(DIAQ_ERR_VALUE, "diaq_fused_plan: bad arguments");
+    if (local_bits < 1 || local_bits > n_bits) return set_error(DIAQ_ERR_SHAPE, "local_bits %d invalid", local_bits);
+    const int T = tile_bits >= kThreadBits + 4 ? kThreadBits + 4 : kThreadBits + 3;
+    for (int i = 0; i < 5; ++i) stats[i] = 0;
+    if (local_bits < T) {  // gate by gate
+        stats[0] = stats[1] = ngates;
+        return DIAQ_OK;
+    }
+    std::vector<PassPlan> plan;
+    const int rc = schedule(local_bits, n_bits, ngates, gates, T, T - kThreadBits, plan);
+    if (rc) return rc;
+    for (const PassPlan &ps : plan) {
+        ++stats[0];
+        if (ps.bits.empty() || ps.members.size() == 1) {
+            ++stats[1];
+            continue;
+        }
+        stats[2] += (int)ps.phases.size();
+        stats[3] += (int)(ps.members.size() - ps.gates.size());
+        for (const Phase &ph : ps.phases) stats[4] += ph.generic;
+    }
+    return DIAQ_OK;
 }
 
 extern "C" int diaq_run_gates_local(int n_bits, int local_bits, int64_t rank, int ngates, const diaq_gate_t *gates,

@@ -155,3 +155,42 @@ def test_analysis_guard_without_device():
         chain_product_analysis(Circuit(15, [GateOp("h", (0,))]))
     with pytest.raises(ValueError):
         chain_product_analysis(Circuit(2, [GateOp("h", (0,))]), order="middle")
+
+
+def _plan(lib, n, ops, tile_bits=12, local_bits=None):
+    import paper_2405_01250_b200 as D
+    from paper_2405_01250_b200.sim import _GateProgram
+    pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
+    prog = _GateProgram([p.compact() for p in pls])
+    st = (ctypes.c_int * 5)()
+    L.check(lib.diaq_fused_plan(n, n if local_bits is None else local_bits, prog.n, prog.arr, tile_bits, st),
+            "diaq_fused_plan")
+    return dict(zip(["passes", "single", "phases", "folded", "smem_phases"], list(st)))
+
+
+def test_fused_schedule_host_only(lib):
+    """The fused-pass scheduler (host code behind diaq_run_gates_fused) on
+    the benchmark layer and on permutation-heavy circuits: CX/X/SWAP runs
+    are folded into the pass addressing, never executed."""
+    n = 28
+    ops = W.random_layered_ops(n, 1, seed=0)
+    st = _plan(lib, n, ops)
+    assert st["folded"] == n // 2 and st["single"] == 0 and st["smem_phases"] == 0
+    assert st["passes"] == 4            # 28 mixing bits through 12-bit tiles (3 low bits shared)
+    # a pure permutation circuit: everything folded, every pass a relabelling copy
+    cx = [("cx", (i, (i + 5) % 20), ()) for i in range(20)] + [("x", (3,), ()), ("swap", (0, 19), ())]
+    st = _plan(lib, 20, cx)
+    assert st["folded"] == len(cx) and st["phases"] == 0
+    # CCX is a permutation but not affine: shared-memory path, not folded
+    st = _plan(lib, 16, [("ccx", (0, 1, 2), ()), ("cx", (3, 4), ())])
+    assert st["folded"] == 1
+    # more than 8 distinct controls outside the tile start a new pass
+    many = [("cx", (27 - i, 0), ()) for i in range(12)]
+    st = _plan(lib, 28, many)
+    assert st["folded"] == 12 and st["passes"] == 2
+    # states smaller than a tile: gate by gate
+    st = _plan(lib, 8, [("h", (0,), ()), ("cx", (0, 1), ())])
+    assert st["passes"] == st["single"] == 2
+    # shard view: a gate mixing a global bit is refused (it needs the partner shard)
+    with pytest.raises(ValueError):
+        _plan(lib, 24, [("h", (0,), ())], local_bits=22)

@@ -47,14 +47,15 @@ def main():
             for _ in range(2):
                 go()
             torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            reps = 3
-            e0.record()
-            for _ in range(reps):
+            reps = 5 if n >= 26 else 20
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+            evs[0].record()
+            for r in range(reps):
                 go()
-            e1.record()
+                evs[r + 1].record()
             torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1) / reps
+            per = sorted(evs[r].elapsed_time(evs[r + 1]) for r in range(reps))
+            ms = per[len(per) // 2]  # median
             print(json.dumps({"tune": sys.argv[1:], "n": n, "gates": prog.n, "tile_bits": tb, "passes": npass.value if tb else prog.n,
                               "ms": round(ms, 3), "gates_per_s": round(prog.n / ms * 1e3, 1),
                               "ms_per_pass": round(ms / max(1, npass.value if tb else prog.n), 4),
