@@ -495,6 +495,24 @@ def secondary_workloads(args, D, L, W, torch) -> dict:
                                              "gates_per_s": round(len(pls5) / dt5, 1), "stats": st5,
                                              "note": "2 shards on one GPU; exchange = device copy (NVLink unmeasured)"}
     del shards
+    # config 5 at its 1-GPU size: n=30 (16 GB state), 20 random layers, norm check
+    ops30 = W.random_layered_ops(30, 20, seed=0)
+    pls30 = D.compile_circuit(D.Circuit(30, [D.GateOp(*o) for o in ops30]), span_limit=30)
+    st30 = D.init_state(30, max_qubits=30)
+    D.run_gates(st30, pls30[:45], inplace=True)  # warm-up (program cache, first launches)
+    st30 = D.init_state(30, max_qubits=30)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(s)
+    D.run_gates(st30, pls30, inplace=True)
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms30 = e0.elapsed_time(e1)
+    out["config5_n30_1gpu"] = {"gates": len(pls30), "layers": 20, "s_per_circuit": round(ms30 / 1e3, 4),
+                               "gates_per_s": round(len(pls30) / ms30 * 1e3, 1),
+                               "norm_err": abs(1.0 - st30.norm()),
+                               "note": "device time (CUDA events) of run_gates on |0..0>, fused passes"}
+    del st30
     out["config3_circuit_n20"] = {"gates": len(pls), "ms_per_circuit": round(ms, 3),
                                   "gates_per_s": round(len(pls) / ms * 1e3, 1),
                                   "run_api_wall_s": round(e2e_s, 4),
