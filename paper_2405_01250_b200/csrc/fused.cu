@@ -37,28 +37,30 @@ constexpr int kThreadBits = 8;      // 256 threads
 constexpr int kLowBits = 3;         // tile rows are 2^3 amplitudes = 128 B
 constexpr int kMaxRegKin = 1;       // mixing operands applied in registers (wider: own pass)
 constexpr int kMaxSel = 4;          // selector (non-mixing) operands
-constexpr int kMaxPassGates = 48;   // gate records staged in smem per pass
+constexpr int kMaxPassGates = 48;   // gate records per pass (kernel parameters)
 constexpr int kMaxPhases = 24;
+constexpr int kMaxCoef = 256;       // coefficient entries per pass (kernel parameters)
+constexpr int kMaxNz = 256;
 constexpr int kPrePhases = 4;       // phases whose register slots are precomputed per CTA (R = 3; 3 at R = 4,
                                     // within the 48 KB of static shared memory)
 
 static_assert(kThreads == (1 << kThreadBits), "thread layout");
 
-struct RegGate {
-    int kin;                  // 0, 1 or 2 mixing operands
-    int rb[kMaxRegKin];       // register bits of the mixing operands, descending (relabelled order)
-    int kout;                 // selector operands
-    int osel[kMaxSel];        // 0: bit `opos` of the tile base; 1: thread bit at tile position opos;
+struct RegGate {               // narrow fields: the records live in the kernel parameters
+    int8_t kin;               // 0 or 1 mixing operands
+    int8_t rb[kMaxRegKin];    // register bits of the mixing operands, descending (relabelled order)
+    int8_t kout;              // selector operands
+    int8_t osel[kMaxSel];     // 0: bit `opos` of the tile base; 1: thread bit at tile position opos;
                               // 2: register bit opos (varies between register groups)
-    int opos[kMaxSel];
-    int rsel;                 // any osel == 2
-    int coef_off;             // coef[coef_off + (b << 2kin) + r * 2^kin + c]   (pass-relative)
-    int nz_off;               // nz[nz_off + (b << kin) + r]
-    int cls_off;              // cls[cls_off + b]: 0 general, 1 identity (skip), 2 swap (kin 1)
+    int8_t opos[kMaxSel];
+    int8_t rsel;              // any osel == 2
     // fast-path classification (host): 0 generic, 1 dense 1-qubit (no selector),
     // 2 diagonal with one selector
-    int op;
-    int mpos;                 // generic phases: tile position of the mixing bit
+    int8_t op;
+    int8_t mpos;              // generic phases: tile position of the mixing bit
+    int16_t coef_off;         // coef[coef_off + (b << 2kin) + r * 2^kin + c]   (pass-relative)
+    int16_t nz_off;           // nz[nz_off + (b << kin) + r]
+    int16_t cls_off;          // host classification table (identity / swap blocks)
 };
 
 // Affine relabelling of tile indices, f -> A f ^ c ^ (XOR of b_i over the set
@@ -69,12 +71,12 @@ struct RegGate {
 constexpr int kMaxPermBase = 8;
 
 struct Affine {
-    int on;
-    int nb;
-    uint32_t c;
-    uint32_t a[kMaxTileBits];    // image of tile bit j
-    int bbit[kMaxPermBase];
-    uint32_t b[kMaxPermBase];
+    int8_t on;
+    int8_t nb;
+    uint16_t c;
+    uint16_t a[kMaxTileBits];    // image of tile bit j
+    int8_t bbit[kMaxPermBase];
+    uint16_t b[kMaxPermBase];
 };
 
 __device__ __forceinline__ uint32_t aff_lin(const Affine &m, uint32_t f, int T) {
@@ -92,31 +94,35 @@ __device__ __forceinline__ uint32_t aff_const(const Affine &m, uint64_t sbase) {
 }
 
 struct Phase {
-    int g0, g1;               // gates [g0, g1) of the pass (pass-relative)
-    int generic;              // 1: gates applied in shared memory (no register bits)
-    int rpos[4];              // tile positions of the register bits, ascending (R entries)
-    int tpos[kMaxTileBits];   // tile positions of the thread bits, ascending (T - R entries)
+    int16_t g0, g1;           // gates [g0, g1) of the pass (pass-relative)
+    int8_t generic;           // 1: gates applied in shared memory (no register bits)
+    int8_t rpos[4];           // tile positions of the register bits, ascending (R entries)
+    int8_t tpos[kMaxTileBits];  // tile positions of the thread bits, ascending (T - R entries)
     Affine post;              // permutation run after the phase's gates, applied by its store
 };
 
+// One pass = one launch; its whole gate program rides in the kernel
+// parameters (__grid_constant__, < 32 KB): every thread reads the same
+// phase / gate / coefficient at the same time, so these are uniform
+// constant-bank loads, not per-thread shared-memory traffic.
 struct TileParams {
     double2 *x;
     int64_t ntiles;
     int tbits;                // T
     int tb[kMaxTileBits];     // ascending state bits of the tile
     int nphases;
-    const Phase *phases;      // device
     int ngates;
-    const RegGate *gates;     // device (pass-relative order)
-    const double2 *coef;      // this pass's tables, staged into shared memory
-    const uint32_t *nz;
-    const uint32_t *cls;
-    int ncoef, nnz, ncls;
+    int ncoef, nnz;
     uint64_t gbase;           // sharded state: rank bits (rank << local_bits) for selector lookups
-    Affine pre;               // permutation run opening the pass, applied by the tile load
     uint64_t tmask;           // state bits of the tile
     uint64_t gstep;           // gridDim.x deposited into the non-tile bits (tile base stride)
+    Affine pre;               // permutation run opening the pass, applied by the tile load
+    Phase ph[kMaxPhases];
+    RegGate g[kMaxPassGates]; // pass-relative order
+    double2 coef[kMaxCoef];
+    uint32_t nz[kMaxNz];
 };
+static_assert(sizeof(TileParams) <= 32764, "kernel parameter space");
 
 // base of tile t + gridDim.x from the base of tile t: add in the number
 // system of the non-tile bits (tile bits forced to 1 carry straight through)
@@ -137,7 +143,7 @@ __device__ __forceinline__ uint64_t insert_zero_bits_dyn(uint64_t g, const int *
 }
 
 template <int R>
-__device__ __forceinline__ uint32_t reg_spread(int j, const int *rpos) {
+__device__ __forceinline__ uint32_t reg_spread(int j, const int8_t *rpos) {
     uint32_t e = 0;
 #pragma unroll
     for (int i = 0; i < R; ++i) e |= (uint32_t)((j >> i) & 1) << rpos[i];
@@ -219,9 +225,8 @@ __device__ __forceinline__ uint64_t ld_base(const uint64_t *s) {
 
 template <int R, int MODE>
 __device__ __forceinline__ void dispatch_gate(double2 (&v)[1 << R], const RegGate &G, uint32_t tpart, const uint64_t *sbase_p,
-                                              const double2 *sc, const uint32_t *snz, const uint32_t *scls) {
+                                              const double2 *sc, const uint32_t *snz) {
     // if-chains, not switches: a jump table would force v[] into local memory
-    (void)scls;
     static_assert(R == 3 || R == 4, "register fast paths cover 8 or 16 amplitudes per thread");
     if (G.op == 1) {
         const double2 *c = sc + G.coef_off;
@@ -284,8 +289,6 @@ template <int R, int MODE>
 __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(const __grid_constant__ TileParams p) {
     extern __shared__ double2 tile[];
     __shared__ uint64_t hi_off[(1 << kMaxTileBits) >> kLowBits];
-    __shared__ Phase sph[kMaxPhases];
-    __shared__ RegGate sg[kMaxPassGates];
     // per-(phase, thread) smem slots of the thread's registers and its thread-bit
     // pattern, computed once per CTA instead of once per tile
     constexpr int kPre = R >= 4 ? kPrePhases - 1 : kPrePhases;
@@ -300,28 +303,20 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
     constexpr int NR = 1 << R;
     const int T = p.tbits;
     const uint32_t tsize = 1u << T;
-    double2 *sc = tile + tsize;
-    uint32_t *snz = reinterpret_cast<uint32_t *>(sc + p.ncoef);
-    uint32_t *scls = snz + p.nnz;
-    for (int i = threadIdx.x; i < p.ncoef; i += blockDim.x) sc[i] = p.coef[i];
-    for (int i = threadIdx.x; i < p.nnz; i += blockDim.x) snz[i] = p.nz[i];
-    for (int i = threadIdx.x; i < p.ncls; i += blockDim.x) scls[i] = p.cls[i];
+    const double2 *sc = p.coef;
+    const uint32_t *snz = p.nz;
     // tile element e -> state offset: low kLowBits tile bits are state bits 0..2
     for (uint32_t h = threadIdx.x; h < (tsize >> kLowBits); h += blockDim.x) {
         uint64_t off = 0;
         for (int j = kLowBits; j < T; ++j) off |= (uint64_t)((h >> (j - kLowBits)) & 1u) << p.tb[j];
         hi_off[h] = off;
     }
-    for (int i = threadIdx.x; i < p.nphases * (int)(sizeof(Phase) / 4); i += blockDim.x)
-        reinterpret_cast<int *>(sph)[i] = reinterpret_cast<const int *>(p.phases)[i];
-    for (int i = threadIdx.x; i < p.ngates * (int)(sizeof(RegGate) / 4); i += blockDim.x)
-        reinterpret_cast<int *>(sg)[i] = reinterpret_cast<const int *>(p.gates)[i];
     __syncthreads();
     constexpr uint32_t lowmask = (1u << kLowBits) - 1u;
     const int per_thread = (int)(tsize >> kThreadBits);
     const int npre = p.nphases < kPre ? p.nphases : kPre;
     for (int ph_i = 0; ph_i < npre; ++ph_i) {
-        const Phase &ph = sph[ph_i];
+        const Phase &ph = p.ph[ph_i];
         uint32_t tpart = 0;
         for (int i = 0; i < T - R; ++i) tpart |= ((threadIdx.x >> i) & 1u) << ph.tpos[i];
         s_tpart[ph_i][threadIdx.x] = tpart;
@@ -365,10 +360,10 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncthreads();
         for (int ph_i = 0; ph_i < p.nphases; ++ph_i) {
-            const Phase &ph = sph[ph_i];
+            const Phase &ph = p.ph[ph_i];
             if (ph.generic) {
                 for (int gi = ph.g0; gi < ph.g1; ++gi) {
-                    smem_gate<MODE>(tl, T, sg[gi], ld_base(&s_sbase), sc, snz);
+                    smem_gate<MODE>(tl, T, p.g[gi], ld_base(&s_sbase), sc, snz);
                     __syncthreads();
                 }
                 continue;
@@ -385,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
 #pragma unroll
                 for (int j = 0; j < NR; ++j) v[j] = tl[swz(tpart | reg_spread<R>(j, ph.rpos))];
             }
-            for (int gi = ph.g0; gi < ph.g1; ++gi) dispatch_gate<R, MODE>(v, sg[gi], tpart, &s_sbase, sc, snz, scls);
+            for (int gi = ph.g0; gi < ph.g1; ++gi) dispatch_gate<R, MODE>(v, p.g[gi], tpart, &s_sbase, sc, snz);
             if (ph.post.on) {
                 __syncthreads();  // relabelled slots belong to other threads' registers: all reads first
                 const uint32_t bc = aff_const(ph.post, ld_base(&s_sbase));
@@ -695,12 +690,14 @@ static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gate
     std::vector<char> inb(64, 0);
     std::vector<int> pbase;  // non-mixing operand bits of the pass's permutation gates (fold bound)
     int nb = 0;
+    int ncoef = 0, nnz = 0;  // the pass's coefficient / mask table entries (kernel parameter bound)
     auto reset = [&]() {
         std::fill(inb.begin(), inb.end(), 0);
         nb = 0;
         for (int b = 0; b < low; ++b) { inb[b] = 1; ++nb; }
         members.clear();
         pbase.clear();
+        ncoef = nnz = 0;
     };
     auto flush = [&]() -> int {
         if (members.empty()) return DIAQ_OK;
@@ -848,9 +845,10 @@ static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gate
         if (pg)
             for (int j = 0; j < gt.k; ++j)
                 if (!((mix >> j) & 1u) && std::find(pbase.begin(), pbase.end(), gt.shifts[j]) == pbase.end()) ++padd;
+        const int gcoef = pg ? 0 : (1 << kout) << (2 * kin), gnz = pg ? 0 : (1 << kout) << kin;
         // phases per pass are bounded too: a pass can need up to one phase per gate
         if (nb + add > T || (int)members.size() >= std::min(kMaxPassGates, kMaxPhases) ||
-            (int)pbase.size() + padd > kMaxPermBase) {
+            (int)pbase.size() + padd > kMaxPermBase || ncoef + gcoef > kMaxCoef || nnz + gnz > kMaxNz) {
             int rc = flush();
             if (rc) return rc;
             reset();
@@ -864,6 +862,8 @@ static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gate
             for (int j = 0; j < gt.k; ++j)
                 if (!((mix >> j) & 1u) && std::find(pbase.begin(), pbase.end(), gt.shifts[j]) == pbase.end())
                     pbase.push_back(gt.shifts[j]);
+        ncoef += gcoef;
+        nnz += gnz;
         members.push_back(i);
     }
     return flush();
@@ -912,41 +912,11 @@ using namespace diaq;
 // A scheduled and packed gate program.  Scheduling 10^3 gates costs about a
 // millisecond of host time -- as much as the passes themselves at n = 20 --
 // so the last few programs are kept per thread, keyed by the exact gate data,
-// together with their device copy (uploaded once per device: a per-call
-// pageable upload would stall the host behind the stream's queued passes).
+// each pass already in its launch-parameter form.
 struct Program {
-    struct Off { size_t ph, g, coef, nz, cls; };
     std::vector<char> key;
     std::vector<PassPlan> plan;
-    std::vector<Off> off;
-    std::vector<char> host;  // per pass [phases | gates | coef | nz | cls], 16-byte aligned
-    mutable std::vector<std::pair<int, char *>> dev;
-
-    const char *device_copy(int &rc) const {
-        int d = 0;
-        cudaGetDevice(&d);
-        for (const auto &e : dev)
-            if (e.first == d) return e.second;
-        char *p = nullptr;
-        if (cudaMalloc((void **)&p, host.size()) != cudaSuccess ||
-            cudaMemcpy(p, host.data(), host.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
-            cudaGetLastError();
-            if (p) cudaFree(p);
-            rc = set_error(DIAQ_ERR_CUDA, "diaq_run_gates_fused: program upload failed");
-            return nullptr;
-        }
-        dev.push_back({d, p});
-        return p;
-    }
-    ~Program() {  // evicted: passes still queued may read the copy
-        int cur = 0;
-        const bool have = cudaGetDevice(&cur) == cudaSuccess;
-        for (const auto &e : dev) {
-            if (cudaSetDevice(e.first) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess) cudaFree(e.second);
-        }
-        if (have) cudaSetDevice(cur);
-        cudaGetLastError();
-    }
+    std::vector<TileParams> params;  // per tiled pass (x, gbase and the grid are filled in at launch)
 };
 
 static std::vector<char> program_key(int n_total, int n_bits, int T, int ngates, const diaq_gate_t *gates) {
@@ -981,27 +951,32 @@ static std::shared_ptr<const Program> build_program(int n_total, int n_bits, int
             plan.push_back(ps);
         }
     }
-    std::vector<Program::Off> &off = prog->off;
-    off.resize(plan.size());
-    size_t cur = 0;
-    auto al = [](size_t v) { return (v + 15) & ~(size_t)15; };
+    prog->params.resize(plan.size());
     for (size_t i = 0; i < plan.size(); ++i) {
         const PassPlan &ps = plan[i];
-        off[i].ph = cur; cur = al(cur + sizeof(Phase) * ps.phases.size());
-        off[i].g = cur; cur = al(cur + sizeof(RegGate) * ps.gates.size());
-        off[i].coef = cur; cur = al(cur + sizeof(double2) * ps.pk.coef.size());
-        off[i].nz = cur; cur = al(cur + sizeof(uint32_t) * ps.pk.nz.size());
-        off[i].cls = cur; cur = al(cur + sizeof(uint32_t) * ps.pk.cls.size());
-    }
-    std::vector<char> &host = prog->host;
-    host.assign(cur + 16, 0);
-    for (size_t i = 0; i < plan.size(); ++i) {
-        const PassPlan &ps = plan[i];
-        if (!ps.phases.empty()) memcpy(&host[off[i].ph], ps.phases.data(), sizeof(Phase) * ps.phases.size());
-        if (!ps.gates.empty()) memcpy(&host[off[i].g], ps.gates.data(), sizeof(RegGate) * ps.gates.size());
-        if (!ps.pk.coef.empty()) memcpy(&host[off[i].coef], ps.pk.coef.data(), sizeof(double2) * ps.pk.coef.size());
-        if (!ps.pk.nz.empty()) memcpy(&host[off[i].nz], ps.pk.nz.data(), sizeof(uint32_t) * ps.pk.nz.size());
-        if (!ps.pk.cls.empty()) memcpy(&host[off[i].cls], ps.pk.cls.data(), sizeof(uint32_t) * ps.pk.cls.size());
+        if (ps.bits.empty() || ps.members.size() == 1) continue;  // standalone gate
+        if ((int)ps.phases.size() > kMaxPhases || (int)ps.gates.size() > kMaxPassGates ||
+            (int)ps.pk.coef.size() > kMaxCoef || (int)ps.pk.nz.size() > kMaxNz) {
+            rc = set_error(DIAQ_ERR_VALUE, "fused pass exceeds its parameter tables");
+            return nullptr;
+        }
+        TileParams &p = prog->params[i];
+        memset(&p, 0, sizeof(p));
+        p.tbits = (int)ps.bits.size();
+        for (int j = 0; j < p.tbits; ++j) {
+            p.tb[j] = ps.bits[j];
+            p.tmask |= 1ull << ps.bits[j];
+        }
+        p.ntiles = (int64_t)1 << (n_bits - p.tbits);
+        p.nphases = (int)ps.phases.size();
+        p.ngates = (int)ps.gates.size();
+        p.ncoef = (int)ps.pk.coef.size();
+        p.nnz = (int)ps.pk.nz.size();
+        p.pre = ps.pre;
+        std::copy(ps.phases.begin(), ps.phases.end(), p.ph);
+        std::copy(ps.gates.begin(), ps.gates.end(), p.g);
+        std::copy(ps.pk.coef.begin(), ps.pk.coef.end(), p.coef);
+        std::copy(ps.pk.nz.begin(), ps.pk.nz.end(), p.nz);
     }
     rc = DIAQ_OK;
     return prog;
@@ -1036,20 +1011,13 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
     cudaStream_t s = (cudaStream_t)stream;
     // tile_bits 12 -> 16 amplitudes per thread (R = 4), else 8 (R = 3); 256 threads
     const int T = tile_bits >= kThreadBits + 4 ? kThreadBits + 4 : kThreadBits + 3;
-    const bool tiled = n_bits >= T;
     const int R = T - kThreadBits;
     int rc = DIAQ_OK;
     std::shared_ptr<const Program> prog = cached_program(n_total, n_bits, T, ngates, gates, rc);
     if (!prog) return rc;
     const std::vector<PassPlan> &plan = prog->plan;
-    const std::vector<Program::Off> &off = prog->off;
     if (npasses) *npasses = (int)plan.size();
-    const char *dbuf = nullptr;
-    if (tiled && !plan.empty()) {
-        dbuf = prog->device_copy(rc);
-        if (!dbuf) return rc;
-    }
-    const size_t smem_max = (sizeof(double2) << kMaxTileBits) + 48 * 1024;
+    const size_t smem_max = (sizeof(double2) << kMaxTileBits);
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(tile_pass_kernel<3, DIAQ_CMUL_FMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
@@ -1060,6 +1028,7 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
     }
     if (events && cudaEventRecord((cudaEvent_t)events[0], s) != cudaSuccess)
         return set_error(DIAQ_ERR_CUDA, "diaq_run_gates_fused: event record failed");
+    thread_local TileParams tparams;
     for (size_t pi = 0; pi < plan.size() && rc == DIAQ_OK; ++pi) {
         const PassPlan &ps = plan[pi];
         if (ps.bits.empty() || ps.members.size() == 1) {
@@ -1067,33 +1036,15 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
             if (sharded) rc = apply_gate_sharded_own(n_total, n_bits, gt.k, gt.g, gt.shifts, rank, state, cmul_mode, s);
             else rc = apply_gate(n_bits, gt.k, gt.g, gt.shifts, state, state, cmul_mode, s);
         } else {
-            TileParams p;
+            TileParams &p = tparams;  // thread-local scratch: the launch copies it
+            p = prog->params[pi];
             p.x = (double2 *)state;
-            p.tbits = (int)ps.bits.size();
-            for (int j = 0; j < p.tbits; ++j) p.tb[j] = ps.bits[j];
-            p.ntiles = (int64_t)1 << (n_bits - p.tbits);
-            p.nphases = (int)ps.phases.size();
-            p.phases = (const Phase *)(dbuf + off[pi].ph);
-            p.ngates = (int)ps.gates.size();
-            p.gates = (const RegGate *)(dbuf + off[pi].g);
-            p.coef = (const double2 *)(dbuf + off[pi].coef);
-            p.nz = (const uint32_t *)(dbuf + off[pi].nz);
-            p.cls = (const uint32_t *)(dbuf + off[pi].cls);
-            p.ncoef = (int)ps.pk.coef.size();
-            p.nnz = (int)ps.pk.nz.size();
-            p.ncls = (int)ps.pk.cls.size();
             p.gbase = sharded ? ((uint64_t)rank << n_bits) : 0ull;
-            p.pre = ps.pre;
-            const size_t tables = sizeof(double2) * p.ncoef + sizeof(uint32_t) * (p.nnz + p.ncls);
             const void *f = R >= 4 ? tile_kernel_ptr<4>(cmul_mode) : tile_kernel_ptr<3>(cmul_mode);
-            int per_sm = 1;
-            const size_t smem = (sizeof(double2) << p.tbits) + tables;
-            if (smem > smem_max) return set_error(DIAQ_ERR_VALUE, "fused pass tables exceed shared memory");
-            per_sm = occupancy(f, smem);
+            const size_t smem = sizeof(double2) << p.tbits;
+            const int per_sm = occupancy(f, smem);
             const int64_t grid =
                 std::max<int64_t>(1, std::min<int64_t>(p.ntiles, (int64_t)sm_count_f() * std::max(1, per_sm)));
-            p.tmask = 0;
-            for (int j = 0; j < p.tbits; ++j) p.tmask |= 1ull << p.tb[j];
             p.gstep = 0;  // deposit grid into the non-tile bits, low to high
             for (int b = 0, k = 0; b < 64 && ((uint64_t)grid >> k) != 0; ++b)
                 if (!((p.tmask >> b) & 1ull)) p.gstep |= (((uint64_t)grid >> k++) & 1ull) << b;
