@@ -15,7 +15,7 @@ import numpy as np
 from .errors import DiaqError, ResourceError, ShapeError, UnsupportedFeatureError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdiaq_b200.so")
+LIB_PATH = os.environ.get("DIAQ_B200_LIB") or os.path.join(HERE, "libdiaq_b200.so")  # override: A/B builds
 
 DIAQ_OK = 0
 DIAQ_ERR_SHAPE = 1
