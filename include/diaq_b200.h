@@ -184,6 +184,19 @@ int diaq_apply_gate_sharded(int n_bits, int local_bits, int k, const double *g_h
 int diaq_run_gates_local(int n_bits, int local_bits, int64_t rank, int ngates, const diaq_gate_t *gates,
                          void *shard, int cmul_mode, int tile_bits, void **events, int *npasses, void *stream);
 
+/* ---- peer memory between the ranks of a sharded state --------
+ * diaq_alloc: a cudaMalloc'd buffer (an allocation base, so exportable);
+ * diaq_ipc_handle: its CUDA IPC handle (DIAQ_IPC_HANDLE_BYTES bytes) for the
+ * other ranks; diaq_ipc_open maps a partner's handle into this process
+ * (NVLink/NVSwitch peer access enabled lazily), so diaq_apply_gate_sharded
+ * can take partner shard pointers as `srcs` and read them in the pass. */
+#define DIAQ_IPC_HANDLE_BYTES 64
+int diaq_alloc(int64_t bytes, void **ptr);
+int diaq_free(void *ptr);
+int diaq_ipc_handle(const void *ptr, void *handle_out);
+int diaq_ipc_open(const void *handle, void **ptr_out);
+int diaq_ipc_close(void *ptr);
+
 /* ---- sampling (reference measure_all_sample, sim.py:142-161) -------------
  * hits[k] = min(#{i : cdf_i <= u_k}, N-1) with cdf = sequential float64
  * cumsum of round(|x_i|^2, 12), reproduced exactly (binade-segmented exact

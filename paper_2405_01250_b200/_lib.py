@@ -24,6 +24,7 @@ DIAQ_ERR_RESOURCE = 3
 DIAQ_ERR_CUDA = 4
 DIAQ_ERR_UNSUPPORTED = 5
 DIAQ_NORM_WORK = 1025
+DIAQ_IPC_HANDLE_BYTES = 64
 
 CMUL_PLAIN = 0
 CMUL_FMA = 1
@@ -86,6 +87,11 @@ _SIGS = {
     "diaq_run_gates_local": ([_INT, _INT, _I64, _INT, ctypes.POINTER(Gate), _P, _INT, _INT, _P, _P, _P], _INT),
     "diaq_shard_plan": ([_INT, _INT, _INT, _P, _P, _I64, _P, _P, _P], _INT),
     "diaq_apply_gate_sharded": ([_INT, _INT, _INT, _P, _P, _I64, _P, _P, _INT, _P], _INT),
+    "diaq_alloc": ([_I64, _P], _INT),
+    "diaq_free": ([_P], _INT),
+    "diaq_ipc_handle": ([_P, _P], _INT),
+    "diaq_ipc_open": ([_P, _P], _INT),
+    "diaq_ipc_close": ([_P], _INT),
     "diaq_sample_hits": ([_I64, _P, _P, _I64, _P, _P, _P], _INT),
     "diaq_timer_create": ([_INT, _P], _INT),
     "diaq_timer_record": ([_P, _P], _INT),
@@ -238,3 +244,55 @@ class Timer:
                 _lib.diaq_timer_destroy(self.n, self.events)
         except Exception:
             pass
+
+
+# ---- library-owned device memory (CUDA IPC exportable) -------------------------
+
+class _Allocation:
+    """One diaq_alloc'd block; freed when the last tensor viewing it dies."""
+
+    def __init__(self, nbytes: int):
+        p = ctypes.c_void_p()
+        call("diaq_alloc", int(nbytes), ctypes.byref(p))
+        self.ptr = int(p.value)
+        self.nbytes = int(nbytes)
+
+    def __del__(self):
+        try:
+            if _lib is not None and self.ptr:
+                _lib.diaq_free(ctypes.c_void_p(self.ptr))
+        except Exception:
+            pass
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of an _Allocation (torch keeps it alive)."""
+
+    def __init__(self, mem: _Allocation, n: int):
+        self._mem = mem
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<c16", "data": (mem.ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def shared_c128(n: int):
+    """(tensor, base pointer): a complex128 device tensor over its own
+    cudaMalloc allocation, so diaq_ipc_handle can export it to other ranks."""
+    mem = _Allocation(16 * int(n))
+    t = torch().as_tensor(_CudaArray(mem, n), device=device())
+    return t, mem.ptr
+
+
+def ipc_handle(ptr: int) -> bytes:
+    buf = ctypes.create_string_buffer(DIAQ_IPC_HANDLE_BYTES)
+    call("diaq_ipc_handle", ctypes.c_void_p(ptr), buf)
+    return buf.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    p = ctypes.c_void_p()
+    call("diaq_ipc_open", ctypes.create_string_buffer(handle, DIAQ_IPC_HANDLE_BYTES), ctypes.byref(p))
+    return int(p.value)
+
+
+def ipc_close(ptr: int) -> None:
+    call("diaq_ipc_close", ctypes.c_void_p(ptr))

@@ -69,10 +69,17 @@ def exchange_schedule(n_bits: int, local_bits: int, g, shifts, world: int):
     return needs
 
 
+def _ptr(t):
+    """device address of a source block: a tensor, a raw (peer) pointer, or None"""
+    if t is None:
+        return None
+    return int(t) if isinstance(t, int) else t.data_ptr()
+
+
 def _cuda_apply(n_bits, local_bits, g, shifts, rank, srcs, y, cmul_mode):
     gd = np.ascontiguousarray(g, dtype=np.complex128)
     sh = np.ascontiguousarray(shifts, dtype=np.int32)
-    arr = (ctypes.c_void_p * len(srcs))(*[(t.data_ptr() if t is not None else None) for t in srcs])
+    arr = (ctypes.c_void_p * len(srcs))(*[_ptr(t) for t in srcs])
     L.call("diaq_apply_gate_sharded", n_bits, local_bits, len(sh), gd.ctypes.data, sh.ctypes.data, int(rank),
            arr, y.data_ptr(), int(cmul_mode), L.stream_handle())
 
@@ -111,6 +118,57 @@ class TorchDistComm:
         return torch.view_as_complex(torch.cat(parts)) if self.rank == 0 else None
 
 
+class PeerComm(TorchDistComm):
+    """Peer-memory transport: every rank maps its partners' shard buffers
+    (CUDA IPC, NVLink/NVSwitch peer access) and the multi-source kernel reads
+    partner amplitudes directly inside the gate pass -- no staging copy, the
+    transfer overlaps the arithmetic.  Cross-shard gates then run out of
+    place into a second buffer (partners read this rank's current one), with
+    one host barrier per such gate: a rank only overwrites a buffer after
+    every partner finished reading it, and only reads a partner's buffer
+    after the partner finished writing it.  torch.distributed (any backend)
+    carries the handles, the barrier and the reductions."""
+
+    peer = True
+
+    def __init__(self, group=None):
+        super().__init__(group)
+        self._opened: list[int] = []
+
+    def share(self, ptrs: list[int]) -> list[list[int]]:
+        """table[q][i] = this process's address of rank q's buffer i."""
+        mine = [L.ipc_handle(p) for p in ptrs]
+        allh = [None] * self.world
+        self.dist.all_gather_object(allh, mine, group=self.group)
+        table = []
+        for q, hs in enumerate(allh):
+            if q == self.rank:
+                table.append(list(ptrs))
+                continue
+            row = [L.ipc_open(h) for h in hs]
+            self._opened += row
+            table.append(row)
+        return table
+
+    def barrier(self) -> None:
+        L.torch().cuda.synchronize()
+        self.dist.barrier(group=self.group)
+
+    def allreduce_sum(self, value: float, like) -> float:
+        import torch
+        t = torch.tensor([value], dtype=torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        return float(t.item())
+
+    def gather(self, local):
+        return super().gather(local.cpu())
+
+    def close(self) -> None:
+        for p in self._opened:
+            L.ipc_close(p)
+        self._opened = []
+
+
 class ShardedState:
     """This rank's 2^L amplitudes of a 2^n state split over `comm.world` ranks."""
 
@@ -124,10 +182,18 @@ class ShardedState:
         self.local_bits = self.n_qubits - self.p
         if self.local_bits < 1:
             raise ValueError("more shards than amplitudes")
-        self.local = local
         self.apply_fn = apply_fn or _cuda_apply
         self.stats = {"gates": 0, "local": 0, "no_comm_global": 0, "exchanged": 0, "bytes_received": 0}
         self._recv = {}
+        self.peer = bool(getattr(comm, "peer", False))
+        if self.peer:  # two exportable buffers: the current state and the next cross-shard result
+            bufs = [L.shared_c128(local.numel()) for _ in range(2)]
+            self._bufs = [t for t, _ in bufs]
+            self._bufs[0].copy_(local)
+            self._peer = comm.share([p for _, p in bufs])  # [rank][buffer] -> address here
+            self._cur = 0
+            local = self._bufs[0]
+        self.local = local
 
     @classmethod
     def basis(cls, n_qubits: int, comm, device=None, apply_fn=None) -> "ShardedState":
@@ -158,6 +224,9 @@ class ShardedState:
             self.apply_fn(n, lb, g, shifts, me, [self.local], self.local, cmul_mode)
             return
         needs = exchange_schedule(n, lb, g, shifts, self.comm.world)
+        if self.peer and any(src != r for r, nd in enumerate(needs) for src in nd.values()):
+            self._apply_peer(g, shifts, needs, cmul_mode)
+            return
         sends = [(q, self.local) for q in range(self.comm.world) if q != me and me in needs[q].values()]
         recvs = [(src, self._recv_buffer(src)) for src in sorted(set(needs[me].values())) if src != me]
         if recvs or sends:
@@ -171,6 +240,22 @@ class ShardedState:
         for b, src in needs[me].items():
             srcs[b] = self.local if src == me else self._recv[src]
         self.apply_fn(n, lb, g, shifts, me, srcs, self.local, cmul_mode)
+
+    def _apply_peer(self, g, shifts, needs, cmul_mode) -> None:
+        """Cross-shard gate reading partner shards in place over peer memory."""
+        n, lb, me = self.n_qubits, self.local_bits, self.comm.rank
+        self.comm.barrier()  # partners finished writing their current buffers / reading our next one
+        kg = len(global_shifts(shifts, lb))
+        srcs = [None] * (1 << kg)
+        for b, src in needs[me].items():
+            srcs[b] = self.local if src == me else self._peer[src][self._cur]
+        remote = sorted({src for src in needs[me].values() if src != me})
+        self.stats["exchanged"] += 1
+        self.stats["bytes_received"] += 16 * self.local.numel() * len(remote)
+        nxt = self._bufs[self._cur ^ 1]
+        self.apply_fn(n, lb, g, shifts, me, srcs, nxt, cmul_mode)
+        self._cur ^= 1
+        self.local = nxt
 
     def _needs_exchange(self, g, shifts) -> bool:
         lb = self.local_bits

@@ -1,0 +1,55 @@
+"""One rank of the peer-memory sharded run (launched by test_gpu_peer.py):
+gloo for handles/barriers, CUDA IPC mappings of the partner shards, and the
+multi-source kernel reading them in place.  Rank 0 writes the gathered
+state to --out."""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--rank", type=int, required=True)
+    ap.add_argument("--world", type=int, required=True)
+    ap.add_argument("--port", type=int, required=True)
+    ap.add_argument("--n", type=int, required=True)
+    ap.add_argument("--layers", type=int, default=2)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--cmul", type=int, default=1)
+    ap.add_argument("--tile", type=int, default=12)
+    ap.add_argument("--out", required=True)
+    a = ap.parse_args()
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2405_01250_b200 as D
+    from paper_2405_01250_b200 import workloads as W
+    from paper_2405_01250_b200.shard import PeerComm, ShardedState
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{a.port}", rank=a.rank, world_size=a.world)
+    torch.cuda.set_device(0)
+    D.sim.FUSE_TILE_BITS = a.tile
+    comm = PeerComm()
+    ops = W.random_layered_ops(a.n, a.layers, seed=a.seed)
+    ops += [("h", (0,), ()), ("cx", (0, a.n - 1), ()), ("ry", (1,), (0.7,)), ("swap", (0, 2), ()),
+            ("cx", (a.n - 1, 0), ()), ("u3", (0,), (0.3, 0.2, 0.1))]
+    pls = D.compile_circuit(D.Circuit(a.n, [D.GateOp(*o) for o in ops]), span_limit=a.n)
+    st = ShardedState.basis(a.n, comm)
+    st.apply_placements(pls, cmul_mode=a.cmul)
+    norm = st.norm()
+    full = st.gather()
+    comm.barrier()  # nobody unmaps or frees while a partner may still read
+    if a.rank == 0:
+        np.save(a.out, full.numpy())
+        with open(a.out + ".stats", "w") as f:
+            f.write(repr({"stats": st.stats, "norm": norm}))
+    comm.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

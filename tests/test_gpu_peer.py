@@ -1,0 +1,56 @@
+"""GPU: the peer-memory transport of the sharded state (CUDA IPC mappings of
+the partner shards read in place by the multi-source kernel).  Two ranks run
+as two processes on the one GPU of the test box -- host barriers only, no
+kernel waits on another -- and must equal the unsharded run bitwise."""
+from __future__ import annotations
+
+import ast
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import paper_2405_01250_b200 as D
+from conftest import ROOT
+from paper_2405_01250_b200 import _lib as L
+from paper_2405_01250_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def _port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("n,tile", [(12, 12), (14, 0), (16, 11)])
+def test_peer_sharded_matches_unsharded(tmp_path, configs, n, tile):
+    cmul = L.CMUL_FMA if configs["meta"]["numpy_cmul"] == "fma" else L.CMUL_PLAIN
+    out = str(tmp_path / "state.npy")
+    port = _port()
+    worker = os.path.join(ROOT, "tests", "_peer_worker.py")
+    procs = [subprocess.Popen([sys.executable, worker, "--rank", str(r), "--world", "2", "--port", str(port),
+                               "--n", str(n), "--cmul", str(cmul), "--tile", str(tile), "--out", out],
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True) for r in range(2)]
+    logs = []
+    try:
+        for p in procs:
+            logs.append(p.communicate(timeout=300)[0])
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+    assert all(p.returncode == 0 for p in procs), "\n".join(logs)
+    got = np.load(out)
+    info = ast.literal_eval(open(out + ".stats").read())
+    assert info["stats"]["exchanged"] > 0 and abs(info["norm"] - 1.0) < 1e-12
+    ops = W.random_layered_ops(n, 2, seed=0)
+    ops += [("h", (0,), ()), ("cx", (0, n - 1), ()), ("ry", (1,), (0.7,)), ("swap", (0, 2), ()),
+            ("cx", (n - 1, 0), ()), ("u3", (0,), (0.3, 0.2, 0.1))]
+    pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
+    want = D.run_gates(D.init_state(n), pls, cmul_mode=cmul).amps
+    assert np.array_equal(got, want)
