@@ -400,13 +400,21 @@ def replica_gates(args, D, L, W, torch, dist, n, world, x, s, dev):
 
 
 def sharded_gates(args, D, L, W, torch, dist, n, world, x, s, dev):
-    """One random layer per step on a 2^(n+p) state sharded over the ranks
-    (NCCL partner exchange for cross-shard gates); weak scaling."""
-    from paper_2405_01250_b200.shard import ShardedState, TorchDistComm
+    """One random layer per step on a 2^(n+p) state sharded over the ranks;
+    weak scaling.  Cross-shard gates read partner shards in place over peer
+    memory (--transport peer, CUDA IPC over NVLink/NVSwitch) or exchange
+    them with NCCL send/recv first (--transport nccl)."""
+    from paper_2405_01250_b200.shard import PeerComm, ShardedState, TorchDistComm
     p = world.bit_length() - 1
     ns = n + p
-    comm = TorchDistComm()
-    st = ShardedState(ns, x.clone(), comm)
+    transport = args.transport
+    comm = PeerComm() if transport == "peer" else TorchDistComm()
+    try:
+        st = ShardedState(ns, x.clone(), comm)
+    except L.DeviceError as e:  # no peer mapping between these GPUs: staged NCCL exchange
+        transport = f"nccl (peer mapping failed: {e})"
+        comm = TorchDistComm()
+        st = ShardedState(ns, x.clone(), comm)
     ops = W.random_layered_ops(ns, 1, seed=0)
     pls = D.compile_circuit(D.Circuit(ns, [D.GateOp(*o) for o in ops]), span_limit=ns)
     st.apply_placements(pls)
@@ -423,8 +431,8 @@ def sharded_gates(args, D, L, W, torch, dist, n, world, x, s, dev):
     torch.cuda.synchronize()
     g_launches = L.launch_count() - gl0
     g_ms = max_over_ranks(dist, ge0.elapsed_time(ge1), dev)
-    extra = {"gates_per_step": len(pls), "steps": g_steps, "mode": f"sharded over {world} ranks (NCCL)",
-             "stats": dict(st.stats)}
+    extra = {"gates_per_step": len(pls), "steps": g_steps, "mode": f"sharded over {world} ranks",
+             "transport": transport, "stats": dict(st.stats)}
     return len(pls) * g_steps, g_ms, g_launches, st.norm(), ns, extra
 
 
@@ -532,6 +540,8 @@ def main():
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--sharded-gates", action="store_true",
                     help="N>1: measure gates on a state sharded over the ranks instead of replicas")
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="sharded gates: partner shards read in place over peer memory, or NCCL-staged")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
