@@ -184,6 +184,16 @@ int diaq_apply_gate_sharded(int n_bits, int local_bits, int k, const double *g_h
 int diaq_run_gates_local(int n_bits, int local_bits, int64_t rank, int ngates, const diaq_gate_t *gates,
                          void *shard, int cmul_mode, int tile_bits, void **events, int *npasses, void *stream);
 
+/* Sharded spmv: y[j] = row row0+j of A x, where x is split over
+ * nparts ranks in slices of 2^part_bits (x_parts[q]: rank q's slice as
+ * addressable here -- own memory or a peer mapping from diaq_ipc_open) and
+ * rows[i] holds diagonal offs[i] for this rank's rows (rows[i][j] = the
+ * element of row row0+j; entries of rows where the diagonal does not exist
+ * are ignored).  Offsets crossing a shard boundary read the partner's x
+ * in the kernel.  Bitwise diaq_spmv. */
+int diaq_spmv_sharded(int64_t n, int64_t nd, const int64_t *offs, const void *const *rows, int64_t row0,
+                      int64_t nrows, const void *const *x_parts, int part_bits, int nparts, void *y, void *stream);
+
 /* ---- peer memory between the ranks of a sharded state --------
  * diaq_alloc: a cudaMalloc'd buffer (an allocation base, so exportable);
  * diaq_ipc_handle: its CUDA IPC handle (DIAQ_IPC_HANDLE_BYTES bytes) for the

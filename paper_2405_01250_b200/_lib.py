@@ -87,6 +87,7 @@ _SIGS = {
     "diaq_run_gates_local": ([_INT, _INT, _I64, _INT, ctypes.POINTER(Gate), _P, _INT, _INT, _P, _P, _P], _INT),
     "diaq_shard_plan": ([_INT, _INT, _INT, _P, _P, _I64, _P, _P, _P], _INT),
     "diaq_apply_gate_sharded": ([_INT, _INT, _INT, _P, _P, _I64, _P, _P, _INT, _P], _INT),
+    "diaq_spmv_sharded": ([_I64, _I64, _P, _P, _I64, _I64, _P, _INT, _INT, _P, _P], _INT),
     "diaq_alloc": ([_I64, _P], _INT),
     "diaq_free": ([_P], _INT),
     "diaq_ipc_handle": ([_P, _P], _INT),

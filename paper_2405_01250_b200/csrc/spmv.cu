@@ -20,6 +20,7 @@
 //     fastest, t = j*(S/T) + b, so the tiles that share an x window run
 //     back to back and x comes from HBM about once.
 #include <algorithm>
+#include <cstring>
 #include <cstdlib>
 #include <vector>
 
@@ -627,6 +628,111 @@ static int spmv_rows(const diaq_matrix_t *a, const void *x, void *y, int64_t r0,
     cudaStreamSynchronize(s);  // host table lifetime
     free(h);
     return rc;
+}
+
+// ---- sharded spmv: this rank's rows, x spread over the ranks ----
+// Rank q holds x[q*2^B, (q+1)*2^B) (B = part_bits) and the rows [row0,
+// row0 + nrows) of every diagonal (rows[i][j] = D_{d_i} at row row0 + j).
+// x_parts are the ranks' x slices as seen from this process: its own, and
+// partners' through CUDA IPC peer mappings (NVLink / NVSwitch) -- so an
+// offset that crosses a shard boundary is a direct peer load inside the
+// kernel, no halo copy.  Same per-row ascending-d arithmetic as diaq_spmv:
+// the sharded product is bitwise the single-GPU one.
+constexpr int kMaxParts = 64;
+
+struct ShardSpmvParams {
+    int64_t row0, nrows;
+    int part_bits, nparts;
+    int nd;
+    double2 *y;
+    const double2 *parts[kMaxParts];
+    const double2 *rows[kParamDiags];
+    int64_t off[kParamDiags];
+    int64_t lo[kParamDiags], hi[kParamDiags];  // global rows where diagonal i exists
+};
+
+template <int ND>
+__global__ void __launch_bounds__(kThreads) spmv_sharded_kernel(const __grid_constant__ ShardSpmvParams p) {
+    const uint64_t pol = policy_evict_first();
+    const uint64_t mask = (1ull << p.part_bits) - 1ull;
+    const int nd = ND > 0 ? ND : p.nd;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p.nrows; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = p.row0 + j;
+        double2 acc = make_double2(0.0, 0.0);
+        if constexpr (ND > 0) {
+            double2 v[ND], xv[ND];
+#pragma unroll
+            for (int i = 0; i < ND; ++i) {
+                if (r >= p.lo[i] && r < p.hi[i]) {
+                    const uint64_t c = (uint64_t)(r + p.off[i]);
+                    v[i] = ld_stream(p.rows[i] + j, pol);
+                    xv[i] = ld_reuse(p.parts[c >> p.part_bits] + (c & mask));
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < ND; ++i)
+                if (r >= p.lo[i] && r < p.hi[i]) acc = cadd(acc, cmul_plain(v[i], xv[i]));
+        } else {
+            for (int i = 0; i < nd; ++i) {
+                if (r >= p.lo[i] && r < p.hi[i]) {
+                    const uint64_t c = (uint64_t)(r + p.off[i]);
+                    acc = cadd(acc, cmul_plain(ld_stream(p.rows[i] + j, pol),
+                                               ld_reuse(p.parts[c >> p.part_bits] + (c & mask))));
+                }
+            }
+        }
+        st_stream(p.y + j, acc);
+    }
+}
+
+extern "C" int diaq_spmv_sharded(int64_t n, int64_t nd, const int64_t *offs, const void *const *rows, int64_t row0,
+                                 int64_t nrows, const void *const *x_parts, int part_bits, int nparts, void *y,
+                                 void *stream) {
+    if (nd < 0 || (nd > 0 && (!offs || !rows)) || !x_parts || !y)
+        return set_error(DIAQ_ERR_VALUE, "diaq_spmv_sharded: null argument");
+    if (nd > kParamDiags) return set_error(DIAQ_ERR_UNSUPPORTED, "diaq_spmv_sharded: more than %d diagonals", kParamDiags);
+    if (nparts < 1 || nparts > kMaxParts || part_bits < 0 || part_bits > 62 || ((int64_t)nparts << part_bits) != n)
+        return set_error(DIAQ_ERR_SHAPE, "diaq_spmv_sharded: %d parts of 2^%d do not tile n=%lld", nparts, part_bits,
+                         (long long)n);
+    if (row0 < 0 || nrows < 0 || row0 + nrows > n) return set_error(DIAQ_ERR_SHAPE, "diaq_spmv_sharded: rows outside n");
+    ShardSpmvParams p;
+    memset(&p, 0, sizeof(p));
+    p.row0 = row0;
+    p.nrows = nrows;
+    p.part_bits = part_bits;
+    p.nparts = nparts;
+    p.nd = (int)nd;
+    p.y = (double2 *)y;
+    for (int q = 0; q < nparts; ++q) {
+        if (!x_parts[q]) return set_error(DIAQ_ERR_VALUE, "diaq_spmv_sharded: x part %d missing", q);
+        p.parts[q] = (const double2 *)x_parts[q];
+    }
+    for (int64_t i = 0; i < nd; ++i) {
+        const int64_t d = offs[i];
+        if (d <= -n || d >= n) return set_error(DIAQ_ERR_VALUE, "diagonal %lld out of range for n_dim=%lld", (long long)d, (long long)n);
+        if (i > 0 && offs[i - 1] >= d) return set_error(DIAQ_ERR_VALUE, "offsets must be strictly ascending");
+        if (!rows[i]) return set_error(DIAQ_ERR_VALUE, "diaq_spmv_sharded: diagonal %lld rows missing", (long long)i);
+        p.rows[i] = (const double2 *)rows[i];
+        p.off[i] = d;
+        p.lo[i] = d < 0 ? -d : 0;
+        p.hi[i] = d > 0 ? n - d : n;
+    }
+    if (nrows == 0) return DIAQ_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    int dev = 0, sms = kSms;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaGetLastError();
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((nrows + kThreads - 1) / kThreads, (int64_t)sms * 8));
+    switch (nd) {
+#define DIAQ_SHARD_ND(K) \
+    case K: spmv_sharded_kernel<K><<<(unsigned)grid, kThreads, 0, s>>>(p); break;
+        DIAQ_SHARD_ND(1) DIAQ_SHARD_ND(2) DIAQ_SHARD_ND(3) DIAQ_SHARD_ND(4) DIAQ_SHARD_ND(5)
+        DIAQ_SHARD_ND(6) DIAQ_SHARD_ND(7) DIAQ_SHARD_ND(8) DIAQ_SHARD_ND(9)
+#undef DIAQ_SHARD_ND
+        default: spmv_sharded_kernel<0><<<(unsigned)grid, kThreads, 0, s>>>(p); break;
+    }
+    count_launch();
+    return check_launch("spmv_sharded_kernel");
 }
 
 extern "C" int diaq_spmv(const diaq_matrix_t *a, const void *x, void *y, void *stream) {

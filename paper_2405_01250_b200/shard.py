@@ -393,3 +393,52 @@ def run_emulated(n_qubits: int, world: int, placements: list[Placement], cmul_mo
             _cuda_apply(n_qubits, lb, g, shifts, r, srcs, states[r].local, mode)
         i += 1
     return [s.local for s in states], stats
+
+
+class ShardedDiaq:
+    """This rank's rows of a DiaQ matrix split like a sharded state: rank q
+    owns rows [q*2^B, (q+1)*2^B), B = n_bits - p.  `rows[i]` holds diagonal
+    offs[i] at those rows (row-indexed, so an offset crossing the shard
+    boundary needs no index shuffle).  spmv reads x from every rank's slice
+    -- its own and partners' through peer mappings (PeerComm.share) -- inside
+    the kernel (diaq_spmv_sharded); bitwise the single-GPU spmv."""
+
+    def __init__(self, n: int, offs, rows, row0: int, nrows: int):
+        self.n = int(n)
+        self.offs = np.ascontiguousarray(offs, dtype=np.int64)
+        self.rows = list(rows)
+        self.row0 = int(row0)
+        self.nrows = int(nrows)
+
+    @classmethod
+    def from_matrix(cls, a, rank: int, world: int) -> "ShardedDiaq":
+        """Row slice of a (device) DiaqMatrix for `rank` of `world` (tests and
+        single-node setups; at scale each rank builds its slice directly)."""
+        import torch
+        n = a.n_dim
+        if world & (world - 1) or n % world:
+            raise ValueError(f"{world} ranks do not split n_dim={n} into power-of-two slices")
+        nrows = n // world
+        row0 = rank * nrows
+        dev = a._device()
+        rows = []
+        for d, st in zip(dev.offs.tolist(), dev.starts.tolist()):
+            t = torch.zeros(nrows, dtype=torch.complex128, device=dev.vals.device)
+            lo, hi = max(0, -d, row0), min(n, n - d, row0 + nrows)
+            if hi > lo:  # element of row r sits at k = r + min(d, 0)
+                k0 = st + lo + min(d, 0)
+                t[lo - row0:hi - row0] = dev.vals[k0:k0 + (hi - lo)]
+            rows.append(t)
+        return cls(n, dev.offs, rows, row0, nrows)
+
+    def spmv(self, x_parts, y=None):
+        """y (this rank's rows) = A x; x_parts[q]: rank q's x slice (tensor or address)."""
+        nparts = len(x_parts)
+        part_bits = (self.n // nparts).bit_length() - 1
+        if y is None:
+            y = L.empty_c128(self.nrows)
+        rows = (ctypes.c_void_p * max(1, len(self.rows)))(*[t.data_ptr() for t in self.rows])
+        parts = (ctypes.c_void_p * nparts)(*[_ptr(t) for t in x_parts])
+        L.call("diaq_spmv_sharded", self.n, len(self.offs), self.offs.ctypes.data if len(self.offs) else None,
+               rows, self.row0, self.nrows, parts, part_bits, nparts, y.data_ptr(), L.stream_handle())
+        return y

@@ -54,3 +54,29 @@ def test_peer_sharded_matches_unsharded(tmp_path, configs, n, tile):
     pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
     want = D.run_gates(D.init_state(n), pls, cmul_mode=cmul).amps
     assert np.array_equal(got, want)
+
+
+def test_peer_sharded_spmv_config4(tmp_path):
+    """Sharded spmv whose +-2^21 offsets cross the shard boundary: partner x
+    read in place through a CUDA IPC mapping, bitwise the single-GPU spmv."""
+    import torch
+    out = str(tmp_path / "y.npy")
+    port = _port()
+    worker = os.path.join(ROOT, "tests", "_peer_worker.py")
+    procs = [subprocess.Popen([sys.executable, worker, "--rank", str(r), "--world", "2", "--port", str(port),
+                               "--n", "22", "--mode", "spmv", "--out", out],
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True) for r in range(2)]
+    logs = []
+    try:
+        for p in procs:
+            logs.append(p.communicate(timeout=300)[0])
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+    assert all(p.returncode == 0 for p in procs), "\n".join(logs)
+    c4 = W.config4(22, seed=0, with_x=True)
+    span = D.build_span_unitary(D.from_dense(c4["u4"], 0.0), c4["positions"], c4["span"])
+    a = D.kron_identity(1, span, c4["right"])
+    want = D.spmv(a, torch.from_numpy(c4["x"]).cuda()).cpu().numpy()
+    assert np.array_equal(np.load(out), want)

@@ -66,3 +66,41 @@ def test_sharded_mixed_gates_match_unsharded(cmul):
     for world in (2, 4, 8):
         shards, _ = run_emulated(n, world, pls, cmul_mode=cmul)
         assert np.array_equal(_full(shards), want), world
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sharded_spmv_config4_slice(world):
+    """Row-sharded spmv with x read across shard boundaries (config-4
+    offsets +-2^21 +-8 cross every boundary at n=22), emulated on one GPU:
+    the concatenated rank outputs are bitwise the single-GPU spmv."""
+    import torch
+    from paper_2405_01250_b200.shard import ShardedDiaq
+    c4 = W.config4(22, seed=0, with_x=True)
+    span = D.build_span_unitary(D.from_dense(c4["u4"], 0.0), c4["positions"], c4["span"])
+    a = D.kron_identity(1, span, c4["right"])
+    x = torch.from_numpy(c4["x"]).cuda()
+    want = D.spmv(a, x).cpu().numpy()
+    parts = list(x.chunk(world))
+    got = [ShardedDiaq.from_matrix(a, r, world).spmv(parts) for r in range(world)]
+    assert np.array_equal(torch.cat(got).cpu().numpy(), want)
+
+
+def test_sharded_spmv_ragged_offsets():
+    """Offsets of every sign and size, including |d| > one shard."""
+    import torch
+    from paper_2405_01250_b200.shard import ShardedDiaq
+    rng = np.random.default_rng(3)
+    n = 256
+    offs = [-200, -65, -64, -3, 0, 1, 63, 64, 130, 255]
+    m = np.zeros((n, n), dtype=complex)
+    for d in offs:
+        k = np.arange(n - abs(d))
+        r, c = (k, k + d) if d >= 0 else (k - d, k)
+        m[r, c] = rng.normal(size=len(k)) + 1j * rng.normal(size=len(k))
+    a = D.from_dense(m, 0.0)
+    x = torch.from_numpy(rng.normal(size=n) + 1j * rng.normal(size=n)).cuda()
+    want = D.spmv(a, x).cpu().numpy()
+    for world in (2, 4, 8):
+        parts = list(x.chunk(world))
+        got = torch.cat([ShardedDiaq.from_matrix(a, r, world).spmv(parts) for r in range(world)])
+        assert np.array_equal(got.cpu().numpy(), want), world
