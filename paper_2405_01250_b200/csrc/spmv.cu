@@ -38,9 +38,13 @@ struct SpmvDiag {
 constexpr int kMaxBands = 4;
 constexpr int kMaxHalo = 32;
 
+constexpr int kMaxParts = 64;
+
 template <int MAXD>
 struct SpmvParams {
     int64_t n;
+    int part_bits;                    // sharded x (kernels instantiated with kParts): slice q of
+    const double2 *parts[kMaxParts];  // 2^part_bits elements at parts[q] (own or peer-mapped)
     int64_t r0, rend;  // rows [r0, rend) of y are produced
     int64_t ntiles, stride_tiles, nstrips, nitems;
     int64_t nchunks;   // raster 1: chunks of `chunk` strips per column
@@ -192,7 +196,7 @@ __global__ void __launch_bounds__(kThreads) spmv_banded_kernel(const __grid_cons
 constexpr int kAsyncThreads = 128;
 
 
-template <int ND>
+template <int ND, bool kParts>
 __global__ void __launch_bounds__(kAsyncThreads) spmv_async_kernel(const __grid_constant__ SpmvParams<kParamDiags> p) {
     __shared__ __align__(16) double2 sd[ND > 0 ? ND : 1][kAsyncThreads];
     __shared__ __align__(16) double2 xs[kMaxBands][kAsyncThreads + 2 * kMaxHalo];
@@ -215,7 +219,12 @@ __global__ void __launch_bounds__(kAsyncThreads) spmv_async_kernel(const __grid_
             const int64_t base = r0t + p.center[bd] - h;
             for (int i = threadIdx.x; i < w; i += kAsyncThreads) {
                 const int64_t idx = base + i;
-                if (idx >= 0 && idx < p.n) cp_async16(&xs[bd][i], p.x + idx, polx);
+                if (idx >= 0 && idx < p.n) {
+                    if constexpr (kParts)  // x slice of the owning rank: a peer load across the boundary
+                        cp_async16(&xs[bd][i], p.parts[idx >> p.part_bits] + (idx & ((1ll << p.part_bits) - 1)), polx);
+                    else
+                        cp_async16(&xs[bd][i], p.x + idx, polx);
+                }
             }
         }
         asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
@@ -451,30 +460,33 @@ static int launch_param_x(const SpmvParams<kParamDiags> &p, cudaStream_t s) {
     return check_launch("spmv_kernel");
 }
 
+template <int ND, bool kParts>
+static int launch_async(const SpmvParams<kParamDiags> &p, cudaStream_t s) {
+    const void *f = (const void *)spmv_async_kernel<ND, kParts>;
+    SpmvParams<kParamDiags> q = p;
+    const int64_t nrows = q.rend - q.r0;
+    const int64_t nt = (nrows + kAsyncThreads - 1) / kAsyncThreads;
+    const int64_t scale = kThreads / kAsyncThreads;  // strip stride in 128-row tiles
+    q.ntiles = nt;
+    q.stride_tiles = q.nstrips > 1 ? q.stride_tiles * scale : nt;
+    q.nstrips = (nt + q.stride_tiles - 1) / q.stride_tiles;
+    q.raster = 0;
+    q.nitems = q.stride_tiles * q.nstrips;
+    int per_sm = 1, dev = 0, sms = kSms;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kAsyncThreads, 0);
+    cudaGetLastError();
+    if (tuning().spmv_ctas_per_sm > 0) per_sm = std::min(per_sm, tuning().spmv_ctas_per_sm);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(q.nitems, (int64_t)sms * std::max(1, per_sm)));
+    spmv_async_kernel<ND, kParts><<<grid, kAsyncThreads, 0, s>>>(q);
+    count_launch();
+    return check_launch("spmv_async_kernel");
+}
+
 template <int ND>
 static int launch_param(const SpmvParams<kParamDiags> &p, cudaStream_t s) {
     if constexpr (ND > 0) {
-        if (p.nbands > 0 && tuning().spmv_async) {
-            const void *f = (const void *)spmv_async_kernel<ND>;
-            SpmvParams<kParamDiags> q = p;
-            const int64_t nrows = q.rend - q.r0;
-            const int64_t nt = (nrows + kAsyncThreads - 1) / kAsyncThreads;
-            const int64_t scale = kThreads / kAsyncThreads;  // strip stride in 128-row tiles
-            q.ntiles = nt;
-            q.stride_tiles = q.nstrips > 1 ? q.stride_tiles * scale : nt;
-            q.nstrips = (nt + q.stride_tiles - 1) / q.stride_tiles;
-            q.raster = 0;
-            q.nitems = q.stride_tiles * q.nstrips;
-            int per_sm = 1, dev = 0, sms = kSms;
-            if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kAsyncThreads, 0);
-            cudaGetLastError();
-            if (tuning().spmv_ctas_per_sm > 0) per_sm = std::min(per_sm, tuning().spmv_ctas_per_sm);
-            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(q.nitems, (int64_t)sms * std::max(1, per_sm)));
-            spmv_async_kernel<ND><<<grid, kAsyncThreads, 0, s>>>(q);
-            count_launch();
-            return check_launch("spmv_async_kernel");
-        }
+        if (p.nbands > 0 && tuning().spmv_async) return launch_async<ND, false>(p, s);
         if (p.nbands > 0 && tuning().spmv_tma) {
             const void *f = (const void *)spmv_tma_kernel<ND>;
             SpmvParams<kParamDiags> q = p;
@@ -638,8 +650,6 @@ static int spmv_rows(const diaq_matrix_t *a, const void *x, void *y, int64_t r0,
 // offset that crosses a shard boundary is a direct peer load inside the
 // kernel, no halo copy.  Same per-row ascending-d arithmetic as diaq_spmv:
 // the sharded product is bitwise the single-GPU one.
-constexpr int kMaxParts = 64;
-
 struct ShardSpmvParams {
     int64_t row0, nrows;
     int part_bits, nparts;
@@ -719,10 +729,49 @@ extern "C" int diaq_spmv_sharded(int64_t n, int64_t nd, const int64_t *offs, con
     }
     if (nrows == 0) return DIAQ_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    int dev = 0, sms = kSms;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaGetLastError();
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((nrows + kThreads - 1) / kThreads, (int64_t)sms * 8));
+    if (nd > 0 && nd <= 12 && tuning().spmv_async) {
+        // banded offsets: the cp.async kernel of diaq_spmv with its x windows
+        // staged from the owning rank's slice (row pointers rebased so the
+        // element of global row r is at row0ptr[r])
+        SpmvParams<kParamDiags> q;
+        memset(&q, 0, sizeof(q));
+        q.n = n;
+        q.r0 = row0;
+        q.rend = row0 + nrows;
+        int64_t ntiles, stride, nstrips;
+        spmv_raster(nrows, nd, offs, &ntiles, &stride, &nstrips);
+        q.ntiles = ntiles;
+        q.stride_tiles = stride;
+        q.nstrips = nstrips;
+        q.y = (double2 *)y - row0;
+        q.nd = (int)nd;
+        q.part_bits = part_bits;
+        for (int qq = 0; qq < nparts; ++qq) q.parts[qq] = p.parts[qq];
+        for (int64_t i = 0; i < nd; ++i) {
+            q.dg[i].off = p.off[i];
+            q.dg[i].row0 = p.rows[i] - row0;
+            q.dg[i].lo = p.lo[i];
+            q.dg[i].hi = p.hi[i];
+        }
+        plan_bands(q);
+        if (q.nbands > 0) {
+            switch (nd) {
+                case 1: return launch_async<1, true>(q, s);
+                case 2: return launch_async<2, true>(q, s);
+                case 3: return launch_async<3, true>(q, s);
+                case 4: return launch_async<4, true>(q, s);
+                case 5: return launch_async<5, true>(q, s);
+                case 6: return launch_async<6, true>(q, s);
+                case 7: return launch_async<7, true>(q, s);
+                case 8: return launch_async<8, true>(q, s);
+                case 9: return launch_async<9, true>(q, s);
+                case 10: return launch_async<10, true>(q, s);
+                case 11: return launch_async<11, true>(q, s);
+                default: return launch_async<12, true>(q, s);
+            }
+        }
+    }
+    int dev = 0, sms = kSms;    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((nrows + kThreads - 1) / kThreads, (int64_t)sms * 8));
     switch (nd) {
 #define DIAQ_SHARD_ND(K) \
     case K: spmv_sharded_kernel<K><<<(unsigned)grid, kThreads, 0, s>>>(p); break;
