@@ -127,6 +127,8 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("DIAQ_BENCH_SAME_GPU"):  # functional check of the N>1 code on one GPU (not a measurement)
+        local = 0
     return rank, world, local
 
 
@@ -222,7 +224,7 @@ def run_ours(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist = init_dist(world, "nccl")
+    dist = init_dist(world, os.environ.get("DIAQ_BENCH_DIST_BACKEND", "nccl"))
     lib = L.load()
     n = args.n
     N = 2**n
@@ -247,6 +249,28 @@ def run_ours(args):
 
     def spmv_launch():
         L.call("diaq_spmv", __import__("ctypes").byref(st), x.data_ptr(), y.data_ptr(), s.cuda_stream)
+
+    # N>1: the 2^(n+p) product kron(I, A) with its rows sharded over the ranks
+    # (each rank builds only its own block); x stays in place on its rank and
+    # the offsets that cross a shard boundary read the partner's x through a
+    # peer mapping inside the kernel.  Falls back to replicas (no data-path
+    # communication) when the GPUs cannot map each other.
+    spmv_mode = "replicas" if world > 1 else "single GPU"
+    if world > 1 and not args.replicas:
+        try:
+            from paper_2405_01250_b200.shard import PeerComm, ShardedDiaq
+            pcomm = PeerComm()
+            sd = ShardedDiaq.from_block(a, rank, world)
+            xs, xptr = L.shared_c128(N)
+            xs.copy_(x)
+            parts = [row[0] for row in pcomm.share([xptr])]
+            pcomm.barrier()
+
+            def spmv_launch():  # noqa: F811 -- the sharded product replaces the replica
+                sd.spmv(parts, y)
+            spmv_mode = f"rows of a 2^{n + world.bit_length() - 1} product sharded over {world} ranks, x via peer loads"
+        except L.DeviceError as e:
+            spmv_mode = f"replicas (peer mapping failed: {e})"
 
     for _ in range(args.warmup):
         spmv_launch()
@@ -325,7 +349,7 @@ def run_ours(args):
     achieved = nbytes / (kern_ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": peak_src,
-                "traffic": prof.get("spmv_dram_bytes_per_launch"),
+                "traffic": prof.get("spmv_dram_bytes_per_launch") if n == N_QUBITS else None,
                 "alg_bytes_per_launch": nbytes, "kernel": "diaq::spmv_async_kernel<9> (cp.async-staged banded spmv)",
                 "frac_of_8TBs_spec": round(achieved / 8000.0, 4)}
     gates_scale = 1 if (world > 1 and args.sharded_gates) else world
@@ -334,7 +358,7 @@ def run_ours(args):
              "roofline": {"bound": "hbm", "achieved": round(gate_bytes / (ms_per_pass * 1e-3) / 1e9, 1),
                           "peak": peak, "unit": "GB/s",
                           "frac": round(gate_bytes / (ms_per_pass * 1e-3) / 1e9 / peak, 4),
-                          "traffic": prof.get("gate_dram_bytes_per_launch"),
+                          "traffic": prof.get("gate_dram_bytes_per_launch") if n == N_QUBITS else None,
                           "alg_bytes_per_launch": gate_bytes,
                           "per": "HBM pass (one kernel launch = one read+write sweep of the state; "
                                  "a fused pass applies several gates)",
@@ -352,11 +376,11 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: seeded Haar-random 2-qubit gate (config 4), normalised Gaussian x",
-        "config": {"workload": "config4 spmv n=28: kron_identity(2^6, span(Haar4,[18,0],19), 2^3)",
+        "config": {"workload": f"config4 spmv n={n}: kron_identity(2^{n - 22}, span(Haar4,[18,0],19), 2^3)",
                    "n_qubits": n, "N": N, "offsets": offs, "alg_bytes_per_step": nbytes,
                    "matrix_bytes": 16 * sum(N - abs(d) for d in offs),
                    "l2": "inputs (47 GB/step) far larger than the 126 MB L2; no flush needed",
-                   "parallelism": f"replicas x{world}", "build_s": round(t_build, 3)},
+                   "parallelism": spmv_mode, "build_s": round(t_build, 3)},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
@@ -410,11 +434,11 @@ def sharded_gates(args, D, L, W, torch, dist, n, world, x, s, dev):
     transport = args.transport
     comm = PeerComm() if transport == "peer" else TorchDistComm()
     try:
-        st = ShardedState(ns, x.clone(), comm)
+        st = ShardedState(ns, x / world ** 0.5, comm)  # every rank's x has norm 1: global norm 1
     except L.DeviceError as e:  # no peer mapping between these GPUs: staged NCCL exchange
         transport = f"nccl (peer mapping failed: {e})"
         comm = TorchDistComm()
-        st = ShardedState(ns, x.clone(), comm)
+        st = ShardedState(ns, x / world ** 0.5, comm)
     ops = W.random_layered_ops(ns, 1, seed=0)
     pls = D.compile_circuit(D.Circuit(ns, [D.GateOp(*o) for o in ops]), span_limit=ns)
     st.apply_placements(pls)
@@ -534,12 +558,14 @@ def main():
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=N_QUBITS)
+    ap.add_argument("--qubits", "--n", dest="n", type=int, default=N_QUBITS)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--sharded-gates", action="store_true",
                     help="N>1: measure gates on a state sharded over the ranks instead of replicas")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: independent spmv replicas instead of the row-sharded product")
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
                     help="sharded gates: partner shards read in place over peer memory, or NCCL-staged")
     args = ap.parse_args()

@@ -136,18 +136,41 @@ class PeerComm(TorchDistComm):
         self._opened: list[int] = []
 
     def share(self, ptrs: list[int]) -> list[list[int]]:
-        """table[q][i] = this process's address of rank q's buffer i."""
-        mine = [L.ipc_handle(p) for p in ptrs]
+        """table[q][i] = this process's address of rank q's buffer i.  Every
+        rank learns whether every other one could map its partners, and all
+        raise DeviceError together if one could not (no rank is left waiting
+        in a collective the others skipped)."""
+        err = None
+        try:
+            mine = [L.ipc_handle(p) for p in ptrs]
+        except Exception as e:  # noqa: BLE001 -- reported to every rank below
+            mine, err = None, repr(e)
         allh = [None] * self.world
         self.dist.all_gather_object(allh, mine, group=self.group)
-        table = []
-        for q, hs in enumerate(allh):
-            if q == self.rank:
-                table.append(list(ptrs))
-                continue
-            row = [L.ipc_open(h) for h in hs]
-            self._opened += row
-            table.append(row)
+        table, opened = [], []
+        if err is None and all(h is not None for h in allh):
+            try:
+                for q, hs in enumerate(allh):
+                    if q == self.rank:
+                        table.append(list(ptrs))
+                        continue
+                    row = []
+                    for h in hs:
+                        row.append(L.ipc_open(h))
+                        opened.append(row[-1])
+                    table.append(row)
+            except Exception as e:  # noqa: BLE001
+                err = repr(e)
+        else:
+            err = err or "a partner could not export its buffers"
+        errs = [None] * self.world
+        self.dist.all_gather_object(errs, err, group=self.group)
+        bad = [e for e in errs if e is not None]
+        if bad:
+            for ptr in opened:
+                L.ipc_close(ptr)
+            raise L.DeviceError(f"peer mapping failed: {bad[0]}")
+        self._opened += opened
         return table
 
     def barrier(self) -> None:
@@ -430,6 +453,27 @@ class ShardedDiaq:
                 t[lo - row0:hi - row0] = dev.vals[k0:k0 + (hi - lo)]
             rows.append(t)
         return cls(n, dev.offs, rows, row0, nrows)
+
+    @classmethod
+    def from_block(cls, a, rank: int, world: int) -> "ShardedDiaq":
+        """This rank's rows of kron(I_world, a) -- a matrix whose shards are
+        diagonal blocks (e.g. kron_identity with the left identity spanning
+        the shard bits): the rank builds only its own 2^B block `a`; global
+        diagonal entries outside the block are the stored zeros of the
+        Kronecker expansion, and their x reads still go to the partner (so
+        the signs of zero match the single-GPU product)."""
+        import torch
+        nloc = a.n_dim
+        dev = a._device()
+        rows = []
+        for d, st in zip(dev.offs.tolist(), dev.starts.tolist()):
+            t = torch.zeros(nloc, dtype=torch.complex128, device=dev.vals.device)
+            lo, hi = max(0, -d), min(nloc, nloc - d)
+            if hi > lo:
+                k0 = st + lo + min(d, 0)
+                t[lo:hi] = dev.vals[k0:k0 + (hi - lo)]
+            rows.append(t)
+        return cls(nloc * world, dev.offs, rows, rank * nloc, nloc)
 
     def spmv(self, x_parts, y=None):
         """y (this rank's rows) = A x; x_parts[q]: rank q's x slice (tensor or address)."""
