@@ -73,6 +73,8 @@ def main():
     ap.add_argument("--tag", required=True)
     ap.add_argument("--full", nargs="*", default=[])
     ap.add_argument("--launches")
+    ap.add_argument("--cmd", default="python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --no-secondary",
+                    help="the profiled command, for the summary header")
     args = ap.parse_args()
     os.makedirs("profiles", exist_ok=True)
     full = {}
@@ -110,8 +112,7 @@ def main():
         total = sum(v[1] for v in agg.values())
         with open(f"profiles/{args.tag}_launch_shares.md", "w") as f:
             f.write(f"# Launch list summary ({args.tag}): ncu gpu__time_duration.sum, --clock-control none\n\n")
-            f.write("Cold-cache, serialised per-launch times of `python bench.py --steps 5 --warmup 3 "
-                    "--no-e2e --no-cpu`; compare shares, not absolutes.\n\n")
+            f.write(f"Cold-cache, serialised per-launch times of `{args.cmd}`; compare shares, not absolutes.\n\n")
             f.write("| kernel | launches | total ms | avg ms | share |\n|---|---|---|---|---|\n")
             for k, (c, ns) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
                 f.write(f"| `{k}` | {c} | {ns / 1e6:.3f} | {ns / c / 1e6:.4f} | {100 * ns / total:.1f}% |\n")
