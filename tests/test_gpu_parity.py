@@ -551,3 +551,27 @@ def test_spmv_tma_pipeline_is_bitwise():
     finally:
         L.tune("spmv_tma", 0)
         L.tune("spmv_tma_stages", 4)
+
+
+def test_fused_program_cache_keys_on_values(cmul):
+    """The per-thread cache of scheduled fused programs is keyed by the exact
+    gate data: same structure with other angles, or the same gates on other
+    qubits, must not reuse a stale program."""
+    n = 14
+    runs = []
+    for seed in (1, 2, 1, 3, 1):  # interleave so cached entries are hit and evicted
+        ops = W.random_layered_ops(n, 2, seed=seed)
+        pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
+        got = D.run_gates(D.init_state(n), pls, cmul_mode=cmul, tile_bits=12).amps
+        want = D.run_gates(D.init_state(n), pls, cmul_mode=cmul, tile_bits=0).amps
+        assert np.array_equal(got, want), seed
+        runs.append(got)
+    assert np.array_equal(runs[0], runs[2]) and np.array_equal(runs[0], runs[4])
+    assert not np.array_equal(runs[0], runs[1])
+    # same angles, operands moved: a different program
+    ops = [("rx", (q,), (0.3,)) for q in range(n)]
+    ops2 = [("rx", (n - 1 - q,), (0.3,)) for q in range(n)] + [("cx", (0, 5), ())]
+    for o in (ops, ops2, ops):
+        pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*x) for x in o]), span_limit=n)
+        assert np.array_equal(D.run_gates(D.init_state(n), pls, cmul_mode=cmul, tile_bits=12).amps,
+                              D.run_gates(D.init_state(n), pls, cmul_mode=cmul, tile_bits=0).amps)
