@@ -194,3 +194,31 @@ def test_fused_schedule_host_only(lib):
     # shard view: a gate mixing a global bit is refused (it needs the partner shard)
     with pytest.raises(ValueError):
         _plan(lib, 24, [("h", (0,), ())], local_bits=22)
+
+
+def test_sharded_and_peer_entry_points_validate_first(lib):
+    """Argument errors of the sharded/peer ABI are reported before any device
+    work (so they behave the same with or without a GPU)."""
+    P = ctypes.c_void_p
+    offs = np.array([-4, 0, 4], dtype=np.int64)
+    rows = (P * 3)(1, 2, 3)
+    parts = (P * 2)(16, 32)
+    y = P(64)
+    # parts do not tile n
+    assert lib.diaq_spmv_sharded(100, 3, offs.ctypes.data, rows, 0, 50, parts, 5, 2, y, None) == L.DIAQ_ERR_SHAPE
+    # rows outside n
+    assert lib.diaq_spmv_sharded(64, 3, offs.ctypes.data, rows, 40, 32, parts, 5, 2, y, None) == L.DIAQ_ERR_SHAPE
+    # offsets not ascending / out of range
+    bad = np.array([0, -4, 4], dtype=np.int64)
+    assert lib.diaq_spmv_sharded(64, 3, bad.ctypes.data, rows, 0, 32, parts, 5, 2, y, None) == L.DIAQ_ERR_VALUE
+    far = np.array([-64, 0, 4], dtype=np.int64)
+    assert lib.diaq_spmv_sharded(64, 3, far.ctypes.data, rows, 0, 32, parts, 5, 2, y, None) == L.DIAQ_ERR_VALUE
+    # a missing x part
+    holes = (P * 2)(16, None)
+    assert lib.diaq_spmv_sharded(64, 3, offs.ctypes.data, rows, 0, 32, holes, 5, 2, y, None) == L.DIAQ_ERR_VALUE
+    assert "x part 1 missing" in L.last_error()
+    # peer-memory helpers
+    assert lib.diaq_alloc(0, ctypes.byref(P())) == L.DIAQ_ERR_VALUE
+    assert lib.diaq_ipc_handle(None, ctypes.create_string_buffer(64)) == L.DIAQ_ERR_VALUE
+    assert lib.diaq_ipc_open(None, ctypes.byref(P())) == L.DIAQ_ERR_VALUE
+    assert lib.diaq_free(None) == L.DIAQ_OK and lib.diaq_ipc_close(None) == L.DIAQ_OK
