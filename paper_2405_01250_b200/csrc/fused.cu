@@ -96,6 +96,13 @@ __device__ __forceinline__ uint32_t aff_const(const Affine &m, uint64_t sbase) {
 struct Phase {
     int16_t g0, g1;           // gates [g0, g1) of the pass (pass-relative)
     int8_t generic;           // 1: gates applied in shared memory (no register bits)
+    // sequence phase: its dense gates hit register bits 0, 1, ... in order
+    // (register bits in first-use order), any other gate is a diagonal on a
+    // non-register bit; nd_before[b] diagonals precede the dense gate on bit
+    // b (nd_before[R]: trailing).  The kernel then unrolls over the register
+    // bit, so every dense step has a compile-time pairing.
+    int8_t seq, ndense;
+    int8_t nd_before[5];
     int8_t rpos[4];           // tile positions of the register bits, ascending (R entries)
     int8_t tpos[kMaxTileBits];  // tile positions of the thread bits, ascending (T - R entries)
     Affine post;              // permutation run after the phase's gates, applied by its store
@@ -223,6 +230,22 @@ __device__ __forceinline__ uint64_t ld_base(const uint64_t *s) {
     return v;
 }
 
+// diagonal gate whose selector is a thread or base bit: one factor for all
+// of this thread's amplitudes
+template <int R, int MODE>
+__device__ __forceinline__ void diag_uniform(double2 (&v)[1 << R], const RegGate &G, uint32_t tpart,
+                                             const uint64_t *sbase_p, const double2 *sc, const uint32_t *snz) {
+    const uint32_t b = G.osel[0] == 0 ? (uint32_t)((ld_base(sbase_p) >> G.opos[0]) & 1ull) : (tpart >> G.opos[0]) & 1u;
+    const double2 d = sc[G.coef_off + (int)b];
+    if (snz[G.nz_off + (int)b] & 1u) {
+#pragma unroll
+        for (int j = 0; j < (1 << R); ++j) v[j] = cmul<MODE>(d, v[j]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < (1 << R); ++j) v[j] = make_double2(0.0, 0.0);
+    }
+}
+
 template <int R, int MODE>
 __device__ __forceinline__ void dispatch_gate(double2 (&v)[1 << R], const RegGate &G, uint32_t tpart, const uint64_t *sbase_p,
                                               const double2 *sc, const uint32_t *snz) {
@@ -282,6 +305,20 @@ __device__ __forceinline__ void smem_gate(double2 *tile, int T, const RegGate &G
             tile[i0] = a0;
             tile[i1] = a1;
         }
+    }
+}
+
+// sequence phase, register bit RB onwards: the diagonals before the dense
+// gate on RB, then that gate with its pairing fixed at compile time
+template <int R, int MODE, int RB>
+__device__ __forceinline__ void seq_steps(double2 (&v)[1 << R], const TileParams &p, const Phase &ph, int &gi,
+                                          uint32_t tpart, const uint64_t *sbase_p, const double2 *sc,
+                                          const uint32_t *snz) {
+    for (int c = 0; c < ph.nd_before[RB]; ++c, ++gi) diag_uniform<R, MODE>(v, p.g[gi], tpart, sbase_p, sc, snz);
+    if (RB < ph.ndense) {
+        dense1_full<R, RB, MODE>(v, sc + p.g[gi].coef_off);
+        ++gi;
+        if constexpr (RB + 1 < R) seq_steps<R, MODE, RB + 1>(v, p, ph, gi, tpart, sbase_p, sc, snz);
     }
 }
 
@@ -380,7 +417,13 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
 #pragma unroll
                 for (int j = 0; j < NR; ++j) v[j] = tl[swz(tpart | reg_spread<R>(j, ph.rpos))];
             }
-            for (int gi = ph.g0; gi < ph.g1; ++gi) dispatch_gate<R, MODE>(v, p.g[gi], tpart, &s_sbase, sc, snz);
+            if (ph.seq) {
+                int gi = ph.g0;
+                seq_steps<R, MODE, 0>(v, p, ph, gi, tpart, &s_sbase, sc, snz);
+                for (int c = 0; c < ph.nd_before[R]; ++c, ++gi) diag_uniform<R, MODE>(v, p.g[gi], tpart, &s_sbase, sc, snz);
+            } else {
+                for (int gi = ph.g0; gi < ph.g1; ++gi) dispatch_gate<R, MODE>(v, p.g[gi], tpart, &s_sbase, sc, snz);
+            }
             if (ph.post.on) {
                 __syncthreads();  // relabelled slots belong to other threads' registers: all reads first
                 const uint32_t bc = aff_const(ph.post, ld_base(&s_sbase));
@@ -787,10 +830,24 @@ static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gate
                 ps.phases.push_back(ph);
                 continue;
             }
-            std::vector<int> rp = sp.used;
+            std::vector<int> rp = sp.used;  // first-use order of the mixing bits
+            const bool seq_try = tuning().fused_seq != 0;
+            if (seq_try) {  // pad with positions no diagonal of the phase selects on
+                std::vector<int> sel;
+                for (int gi : sp.mem) {
+                    const diaq_gate_t &gt = gates[gi];
+                    const uint32_t mix = mixing_mask(gt.k, gt.g);
+                    for (int o = 0; o < gt.k; ++o)
+                        if (!((mix >> o) & 1u)) sel.push_back(tile_pos(ps.bits, gt.shifts[o]));
+                }
+                for (int tp = 0; (int)rp.size() < R && tp < (int)ps.bits.size(); ++tp)
+                    if (std::find(rp.begin(), rp.end(), tp) == rp.end() &&
+                        std::find(sel.begin(), sel.end(), tp) == sel.end())
+                        rp.push_back(tp);
+            }
             for (int tp = 0; (int)rp.size() < R; ++tp)
                 if (std::find(rp.begin(), rp.end(), tp) == rp.end()) rp.push_back(tp);
-            std::sort(rp.begin(), rp.end());
+            if (!seq_try) std::sort(rp.begin(), rp.end());
             for (int q = 0; q < R; ++q) ph.rpos[q] = rp[q];
             int tq = 0;
             for (int tp = 0; tp < (int)ps.bits.size(); ++tp)
@@ -804,6 +861,27 @@ static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gate
             }
             ph.g1 = (int)ps.gates.size();
             ph.post = sp.post.pack();
+            if (seq_try) {  // sequence form?
+                int nd = 0, cnt = 0;
+                bool ok = true;
+                for (int g = ph.g0; g < ph.g1 && ok; ++g) {
+                    const RegGate &G = ps.gates[g];
+                    if (G.op == 1 && G.rb[0] == nd && nd < R) {
+                        ph.nd_before[nd++] = (int8_t)cnt;
+                        cnt = 0;
+                    } else if (G.op == 2 && G.osel[0] != 2 && cnt < 127) {
+                        ++cnt;
+                    } else {
+                        ok = false;
+                    }
+                }
+                if (ok) {
+                    ph.seq = 1;
+                    ph.ndense = (int8_t)nd;
+                    for (int b = nd; b <= R; ++b) ph.nd_before[b] = 0;
+                    ph.nd_before[R] = (int8_t)cnt;
+                }
+            }
             ps.phases.push_back(ph);
         }
         if ((int)ps.phases.size() > kMaxPhases || (int)ps.gates.size() > kMaxPassGates)

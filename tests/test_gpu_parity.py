@@ -405,9 +405,15 @@ def test_fused_passes_match_unfused(cmul):
                                gate=(u, [a - lo, b - lo])))
         x0 = D.StateVector(n, W.random_state(rng, 2**n))
         want = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=0).amps
-        for tb in (6, 8, 11, 12):
-            got = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=tb).amps
-            assert np.array_equal(got, want), (n, tb)
+        from paper_2405_01250_b200 import _lib as L
+        for seq in (1, 0):  # sequence phases (unrolled register bits) and the generic gate loop
+            L.tune("fused_seq", seq)
+            try:
+                for tb in (6, 8, 11, 12):
+                    got = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=tb).amps
+                    assert np.array_equal(got, want), (n, tb, seq)
+            finally:
+                L.tune("fused_seq", 1)
 
 
 def _perm_gate(q):
