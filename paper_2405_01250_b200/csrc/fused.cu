@@ -24,6 +24,9 @@
 // those bits are fixed, so they only select which sub-block of the gate
 // applies (the same argument as the sharded kernel, apply.cu).
 #include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -124,6 +127,10 @@ struct TileParams {
     uint64_t tmask;           // state bits of the tile
     uint64_t gstep;           // gridDim.x deposited into the non-tile bits (tile base stride)
     Affine pre;               // permutation run opening the pass, applied by the tile load
+    double2 *y;               // destination (== x: in place)
+    int gperm;                // store through the global map (out of place)
+    uint64_t gconst;          // its constant, rank bits folded in
+    uint64_t gcol[64];        // image of local state bit j
     Phase ph[kMaxPhases];
     RegGate g[kMaxPassGates]; // pass-relative order
     double2 coef[kMaxCoef];
@@ -337,6 +344,7 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
     __shared__ uint16_t s_lt[kThreads];
     __shared__ uint16_t s_lk[1 << (kMaxTileBits - kThreadBits)];
     __shared__ uint64_t s_sbase;  // current tile's base | rank bits (selector lookups)
+    __shared__ uint64_t s_ghi[(1 << kMaxTileBits) >> kLowBits];  // global map of each tile row offset
     constexpr int NR = 1 << R;
     const int T = p.tbits;
     const uint32_t tsize = 1u << T;
@@ -367,6 +375,23 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
     if (p.pre.on) {
         s_lt[threadIdx.x] = (uint16_t)swz(aff_lin(p.pre, threadIdx.x, T));
         if (threadIdx.x < (tsize >> kThreadBits)) s_lk[threadIdx.x] = (uint16_t)swz(aff_lin(p.pre, threadIdx.x << kThreadBits, T));
+    }
+    __shared__ uint64_t glo[1 << kLowBits];  // global map of the in-row offsets
+    if (p.gperm) {
+        for (uint32_t h = threadIdx.x; h < (tsize >> kLowBits); h += blockDim.x) {
+            uint64_t o = hi_off[h], r = 0;
+            while (o) {
+                r ^= p.gcol[__ffsll((long long)o) - 1];
+                o &= o - 1;
+            }
+            s_ghi[h] = r;
+        }
+        if (threadIdx.x < (1u << kLowBits)) {
+            uint64_t r = 0;
+            for (int b = 0; b < kLowBits; ++b)
+                if ((threadIdx.x >> b) & 1u) r ^= p.gcol[b];
+            glo[threadIdx.x] = r;
+        }
     }
     // HBM -> smem with cp.async, coalesced (consecutive e are consecutive
     // state indices in runs of 8); every element of the tile in flight at once
@@ -444,9 +469,21 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
             }
             __syncthreads();
         }
-        for (int k = 0; k < per_thread; ++k) {
-            const uint32_t e = threadIdx.x + (uint32_t)k * kThreads;
-            st_stream(p.x + base + (e & lowmask) + hi_off[e >> kLowBits], tl[swz(e)]);
+        if (p.gperm) {  // trailing permutation run: element i goes to A i ^ c in the other buffer
+            uint64_t ab = p.gconst, o = base;
+            while (o) {
+                ab ^= p.gcol[__ffsll((long long)o) - 1];
+                o &= o - 1;
+            }
+            for (int k = 0; k < per_thread; ++k) {
+                const uint32_t e = threadIdx.x + (uint32_t)k * kThreads;
+                st_stream(p.y + (ab ^ s_ghi[e >> kLowBits] ^ glo[e & lowmask]), tl[swz(e)]);
+            }
+        } else {
+            for (int k = 0; k < per_thread; ++k) {
+                const uint32_t e = threadIdx.x + (uint32_t)k * kThreads;
+                st_stream(p.y + base + (e & lowmask) + hi_off[e >> kLowBits], tl[swz(e)]);
+            }
         }
         __syncthreads();
         base = next_base(base, p);
@@ -485,6 +522,14 @@ struct PassPlan {
     std::vector<RegGate> gates;   // pass-relative
     Packed pk;                    // pass-relative coefficient tables
     Affine pre;                   // permutation run opening the pass (pre.on = 0: none)
+    // trailing permutation run leaving the tile, composed over the whole
+    // local index and applied by the final store (out of place): new index =
+    // XOR of gcol[j] over the set old bits j ^ gc ^ XOR of ggcol[g] over the
+    // set global (rank) bits g
+    bool gon = false;
+    size_t tail = SIZE_MAX;
+    std::vector<uint64_t> gcol, ggcol;
+    uint64_t gc = 0;
 };
 
 static int tile_pos(const std::vector<int> &bits, int shift) {
@@ -605,6 +650,58 @@ struct HostAffine {
         a.nb = (int)base.size();
         for (size_t b = 0; b < base.size(); ++b) a.bbit[b] = base[b];
         return a;
+    }
+};
+
+// A run of permutation gates composed over the whole local index (the
+// trailing run of a pass whose targets leave the tile): old local index i
+// moves to new index A i ^ c ^ (sum over set global (rank) bits of gcol).
+// Applied by the pass's final store -- out of place, since amplitudes move
+// between tiles.
+struct GlobalAffine {
+    struct Expr {
+        uint64_t m = 0;  // local input bits
+        uint64_t g = 0;  // global input bits (bit index - n)
+        bool c = false;
+        Expr operator^(const Expr &o) const { return Expr{m ^ o.m, g ^ o.g, c != o.c}; }
+        bool operator!=(const Expr &o) const { return m != o.m || g != o.g || c != o.c; }
+    };
+    int n = 0;
+    bool on = false;
+    std::vector<Expr> row;  // new local bit o as a combination of old bits
+
+    void init(int nbits) {
+        n = nbits;
+        on = false;
+        row.assign(n, Expr{});
+        for (int o = 0; o < n; ++o) row[o].m = 1ull << o;
+    }
+    bool fold(const diaq_gate_t &gt, const PermGate &pg) {
+        const int k = gt.k;
+        std::vector<Expr> in(k), out(k);
+        for (int i = 0; i < k; ++i) {
+            const int sh = gt.shifts[i];
+            if (sh < n) {
+                in[i] = row[sh];
+            } else {
+                if (sh - n >= 64) return false;
+                in[i].g = 1ull << (sh - n);
+            }
+        }
+        for (int i = 0; i < k; ++i) {  // operand i is gate-index bit k-1-i
+            const int gb = k - 1 - i;
+            Expr e;
+            e.c = (pg.d >> gb) & 1u;
+            for (int m = 0; m < k; ++m)
+                if ((pg.col[m] >> gb) & 1u) e = e ^ in[k - 1 - m];
+            out[i] = e;
+        }
+        for (int i = 0; i < k; ++i)
+            if (gt.shifts[i] >= n && out[i] != in[i]) return false;  // a global bit cannot move
+        for (int i = 0; i < k; ++i)
+            if (gt.shifts[i] < n) row[gt.shifts[i]] = out[i];
+        on = true;
+        return true;
     }
 };
 
@@ -734,6 +831,7 @@ static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gate
     std::vector<int> pbase;  // non-mixing operand bits of the pass's permutation gates (fold bound)
     int nb = 0;
     int ncoef = 0, nnz = 0;  // the pass's coefficient / mask table entries (kernel parameter bound)
+    size_t tail = SIZE_MAX;  // members[tail..]: permutation run folded over the whole index (final store)
     auto reset = [&]() {
         std::fill(inb.begin(), inb.end(), 0);
         nb = 0;
@@ -741,6 +839,7 @@ static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gate
         members.clear();
         pbase.clear();
         ncoef = nnz = 0;
+        tail = SIZE_MAX;
     };
     auto flush = [&]() -> int {
         if (members.empty()) return DIAQ_OK;
@@ -764,7 +863,8 @@ static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gate
         HostAffine pre;
         pre.init((int)ps.bits.size());
         bool open = false;
-        for (size_t i = 0; i < members.size(); ++i) {
+        const size_t body = std::min(tail, members.size());
+        for (size_t i = 0; i < body; ++i) {
             const int gi = members[i];
             const diaq_gate_t &gt = gates[gi];
             if (perm[(size_t)gi].ok) {
@@ -815,6 +915,24 @@ static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gate
             open = false;
         }
         ps.pre = pre.pack();
+        if (tail < members.size()) {  // trailing run leaving the tile: one map over the whole local index
+            GlobalAffine ga;
+            ga.init(n_bits);
+            for (size_t i = tail; i < members.size(); ++i)
+                if (!ga.fold(gates[members[i]], perm[(size_t)members[i]]))
+                    return set_error(DIAQ_ERR_VALUE, "fused pass: permutation moves a global bit");
+            ps.tail = tail;
+            ps.gon = true;
+            ps.gcol.assign((size_t)n_bits, 0);
+            ps.ggcol.assign(64, 0);
+            for (int o = 0; o < n_bits; ++o) {
+                for (int j = 0; j < n_bits; ++j)
+                    if ((ga.row[o].m >> j) & 1ull) ps.gcol[j] |= 1ull << o;
+                for (int g = 0; g < 64; ++g)
+                    if ((ga.row[o].g >> g) & 1ull) ps.ggcol[g] |= 1ull << o;
+                if (ga.row[o].c) ps.gc |= 1ull << o;
+            }
+        }
         // 2. pack
         for (const Spec &sp : specs) {
             Phase ph;
@@ -908,6 +1026,27 @@ static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gate
             }
         }
         const bool pg = perm[(size_t)i].ok;
+        if (!pg && tail != SIZE_MAX) {  // a gate after a global permutation tail opens the next pass
+            int rc = flush();
+            if (rc) return rc;
+            reset();
+            add = 0;
+            for (int j = 0; j < gt.k; ++j)
+                if (((mix >> j) & 1u) && !inb[gt.shifts[j]]) ++add;
+        }
+        if (pg && !members.empty() && tuning().fused_gperm) {
+            // a permutation that does not fit the tile (or follows one that did
+            // not) joins the pass's global tail instead of opening a pass
+            int padd0 = 0;
+            for (int j = 0; j < gt.k; ++j)
+                if (!((mix >> j) & 1u) && std::find(pbase.begin(), pbase.end(), gt.shifts[j]) == pbase.end()) ++padd0;
+            if (tail != SIZE_MAX || kin > T - low || nb + add > T || (int)pbase.size() + padd0 > kMaxPermBase ||
+                (int)members.size() >= std::min(kMaxPassGates, kMaxPhases)) {
+                if (tail == SIZE_MAX) tail = members.size();
+                members.push_back(i);
+                continue;
+            }
+        }
         if (pg ? (kin > T - low) : (kin > kMaxRegKin || kin > R || kout > kMaxSel)) {  // standalone pass
             int rc = flush();
             if (rc) return rc;
@@ -997,6 +1136,20 @@ struct Program {
     std::vector<TileParams> params;  // per tiled pass (x, gbase and the grid are filled in at launch)
 };
 
+static void debug_plan(const std::vector<PassPlan> &plan) {
+    {
+        for (size_t i = 0; i < plan.size(); ++i) {
+            const PassPlan &ps = plan[i];
+            fprintf(stderr, "pass %zu: %zu gates, bits", i, ps.members.size());
+            for (int b : ps.bits) fprintf(stderr, " %d", b);
+            fprintf(stderr, "%s\n", ps.pre.on ? " [pre-perm]" : "");
+            for (const Phase &ph : ps.phases)
+                fprintf(stderr, "  phase g[%d,%d) generic=%d seq=%d ndense=%d post=%d rpos %d %d %d %d\n", ph.g0, ph.g1,
+                        ph.generic, ph.seq, ph.ndense, ph.post.on, ph.rpos[0], ph.rpos[1], ph.rpos[2], ph.rpos[3]);
+        }
+    }
+}
+
 static std::vector<char> program_key(int n_total, int n_bits, int T, int ngates, const diaq_gate_t *gates) {
     std::vector<char> key;
     auto put = [&](const void *p, size_t n) {
@@ -1029,6 +1182,7 @@ static std::shared_ptr<const Program> build_program(int n_total, int n_bits, int
             plan.push_back(ps);
         }
     }
+    if (getenv("DIAQ_PLAN_DEBUG")) debug_plan(plan);
     prog->params.resize(plan.size());
     for (size_t i = 0; i < plan.size(); ++i) {
         const PassPlan &ps = plan[i];
@@ -1051,6 +1205,11 @@ static std::shared_ptr<const Program> build_program(int n_total, int n_bits, int
         p.ncoef = (int)ps.pk.coef.size();
         p.nnz = (int)ps.pk.nz.size();
         p.pre = ps.pre;
+        p.gperm = ps.gon ? 1 : 0;
+        if (ps.gon) {
+            for (size_t j = 0; j < ps.gcol.size() && j < 64; ++j) p.gcol[j] = ps.gcol[j];
+            p.gconst = ps.gc;  // rank bits folded in at launch
+        }
         std::copy(ps.phases.begin(), ps.phases.end(), p.ph);
         std::copy(ps.gates.begin(), ps.gates.end(), p.g);
         std::copy(ps.pk.coef.begin(), ps.pk.coef.end(), p.coef);
@@ -1107,17 +1266,52 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
     if (events && cudaEventRecord((cudaEvent_t)events[0], s) != cudaSuccess)
         return set_error(DIAQ_ERR_CUDA, "diaq_run_gates_fused: event record failed");
     thread_local TileParams tparams;
-    for (size_t pi = 0; pi < plan.size() && rc == DIAQ_OK; ++pi) {
+    // Buffers: a pass with a global permutation tail writes the other buffer
+    // (amplitudes move between tiles); every other pass may run in place or
+    // out of place.  Flip one flexible pass when the forced flips are odd,
+    // so the result lands in `state` (else copy it back at the end).
+    const size_t np = plan.size();
+    std::vector<char> flip(np, 0);
+    int nflip = 0, flexible = -1;
+    for (size_t pi = 0; pi < np; ++pi) {
+        const PassPlan &ps = plan[pi];
+        const bool tiled_pass = !(ps.bits.empty() || ps.members.size() == 1);
+        if (tiled_pass && ps.gon) {
+            flip[pi] = 1;
+            ++nflip;
+        } else if (tiled_pass || !sharded) {
+            flexible = (int)pi;
+        }
+    }
+    if ((nflip & 1) && flexible >= 0) {
+        flip[(size_t)flexible] = 1;
+        ++nflip;
+    }
+    double2 *bufs[2] = {(double2 *)state, nullptr};
+    if (nflip > 0) {
+        if (cudaMallocAsync((void **)&bufs[1], (size_t)16 << n_bits, s) != cudaSuccess) {
+            cudaGetLastError();
+            return set_error(DIAQ_ERR_RESOURCE, "diaq_run_gates_fused: no room for a %llu-byte permutation buffer",
+                             (unsigned long long)((size_t)16 << n_bits));
+        }
+    }
+    int cur = 0;
+    for (size_t pi = 0; pi < np && rc == DIAQ_OK; ++pi) {
+        const int nxt = flip[pi] ? 1 - cur : cur;
         const PassPlan &ps = plan[pi];
         if (ps.bits.empty() || ps.members.size() == 1) {
             const diaq_gate_t &gt = gates[ps.members[0]];
-            if (sharded) rc = apply_gate_sharded_own(n_total, n_bits, gt.k, gt.g, gt.shifts, rank, state, cmul_mode, s);
-            else rc = apply_gate(n_bits, gt.k, gt.g, gt.shifts, state, state, cmul_mode, s);
+            if (sharded) rc = apply_gate_sharded_own(n_total, n_bits, gt.k, gt.g, gt.shifts, rank, bufs[cur], cmul_mode, s);
+            else rc = apply_gate(n_bits, gt.k, gt.g, gt.shifts, bufs[cur], bufs[nxt], cmul_mode, s);
         } else {
             TileParams &p = tparams;  // thread-local scratch: the launch copies it
             p = prog->params[pi];
-            p.x = (double2 *)state;
+            p.x = bufs[cur];
+            p.y = bufs[nxt];
             p.gbase = sharded ? ((uint64_t)rank << n_bits) : 0ull;
+            if (p.gperm && sharded)  // controls on global bits: constants of this rank
+                for (int g = 0; g < 64 && g < n_total - n_bits; ++g)
+                    if (((uint64_t)rank >> g) & 1ull) p.gconst ^= ps.ggcol[(size_t)g];
             const void *f = R >= 4 ? tile_kernel_ptr<4>(cmul_mode) : tile_kernel_ptr<3>(cmul_mode);
             const size_t smem = sizeof(double2) << p.tbits;
             const int per_sm = occupancy(f, smem);
@@ -1135,7 +1329,12 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
         // its first gate, the others record zero-length intervals
         if (events && rc == DIAQ_OK)
             for (int gi : ps.members) cudaEventRecord((cudaEvent_t)events[gi + 1], s);
+        cur = nxt;
     }
+    if (rc == DIAQ_OK && cur != 0 &&
+        cudaMemcpyAsync(state, bufs[1], (size_t)16 << n_bits, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        rc = set_error(DIAQ_ERR_CUDA, "diaq_run_gates_fused: copy back failed");
+    if (bufs[1]) cudaFreeAsync(bufs[1], s);
     return rc;
 }
 
@@ -1157,6 +1356,7 @@ extern "C" int diaq_fused_plan(int n_bits, int local_bits, int ngates, const dia
     std::vector<PassPlan> plan;
     const int rc = schedule(local_bits, n_bits, ngates, gates, T, T - kThreadBits, plan);
     if (rc) return rc;
+    if (getenv("DIAQ_PLAN_DEBUG")) debug_plan(plan);
     for (const PassPlan &ps : plan) {
         ++stats[0];
         if (ps.bits.empty() || ps.members.size() == 1) {

@@ -176,7 +176,20 @@ def test_fused_schedule_host_only(lib):
     ops = W.random_layered_ops(n, 1, seed=0)
     st = _plan(lib, n, ops)
     assert st["folded"] == n // 2 and st["single"] == 0 and st["smem_phases"] == 0
-    assert st["passes"] == 4            # 28 mixing bits through 12-bit tiles (3 low bits shared)
+    # 28 mixing bits through 12-bit tiles (3 low bits shared): two compute
+    # passes; the CX run whose targets leave the tile rides the second pass's store
+    assert st["passes"] == 2
+    L.tune("fused_gperm", 0)
+    try:
+        assert _plan(lib, n, ops)["passes"] == 4  # tile-only folding: two relabelling copy passes
+        many = [("cx", (27 - i, 0), ()) for i in range(12)]
+        st = _plan(lib, 28, many)   # more than 8 distinct controls outside the tile start a new pass
+        assert st["folded"] == 12 and st["passes"] == 2
+    finally:
+        L.tune("fused_gperm", 1)
+    many = [("h", (27,), ())] + [("cx", (27 - i, 0), ()) for i in range(12)]
+    st = _plan(lib, 28, many)     # ... or join the global tail of the pass
+    assert st["folded"] == 12 and st["passes"] == 1
     # a pure permutation circuit: everything folded, every pass a relabelling copy
     cx = [("cx", (i, (i + 5) % 20), ()) for i in range(20)] + [("x", (3,), ()), ("swap", (0, 19), ())]
     st = _plan(lib, 20, cx)
@@ -184,10 +197,6 @@ def test_fused_schedule_host_only(lib):
     # CCX is a permutation but not affine: shared-memory path, not folded
     st = _plan(lib, 16, [("ccx", (0, 1, 2), ()), ("cx", (3, 4), ())])
     assert st["folded"] == 1
-    # more than 8 distinct controls outside the tile start a new pass
-    many = [("cx", (27 - i, 0), ()) for i in range(12)]
-    st = _plan(lib, 28, many)
-    assert st["folded"] == 12 and st["passes"] == 2
     # states smaller than a tile: gate by gate
     st = _plan(lib, 8, [("h", (0,), ()), ("cx", (0, 1), ())])
     assert st["passes"] == st["single"] == 2

@@ -424,8 +424,8 @@ def _perm_gate(q):
     return m
 
 
-@pytest.mark.parametrize("fold", [1, 0], ids=["folded", "executed"])
-def test_fused_permutation_runs(cmul, fold):
+@pytest.mark.parametrize("fold,gperm", [(1, 1), (1, 0), (0, 0)], ids=["folded-global", "folded-tile", "executed"])
+def test_fused_permutation_runs(cmul, fold, gperm):
     """X / CX / SWAP runs (and any 2-qubit 0/1 permutation) folded into the
     passes' shared-memory addressing: runs opening a pass, closing a phase,
     after a shared-memory phase, with controls inside and outside the tile
@@ -433,6 +433,7 @@ def test_fused_permutation_runs(cmul, fold):
     from paper_2405_01250_b200 import _lib as L
     rng = np.random.default_rng(21)
     L.tune("fused_perm", fold)
+    L.tune("fused_gperm", gperm)
     try:
         for n in (9, 12, 16, 20):
             ops = [("cx", (int(n - 1 - i), int(i % 3)), ()) for i in range(min(n - 3, 12))]  # high controls
@@ -462,8 +463,20 @@ def test_fused_permutation_runs(cmul, fold):
         x0 = D.StateVector(n, W.random_state(rng, 2**n))
         want = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=0).amps
         assert np.array_equal(D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=11).amps, want)
+        # odd and even numbers of out-of-place passes, the caller's buffer updated in place
+        for k in (1, 2, 3):
+            ops = []
+            for layer in range(k):
+                ops += W.random_layered_ops(n, 1, seed=layer)
+            pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
+            st = D.StateVector(n, W.random_state(rng, 2**n))
+            want = D.run_gates(st, pls, cmul_mode=cmul, tile_bits=0).amps
+            out = D.run_gates(st, pls, cmul_mode=cmul, tile_bits=12, inplace=True)
+            assert out.device_amps.data_ptr() == st.device_amps.data_ptr()
+            assert np.array_equal(out.amps, want), k
     finally:
         L.tune("fused_perm", 1)
+        L.tune("fused_gperm", 1)
 
 
 def test_spmv_host_pipeline_chunks(monkeypatch):
