@@ -231,6 +231,11 @@ int diaq_timer_destroy(int n, void **events);
 int diaq_run_gates_fused(int n_bits, int ngates, const diaq_gate_t *gates, void *state, int cmul_mode,
                          int tile_bits, void **events, int *npasses, void *stream);
 
+/* The fused passes take a state-sized permutation buffer from the device's
+ * default stream-ordered pool and keep freed pool memory reserved for the
+ * next call; diaq_trim_pool synchronises the device and returns it. */
+int diaq_trim_pool(void);
+
 /* Host-only view of the fused schedule (no device work): stats[0] HBM
  * passes, [1] of them single-gate (gate kernel), [2] register/smem phases
  * in the tiled passes, [3] permutation gates folded into pass addressing,

@@ -81,6 +81,7 @@ _SIGS = {
     "diaq_apply_gate": ([_INT, _INT, _P, _P, _P, _P, _INT, _P], _INT),
     "diaq_run_gates": ([_INT, _INT, ctypes.POINTER(Gate), _P, _INT, _P, _P], _INT),
     "diaq_run_gates_fused": ([_INT, _INT, ctypes.POINTER(Gate), _P, _INT, _INT, _P, _P, _P], _INT),
+    "diaq_trim_pool": ([], _INT),
     "diaq_fused_plan": ([_INT, _INT, _INT, ctypes.POINTER(Gate), _INT, _P], _INT),
     "diaq_init_basis": ([_I64, _P, _I64, _P], _INT),
     "diaq_norm2": ([_I64, _P, _P, _P], _INT),

@@ -1240,6 +1240,28 @@ static std::shared_ptr<const Program> cached_program(int n_total, int n_bits, in
     return prog;
 }
 
+// The out-of-place permutation buffer is as large as the state (4 GiB at
+// n = 28) and is taken from the device's default stream-ordered pool on
+// every call; the pool would hand that memory back to the driver at each
+// synchronisation and re-map it on the next call (milliseconds).  Keep freed
+// pool memory reserved instead (once per device); diaq_trim_pool releases it.
+static void keep_pool_reserved() {
+    static bool done[64] = {false};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+        cudaGetLastError();
+        return;
+    }
+    if (done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    done[dev] = true;
+}
+
 static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const diaq_gate_t *gates, void *state,
                      int cmul_mode, int tile_bits, void **events, int *npasses, void *stream) {
     if (ngates < 0 || (ngates > 0 && !gates) || !state)
@@ -1289,6 +1311,7 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
     }
     double2 *bufs[2] = {(double2 *)state, nullptr};
     if (nflip > 0) {
+        keep_pool_reserved();
         if (cudaMallocAsync((void **)&bufs[1], (size_t)16 << n_bits, s) != cudaSuccess) {
             cudaGetLastError();
             return set_error(DIAQ_ERR_RESOURCE, "diaq_run_gates_fused: no room for a %llu-byte permutation buffer",
@@ -1336,6 +1359,17 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
         rc = set_error(DIAQ_ERR_CUDA, "diaq_run_gates_fused: copy back failed");
     if (bufs[1]) cudaFreeAsync(bufs[1], s);
     return rc;
+}
+
+extern "C" int diaq_trim_pool(void) {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess || cudaMemPoolTrimTo(pool, 0) != cudaSuccess) {
+        const cudaError_t e = cudaGetLastError();
+        return set_error(DIAQ_ERR_CUDA, "diaq_trim_pool: %s", cudaGetErrorString(e));
+    }
+    return DIAQ_OK;
 }
 
 extern "C" int diaq_run_gates_fused(int n_bits, int ngates, const diaq_gate_t *gates, void *state, int cmul_mode,
