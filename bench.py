@@ -419,7 +419,7 @@ def replica_gates(args, D, L, W, torch, dist, n, world, x, s, dev):
     g_ms = max_over_ranks(dist, ge0.elapsed_time(ge1), dev)
     g_norm = state.norm()
     extra = {"gates_per_step": len(pls), "steps": g_steps, "mode": f"replicas x{world}",
-             "fused_tile_bits": D.sim.FUSE_TILE_BITS, "hbm_passes": int(g_launches)}
+             "fused_tile_bits": D.sim.FUSE_TILE_BITS if D.sim.FUSE_TILE_BITS > 0 else "auto (11 or 12: fewer passes, ties 11)", "hbm_passes": int(g_launches)}
     return len(pls) * g_steps, g_ms, g_launches, g_norm, n, extra
 
 

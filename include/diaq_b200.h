@@ -225,7 +225,8 @@ int diaq_timer_destroy(int n, void **events);
  * mixing operand bits fit in a tile of 2^tile_bits amplitudes (low bits
  * included) are applied in ONE pass over HBM through shared memory.
  * Operands a gate does not mix (controls, diagonal gates) may lie outside
- * the tile.  tile_bits <= 0 picks the default (11); *npasses (optional)
+ * the tile.  tile_bits 11 or 12; <= 0 schedules both and keeps the one
+ * with fewer passes (ties: 11); *npasses (optional)
  * receives the number of HBM passes.  events: as diaq_run_gates (a pass's
  * time is attributed to its first gate). */
 int diaq_run_gates_fused(int n_bits, int ngates, const diaq_gate_t *gates, void *state, int cmul_mode,

@@ -1268,12 +1268,23 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
         return set_error(DIAQ_ERR_VALUE, "diaq_run_gates_fused: bad arguments");
     const bool sharded = n_total > n_bits;
     cudaStream_t s = (cudaStream_t)stream;
-    // tile_bits 12 -> 16 amplitudes per thread (R = 4), else 8 (R = 3); 256 threads
-    const int T = tile_bits >= kThreadBits + 4 ? kThreadBits + 4 : kThreadBits + 3;
-    const int R = T - kThreadBits;
+    // tile_bits 12 -> 16 amplitudes per thread (R = 4), 11 -> 8 (R = 3); 256
+    // threads.  tile_bits <= 0: schedule both, keep the one with fewer HBM
+    // passes (a tie goes to 11: smaller tiles keep 3 CTAs per SM)
+    int T = tile_bits >= kThreadBits + 4 ? kThreadBits + 4 : kThreadBits + 3;
     int rc = DIAQ_OK;
     std::shared_ptr<const Program> prog = cached_program(n_total, n_bits, T, ngates, gates, rc);
     if (!prog) return rc;
+    if (tile_bits <= 0) {
+        T = kThreadBits + 3;
+        std::shared_ptr<const Program> big = cached_program(n_total, n_bits, kThreadBits + 4, ngates, gates, rc);
+        if (!big) return rc;
+        if (big->plan.size() < prog->plan.size()) {
+            prog = big;
+            T = kThreadBits + 4;
+        }
+    }
+    const int R = T - kThreadBits;
     const std::vector<PassPlan> &plan = prog->plan;
     if (npasses) *npasses = (int)plan.size();
     const size_t smem_max = (sizeof(double2) << kMaxTileBits);

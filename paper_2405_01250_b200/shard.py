@@ -301,7 +301,7 @@ class ShardedState:
             if comp is None:
                 raise ValueError(f"sharded apply needs compact placements, got {p!r}")
             comps.append(comp)
-        if self.apply_fn is not _cuda_apply or sim.FUSE_TILE_BITS <= 0:
+        if self.apply_fn is not _cuda_apply or sim.FUSE_TILE_BITS == 0:
             for g, shifts in comps:
                 self.apply_gate(g, shifts, mode)
             return
@@ -368,7 +368,7 @@ def run_emulated(n_qubits: int, world: int, placements: list[Placement], cmul_mo
     lb = states[0].local_bits
     stats = {"gates": 0, "local": 0, "no_comm_global": 0, "exchanged": 0}
     comps = [p.compact() for p in placements]
-    fuse = sim.FUSE_TILE_BITS > 0
+    fuse = sim.FUSE_TILE_BITS != 0
 
     def crosses(g, shifts):
         if all(s < lb for s in shifts):

@@ -50,9 +50,11 @@ def _probe_numpy_cmul() -> int:
 # rounding of the gate-apply complex multiply; defaults to this host's numpy
 CMUL_MODE = _probe_numpy_cmul()
 
-# shared-memory tile of the fused multi-gate passes (diaq_run_gates_fused);
-# 0 applies every gate as its own HBM sweep.  Results are identical.
-FUSE_TILE_BITS = 12
+# shared-memory tile of the fused multi-gate passes (diaq_run_gates_fused):
+# 11 or 12 bits, -1 lets the library pick per circuit (fewer HBM passes;
+# ties go to 11); 0 applies every gate as its own HBM sweep.  Results are
+# identical.
+FUSE_TILE_BITS = -1
 
 
 class StateVector:
@@ -287,7 +289,7 @@ def run_gates(state: StateVector, placements: list[Placement], cmul_mode: int | 
             prog = _GateProgram.for_placements(placements[i:j])
             evs = timer.slice_ptr(i) if timer is not None else None
             tb = FUSE_TILE_BITS if tile_bits is None else tile_bits
-            if tb > 0:
+            if tb != 0:
                 L.call("diaq_run_gates_fused", n_bits, prog.n, prog.arr, xd.data_ptr(), int(mode), int(tb), evs,
                        None, s)
             else:

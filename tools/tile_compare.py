@@ -6,7 +6,7 @@ for n, layers in ((28, 1), (30, 20), (20, 40)):
     ops = W.random_layered_ops(n, layers, seed=0)
     pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
     st = D.init_state(n, max_qubits=30)
-    for tb in (11, 12):
+    for tb in (11, 12, -1):
         D.run_gates(st, pls, inplace=True, tile_bits=tb)
         torch.cuda.synchronize()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
