@@ -38,10 +38,11 @@ namespace diaq {
 constexpr int kMaxTileBits = 12;
 constexpr int kThreadBits = 8;      // 256 threads
 constexpr int kLowBits = 3;         // tile rows are 2^3 amplitudes = 128 B
-constexpr int kMaxRegKin = 1;       // mixing operands applied in registers (wider: own pass)
+constexpr int kMaxRegKin = 2;       // mixing operands of a fused gate (2: shared-memory path; wider: own pass)
 constexpr int kMaxSel = 4;          // selector (non-mixing) operands
 constexpr int kMaxPassGates = 48;   // gate records per pass (kernel parameters)
 constexpr int kMaxPhases = 24;
+constexpr int kRetryNoDense2 = 1000;  // schedule(): internal, re-plan without register 2-qubit gates
 constexpr int kMaxCoef = 256;       // coefficient entries per pass (kernel parameters)
 constexpr int kMaxNz = 256;
 constexpr int kPrePhases = 4;       // phases whose register slots are precomputed per CTA (R = 3; 3 at R = 4,
@@ -60,7 +61,7 @@ struct RegGate {               // narrow fields: the records live in the kernel 
     // fast-path classification (host): 0 generic, 1 dense 1-qubit (no selector),
     // 2 diagonal with one selector
     int8_t op;
-    int8_t mpos;              // generic phases: tile position of the mixing bit
+    int8_t mpos[kMaxRegKin];  // generic phases: tile positions of the mixing bits (relabelled order)
     int16_t coef_off;         // coef[coef_off + (b << 2kin) + r * 2^kin + c]   (pass-relative)
     int16_t nz_off;           // nz[nz_off + (b << kin) + r]
     int16_t cls_off;          // host classification table (identity / swap blocks)
@@ -106,6 +107,7 @@ struct Phase {
     // bit, so every dense step has a compile-time pairing.
     int8_t seq, ndense;
     int8_t nd_before[5];
+    int8_t kind[5];           // sequence phase: 1 = dense 1-qubit gate on bit b, 2 = dense 2-qubit on (b, b+1)
     int8_t rpos[4];           // tile positions of the register bits, ascending (R entries)
     int8_t tpos[kMaxTileBits];  // tile positions of the thread bits, ascending (T - R entries)
     Affine post;              // permutation run after the phase's gates, applied by its store
@@ -205,6 +207,29 @@ __device__ __forceinline__ void dense1_full(double2 (&v)[1 << R], const double2 
     }
 }
 
+// dense two-qubit gate (all 16 entries nonzero) on register bits RA (its
+// gate-index MSB, the operand with the larger state bit) and RB: four
+// amplitude groups per 16 registers, ascending columns, first term as is
+template <int R, int RA, int RB, int MODE>
+__device__ __forceinline__ void dense2_full(double2 (&v)[1 << R], const double2 *c) {
+    constexpr int LO = RA < RB ? RA : RB, HI = RA < RB ? RB : RA;
+#pragma unroll
+    for (int g = 0; g < (1 << (R - 2)); ++g) {
+        int j0 = ((g >> LO) << (LO + 1)) | (g & ((1 << LO) - 1));
+        j0 = ((j0 >> HI) << (HI + 1)) | (j0 & ((1 << HI) - 1));
+        const int jq[4] = {j0, j0 | (1 << RB), j0 | (1 << RA), j0 | (1 << RA) | (1 << RB)};
+        const double2 x0 = v[jq[0]], x1 = v[jq[1]], x2 = v[jq[2]], x3 = v[jq[3]];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            double2 a = cmul<MODE>(c[r * 4], x0);
+            a = cadd(a, cmul<MODE>(c[r * 4 + 1], x1));
+            a = cadd(a, cmul<MODE>(c[r * 4 + 2], x2));
+            a = cadd(a, cmul<MODE>(c[r * 4 + 3], x3));
+            v[jq[r]] = a;
+        }
+    }
+}
+
 template <int R, int RB, int MODE>
 __device__ __forceinline__ void diag_reg(double2 (&v)[1 << R], double2 d0, double2 d1, uint32_t z0, uint32_t z1) {
 #pragma unroll
@@ -281,16 +306,25 @@ __device__ __forceinline__ void dispatch_gate(double2 (&v)[1 << R], const RegGat
     }
 }
 
-// Generic gate (any selectors, <= 1 mixing bit) applied in the shared-memory
-// tile: the cold path for gates the register fast paths do not cover.
+// Generic gate (any selectors, <= 2 mixing bits) applied in the shared-memory
+// tile: the cold path for gates the register fast paths do not cover (and
+// dense two-qubit gates).  Same per-amplitude order as gate_kernel: ascending
+// relabelled column, from +0, exactly-zero entries skipped.
 template <int MODE>
 __device__ __forceinline__ void smem_gate(double2 *tile, int T, const RegGate &G, uint64_t base, const double2 *sc,
                                           const uint32_t *snz) {
     const int kin = G.kin;
     const uint32_t ngroups = 1u << (T - kin);
+    const int p0 = G.mpos[0], p1 = G.mpos[1];
+    const int lo = p0 < p1 ? p0 : p1, hi = p0 < p1 ? p1 : p0;
     for (uint32_t grp = threadIdx.x; grp < ngroups; grp += blockDim.x) {
         uint32_t e0 = grp;
-        if (kin) e0 = ((e0 >> G.mpos) << (G.mpos + 1)) | (e0 & ((1u << G.mpos) - 1u));
+        if (kin == 1) {
+            e0 = ((e0 >> p0) << (p0 + 1)) | (e0 & ((1u << p0) - 1u));
+        } else if (kin == 2) {
+            e0 = ((e0 >> lo) << (lo + 1)) | (e0 & ((1u << lo) - 1u));
+            e0 = ((e0 >> hi) << (hi + 1)) | (e0 & ((1u << hi) - 1u));
+        }
         uint32_t b = 0;
         for (int s = 0; s < G.kout; ++s) {
             const uint32_t bit = G.osel[s] ? (e0 >> G.opos[s]) & 1u : (uint32_t)((base >> G.opos[s]) & 1ull);
@@ -301,8 +335,8 @@ __device__ __forceinline__ void smem_gate(double2 *tile, int T, const RegGate &G
         if (kin == 0) {
             const uint32_t i0 = swz(e0);
             tile[i0] = (nz[0] & 1u) ? cadd(make_double2(0.0, 0.0), cmul<MODE>(c[0], tile[i0])) : make_double2(0.0, 0.0);
-        } else {
-            const uint32_t i0 = swz(e0), i1 = swz(e0 | (1u << G.mpos));
+        } else if (kin == 1) {
+            const uint32_t i0 = swz(e0), i1 = swz(e0 | (1u << p0));
             const double2 x0 = tile[i0], x1 = tile[i1];
             double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
             if (nz[0] & 1u) a0 = cadd(a0, cmul<MODE>(c[0], x0));
@@ -311,6 +345,32 @@ __device__ __forceinline__ void smem_gate(double2 *tile, int T, const RegGate &G
             if (nz[1] & 2u) a1 = cadd(a1, cmul<MODE>(c[3], x1));
             tile[i0] = a0;
             tile[i1] = a1;
+        } else {
+            uint32_t idx[4];
+            double2 x[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {  // gate column q = (bit at p0, bit at p1)
+                idx[q] = swz(e0 | ((uint32_t)(q >> 1) << p0) | ((uint32_t)(q & 1) << p1));
+                x[q] = tile[idx[q]];
+            }
+            if ((nz[0] & nz[1] & nz[2] & nz[3] & 15u) == 15u) {  // dense (Haar4 ...): branch-free
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    double2 a = cadd(make_double2(0.0, 0.0), cmul<MODE>(c[r * 4], x[0]));
+#pragma unroll
+                    for (int q = 1; q < 4; ++q) a = cadd(a, cmul<MODE>(c[r * 4 + q], x[q]));
+                    tile[idx[r]] = a;
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    double2 a = make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if ((nz[r] >> q) & 1u) a = cadd(a, cmul<MODE>(c[r * 4 + q], x[q]));
+                    tile[idx[r]] = a;
+                }
+            }
         }
     }
 }
@@ -322,10 +382,16 @@ __device__ __forceinline__ void seq_steps(double2 (&v)[1 << R], const TileParams
                                           uint32_t tpart, const uint64_t *sbase_p, const double2 *sc,
                                           const uint32_t *snz) {
     for (int c = 0; c < ph.nd_before[RB]; ++c, ++gi) diag_uniform<R, MODE>(v, p.g[gi], tpart, sbase_p, sc, snz);
-    if (RB < ph.ndense) {
+    if (ph.kind[RB] == 1) {
         dense1_full<R, RB, MODE>(v, sc + p.g[gi].coef_off);
         ++gi;
         if constexpr (RB + 1 < R) seq_steps<R, MODE, RB + 1>(v, p, ph, gi, tpart, sbase_p, sc, snz);
+    } else if (ph.kind[RB] == 2) {
+        if constexpr (RB + 1 < R) {
+            dense2_full<R, RB, RB + 1, MODE>(v, sc + p.g[gi].coef_off);
+            ++gi;
+            if constexpr (RB + 2 < R) seq_steps<R, MODE, RB + 2>(v, p, ph, gi, tpart, sbase_p, sc, snz);
+        }
     }
 }
 
@@ -776,6 +842,11 @@ static int pack_reg_gate(const diaq_gate_t &gt, const std::vector<int> &bits, co
     G.op = 0;
     if (G.kin == 1 && G.kout == 0) G.op = 1;
     else if (G.kin == 0 && G.kout == 1) G.op = 2;
+    else if (G.kin == 2 && G.kout == 0) {  // dense two-qubit: register path only when every entry is nonzero
+        bool full = true;
+        for (int r = 0; r < 4; ++r) full = full && (pk.nz[G.nz_off + r] & 15u) == 15u;
+        if (full) G.op = 3;
+    }
     return DIAQ_OK;
 }
 
@@ -801,11 +872,14 @@ static int pack_smem_gate(const diaq_gate_t &gt, const std::vector<int> &bits, P
     int mshift = -1;
     for (int i = 0; i < gt.k; ++i)
         if ((mix >> i) & 1u) mshift = gt.shifts[i];
-    // pack_reg_gate needs the mixing bit among the registers: give it one fake register
-    if (mshift >= 0) ph.rpos[0] = tile_pos(bits, mshift);
-    const int rc = pack_reg_gate(gt, bits, ph, 1, pk, G);
+    // pack_reg_gate needs the mixing bits among the registers: give it fake ones
+    int nm = 0;
+    for (int i = 0; i < gt.k; ++i)
+        if ((mix >> i) & 1u) ph.rpos[nm++] = (int8_t)tile_pos(bits, gt.shifts[i]);
+    (void)mshift;
+    const int rc = pack_reg_gate(gt, bits, ph, nm > 0 ? nm : 1, pk, G);
     if (rc) return rc;
-    G.mpos = mshift >= 0 ? tile_pos(bits, mshift) : 0;
+    for (int j = 0; j < kMaxRegKin; ++j) G.mpos[j] = j < G.kin ? ph.rpos[G.rb[j]] : 0;
     for (int s = 0; s < G.kout; ++s)
         if (G.osel[s] == 2) return set_error(DIAQ_ERR_VALUE, "smem gate selector on a register bit");
     G.op = 0;
@@ -817,14 +891,25 @@ static int pack_smem_gate(const diaq_gate_t &gt, const std::vector<int> &bits, P
 // union of its gates' mixing bits fits in R registers.  Gates that cannot
 // be applied in registers (more than 2 mixing or 4 selector operands)
 // become standalone single-gate passes (gate_kernel).
-static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gates, int T, int R,
-                    std::vector<PassPlan> &plan) {
+static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t *gates, int T, int R,
+                         std::vector<PassPlan> &plan, bool allow_d2) {
     const int low = std::min(kLowBits, n_bits);
     std::vector<char> fast((size_t)ngates);  // register fast-path classification, once per gate
     std::vector<PermGate> perm((size_t)ngates);
+    std::vector<char> d2((size_t)ngates, 0);  // dense two-qubit gate for the register path (sequence phases)
     for (int i = 0; i < ngates; ++i) {
         fast[(size_t)i] = (gates[i].k >= 1 && gates[i].k <= 5) ? fast_op(gates[i]) : 0;
         if (tuning().fused_perm && gates[i].k >= 1 && gates[i].k <= 5) perm[(size_t)i] = perm_affine(gates[i]);
+        if (allow_d2 && tuning().fused_dense2 && tuning().fused_seq && !perm[(size_t)i].ok && gates[i].k >= 2 &&
+            gates[i].k <= 5) {
+            const diaq_gate_t &gt = gates[i];
+            const uint32_t mix = mixing_mask(gt.k, gt.g);
+            int kin = 0;
+            for (int o = 0; o < gt.k; ++o) kin += (mix >> o) & 1u;
+            bool full = kin == 2 && gt.k == 2;  // no selectors: every entry of the 4x4 nonzero
+            for (int e = 0; full && e < 16; ++e) full = !(gt.g[2 * e] == 0.0 && gt.g[2 * e + 1] == 0.0);
+            d2[(size_t)i] = full;
+        }
     }
     std::vector<int> members;
     std::vector<char> inb(64, 0);
@@ -858,6 +943,8 @@ static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gate
             std::vector<int> mem;
             std::vector<int> used;
             HostAffine post;
+            bool seq_ok = true;  // still a sequence phase (dense steps on fresh register bits in order)
+            bool has_d2 = false;
         };
         std::vector<Spec> specs;
         HostAffine pre;
@@ -884,25 +971,51 @@ static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gate
                     return set_error(DIAQ_ERR_VALUE, "fused pass: permutation fold overflow");
                 continue;
             }
-            if (fast[(size_t)gi]) {
+            if (fast[(size_t)gi] || d2[(size_t)gi]) {
                 const uint32_t mix = mixing_mask(gt.k, gt.g);
-                std::vector<int> add;
+                const bool isd2 = d2[(size_t)gi] != 0;
+                int kin = 0;
+                for (int o = 0; o < gt.k; ++o) kin += (mix >> o) & 1u;
+                // mixing bits in relabelled order (descending state bit): a two-qubit
+                // gate's gate-index MSB takes the lower register bit of its pair
+                std::vector<int> mops;
                 for (int o = 0; o < gt.k; ++o)
-                    if ((mix >> o) & 1u) {
+                    if ((mix >> o) & 1u) mops.push_back(o);
+                std::sort(mops.begin(), mops.end(), [&](int a, int b) { return gt.shifts[a] > gt.shifts[b]; });
+                std::vector<int> add;
+                for (int o : mops) {
+                    const int tp = tile_pos(ps.bits, gt.shifts[o]);
+                    if ((!open || std::find(specs.back().used.begin(), specs.back().used.end(), tp) ==
+                                      specs.back().used.end()) &&
+                        std::find(add.begin(), add.end(), tp) == add.end())
+                        add.push_back(tp);
+                }
+                // does the gate keep the open phase a sequence phase?
+                bool keeps = (int)add.size() == kin;  // dense steps on fresh bits only
+                if (kin == 0 && open) {               // a diagonal must not select a register bit
+                    for (int o = 0; o < gt.k; ++o) {
                         const int tp = tile_pos(ps.bits, gt.shifts[o]);
-                        if ((!open || std::find(specs.back().used.begin(), specs.back().used.end(), tp) ==
-                                          specs.back().used.end()) &&
-                            std::find(add.begin(), add.end(), tp) == add.end())
-                            add.push_back(tp);
+                        if (tp >= 0 && std::find(specs.back().used.begin(), specs.back().used.end(), tp) !=
+                                           specs.back().used.end())
+                            keeps = false;
                     }
-                if (open && (int)(specs.back().used.size() + add.size()) <= R) {
+                }
+                const bool fits = open && (int)(specs.back().used.size() + add.size()) <= R;
+                const bool join = fits && (keeps || (!specs.back().has_d2 && !isd2)) &&
+                                  (!isd2 || specs.back().seq_ok);
+                if (join) {
                     specs.back().mem.push_back(gi);
                     specs.back().used.insert(specs.back().used.end(), add.begin(), add.end());
+                    specs.back().seq_ok = specs.back().seq_ok && keeps;
+                    specs.back().has_d2 = specs.back().has_d2 || isd2;
                 } else {
                     Spec sp;
                     sp.mem = {gi};
-                    sp.used = add;
+                    std::vector<int> all;
+                    for (int o : mops) all.push_back(tile_pos(ps.bits, gt.shifts[o]));
+                    sp.used = all;
                     sp.post.init((int)ps.bits.size());
+                    sp.has_d2 = isd2;
                     specs.push_back(sp);
                     open = true;
                 }
@@ -982,10 +1095,18 @@ static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gate
             if (seq_try) {  // sequence form?
                 int nd = 0, cnt = 0;
                 bool ok = true;
+                for (int b = 0; b < 5; ++b) ph.kind[b] = 0;
                 for (int g = ph.g0; g < ph.g1 && ok; ++g) {
                     const RegGate &G = ps.gates[g];
                     if (G.op == 1 && G.rb[0] == nd && nd < R) {
+                        ph.kind[nd] = 1;
                         ph.nd_before[nd++] = (int8_t)cnt;
+                        cnt = 0;
+                    } else if (G.op == 3 && G.rb[0] == nd && G.rb[1] == nd + 1 && nd + 1 < R) {
+                        ph.kind[nd] = 2;
+                        ph.nd_before[nd] = (int8_t)cnt;
+                        ph.nd_before[nd + 1] = 0;
+                        nd += 2;
                         cnt = 0;
                     } else if (G.op == 2 && G.osel[0] != 2 && cnt < 127) {
                         ++cnt;
@@ -1000,6 +1121,9 @@ static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gate
                     ph.nd_before[R] = (int8_t)cnt;
                 }
             }
+            if (!ph.seq)  // a dense two-qubit gate runs only in a sequence phase
+                for (int g = ph.g0; g < ph.g1; ++g)
+                    if (ps.gates[g].op == 3) return kRetryNoDense2;
             ps.phases.push_back(ph);
         }
         if ((int)ps.phases.size() > kMaxPhases || (int)ps.gates.size() > kMaxPassGates)
@@ -1084,6 +1208,16 @@ static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gate
         members.push_back(i);
     }
     return flush();
+}
+
+static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gates, int T, int R,
+                    std::vector<PassPlan> &plan) {
+    int rc = schedule_once(n_bits, n_total, ngates, gates, T, R, plan, true);
+    if (rc == kRetryNoDense2) {  // a two-qubit gate landed outside a sequence phase: shared-memory path for all
+        plan.clear();
+        rc = schedule_once(n_bits, n_total, ngates, gates, T, R, plan, false);
+    }
+    return rc;
 }
 
 int apply_gate(int n_bits, int k, const double *g, const int *shifts, const void *x, void *y, int cmul_mode,

@@ -594,3 +594,31 @@ def test_fused_program_cache_keys_on_values(cmul):
         pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*x) for x in o]), span_limit=n)
         assert np.array_equal(D.run_gates(D.init_state(n), pls, cmul_mode=cmul, tile_bits=12).amps,
                               D.run_gates(D.init_state(n), pls, cmul_mode=cmul, tile_bits=0).amps)
+
+
+def test_fused_two_qubit_gates(cmul):
+    """Dense two-qubit gates (Haar4, and controlled Haar4 with a selector)
+    fused into the passes through the shared-memory path: bitwise the
+    gate-by-gate kernel, at every tile size."""
+    rng = np.random.default_rng(17)
+    for n in (12, 16, 20):
+        pls = []
+        for i in range(24):
+            a, b, c = (int(v) for v in rng.choice(n, size=3, replace=False))
+            u = W.haar(rng, 4)
+            if i % 3 == 2:  # controlled-U: block diag(I4, U) on (c, a, b)
+                g = np.eye(8, dtype=complex)
+                g[4:, 4:] = u
+                qs = [c, a, b]
+            else:
+                g, qs = u, [a, b]
+            lo, hi = min(qs), max(qs)
+            pls.append(D.Placement(2**lo, None, 2 ** (n - 1 - hi), lo, hi, "u",
+                                   gate=(g, [q - lo for q in qs])))
+            if i % 4 == 0:
+                pls += D.compile_circuit(D.Circuit(n, [D.GateOp("rx", (a,), (0.3 * i,)),
+                                                       D.GateOp("cx", (b, c), ())]), span_limit=n)
+        x0 = D.StateVector(n, W.random_state(rng, 2**n))
+        want = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=0).amps
+        for tb in (11, 12, -1):
+            assert np.array_equal(D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=tb).amps, want), (n, tb)
