@@ -527,6 +527,21 @@ def secondary_workloads(args, D, L, W, torch) -> dict:
                                              "gates_per_s": round(len(pls5) / dt5, 1), "stats": st5,
                                              "note": "2 shards on one GPU; exchange = device copy (NVLink unmeasured)"}
     del shards
+    # the metric's Haar4 gate kind at n=28: a layer of 14 Haar-random two-qubit
+    # gates on a seeded random matching (fused passes, device time per layer)
+    rng = np.random.default_rng(0)
+    perm = rng.permutation(28)
+    pls_h = []
+    for i in range(14):
+        qa, qb = int(perm[2 * i]), int(perm[2 * i + 1])
+        lo, hi = min(qa, qb), max(qa, qb)
+        pls_h.append(D.Placement(2**lo, None, 2 ** (27 - hi), lo, hi, "haar",
+                                 gate=(W.haar(rng, 4), [qa - lo, qb - lo])))
+    st_h = D.init_state(28)
+    ms_h = dev_time(lambda: D.run_gates(st_h, pls_h, inplace=True), 3)
+    out["haar4_layer_n28"] = {"gates": len(pls_h), "ms_per_layer": round(ms_h, 3),
+                              "gates_per_s": round(len(pls_h) / ms_h * 1e3, 1)}
+    del st_h
     # config 5 at its 1-GPU size: n=30 (16 GB state), 20 random layers, norm check
     ops30 = W.random_layered_ops(30, 20, seed=0)
     pls30 = D.compile_circuit(D.Circuit(30, [D.GateOp(*o) for o in ops30]), span_limit=30)
