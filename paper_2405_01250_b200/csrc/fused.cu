@@ -1422,13 +1422,19 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
     const std::vector<PassPlan> &plan = prog->plan;
     if (npasses) *npasses = (int)plan.size();
     const size_t smem_max = (sizeof(double2) << kMaxTileBits);
-    static bool attr_set = false;
-    if (!attr_set) {
+    static bool attr_set[64] = {false};  // per device (one process may drive several)
+    int cur_dev = 0;
+    if (cudaGetDevice(&cur_dev) != cudaSuccess || cur_dev < 0 || cur_dev >= 64) {
+        cudaGetLastError();
+        cur_dev = 0;
+    }
+    if (!attr_set[cur_dev]) {
         cudaFuncSetAttribute(tile_pass_kernel<3, DIAQ_CMUL_FMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
         cudaFuncSetAttribute(tile_pass_kernel<3, DIAQ_CMUL_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
         cudaFuncSetAttribute(tile_pass_kernel<4, DIAQ_CMUL_FMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
         cudaFuncSetAttribute(tile_pass_kernel<4, DIAQ_CMUL_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
-        attr_set = true;
+        cudaGetLastError();
+        attr_set[cur_dev] = true;
     }
     if (events && cudaEventRecord((cudaEvent_t)events[0], s) != cudaSuccess)
         return set_error(DIAQ_ERR_CUDA, "diaq_run_gates_fused: event record failed");

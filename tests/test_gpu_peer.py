@@ -80,3 +80,21 @@ def test_peer_sharded_spmv_config4(tmp_path):
     a = D.kron_identity(1, span, c4["right"])
     want = D.spmv(a, torch.from_numpy(c4["x"]).cuda()).cpu().numpy()
     assert np.array_equal(np.load(out), want)
+
+
+def test_bench_multi_rank_paths_on_one_gpu(tmp_path):
+    """bench.py's N>1 code (row-sharded spmv with peer x loads, sharded gates
+    over the peer transport) end to end with two ranks on the one GPU
+    (gloo, host barriers only): a functional check, not a measurement."""
+    import json
+    env = dict(os.environ, DIAQ_BENCH_SAME_GPU="1", DIAQ_BENCH_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "2", "--warmup", "3", "--no-e2e", "--no-cpu", "--no-secondary",
+           "--qubits", "23", "--sharded-gates"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-3000:]
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and "peer loads" in line["config"]["parallelism"]
+    assert line["gates"]["transport"] == "peer" and line["gates"]["stats"]["exchanged"] > 0
+    assert abs(line["gates"]["norm_after"] - 1.0) < 1e-10
