@@ -4,6 +4,9 @@
 #include <cstdio>
 #include <string>
 
+#include <mutex>
+#include <vector>
+
 #include "common.cuh"
 
 namespace diaq {
@@ -24,6 +27,51 @@ int set_error(int code, const char *fmt, ...) {
 }
 
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+int sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+        cudaGetLastError();
+        return kSms;
+    }
+    if (!cached[dev]) {
+        int sms = kSms;
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+            cudaGetLastError();
+            sms = kSms;
+        }
+        cached[dev] = sms;
+    }
+    return cached[dev];
+}
+
+int occupancy(const void *kernel, int threads, size_t smem) {
+    struct Key {
+        int dev;
+        const void *f;
+        int threads;
+        size_t smem;
+        int per_sm;
+    };
+    static std::mutex mu;
+    static std::vector<Key> memo;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) cudaGetLastError();
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (const Key &k : memo)
+            if (k.dev == dev && k.f == kernel && k.threads == threads && k.smem == smem) return k.per_sm;
+    }
+    int per_sm = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess || per_sm < 1) {
+        cudaGetLastError();
+        per_sm = 1;
+    }
+    std::lock_guard<std::mutex> lk(mu);
+    memo.push_back({dev, kernel, threads, smem, per_sm});
+    return per_sm;
+}
 
 int check_launch(const char *what) {
     const cudaError_t e = cudaGetLastError();

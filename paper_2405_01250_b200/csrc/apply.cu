@@ -189,13 +189,6 @@ __global__ void norm2_final(const double *part, int nparts, double *out) {
     }
 }
 
-static int sm_count() {
-    int dev = 0, sms = kSms;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaGetLastError();
-    return sms;
-}
-
 // Relabel a k-qubit gate so operand order follows descending state-bit
 // shift (see file comment) and pack it for gate_kernel.
 template <int K>

@@ -150,6 +150,11 @@ struct Tuning {
     int kron_ctas_per_sm = 32;  // CTAs per SM launched (4 resident; later ones refill)
 };
 Tuning &tuning();
+// SM count of the current device and resident CTAs per SM of a kernel,
+// asked of the runtime once per (device, kernel, block, smem) -- each query
+// costs microseconds, which is the whole budget of a small launch
+int sm_count();
+int occupancy(const void *kernel, int threads, size_t smem);
 int set_error(int code, const char *fmt, ...);
 void count_launch(int n = 1);
 int check_launch(const char *what);

@@ -247,9 +247,7 @@ to_dense_kernel(double2 *m, int64_t n, const GatherDiag *__restrict__ dg) {
 }
 
 static int grid_x(int64_t len, int nd) {
-    int dev = 0, sms = kSms;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaGetLastError();
+    const int sms = sm_count();
     const int64_t want = (len + kThreads - 1) / kThreads;
     const int64_t cap = std::max<int64_t>(1, (int64_t)sms * 8 / std::max(1, nd));
     return (int)std::max<int64_t>(1, std::min<int64_t>(want, cap));
@@ -318,9 +316,7 @@ extern "C" int diaq_kron_identity(int64_t left, const diaq_matrix_t *m, int64_t 
         }
         p.end = p.beg[cnt - 1] + p.dg[cnt - 1].len;
         if (flat) {
-            int dev = 0, sms = kSms;
-            if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaGetLastError();
+            const int sms = sm_count();
             const int64_t want = (p.end / 2 + kThreads - 1) / kThreads;
             const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * tuning().kron_ctas_per_sm));
             if (p.pow2)

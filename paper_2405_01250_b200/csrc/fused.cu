@@ -1225,31 +1225,6 @@ int apply_gate(int n_bits, int k, const double *g, const int *shifts, const void
 int apply_gate_sharded_own(int n_bits, int local_bits, int k, const double *g, const int *shifts, int64_t rank,
                            void *shard, int cmul_mode, cudaStream_t s);
 
-// resident CTAs per SM for (kernel, dynamic smem), and the SM count: asked
-// of the runtime once per process (each query costs microseconds per pass)
-static int occupancy(const void *f, size_t smem) {
-    thread_local std::vector<std::pair<std::pair<const void *, size_t>, int>> memo;
-    for (const auto &m : memo)
-        if (m.first.first == f && m.first.second == smem) return m.second;
-    int per_sm = 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kThreads, smem) != cudaSuccess) {
-        cudaGetLastError();
-        per_sm = 1;
-    }
-    memo.push_back({{f, smem}, per_sm});
-    return per_sm;
-}
-
-static int sm_count_f() {
-    thread_local int cached = 0;
-    if (cached) return cached;
-    int dev = 0, sms = kSms;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaGetLastError();
-    cached = sms;
-    return sms;
-}
-
 template <int R>
 static const void *tile_kernel_ptr(int cmul_mode) {
     return cmul_mode == DIAQ_CMUL_FMA ? (const void *)tile_pass_kernel<R, DIAQ_CMUL_FMA>
@@ -1488,9 +1463,9 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
                     if (((uint64_t)rank >> g) & 1ull) p.gconst ^= ps.ggcol[(size_t)g];
             const void *f = R >= 4 ? tile_kernel_ptr<4>(cmul_mode) : tile_kernel_ptr<3>(cmul_mode);
             const size_t smem = sizeof(double2) << p.tbits;
-            const int per_sm = occupancy(f, smem);
+            const int per_sm = occupancy(f, kThreads, smem);
             const int64_t grid =
-                std::max<int64_t>(1, std::min<int64_t>(p.ntiles, (int64_t)sm_count_f() * std::max(1, per_sm)));
+                std::max<int64_t>(1, std::min<int64_t>(p.ntiles, (int64_t)sm_count() * std::max(1, per_sm)));
             p.gstep = 0;  // deposit grid into the non-tile bits, low to high
             for (int b = 0, k = 0; b < 64 && ((uint64_t)grid >> k) != 0; ++b)
                 if (!((p.tmask >> b) & 1ull)) p.gstep |= (((uint64_t)grid >> k++) & 1ull) << b;

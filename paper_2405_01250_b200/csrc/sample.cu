@@ -123,9 +123,7 @@ __global__ void sample_search_kernel(const double *c, int64_t n, const double *u
 }
 
 static int grid_of(int64_t n) {
-    int dev = 0, sms = kSms;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaGetLastError();
+    const int sms = sm_count();
     return (int)std::max<int64_t>(1, std::min<int64_t>((n + kThreads - 1) / kThreads, (int64_t)sms * 8));
 }
 

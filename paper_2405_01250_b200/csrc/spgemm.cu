@@ -186,8 +186,7 @@ extern "C" int diaq_spgemm(const diaq_matrix_t *a, const diaq_matrix_t *b, diaq_
         cd.pend = (int32_t)hp.size();
         maxlen = std::max(maxlen, cd.len);
     }
-    int dev = 0, sms = kSms;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = sm_count();
     if (cudaMemsetAsync(keep_dev, 0, (size_t)c->nd, s) != cudaSuccess)
         return set_error(DIAQ_ERR_CUDA, "diaq_spgemm: memset failed");
     const int64_t want = (maxlen + kThreads - 1) / kThreads;

@@ -439,13 +439,8 @@ void spmv_raster(int64_t n, int64_t nd, const int64_t *offs, int64_t *ntiles, in
 }
 
 static int grid_for(const void *func, int64_t items, int ctas_per_sm = 0) {
-    int dev = 0, sms = kSms, per_sm = 1;
-    if (cudaGetDevice(&dev) == cudaSuccess)
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, func, kThreads, 0) != cudaSuccess ||
-        per_sm < 1)
-        per_sm = 1;
-    cudaGetLastError();
+    const int sms = sm_count();
+    int per_sm = occupancy(func, kThreads, 0);
     if (ctas_per_sm > 0 && ctas_per_sm < per_sm) per_sm = ctas_per_sm;
     const int64_t g = std::min<int64_t>(items, (int64_t)sms * per_sm);
     return (int)std::max<int64_t>(g, 1);
@@ -472,10 +467,8 @@ static int launch_async(const SpmvParams<kParamDiags> &p, cudaStream_t s) {
     q.nstrips = (nt + q.stride_tiles - 1) / q.stride_tiles;
     q.raster = 0;
     q.nitems = q.stride_tiles * q.nstrips;
-    int per_sm = 1, dev = 0, sms = kSms;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kAsyncThreads, 0);
-    cudaGetLastError();
+    const int sms = sm_count();
+    int per_sm = occupancy(f, kAsyncThreads, 0);
     if (tuning().spmv_ctas_per_sm > 0) per_sm = std::min(per_sm, tuning().spmv_ctas_per_sm);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(q.nitems, (int64_t)sms * std::max(1, per_sm)));
     spmv_async_kernel<ND, kParts><<<grid, kAsyncThreads, 0, s>>>(q);

@@ -57,12 +57,13 @@ class Diagonal:
 class _Dev:
     """Device arena + host offset/start tables."""
 
-    __slots__ = ("offs", "starts", "vals")
+    __slots__ = ("offs", "starts", "vals", "st")
 
     def __init__(self, offs: np.ndarray, starts: np.ndarray, vals):
         self.offs = offs
         self.starts = starts
         self.vals = vals
+        self.st = None  # diaq_matrix_t, built once (the arena never moves)
 
 
 class DiaqMatrix:
@@ -134,7 +135,9 @@ class DiaqMatrix:
 
     def _struct(self) -> L.Matrix:
         dv = self._device()
-        return L.mat_struct(self.n_dim, dv.offs, dv.starts, dv.vals)
+        if dv.st is None:
+            dv.st = L.mat_struct(self.n_dim, dv.offs, dv.starts, dv.vals)
+        return dv.st
 
     def device_arena(self):
         """(offsets, starts, torch complex128 arena) -- the device layout."""
