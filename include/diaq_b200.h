@@ -217,7 +217,8 @@ int diaq_sample_hits(int64_t n_amps, const void *x, const double *u_host, int64_
 /* ---- timing (per-gate CUDA events, resolved after the loop) ---------------- */
 int diaq_timer_create(int n, void **events);
 int diaq_timer_record(void *event, void *stream);
-/* waits for events[n-1]; ms_out[i] = milliseconds from events[i] to events[i+1] */
+/* waits for events[n-1]; ms_out[i] = milliseconds from events[i] to events[i+1]
+ * (from the last recorded event before i+1; 0 if events[i+1] was never recorded) */
 int diaq_timer_elapsed(int n, void **events, float *ms_out);
 int diaq_timer_destroy(int n, void **events);
 
@@ -227,8 +228,9 @@ int diaq_timer_destroy(int n, void **events);
  * Operands a gate does not mix (controls, diagonal gates) may lie outside
  * the tile.  tile_bits 11 or 12; <= 0 schedules both and keeps the one
  * with fewer passes (ties: 11); *npasses (optional)
- * receives the number of HBM passes.  events: as diaq_run_gates (a pass's
- * time is attributed to its first gate). */
+ * receives the number of HBM passes.  events: as diaq_run_gates, except
+ * that a pass records only its last gate's event (its time lands on that
+ * gate; diaq_timer_elapsed reads the unrecorded intervals as 0). */
 int diaq_run_gates_fused(int n_bits, int ngates, const diaq_gate_t *gates, void *state, int cmul_mode,
                          int tile_bits, void **events, int *npasses, void *stream);
 

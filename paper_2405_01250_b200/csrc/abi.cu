@@ -167,9 +167,19 @@ extern "C" int diaq_timer_elapsed(int n, void **events, float *ms_out) {
     if (n < 1 || !events || !ms_out) return set_error(DIAQ_ERR_VALUE, "diaq_timer_elapsed: bad arguments");
     if (cudaEventSynchronize((cudaEvent_t)events[n - 1]) != cudaSuccess)
         return set_error(DIAQ_ERR_CUDA, "cudaEventSynchronize: %s", cudaGetErrorString(cudaGetLastError()));
-    for (int i = 0; i + 1 < n; ++i)
-        if (cudaEventElapsedTime(&ms_out[i], (cudaEvent_t)events[i], (cudaEvent_t)events[i + 1]) != cudaSuccess)
-            return set_error(DIAQ_ERR_CUDA, "cudaEventElapsedTime: %s", cudaGetErrorString(cudaGetLastError()));
+    // events a fused pass did not record (all its gates but the last) read as
+    // zero-length intervals; the others are measured from the last recorded one
+    cudaEvent_t last = (cudaEvent_t)events[0];
+    for (int i = 0; i + 1 < n; ++i) {
+        float ms = 0.0f;
+        if (cudaEventElapsedTime(&ms, last, (cudaEvent_t)events[i + 1]) == cudaSuccess) {
+            ms_out[i] = ms;
+            last = (cudaEvent_t)events[i + 1];
+        } else {
+            cudaGetLastError();
+            ms_out[i] = 0.0f;
+        }
+    }
     return DIAQ_OK;
 }
 

@@ -1474,10 +1474,10 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
             count_launch();
             rc = check_launch("tile_pass_kernel");
         }
-        // events[i]..events[i+1] bracket gate i; a fused pass's time lands on
-        // its first gate, the others record zero-length intervals
-        if (events && rc == DIAQ_OK)
-            for (int gi : ps.members) cudaEventRecord((cudaEvent_t)events[gi + 1], s);
+        // events[i]..events[i+1] bracket gate i; a fused pass records only its
+        // last gate's event (one record per pass, not per gate), so the pass's
+        // time lands on that gate and diaq_timer_elapsed reads the others as 0
+        if (events && rc == DIAQ_OK) cudaEventRecord((cudaEvent_t)events[ps.members.back() + 1], s);
         cur = nxt;
     }
     if (rc == DIAQ_OK && cur != 0 &&

@@ -94,6 +94,8 @@ def test_dense_backend_and_fusion_agree():
     assert np.abs(diaq.state - fused.state).max() < 1e-12
     assert set(diaq.timings_ns) >= {"compile", "apply_total", "sample", "total", "per_gate"}
     assert len(diaq.timings_ns["per_gate"]) == len(ops)
+    pg = list(diaq.timings_ns["per_gate"].values())
+    assert all(t >= 0 for t in pg) and sum(pg) > 0  # a fused pass's time lands on its last gate
 
 
 def test_placement_edge_bits_and_reversed_operands():
