@@ -891,6 +891,10 @@ static int pack_smem_gate(const diaq_gate_t &gt, const std::vector<int> &bits, P
 // union of its gates' mixing bits fits in R registers.  Gates that cannot
 // be applied in registers (more than 2 mixing or 4 selector operands)
 // become standalone single-gate passes (gate_kernel).
+// set while re-planning a call without the out-of-place permutation tails
+// (no room for the state-sized buffer they need)
+static thread_local bool t_no_gperm = false;
+
 static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t *gates, int T, int R,
                          std::vector<PassPlan> &plan, bool allow_d2) {
     const int low = std::min(kLowBits, n_bits);
@@ -1158,7 +1162,7 @@ static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t 
             for (int j = 0; j < gt.k; ++j)
                 if (((mix >> j) & 1u) && !inb[gt.shifts[j]]) ++add;
         }
-        if (pg && !members.empty() && tuning().fused_gperm) {
+        if (pg && !members.empty() && tuning().fused_gperm && !t_no_gperm) {
             // a permutation that does not fit the tile (or follows one that did
             // not) joins the pass's global tail instead of opening a pass
             int padd0 = 0;
@@ -1265,7 +1269,9 @@ static std::vector<char> program_key(int n_total, int n_bits, int T, int ngates,
         const char *c = (const char *)p;
         key.insert(key.end(), c, c + n);
     };
-    const int head[5] = {n_total, n_bits, T, ngates, tuning().fused_perm};
+    // every tuning switch the schedule depends on is part of the key
+    const int head[8] = {n_total, n_bits, T, ngates, tuning().fused_perm,
+                         tuning().fused_gperm && !t_no_gperm, tuning().fused_seq, tuning().fused_dense2};
     put(head, sizeof(head));
     for (int i = 0; i < ngates; ++i) {
         const diaq_gate_t &gt = gates[i];
@@ -1440,8 +1446,15 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
         keep_pool_reserved();
         if (cudaMallocAsync((void **)&bufs[1], (size_t)16 << n_bits, s) != cudaSuccess) {
             cudaGetLastError();
-            return set_error(DIAQ_ERR_RESOURCE, "diaq_run_gates_fused: no room for a %llu-byte permutation buffer",
-                             (unsigned long long)((size_t)16 << n_bits));
+            if (t_no_gperm)
+                return set_error(DIAQ_ERR_RESOURCE, "diaq_run_gates_fused: no room for a %llu-byte buffer",
+                                 (unsigned long long)((size_t)16 << n_bits));
+            // no room for the state-sized buffer: plan without global permutation
+            // tails (they become in-tile folds or their own passes), all in place
+            t_no_gperm = true;
+            rc = run_fused(n_total, n_bits, rank, ngates, gates, state, cmul_mode, tile_bits, events, npasses, stream);
+            t_no_gperm = false;
+            return rc;
         }
     }
     int cur = 0;
