@@ -100,6 +100,7 @@ extern "C" int diaq_tune(const char *key, int64_t value) {
     else if (k == "spmv_async") t.spmv_async = (int)value;
     else if (k == "gate_ctas_per_sm") t.gate_ctas_per_sm = (int)(value < 1 ? 1 : value);
     else if (k == "fused_dense2") t.fused_dense2 = (int)value;
+    else if (k == "fused_gperm_rows") t.fused_gperm_rows = (int)value;
     else if (k == "fused_gperm") t.fused_gperm = (int)value;
     else if (k == "fused_seq") t.fused_seq = (int)value;
     else if (k == "fused_perm") t.fused_perm = (int)value;

@@ -143,6 +143,7 @@ struct Tuning {
     int spmv_async = 1;        // banded path through cp.async (LDGSTS) staging (default: fastest)
     int gate_ctas_per_sm = 32;
     int fused_dense2 = 1;      // dense two-qubit gates in registers (sequence phases)
+    int fused_gperm_rows = 0;  // 1: global tails only while they keep 128-byte rows whole (measured slower: an extra pass costs more than partial-row writes)
     int fused_gperm = 1;       // trailing permutation runs leaving the tile folded into the pass's store
     int fused_seq = 1;         // sequence phases (compile-time register bit per dense step)
     int fused_perm = 1;        // fold permutation gates (X/CX/SWAP) into the fused passes' smem addressing

@@ -921,6 +921,7 @@ static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t 
     int nb = 0;
     int ncoef = 0, nnz = 0;  // the pass's coefficient / mask table entries (kernel parameter bound)
     size_t tail = SIZE_MAX;  // members[tail..]: permutation run folded over the whole index (final store)
+    GlobalAffine tail_map;   // that run's composition so far
     auto reset = [&]() {
         std::fill(inb.begin(), inb.end(), 0);
         nb = 0;
@@ -1170,9 +1171,28 @@ static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t 
                 if (!((mix >> j) & 1u) && std::find(pbase.begin(), pbase.end(), gt.shifts[j]) == pbase.end()) ++padd0;
             if (tail != SIZE_MAX || kin > T - low || nb + add > T || (int)pbase.size() + padd0 > kMaxPermBase ||
                 (int)members.size() >= std::min(kMaxPassGates, kMaxPhases)) {
-                if (tail == SIZE_MAX) tail = members.size();
-                members.push_back(i);
-                continue;
+                // the tail must keep 128-byte rows whole (its store writes whole
+                // rows): no output bit above the row may depend on a row bit,
+                // else partial-sector writes cost read-modify-write traffic
+                GlobalAffine trial;
+                if (tail == SIZE_MAX) trial.init(n_bits);
+                else trial = tail_map;
+                bool rows = trial.fold(gt, perm[(size_t)i]);
+                for (int o = low; o < n_bits && rows && tuning().fused_gperm_rows; ++o)
+                    if (trial.row[o].m & ((1ull << low) - 1ull)) rows = false;
+                if (rows) {
+                    tail_map = trial;
+                    if (tail == SIZE_MAX) tail = members.size();
+                    members.push_back(i);
+                    continue;
+                }
+                // it opens the next pass, where its bits can join the tile
+                int rc = flush();
+                if (rc) return rc;
+                reset();
+                add = 0;
+                for (int j = 0; j < gt.k; ++j)
+                    if (((mix >> j) & 1u) && !inb[gt.shifts[j]]) ++add;
             }
         }
         if (pg ? (kin > T - low) : (kin > kMaxRegKin || kin > R || kout > kMaxSel)) {  // standalone pass
@@ -1270,8 +1290,9 @@ static std::vector<char> program_key(int n_total, int n_bits, int T, int ngates,
         key.insert(key.end(), c, c + n);
     };
     // every tuning switch the schedule depends on is part of the key
-    const int head[8] = {n_total, n_bits, T, ngates, tuning().fused_perm,
-                         tuning().fused_gperm && !t_no_gperm, tuning().fused_seq, tuning().fused_dense2};
+    const int head[9] = {n_total, n_bits, T, ngates, tuning().fused_perm,
+                         tuning().fused_gperm && !t_no_gperm, tuning().fused_seq, tuning().fused_dense2,
+                         tuning().fused_gperm_rows};
     put(head, sizeof(head));
     for (int i = 0; i < ngates; ++i) {
         const diaq_gate_t &gt = gates[i];
