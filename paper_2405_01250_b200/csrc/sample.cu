@@ -146,7 +146,12 @@ extern "C" int diaq_sample_hits(int64_t n, const void *x, const double *u_host, 
         return set_error(DIAQ_ERR_VALUE, "diaq_sample_hits: bad arguments");
     cudaStream_t s = (cudaStream_t)stream;
     int rc = DIAQ_OK;
-    const int64_t C = std::min<int64_t>(n, (int64_t)1 << 22);  // scan chunk
+    // scan chunks grow geometrically: the running sum's binades (each a
+    // segment of exact integer scan) double in length along the index, so a
+    // chunk about twice the last segment wastes little work past an exit and
+    // keeps the host round trips to ~ one per binade
+    const int64_t C = std::min<int64_t>(n, (int64_t)1 << 26);
+    int64_t want = std::min<int64_t>(C, (int64_t)1 << 16);
     double *q = nullptr, *c = nullptr, *part = nullptr, *ud = nullptr;
     long long *k = nullptr, *S = nullptr, *hd = nullptr;
     unsigned char *tie = nullptr;
@@ -198,7 +203,7 @@ extern "C" int diaq_sample_hits(int64_t n, const void *x, const double *u_host, 
             long long kbase = (long long)std::ldexp(cur, 52 - eb);  // exact integer in [2^52, 2^53)
             // walk chunks until the segment ends
             while (i < n) {
-                const int64_t cnt = std::min<int64_t>(C, n - i);
+                const int64_t cnt = std::min<int64_t>(want, n - i);
                 const int g = grid_of(cnt);
                 sample_k_kernel<<<g, kThreads, 0, s>>>(q, i, cnt, scale, k, tie);
                 cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, k, S, (int)cnt, s);
@@ -220,8 +225,10 @@ extern "C" int diaq_sample_hits(int64_t n, const void *x, const double *u_host, 
                 if (ex == ~0ull) {
                     kbase += last;
                     i += cnt;
+                    want = std::min<int64_t>(C, want * 2);
                     continue;
                 }
+                want = std::min<int64_t>(C, std::max<int64_t>((int64_t)1 << 16, 2 * (upto + 1)));
                 // the exiting element: one float64 step on the host, then a new segment
                 long long sprev = 0;
                 double qx = 0.0;
@@ -231,8 +238,8 @@ extern "C" int diaq_sample_hits(int64_t n, const void *x, const double *u_host, 
                 const double cprev = (double)(kbase + sprev) * U;
                 volatile double sum = cprev + qx;  // IEEE add, round to nearest even
                 cur = sum;
+                // pageable source: staged before the call returns, so &cur may be reused
                 DIAQ_CK(cudaMemcpyAsync(c + i + upto, &cur, sizeof(double), cudaMemcpyHostToDevice, s));
-                DIAQ_CK(cudaStreamSynchronize(s));  // &cur is reused
                 i += upto + 1;
                 break;
             }
