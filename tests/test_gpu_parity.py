@@ -622,3 +622,59 @@ def test_fused_two_qubit_gates(cmul):
         want = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=0).amps
         for tb in (11, 12, -1):
             assert np.array_equal(D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=tb).amps, want), (n, tb)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fused_scheduler_fuzz(cmul, seed):
+    """Seeded random circuits over every gate kind the scheduler routes
+    differently (dense/sparse 1-qubit, diagonals with and without selectors,
+    X/CX/SWAP runs inside and across tiles, affine 2-qubit permutations,
+    CCX, dense and controlled two-qubit gates), fused at every tile setting
+    and with every scheduling switch, bitwise against gate by gate."""
+    from paper_2405_01250_b200 import _lib as L
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(11, 19))
+    names1 = ["h", "x", "y", "z", "s", "t", "rx", "ry", "rz", "u3", "sdg"]
+    pls = []
+    for _ in range(int(rng.integers(40, 90))):
+        kind = rng.integers(8)
+        q = [int(v) for v in rng.choice(n, size=3, replace=False)]
+        if kind <= 2:
+            nm = names1[int(rng.integers(len(names1)))]
+            par = {"rx": (0.7,), "ry": (1.1,), "rz": (2.3,), "u3": (0.1, 0.2, 0.3)}.get(nm, ())
+            ops = [(nm, (q[0],), par)]
+        elif kind == 3:
+            ops = [("cx", (q[0], q[1]), ()), ("cx", (q[1], q[2]), ()), ("swap", (q[0], q[2]), ())]
+        elif kind == 4:
+            ops = [("cz", (q[0], q[1]), ()), ("ccx", (q[0], q[1], q[2]), ())]
+        else:
+            ops = []
+            if kind == 5:
+                g, qs = W.haar(rng, 4), [q[0], q[1]]
+            elif kind == 6:
+                g = np.eye(8, dtype=complex)
+                g[4:, 4:] = W.haar(rng, 4)
+                qs = q
+            else:
+                g, qs = _perm_gate([2, 0, 3, 1]), [q[0], q[1]]
+            lo, hi = min(qs), max(qs)
+            pls.append(D.Placement(2**lo, None, 2 ** (n - 1 - hi), lo, hi, "u", gate=(g, [v - lo for v in qs])))
+        if ops:
+            pls += D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
+    x0 = D.StateVector(n, W.random_state(rng, 2**n))
+    want = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=0).amps
+    switches = [{}, {"fused_seq": 0}, {"fused_gperm": 0}, {"fused_dense2": 0}, {"fused_perm": 0},
+                {"fused_gperm_rows": 1}]
+    try:
+        for sw in switches:
+            for k, v in sw.items():
+                L.tune(k, v)
+            for tb in (11, 12, -1):
+                got = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=tb).amps
+                assert np.array_equal(got, want), (seed, n, tb, sw)
+            for k in sw:
+                L.tune(k, {"fused_gperm_rows": 0}.get(k, 1))
+    finally:
+        for k, v in (("fused_seq", 1), ("fused_gperm", 1), ("fused_dense2", 1), ("fused_perm", 1),
+                     ("fused_gperm_rows", 0)):
+            L.tune(k, v)
