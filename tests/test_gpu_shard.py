@@ -104,3 +104,39 @@ def test_sharded_spmv_ragged_offsets():
         parts = list(x.chunk(world))
         got = torch.cat([ShardedDiaq.from_matrix(a, r, world).spmv(parts) for r in range(world)])
         assert np.array_equal(got.cpu().numpy(), want), world
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_sharded_fuzz(cmul, seed):
+    """Seeded random circuits (rotations, CX/SWAP chains with controls and
+    targets on global bits, CZ, CCX, Haar4) on emulated shards: fused local
+    runs with rank-dependent controls, permutation tails, and exchanges,
+    bitwise against the single-state run."""
+    rng = np.random.default_rng(500 + seed)
+    n = int(rng.integers(12, 17))
+    ops = []
+    for _ in range(int(rng.integers(30, 60))):
+        q = [int(v) for v in rng.choice(np.arange(2, n), size=3, replace=False)]  # qubits 0, 1: the global bits
+        if rng.integers(3) == 0:
+            q[0] = int(rng.integers(2))
+        k = int(rng.integers(6))
+        if k == 0:
+            ops.append((["rx", "ry", "rz", "h"][int(rng.integers(4))], (q[0],), (0.4,) if k == 0 else ()))
+        elif k == 1:
+            ops += [("cx", (q[0], q[1]), ()), ("cx", (1 - (q[0] & 1) if q[0] < 2 else 0, q[2]), ()),
+                    ("cx", (q[2], 1), ())]
+        elif k == 2:
+            ops += [("swap", (q[0], q[1]), ()), ("x", (q[2],), ())]
+        elif k == 3:
+            ops += [("cz", (q[0], q[1]), ()), ("ccx", tuple(q), ())]
+        else:
+            ops += [("ry", (q[1],), (1.3,)), ("rz", (0,), (0.9,))]
+    ops = [(a, b, c if a in ("rx", "ry", "rz") else ()) for a, b, c in ops]
+    pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
+    a, b = (int(v) for v in rng.choice(n, size=2, replace=False))
+    lo, hi = min(a, b), max(a, b)
+    pls.append(D.Placement(2**lo, None, 2 ** (n - 1 - hi), lo, hi, "haar", gate=(W.haar(rng, 4), [a - lo, b - lo])))
+    want = D.run_gates(D.init_state(n), pls, cmul_mode=cmul).amps
+    for world in (2, 4):
+        shards, _ = run_emulated(n, world, pls, cmul_mode=cmul)
+        assert np.array_equal(_full(shards), want), (seed, n, world)
