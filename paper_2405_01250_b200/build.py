@@ -40,20 +40,35 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-shared", "-o", LIB + ".tmp", *sources(),
-           "-I", os.path.join(ROOT, "include"), "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
     env = dict(os.environ)
     env.setdefault("CC", "/usr/bin/gcc")
-    proc = subprocess.run(cmd, capture_output=True, text=True, env=env,
-                          **({"cwd": ROOT}))
+    objdir = os.path.join(ROOT, "build", "obj")
+    os.makedirs(objdir, exist_ok=True)
+
+    def compile_one(src: str):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [nvcc, *NVCC_FLAGS, "-c", "-o", obj, src, "-I", os.path.join(ROOT, "include")]
+        return obj, subprocess.run(cmd, capture_output=True, text=True, env=env, cwd=ROOT)
+
+    # one nvcc per translation unit, in parallel (fused.cu dominates)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(sources()), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(compile_one, sources()))
+    log = "".join(p.stdout + p.stderr for _, p in results)
+    if any(p.returncode != 0 for _, p in results):
+        sys.stderr.write(log)
+        raise RuntimeError("nvcc build of libdiaq_b200.so failed")
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp",
+           *[o for o, _ in results], "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+    proc = subprocess.run(cmd, capture_output=True, text=True, env=env, cwd=ROOT)
     if proc.returncode != 0:
         sys.stderr.write(proc.stdout + proc.stderr)
-        raise RuntimeError("nvcc build of libdiaq_b200.so failed")
+        raise RuntimeError("nvcc link of libdiaq_b200.so failed")
     if verbose:
-        sys.stderr.write(proc.stderr)
+        sys.stderr.write(log)
     os.replace(LIB + ".tmp", LIB)
     with open(os.path.join(HERE, "ptxas.log"), "w") as f:
-        f.write(proc.stderr)
+        f.write(log)
     return LIB
 
 

@@ -111,6 +111,16 @@ __device__ __forceinline__ double2 cmul(double2 v, double2 x) {
     else return cmul_plain(v, x);
 }
 
+// products with a coefficient whose other part is an exact zero (see
+// fused.cu dense1_full): equal to both cmul forms up to the sign of a zero
+__device__ __forceinline__ double2 cmul_re(double vr, double2 x) {
+    return make_double2(__dmul_rn(vr, x.x), __dmul_rn(vr, x.y));
+}
+
+__device__ __forceinline__ double2 cmul_im(double vi, double2 x) {
+    return make_double2(-__dmul_rn(vi, x.y), __dmul_rn(vi, x.x));
+}
+
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) {
     return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
 }
@@ -146,6 +156,7 @@ struct Tuning {
     int fused_gperm_rows = 0;  // 1: global tails only while they keep 128-byte rows whole (measured slower: an extra pass costs more than partial-row writes)
     int fused_gperm = 1;       // trailing permutation runs leaving the tile folded into the pass's store
     int fused_seq = 1;         // sequence phases (compile-time register bit per dense step)
+    int fused_nbuf = 0;        // fused pass tile buffers: 0 auto (2 unless it costs occupancy), 1, 2
     int fused_perm = 1;        // fold permutation gates (X/CX/SWAP) into the fused passes' smem addressing
     int kron_flat = 1;         // kron_identity as one arena-linear store stream
     int kron_ctas_per_sm = 32;  // CTAs per SM launched (4 resident; later ones refill)

@@ -61,6 +61,9 @@ struct RegGate {               // narrow fields: the records live in the kernel 
     // fast-path classification (host): 0 generic, 1 dense 1-qubit (no selector),
     // 2 diagonal with one selector
     int8_t op;
+    // dense 1-qubit coefficient shape (host): 0 complex, 1 all entries real
+    // (RY, H), 2 real diagonal / imaginary off-diagonal (RX)
+    int8_t shape;
     int8_t mpos[kMaxRegKin];  // generic phases: tile positions of the mixing bits (relabelled order)
     int16_t coef_off;         // coef[coef_off + (b << 2kin) + r * 2^kin + c]   (pass-relative)
     int16_t nz_off;           // nz[nz_off + (b << kin) + r]
@@ -83,7 +86,7 @@ struct Affine {
     uint16_t b[kMaxPermBase];
 };
 
-__device__ __forceinline__ uint32_t aff_lin(const Affine &m, uint32_t f, int T) {
+__host__ __device__ __forceinline__ uint32_t aff_lin(const Affine &m, uint32_t f, int T) {
     uint32_t r = 0;
     for (int j = 0; j < T; ++j)
         if ((f >> j) & 1u) r ^= m.a[j];
@@ -111,6 +114,12 @@ struct Phase {
     int8_t rpos[4];           // tile positions of the register bits, ascending (R entries)
     int8_t tpos[kMaxTileBits];  // tile positions of the thread bits, ascending (T - R entries)
     Affine post;              // permutation run after the phase's gates, applied by its store
+    // swizzled smem slot of register j's part of the index (swz is linear
+    // over GF(2), and thread and register bits are disjoint): register j of
+    // a thread lives at swz(tpart) ^ pj[j]; its post-permutation slot at
+    // swz(A tpart ^ c) ^ ppj[j]
+    uint16_t pj[16];
+    uint16_t ppj[16];
 };
 
 // One pass = one launch; its whole gate program rides in the kernel
@@ -131,6 +140,7 @@ struct TileParams {
     Affine pre;               // permutation run opening the pass, applied by the tile load
     double2 *y;               // destination (== x: in place)
     int gperm;                // store through the global map (out of place)
+    int nbuf;                 // tile buffers in dynamic smem: 2 = prefetch the next tile during this one
     uint64_t gconst;          // its constant, rank bits folded in
     uint64_t gcol[64];        // image of local state bit j
     Phase ph[kMaxPhases];
@@ -146,7 +156,7 @@ __device__ __forceinline__ uint64_t next_base(uint64_t base, const TileParams &p
     return ((base | p.tmask) + p.gstep) & ~p.tmask;
 }
 
-__device__ __forceinline__ uint32_t swz(uint32_t e) {
+__host__ __device__ __forceinline__ uint32_t swz(uint32_t e) {
     return e ^ (((e >> 3) ^ (e >> 6) ^ (e >> 9)) & 7u);
 }
 
@@ -193,8 +203,13 @@ __device__ __forceinline__ void dense1(double2 (&v)[1 << R], const double2 *c, u
 }
 
 // all four entries nonzero (RX, RY, H, U3 ...): branch-free, so the
-// compiler interleaves the 2^R independent multiply-add chains
-template <int R, int B1, int MODE>
+// compiler interleaves the 2^R independent multiply-add chains.
+// SHAPE 1 (every entry real) / 2 (real diagonal, imaginary off-diagonal):
+// an entry's zero part contributes an exact +-0 to each product, so
+//   (vr + 0i) x = (vr xr, vr xi),   (0 + vi i) x = (-(vi xi), vi xr)
+// in both numpy multiply forms (plain and FMA) up to the sign of an exact
+// zero -- 6 instead of 10 FP64 operations per amplitude, same values.
+template <int R, int B1, int MODE, int SHAPE = 0>
 __device__ __forceinline__ void dense1_full(double2 (&v)[1 << R], const double2 *c) {
     const double2 c00 = c[0], c01 = c[1], c10 = c[2], c11 = c[3];
 #pragma unroll
@@ -202,9 +217,24 @@ __device__ __forceinline__ void dense1_full(double2 (&v)[1 << R], const double2 
         const int j0 = ((g >> B1) << (B1 + 1)) | (g & ((1 << B1) - 1));
         const int j1 = j0 | (1 << B1);
         const double2 x0 = v[j0], x1 = v[j1];
-        v[j0] = cadd(cmul<MODE>(c00, x0), cmul<MODE>(c01, x1));
-        v[j1] = cadd(cmul<MODE>(c10, x0), cmul<MODE>(c11, x1));
+        if constexpr (SHAPE == 1) {
+            v[j0] = cadd(cmul_re(c00.x, x0), cmul_re(c01.x, x1));
+            v[j1] = cadd(cmul_re(c10.x, x0), cmul_re(c11.x, x1));
+        } else if constexpr (SHAPE == 2) {
+            v[j0] = cadd(cmul_re(c00.x, x0), cmul_im(c01.y, x1));
+            v[j1] = cadd(cmul_im(c10.y, x0), cmul_re(c11.x, x1));
+        } else {
+            v[j0] = cadd(cmul<MODE>(c00, x0), cmul<MODE>(c01, x1));
+            v[j1] = cadd(cmul<MODE>(c10, x0), cmul<MODE>(c11, x1));
+        }
     }
+}
+
+template <int R, int B1, int MODE>
+__device__ __forceinline__ void dense1_shaped(double2 (&v)[1 << R], const double2 *c, int shape) {
+    if (shape == 1) dense1_full<R, B1, MODE, 1>(v, c);
+    else if (shape == 2) dense1_full<R, B1, MODE, 2>(v, c);
+    else dense1_full<R, B1, MODE, 0>(v, c);
 }
 
 // dense two-qubit gate (all 16 entries nonzero) on register bits RA (its
@@ -230,15 +260,14 @@ __device__ __forceinline__ void dense2_full(double2 (&v)[1 << R], const double2 
     }
 }
 
+// Diagonal factors are applied branch-free: an entry whose nz bit is clear is
+// stored as exactly 0 + 0i, and 0 * x is the skipped term's +-0 (finite
+// states), so values are unchanged; a uniform branch here would make ptxas
+// copy the whole amplitude set at every iteration of the diagonal loops.
 template <int R, int RB, int MODE>
-__device__ __forceinline__ void diag_reg(double2 (&v)[1 << R], double2 d0, double2 d1, uint32_t z0, uint32_t z1) {
+__device__ __forceinline__ void diag_reg(double2 (&v)[1 << R], double2 d0, double2 d1) {
 #pragma unroll
-    for (int j = 0; j < (1 << R); ++j) {
-        const bool hi = (j >> RB) & 1;
-        const double2 d = hi ? d1 : d0;
-        const bool nz = hi ? (z1 & 1u) : (z0 & 1u);
-        v[j] = nz ? cmul<MODE>(d, v[j]) : make_double2(0.0, 0.0);
-    }
+    for (int j = 0; j < (1 << R); ++j) v[j] = cmul<MODE>(((j >> RB) & 1) ? d1 : d0, v[j]);
 }
 
 
@@ -269,13 +298,9 @@ __device__ __forceinline__ void diag_uniform(double2 (&v)[1 << R], const RegGate
                                              const uint64_t *sbase_p, const double2 *sc, const uint32_t *snz) {
     const uint32_t b = G.osel[0] == 0 ? (uint32_t)((ld_base(sbase_p) >> G.opos[0]) & 1ull) : (tpart >> G.opos[0]) & 1u;
     const double2 d = sc[G.coef_off + (int)b];
-    if (snz[G.nz_off + (int)b] & 1u) {
+    (void)snz;
 #pragma unroll
-        for (int j = 0; j < (1 << R); ++j) v[j] = cmul<MODE>(d, v[j]);
-    } else {
-#pragma unroll
-        for (int j = 0; j < (1 << R); ++j) v[j] = make_double2(0.0, 0.0);
-    }
+    for (int j = 0; j < (1 << R); ++j) v[j] = cmul<MODE>(d, v[j]);
 }
 
 template <int R, int MODE>
@@ -286,21 +311,19 @@ __device__ __forceinline__ void dispatch_gate(double2 (&v)[1 << R], const RegGat
     if (G.op == 1) {
         const double2 *c = sc + G.coef_off;
         const uint32_t n0 = snz[G.nz_off], n1 = snz[G.nz_off + 1];
-        if ((n0 & n1 & 3u) == 3u) DIAQ_RB_DISPATCH(R, G.rb[0], (dense1_full<R, RB_, MODE>(v, c)));
+        if ((n0 & n1 & 3u) == 3u) DIAQ_RB_DISPATCH(R, G.rb[0], (dense1_shaped<R, RB_, MODE>(v, c, G.shape)));
         else DIAQ_RB_DISPATCH(R, G.rb[0], (dense1<R, RB_, MODE>(v, c, n0, n1)));
         return;
     }
     if (G.op == 2) {
         const double2 d0 = sc[G.coef_off], d1 = sc[G.coef_off + 1];
-        const uint32_t z0 = snz[G.nz_off], z1 = snz[G.nz_off + 1];
         if (G.osel[0] == 2) {
-            DIAQ_RB_DISPATCH(R, G.opos[0], (diag_reg<R, RB_, MODE>(v, d0, d1, z0, z1)));
+            DIAQ_RB_DISPATCH(R, G.opos[0], (diag_reg<R, RB_, MODE>(v, d0, d1)));
         } else {
             const uint32_t b = G.osel[0] == 0 ? (uint32_t)((ld_base(sbase_p) >> G.opos[0]) & 1ull) : (tpart >> G.opos[0]) & 1u;
             const double2 d = b ? d1 : d0;
-            const bool nz = b ? (z1 & 1u) : (z0 & 1u);
 #pragma unroll
-            for (int j = 0; j < (1 << R); ++j) v[j] = nz ? cmul<MODE>(d, v[j]) : make_double2(0.0, 0.0);
+            for (int j = 0; j < (1 << R); ++j) v[j] = cmul<MODE>(d, v[j]);
         }
         return;
     }
@@ -381,9 +404,13 @@ template <int R, int MODE, int RB>
 __device__ __forceinline__ void seq_steps(double2 (&v)[1 << R], const TileParams &p, const Phase &ph, int &gi,
                                           uint32_t tpart, const uint64_t *sbase_p, const double2 *sc,
                                           const uint32_t *snz) {
+    // unrolled by 2: a complex multiply cannot land in its input registers
+    // (both parts read both inputs), so a rolled loop pays a register copy of
+    // the amplitude set per gate to return to the loop-carried assignment
+#pragma unroll 2
     for (int c = 0; c < ph.nd_before[RB]; ++c, ++gi) diag_uniform<R, MODE>(v, p.g[gi], tpart, sbase_p, sc, snz);
     if (ph.kind[RB] == 1) {
-        dense1_full<R, RB, MODE>(v, sc + p.g[gi].coef_off);
+        dense1_shaped<R, RB, MODE>(v, sc + p.g[gi].coef_off, p.g[gi].shape);
         ++gi;
         if constexpr (RB + 1 < R) seq_steps<R, MODE, RB + 1>(v, p, ph, gi, tpart, sbase_p, sc, snz);
     } else if (ph.kind[RB] == 2) {
@@ -397,23 +424,22 @@ __device__ __forceinline__ void seq_steps(double2 (&v)[1 << R], const TileParams
 
 template <int R, int MODE>
 __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(const __grid_constant__ TileParams p) {
+    // dynamic smem: nbuf tiles, then the row-offset table, then (gperm) the
+    // global-map table -- sized by T, so small tiles leave room for 3 CTAs
     extern __shared__ double2 tile[];
-    __shared__ uint64_t hi_off[(1 << kMaxTileBits) >> kLowBits];
-    // per-(phase, thread) smem slots of the thread's registers and its thread-bit
-    // pattern, computed once per CTA instead of once per tile
-    constexpr int kPre = R >= 4 ? kPrePhases - 1 : kPrePhases;
-    __shared__ uint16_t s_off[kPre][1 << R][kThreads];
-    __shared__ uint32_t s_tpart[kPre][kThreads];
-    // folded permutations: swizzled images of the thread part / register part
-    __shared__ uint16_t s_pt[kPre][kThreads];
-    __shared__ uint16_t s_pj[kPre][1 << R];
+    const int T = p.tbits;
+    const uint32_t tsize = 1u << T;
+    uint64_t *hi_off = (uint64_t *)(tile + ((size_t)p.nbuf << T));
+    uint64_t *s_ghi = hi_off + (tsize >> kLowBits);  // global map of each tile row offset
+    // per-(phase, thread) index part of the thread bits, computed once per
+    // CTA instead of once per tile (register parts ride in the phase record)
+    constexpr int kPre = kPrePhases;
+    __shared__ uint16_t s_tpart[kPre][kThreads];
+    __shared__ uint16_t s_pt[kPre][kThreads];  // folded permutations: swizzled image of the thread part
     __shared__ uint16_t s_lt[kThreads];
     __shared__ uint16_t s_lk[1 << (kMaxTileBits - kThreadBits)];
     __shared__ uint64_t s_sbase;  // current tile's base | rank bits (selector lookups)
-    __shared__ uint64_t s_ghi[(1 << kMaxTileBits) >> kLowBits];  // global map of each tile row offset
     constexpr int NR = 1 << R;
-    const int T = p.tbits;
-    const uint32_t tsize = 1u << T;
     const double2 *sc = p.coef;
     const uint32_t *snz = p.nz;
     // tile element e -> state offset: low kLowBits tile bits are state bits 0..2
@@ -430,13 +456,8 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
         const Phase &ph = p.ph[ph_i];
         uint32_t tpart = 0;
         for (int i = 0; i < T - R; ++i) tpart |= ((threadIdx.x >> i) & 1u) << ph.tpos[i];
-        s_tpart[ph_i][threadIdx.x] = tpart;
-#pragma unroll
-        for (int j = 0; j < NR; ++j) s_off[ph_i][j][threadIdx.x] = (uint16_t)swz(tpart | reg_spread<R>(j, ph.rpos));
-        if (ph.post.on) {  // swz is linear over GF(2): slot = swz(A tpart) ^ swz(A spread(j)) ^ swz(const)
-            s_pt[ph_i][threadIdx.x] = (uint16_t)swz(aff_lin(ph.post, tpart, T));
-            if (threadIdx.x < NR) s_pj[ph_i][threadIdx.x] = (uint16_t)swz(aff_lin(ph.post, reg_spread<R>(threadIdx.x, ph.rpos), T));
-        }
+        s_tpart[ph_i][threadIdx.x] = (uint16_t)tpart;
+        if (ph.post.on) s_pt[ph_i][threadIdx.x] = (uint16_t)swz(aff_lin(ph.post, tpart, T));
     }
     if (p.pre.on) {
         s_lt[threadIdx.x] = (uint16_t)swz(aff_lin(p.pre, threadIdx.x, T));
@@ -478,14 +499,23 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     __syncthreads();
-    // (a second tile buffer to prefetch into was measured slower: it costs a
-    // resident CTA per SM, and the pass is issue-bound, not latency-bound)
+    // nbuf 2: the next tile streams into the other buffer while this one is
+    // computed (its latency hidden inside the CTA); nbuf 1: refill after the
+    // store, latency hidden only by the other resident CTAs
     uint64_t base = insert_zero_bits_dyn((uint64_t)blockIdx.x, p.tb, T);
     if ((int64_t)blockIdx.x < p.ntiles) fetch(base, tile);
-    double2 *tl = tile;
+    int buf = 0;
     for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+        const uint64_t nbase = next_base(base, p);
+        const bool more = t + gridDim.x < p.ntiles;
+        double2 *tl = tile + ((size_t)buf << T);
         if (threadIdx.x == 0) s_sbase = base | p.gbase;  // full-state index bits for selectors
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        if (p.nbuf == 2 && more) {
+            fetch(nbase, tile + ((size_t)(buf ^ 1) << T));
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
         __syncthreads();
         for (int ph_i = 0; ph_i < p.nphases; ++ph_i) {
             const Phase &ph = p.ph[ph_i];
@@ -500,38 +530,30 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
             uint32_t tpart;
             if (ph_i < kPre) {
                 tpart = s_tpart[ph_i][threadIdx.x];
-#pragma unroll
-                for (int j = 0; j < NR; ++j) v[j] = tl[s_off[ph_i][j][threadIdx.x]];
             } else {
                 tpart = 0;
                 for (int i = 0; i < T - R; ++i) tpart |= ((threadIdx.x >> i) & 1u) << ph.tpos[i];
-#pragma unroll
-                for (int j = 0; j < NR; ++j) v[j] = tl[swz(tpart | reg_spread<R>(j, ph.rpos))];
             }
+            const uint32_t tsw = swz(tpart);
+#pragma unroll
+            for (int j = 0; j < NR; ++j) v[j] = tl[tsw ^ ph.pj[j]];
             if (ph.seq) {
                 int gi = ph.g0;
                 seq_steps<R, MODE, 0>(v, p, ph, gi, tpart, &s_sbase, sc, snz);
+#pragma unroll 2
                 for (int c = 0; c < ph.nd_before[R]; ++c, ++gi) diag_uniform<R, MODE>(v, p.g[gi], tpart, &s_sbase, sc, snz);
             } else {
                 for (int gi = ph.g0; gi < ph.g1; ++gi) dispatch_gate<R, MODE>(v, p.g[gi], tpart, &s_sbase, sc, snz);
             }
             if (ph.post.on) {
                 __syncthreads();  // relabelled slots belong to other threads' registers: all reads first
-                const uint32_t bc = aff_const(ph.post, ld_base(&s_sbase));
-                if (ph_i < kPre) {
-                    const uint32_t pt = s_pt[ph_i][threadIdx.x] ^ swz(bc);
+                const uint32_t bc = swz(aff_const(ph.post, ld_base(&s_sbase)));
+                const uint32_t pt = (ph_i < kPre ? (uint32_t)s_pt[ph_i][threadIdx.x] : swz(aff_lin(ph.post, tpart, T))) ^ bc;
 #pragma unroll
-                    for (int j = 0; j < NR; ++j) tl[pt ^ s_pj[ph_i][j]] = v[j];
-                } else {
-#pragma unroll
-                    for (int j = 0; j < NR; ++j) tl[swz(aff_lin(ph.post, tpart | reg_spread<R>(j, ph.rpos), T) ^ bc)] = v[j];
-                }
-            } else if (ph_i < kPre) {
-#pragma unroll
-                for (int j = 0; j < NR; ++j) tl[s_off[ph_i][j][threadIdx.x]] = v[j];
+                for (int j = 0; j < NR; ++j) tl[pt ^ ph.ppj[j]] = v[j];
             } else {
 #pragma unroll
-                for (int j = 0; j < NR; ++j) tl[swz(tpart | reg_spread<R>(j, ph.rpos))] = v[j];
+                for (int j = 0; j < NR; ++j) tl[tsw ^ ph.pj[j]] = v[j];
             }
             __syncthreads();
         }
@@ -552,8 +574,9 @@ __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(con
             }
         }
         __syncthreads();
-        base = next_base(base, p);
-        if (t + gridDim.x < p.ntiles) fetch(base, tile);  // refill as soon as the tile is drained
+        base = nbase;
+        if (p.nbuf == 2) buf ^= 1;
+        else if (more) fetch(base, tile);  // refill as soon as the tile is drained
     }
 }
 
@@ -840,7 +863,17 @@ static int pack_reg_gate(const diaq_gate_t &gt, const std::vector<int> &bits, co
         pk.cls.push_back(ident ? 1u : (swap ? 2u : 0u));
     }
     G.op = 0;
-    if (G.kin == 1 && G.kout == 0) G.op = 1;
+    G.shape = 0;
+    if (G.kin == 1 && G.kout == 0) {
+        G.op = 1;
+        const double2 *c = &pk.coef[G.coef_off];
+        bool real = true, rx = true;
+        for (int e = 0; e < 4; ++e) {
+            real = real && c[e].y == 0.0;
+            rx = rx && ((e == 0 || e == 3) ? c[e].y == 0.0 : c[e].x == 0.0);
+        }
+        G.shape = real ? 1 : (rx ? 2 : 0);
+    }
     else if (G.kin == 0 && G.kout == 1) G.op = 2;
     else if (G.kin == 2 && G.kout == 0) {  // dense two-qubit: register path only when every entry is nonzero
         bool full = true;
@@ -1097,6 +1130,12 @@ static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t 
             }
             ph.g1 = (int)ps.gates.size();
             ph.post = sp.post.pack();
+            for (int j = 0; j < 16; ++j) {
+                uint32_t e = 0;
+                for (int q = 0; q < R; ++q) e |= (uint32_t)((j >> q) & 1) << ph.rpos[q];
+                ph.pj[j] = j < (1 << R) ? (uint16_t)swz(e) : 0;
+                ph.ppj[j] = (j < (1 << R) && ph.post.on) ? (uint16_t)swz(aff_lin(ph.post, e, (int)ps.bits.size())) : 0;
+            }
             if (seq_try) {  // sequence form?
                 int nd = 0, cnt = 0;
                 bool ok = true;
@@ -1423,7 +1462,7 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
     const int R = T - kThreadBits;
     const std::vector<PassPlan> &plan = prog->plan;
     if (npasses) *npasses = (int)plan.size();
-    const size_t smem_max = (sizeof(double2) << kMaxTileBits);
+    const size_t smem_max = 2 * (sizeof(double2) << kMaxTileBits) + 2 * (sizeof(uint64_t) << (kMaxTileBits - kLowBits));
     static bool attr_set[64] = {false};  // per device (one process may drive several)
     int cur_dev = 0;
     if (cudaGetDevice(&cur_dev) != cudaSuccess || cur_dev < 0 || cur_dev >= 64) {
@@ -1496,8 +1535,21 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
                 for (int g = 0; g < 64 && g < n_total - n_bits; ++g)
                     if (((uint64_t)rank >> g) & 1ull) p.gconst ^= ps.ggcol[(size_t)g];
             const void *f = R >= 4 ? tile_kernel_ptr<4>(cmul_mode) : tile_kernel_ptr<3>(cmul_mode);
-            const size_t smem = sizeof(double2) << p.tbits;
-            const int per_sm = occupancy(f, kThreads, smem);
+            auto smem_for = [&](int nb) {
+                return ((sizeof(double2) * nb) << p.tbits) + ((sizeof(uint64_t) * (p.gperm ? 2 : 1)) << (p.tbits - kLowBits));
+            };
+            // two tile buffers (prefetch) unless that costs a resident CTA
+            const int knob = tuning().fused_nbuf;
+            int per_sm = occupancy(f, kThreads, smem_for(1));
+            p.nbuf = 1;
+            if (knob != 1) {
+                const int per_sm2 = occupancy(f, kThreads, smem_for(2));
+                if (knob == 2 || per_sm2 >= per_sm) {
+                    p.nbuf = 2;
+                    per_sm = per_sm2;
+                }
+            }
+            const size_t smem = smem_for(p.nbuf);
             const int64_t grid =
                 std::max<int64_t>(1, std::min<int64_t>(p.ntiles, (int64_t)sm_count() * std::max(1, per_sm)));
             p.gstep = 0;  // deposit grid into the non-tile bits, low to high
