@@ -397,6 +397,13 @@ def run_ours(args):
     return 0
 
 
+def jit_stats(L):
+    import ctypes
+    st = (ctypes.c_int64 * 6)()
+    L.call("diaq_jit_stats", ctypes.addressof(st))
+    return dict(zip(["compiled", "failed", "launches", "modules", "pending", "compile_ms"], list(st)))
+
+
 def replica_gates(args, D, L, W, torch, dist, n, world, x, s, dev):
     """Each rank applies one random layer per step to its own 2^n state (fused
     shared-memory passes; bitwise equal to gate-by-gate)."""
@@ -405,7 +412,14 @@ def replica_gates(args, D, L, W, torch, dist, n, world, x, s, dev):
     state = D.StateVector(n, x.clone())
     for _ in range(max(1, args.warmup // 2)):
         state = D.run_gates(state, pls, inplace=True)
+    # the passes' specialised kernels compile in the background during the
+    # warm-up (one-time, per pass structure); time the steady state
+    t_jit = time.perf_counter()
+    L.call("diaq_jit_wait", -1.0)
+    jit_wait_s = time.perf_counter() - t_jit
+    state = D.run_gates(state, pls, inplace=True)
     torch.cuda.synchronize()
+    jst0 = jit_stats(L)
     g_steps = max(2, min(args.steps, 10))
     ge0 = torch.cuda.Event(enable_timing=True)
     ge1 = torch.cuda.Event(enable_timing=True)
@@ -416,10 +430,15 @@ def replica_gates(args, D, L, W, torch, dist, n, world, x, s, dev):
     ge1.record(s)
     torch.cuda.synchronize()
     g_launches = L.launch_count() - gl0
+    jst1 = jit_stats(L)
     g_ms = max_over_ranks(dist, ge0.elapsed_time(ge1), dev)
     g_norm = state.norm()
     extra = {"gates_per_step": len(pls), "steps": g_steps, "mode": f"replicas x{world}",
-             "fused_tile_bits": D.sim.FUSE_TILE_BITS if D.sim.FUSE_TILE_BITS > 0 else "auto (11 or 12: fewer passes, ties 11)", "hbm_passes": int(g_launches)}
+             "fused_tile_bits": D.sim.FUSE_TILE_BITS if D.sim.FUSE_TILE_BITS > 0 else "auto (11 or 12: fewer passes, ties 11)", "hbm_passes": int(g_launches),
+             "specialised_passes": {"launches_timed": jst1["launches"] - jst0["launches"], "compiled": jst1["compiled"],
+                                    "failed": jst1["failed"], "compile_cpu_ms": jst1["compile_ms"],
+                                    "wait_after_warmup_s": round(jit_wait_s, 3),
+                                    "note": "NVRTC per pass structure, background thread; one-time"}}
     return len(pls) * g_steps, g_ms, g_launches, g_norm, n, extra
 
 
@@ -507,6 +526,8 @@ def secondary_workloads(args, D, L, W, torch) -> dict:
     ops = W.random_layered_ops(20, 40, seed=0)
     pls = D.compile_circuit(D.Circuit(20, [D.GateOp(*o) for o in ops]), span_limit=20)
     st = D.init_state(20)
+    D.run_gates(st, pls, inplace=True)
+    L.call("diaq_jit_wait", -1.0)  # specialised passes (one-time compile)
     ms = dev_time(lambda: D.run_gates(st, pls, inplace=True), 3)
     t0 = time.perf_counter()
     res = D.run(D.Circuit(20, [D.GateOp(*o) for o in ops]), shots=1024, seed=0, span_limit=20)
@@ -538,6 +559,8 @@ def secondary_workloads(args, D, L, W, torch) -> dict:
         pls_h.append(D.Placement(2**lo, None, 2 ** (27 - hi), lo, hi, "haar",
                                  gate=(W.haar(rng, 4), [qa - lo, qb - lo])))
     st_h = D.init_state(28)
+    D.run_gates(st_h, pls_h, inplace=True)
+    L.call("diaq_jit_wait", -1.0)
     ms_h = dev_time(lambda: D.run_gates(st_h, pls_h, inplace=True), 3)
     out["haar4_layer_n28"] = {"gates": len(pls_h), "ms_per_layer": round(ms_h, 3),
                               "gates_per_s": round(len(pls_h) / ms_h * 1e3, 1)}
@@ -546,7 +569,8 @@ def secondary_workloads(args, D, L, W, torch) -> dict:
     ops30 = W.random_layered_ops(30, 20, seed=0)
     pls30 = D.compile_circuit(D.Circuit(30, [D.GateOp(*o) for o in ops30]), span_limit=30)
     st30 = D.init_state(30, max_qubits=30)
-    D.run_gates(st30, pls30[:45], inplace=True)  # warm-up (program cache, first launches)
+    D.run_gates(st30, pls30, inplace=True)  # warm-up (program cache, specialised passes)
+    L.call("diaq_jit_wait", -1.0)
     st30 = D.init_state(30, max_qubits=30)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()

@@ -246,6 +246,27 @@ int diaq_trim_pool(void);
  * shard, as diaq_run_gates_local. */
 int diaq_fused_plan(int n_bits, int local_bits, int ngates, const diaq_gate_t *gates, int tile_bits, int *stats);
 
+/* ---- specialised fused passes (NVRTC) ------------------------------------
+ * Each tiled pass is also compiled at run time with its structure (tile
+ * bits, phases, gate records) constant -- the same device code as the AOT
+ * pass kernel, bitwise the same results, without the per-gate decode.
+ * Compiles run on a background thread (knob fused_jit: 0 off, 1 async,
+ * 2 compile before the first launch); until a pass's kernel is ready the
+ * AOT kernel runs it. */
+/* wait until no specialised pass is compiling (timeout_s < 0: no limit) */
+int diaq_jit_wait(double timeout_s);
+/* stats[0] passes compiled, [1] failed, [2] specialised launches,
+ * [3] modules loaded, [4] pending, [5] total compile milliseconds */
+int diaq_jit_stats(int64_t *stats);
+/* last compile / load error text ("" if none) */
+const char *diaq_jit_last_error(void);
+/* host-only: schedule and compile a program's specialised passes now (no
+ * device, no cache); *seconds compile time, *kernels passes compiled.
+ * seconds == NULL: submit them to the background compile queue instead
+ * (as the first diaq_run_gates_fused call of the program would) and return. */
+int diaq_fused_jit_compile(int n_bits, int local_bits, int ngates, const diaq_gate_t *gates, int tile_bits,
+                           int cmul_mode, double *seconds, int *kernels);
+
 /* ---- state helpers ------------------------------------------------------ */
 /* |index> (reference init_state, sim.py:53-59) */
 int diaq_init_basis(int64_t n_amps, void *x, int64_t index, void *stream);

@@ -83,6 +83,10 @@ _SIGS = {
     "diaq_run_gates_fused": ([_INT, _INT, ctypes.POINTER(Gate), _P, _INT, _INT, _P, _P, _P], _INT),
     "diaq_trim_pool": ([], _INT),
     "diaq_fused_plan": ([_INT, _INT, _INT, ctypes.POINTER(Gate), _INT, _P], _INT),
+    "diaq_jit_wait": ([ctypes.c_double], _INT),
+    "diaq_jit_stats": ([_P], _INT),
+    "diaq_jit_last_error": ([], ctypes.c_char_p),
+    "diaq_fused_jit_compile": ([_INT, _INT, _INT, ctypes.POINTER(Gate), _INT, _INT, _P, _P], _INT),
     "diaq_init_basis": ([_I64, _P, _I64, _P], _INT),
     "diaq_norm2": ([_I64, _P, _P, _P], _INT),
     "diaq_run_gates_local": ([_INT, _INT, _I64, _INT, ctypes.POINTER(Gate), _P, _INT, _INT, _P, _P, _P], _INT),
@@ -122,6 +126,10 @@ def load():
         fn.argtypes = args
         fn.restype = res
     _lib = lib
+    # DIAQ_TUNE="key=value,...": library knobs for experiments (diaq_tune)
+    for kv in filter(None, os.environ.get("DIAQ_TUNE", "").split(",")):
+        k, v = kv.split("=")
+        check(lib.diaq_tune(k.strip().encode(), int(v)), "diaq_tune")
     return lib
 
 

@@ -29,555 +29,18 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
+#include "fused_dev.cuh"
+#include "fused_jit.cuh"
 
 namespace diaq {
 
-constexpr int kMaxTileBits = 12;
-constexpr int kThreadBits = 8;      // 256 threads
-constexpr int kLowBits = 3;         // tile rows are 2^3 amplitudes = 128 B
-constexpr int kMaxRegKin = 2;       // mixing operands of a fused gate (2: shared-memory path; wider: own pass)
-constexpr int kMaxSel = 4;          // selector (non-mixing) operands
-constexpr int kMaxPassGates = 48;   // gate records per pass (kernel parameters)
-constexpr int kMaxPhases = 24;
-constexpr int kRetryNoDense2 = 1000;  // schedule(): internal, re-plan without register 2-qubit gates
-constexpr int kMaxCoef = 256;       // coefficient entries per pass (kernel parameters)
-constexpr int kMaxNz = 256;
-constexpr int kPrePhases = 4;       // phases whose register slots are precomputed per CTA (R = 3; 3 at R = 4,
-                                    // within the 48 KB of static shared memory)
-
-static_assert(kThreads == (1 << kThreadBits), "thread layout");
-
-struct RegGate {               // narrow fields: the records live in the kernel parameters
-    int8_t kin;               // 0 or 1 mixing operands
-    int8_t rb[kMaxRegKin];    // register bits of the mixing operands, descending (relabelled order)
-    int8_t kout;              // selector operands
-    int8_t osel[kMaxSel];     // 0: bit `opos` of the tile base; 1: thread bit at tile position opos;
-                              // 2: register bit opos (varies between register groups)
-    int8_t opos[kMaxSel];
-    int8_t rsel;              // any osel == 2
-    // fast-path classification (host): 0 generic, 1 dense 1-qubit (no selector),
-    // 2 diagonal with one selector
-    int8_t op;
-    // dense 1-qubit coefficient shape (host): 0 complex, 1 all entries real
-    // (RY, H), 2 real diagonal / imaginary off-diagonal (RX)
-    int8_t shape;
-    int8_t mpos[kMaxRegKin];  // generic phases: tile positions of the mixing bits (relabelled order)
-    int16_t coef_off;         // coef[coef_off + (b << 2kin) + r * 2^kin + c]   (pass-relative)
-    int16_t nz_off;           // nz[nz_off + (b << kin) + r]
-    int16_t cls_off;          // host classification table (identity / swap blocks)
-};
-
-// Affine relabelling of tile indices, f -> A f ^ c ^ (XOR of b_i over the set
-// full-state bits bbit_i): how a run of permutation gates (X, CX, SWAP, any
-// gate whose matrix is a 0/1 permutation affine in the index bits) moves
-// amplitudes.  Such runs are not executed: they are folded into the smem
-// slot each amplitude is written to (phase store / tile load).
-constexpr int kMaxPermBase = 8;
-
-struct Affine {
-    int8_t on;
-    int8_t nb;
-    uint16_t c;
-    uint16_t a[kMaxTileBits];    // image of tile bit j
-    int8_t bbit[kMaxPermBase];
-    uint16_t b[kMaxPermBase];
-};
-
-__host__ __device__ __forceinline__ uint32_t aff_lin(const Affine &m, uint32_t f, int T) {
-    uint32_t r = 0;
-    for (int j = 0; j < T; ++j)
-        if ((f >> j) & 1u) r ^= m.a[j];
-    return r;
-}
-
-__device__ __forceinline__ uint32_t aff_const(const Affine &m, uint64_t sbase) {
-    uint32_t r = m.c;
-    for (int i = 0; i < m.nb; ++i)
-        if ((sbase >> m.bbit[i]) & 1ull) r ^= m.b[i];
-    return r;
-}
-
-struct Phase {
-    int16_t g0, g1;           // gates [g0, g1) of the pass (pass-relative)
-    int8_t generic;           // 1: gates applied in shared memory (no register bits)
-    // sequence phase: its dense gates hit register bits 0, 1, ... in order
-    // (register bits in first-use order), any other gate is a diagonal on a
-    // non-register bit; nd_before[b] diagonals precede the dense gate on bit
-    // b (nd_before[R]: trailing).  The kernel then unrolls over the register
-    // bit, so every dense step has a compile-time pairing.
-    int8_t seq, ndense;
-    int8_t nd_before[5];
-    int8_t kind[5];           // sequence phase: 1 = dense 1-qubit gate on bit b, 2 = dense 2-qubit on (b, b+1)
-    int8_t rpos[4];           // tile positions of the register bits, ascending (R entries)
-    int8_t tpos[kMaxTileBits];  // tile positions of the thread bits, ascending (T - R entries)
-    Affine post;              // permutation run after the phase's gates, applied by its store
-    // swizzled smem slot of register j's part of the index (swz is linear
-    // over GF(2), and thread and register bits are disjoint): register j of
-    // a thread lives at swz(tpart) ^ pj[j]; its post-permutation slot at
-    // swz(A tpart ^ c) ^ ppj[j]
-    uint16_t pj[16];
-    uint16_t ppj[16];
-};
-
-// One pass = one launch; its whole gate program rides in the kernel
-// parameters (__grid_constant__, < 32 KB): every thread reads the same
-// phase / gate / coefficient at the same time, so these are uniform
-// constant-bank loads, not per-thread shared-memory traffic.
-struct TileParams {
-    double2 *x;
-    int64_t ntiles;
-    int tbits;                // T
-    int tb[kMaxTileBits];     // ascending state bits of the tile
-    int nphases;
-    int ngates;
-    int ncoef, nnz;
-    uint64_t gbase;           // sharded state: rank bits (rank << local_bits) for selector lookups
-    uint64_t tmask;           // state bits of the tile
-    uint64_t gstep;           // gridDim.x deposited into the non-tile bits (tile base stride)
-    Affine pre;               // permutation run opening the pass, applied by the tile load
-    double2 *y;               // destination (== x: in place)
-    int gperm;                // store through the global map (out of place)
-    int nbuf;                 // tile buffers in dynamic smem: 2 = prefetch the next tile during this one
-    uint64_t gconst;          // its constant, rank bits folded in
-    uint64_t gcol[64];        // image of local state bit j
-    Phase ph[kMaxPhases];
-    RegGate g[kMaxPassGates]; // pass-relative order
-    double2 coef[kMaxCoef];
-    uint32_t nz[kMaxNz];
-};
-static_assert(sizeof(TileParams) <= 32764, "kernel parameter space");
-
-// base of tile t + gridDim.x from the base of tile t: add in the number
-// system of the non-tile bits (tile bits forced to 1 carry straight through)
-__device__ __forceinline__ uint64_t next_base(uint64_t base, const TileParams &p) {
-    return ((base | p.tmask) + p.gstep) & ~p.tmask;
-}
-
-__host__ __device__ __forceinline__ uint32_t swz(uint32_t e) {
-    return e ^ (((e >> 3) ^ (e >> 6) ^ (e >> 9)) & 7u);
-}
-
-__device__ __forceinline__ uint64_t insert_zero_bits_dyn(uint64_t g, const int *sh, int k) {
-    for (int i = 0; i < k; ++i) {
-        const uint64_t low = g & ((1ull << sh[i]) - 1ull);
-        g = ((g >> sh[i]) << (sh[i] + 1)) | low;
-    }
-    return g;
-}
-
-template <int R>
-__device__ __forceinline__ uint32_t reg_spread(int j, const int8_t *rpos) {
-    uint32_t e = 0;
-#pragma unroll
-    for (int i = 0; i < R; ++i) e |= (uint32_t)((j >> i) & 1) << rpos[i];
-    return e;
-}
-
-// ---- fast paths (R = 3 register bits) --------------------------------------
-
-template <int R, int B1, int MODE>
-__device__ __forceinline__ void dense1(double2 (&v)[1 << R], const double2 *c, uint32_t n0, uint32_t n1) {
-    const double2 c00 = c[0], c01 = c[1], c10 = c[2], c11 = c[3];
-#pragma unroll
-    for (int g = 0; g < (1 << (R - 1)); ++g) {
-        const int j0 = ((g >> B1) << (B1 + 1)) | (g & ((1 << B1) - 1));
-        const int j1 = j0 | (1 << B1);
-        const double2 x0 = v[j0], x1 = v[j1];
-        // acc starts at +0; +0 + t == t except for the sign of an exact zero,
-        // so the first term is taken as is (values unchanged, one add saved)
-        double2 a0, a1;
-        if ((n0 & 3u) == 3u) a0 = cadd(cmul<MODE>(c00, x0), cmul<MODE>(c01, x1));
-        else if (n0 & 1u) a0 = cmul<MODE>(c00, x0);
-        else if (n0 & 2u) a0 = cmul<MODE>(c01, x1);
-        else a0 = make_double2(0.0, 0.0);
-        if ((n1 & 3u) == 3u) a1 = cadd(cmul<MODE>(c10, x0), cmul<MODE>(c11, x1));
-        else if (n1 & 1u) a1 = cmul<MODE>(c10, x0);
-        else if (n1 & 2u) a1 = cmul<MODE>(c11, x1);
-        else a1 = make_double2(0.0, 0.0);
-        v[j0] = a0;
-        v[j1] = a1;
-    }
-}
-
-// all four entries nonzero (RX, RY, H, U3 ...): branch-free, so the
-// compiler interleaves the 2^R independent multiply-add chains.
-// SHAPE 1 (every entry real) / 2 (real diagonal, imaginary off-diagonal):
-// an entry's zero part contributes an exact +-0 to each product, so
-//   (vr + 0i) x = (vr xr, vr xi),   (0 + vi i) x = (-(vi xi), vi xr)
-// in both numpy multiply forms (plain and FMA) up to the sign of an exact
-// zero -- 6 instead of 10 FP64 operations per amplitude, same values.
-template <int R, int B1, int MODE, int SHAPE = 0>
-__device__ __forceinline__ void dense1_full(double2 (&v)[1 << R], const double2 *c) {
-    const double2 c00 = c[0], c01 = c[1], c10 = c[2], c11 = c[3];
-#pragma unroll
-    for (int g = 0; g < (1 << (R - 1)); ++g) {
-        const int j0 = ((g >> B1) << (B1 + 1)) | (g & ((1 << B1) - 1));
-        const int j1 = j0 | (1 << B1);
-        const double2 x0 = v[j0], x1 = v[j1];
-        if constexpr (SHAPE == 1) {
-            v[j0] = cadd(cmul_re(c00.x, x0), cmul_re(c01.x, x1));
-            v[j1] = cadd(cmul_re(c10.x, x0), cmul_re(c11.x, x1));
-        } else if constexpr (SHAPE == 2) {
-            v[j0] = cadd(cmul_re(c00.x, x0), cmul_im(c01.y, x1));
-            v[j1] = cadd(cmul_im(c10.y, x0), cmul_re(c11.x, x1));
-        } else {
-            v[j0] = cadd(cmul<MODE>(c00, x0), cmul<MODE>(c01, x1));
-            v[j1] = cadd(cmul<MODE>(c10, x0), cmul<MODE>(c11, x1));
-        }
-    }
-}
-
-template <int R, int B1, int MODE>
-__device__ __forceinline__ void dense1_shaped(double2 (&v)[1 << R], const double2 *c, int shape) {
-    if (shape == 1) dense1_full<R, B1, MODE, 1>(v, c);
-    else if (shape == 2) dense1_full<R, B1, MODE, 2>(v, c);
-    else dense1_full<R, B1, MODE, 0>(v, c);
-}
-
-// dense two-qubit gate (all 16 entries nonzero) on register bits RA (its
-// gate-index MSB, the operand with the larger state bit) and RB: four
-// amplitude groups per 16 registers, ascending columns, first term as is
-template <int R, int RA, int RB, int MODE>
-__device__ __forceinline__ void dense2_full(double2 (&v)[1 << R], const double2 *c) {
-    constexpr int LO = RA < RB ? RA : RB, HI = RA < RB ? RB : RA;
-#pragma unroll
-    for (int g = 0; g < (1 << (R - 2)); ++g) {
-        int j0 = ((g >> LO) << (LO + 1)) | (g & ((1 << LO) - 1));
-        j0 = ((j0 >> HI) << (HI + 1)) | (j0 & ((1 << HI) - 1));
-        const int jq[4] = {j0, j0 | (1 << RB), j0 | (1 << RA), j0 | (1 << RA) | (1 << RB)};
-        const double2 x0 = v[jq[0]], x1 = v[jq[1]], x2 = v[jq[2]], x3 = v[jq[3]];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            double2 a = cmul<MODE>(c[r * 4], x0);
-            a = cadd(a, cmul<MODE>(c[r * 4 + 1], x1));
-            a = cadd(a, cmul<MODE>(c[r * 4 + 2], x2));
-            a = cadd(a, cmul<MODE>(c[r * 4 + 3], x3));
-            v[jq[r]] = a;
-        }
-    }
-}
-
-// Diagonal factors are applied branch-free: an entry whose nz bit is clear is
-// stored as exactly 0 + 0i, and 0 * x is the skipped term's +-0 (finite
-// states), so values are unchanged; a uniform branch here would make ptxas
-// copy the whole amplitude set at every iteration of the diagonal loops.
-template <int R, int RB, int MODE>
-__device__ __forceinline__ void diag_reg(double2 (&v)[1 << R], double2 d0, double2 d1) {
-#pragma unroll
-    for (int j = 0; j < (1 << R); ++j) v[j] = cmul<MODE>(((j >> RB) & 1) ? d1 : d0, v[j]);
-}
-
-
-
-// compile-time dispatch of a runtime register bit b in [0, R)
-#define DIAQ_RB_DISPATCH(R_, b_, CALL)                              \
-    do {                                                            \
-        if ((b_) == 0) { constexpr int RB_ = 0; CALL; }             \
-        else if ((b_) == 1) { constexpr int RB_ = 1; CALL; }        \
-        else if ((R_) == 3 || (b_) == 2) { constexpr int RB_ = 2; CALL; } \
-        else { constexpr int RB_ = (R_) >= 4 ? 3 : 2; CALL; }       \
-    } while (0)
-
-
-// the tile's full-state base lives in shared memory and is re-read where a
-// selector needs it (an asm load: not hoisted into a register held across
-// the gate loop, where it would push the fast paths into spills)
-__device__ __forceinline__ uint64_t ld_base(const uint64_t *s) {
-    uint64_t v;
-    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(smem_u32(s)));
-    return v;
-}
-
-// diagonal gate whose selector is a thread or base bit: one factor for all
-// of this thread's amplitudes
-template <int R, int MODE>
-__device__ __forceinline__ void diag_uniform(double2 (&v)[1 << R], const RegGate &G, uint32_t tpart,
-                                             const uint64_t *sbase_p, const double2 *sc, const uint32_t *snz) {
-    const uint32_t b = G.osel[0] == 0 ? (uint32_t)((ld_base(sbase_p) >> G.opos[0]) & 1ull) : (tpart >> G.opos[0]) & 1u;
-    const double2 d = sc[G.coef_off + (int)b];
-    (void)snz;
-#pragma unroll
-    for (int j = 0; j < (1 << R); ++j) v[j] = cmul<MODE>(d, v[j]);
-}
-
-template <int R, int MODE>
-__device__ __forceinline__ void dispatch_gate(double2 (&v)[1 << R], const RegGate &G, uint32_t tpart, const uint64_t *sbase_p,
-                                              const double2 *sc, const uint32_t *snz) {
-    // if-chains, not switches: a jump table would force v[] into local memory
-    static_assert(R == 3 || R == 4, "register fast paths cover 8 or 16 amplitudes per thread");
-    if (G.op == 1) {
-        const double2 *c = sc + G.coef_off;
-        const uint32_t n0 = snz[G.nz_off], n1 = snz[G.nz_off + 1];
-        if ((n0 & n1 & 3u) == 3u) DIAQ_RB_DISPATCH(R, G.rb[0], (dense1_shaped<R, RB_, MODE>(v, c, G.shape)));
-        else DIAQ_RB_DISPATCH(R, G.rb[0], (dense1<R, RB_, MODE>(v, c, n0, n1)));
-        return;
-    }
-    if (G.op == 2) {
-        const double2 d0 = sc[G.coef_off], d1 = sc[G.coef_off + 1];
-        if (G.osel[0] == 2) {
-            DIAQ_RB_DISPATCH(R, G.opos[0], (diag_reg<R, RB_, MODE>(v, d0, d1)));
-        } else {
-            const uint32_t b = G.osel[0] == 0 ? (uint32_t)((ld_base(sbase_p) >> G.opos[0]) & 1ull) : (tpart >> G.opos[0]) & 1u;
-            const double2 d = b ? d1 : d0;
-#pragma unroll
-            for (int j = 0; j < (1 << R); ++j) v[j] = cmul<MODE>(d, v[j]);
-        }
-        return;
-    }
-}
-
-// Generic gate (any selectors, <= 2 mixing bits) applied in the shared-memory
-// tile: the cold path for gates the register fast paths do not cover (and
-// dense two-qubit gates).  Same per-amplitude order as gate_kernel: ascending
-// relabelled column, from +0, exactly-zero entries skipped.
-template <int MODE>
-__device__ __forceinline__ void smem_gate(double2 *tile, int T, const RegGate &G, uint64_t base, const double2 *sc,
-                                          const uint32_t *snz) {
-    const int kin = G.kin;
-    const uint32_t ngroups = 1u << (T - kin);
-    const int p0 = G.mpos[0], p1 = G.mpos[1];
-    const int lo = p0 < p1 ? p0 : p1, hi = p0 < p1 ? p1 : p0;
-    for (uint32_t grp = threadIdx.x; grp < ngroups; grp += blockDim.x) {
-        uint32_t e0 = grp;
-        if (kin == 1) {
-            e0 = ((e0 >> p0) << (p0 + 1)) | (e0 & ((1u << p0) - 1u));
-        } else if (kin == 2) {
-            e0 = ((e0 >> lo) << (lo + 1)) | (e0 & ((1u << lo) - 1u));
-            e0 = ((e0 >> hi) << (hi + 1)) | (e0 & ((1u << hi) - 1u));
-        }
-        uint32_t b = 0;
-        for (int s = 0; s < G.kout; ++s) {
-            const uint32_t bit = G.osel[s] ? (e0 >> G.opos[s]) & 1u : (uint32_t)((base >> G.opos[s]) & 1ull);
-            b |= bit << (G.kout - 1 - s);
-        }
-        const double2 *c = sc + G.coef_off + ((int)b << (2 * kin));
-        const uint32_t *nz = snz + G.nz_off + ((int)b << kin);
-        if (kin == 0) {
-            const uint32_t i0 = swz(e0);
-            tile[i0] = (nz[0] & 1u) ? cadd(make_double2(0.0, 0.0), cmul<MODE>(c[0], tile[i0])) : make_double2(0.0, 0.0);
-        } else if (kin == 1) {
-            const uint32_t i0 = swz(e0), i1 = swz(e0 | (1u << p0));
-            const double2 x0 = tile[i0], x1 = tile[i1];
-            double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
-            if (nz[0] & 1u) a0 = cadd(a0, cmul<MODE>(c[0], x0));
-            if (nz[0] & 2u) a0 = cadd(a0, cmul<MODE>(c[1], x1));
-            if (nz[1] & 1u) a1 = cadd(a1, cmul<MODE>(c[2], x0));
-            if (nz[1] & 2u) a1 = cadd(a1, cmul<MODE>(c[3], x1));
-            tile[i0] = a0;
-            tile[i1] = a1;
-        } else {
-            uint32_t idx[4];
-            double2 x[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {  // gate column q = (bit at p0, bit at p1)
-                idx[q] = swz(e0 | ((uint32_t)(q >> 1) << p0) | ((uint32_t)(q & 1) << p1));
-                x[q] = tile[idx[q]];
-            }
-            if ((nz[0] & nz[1] & nz[2] & nz[3] & 15u) == 15u) {  // dense (Haar4 ...): branch-free
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    double2 a = cadd(make_double2(0.0, 0.0), cmul<MODE>(c[r * 4], x[0]));
-#pragma unroll
-                    for (int q = 1; q < 4; ++q) a = cadd(a, cmul<MODE>(c[r * 4 + q], x[q]));
-                    tile[idx[r]] = a;
-                }
-            } else {
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    double2 a = make_double2(0.0, 0.0);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        if ((nz[r] >> q) & 1u) a = cadd(a, cmul<MODE>(c[r * 4 + q], x[q]));
-                    tile[idx[r]] = a;
-                }
-            }
-        }
-    }
-}
-
-// sequence phase, register bit RB onwards: the diagonals before the dense
-// gate on RB, then that gate with its pairing fixed at compile time
-template <int R, int MODE, int RB>
-__device__ __forceinline__ void seq_steps(double2 (&v)[1 << R], const TileParams &p, const Phase &ph, int &gi,
-                                          uint32_t tpart, const uint64_t *sbase_p, const double2 *sc,
-                                          const uint32_t *snz) {
-    // unrolled by 2: a complex multiply cannot land in its input registers
-    // (both parts read both inputs), so a rolled loop pays a register copy of
-    // the amplitude set per gate to return to the loop-carried assignment
-#pragma unroll 2
-    for (int c = 0; c < ph.nd_before[RB]; ++c, ++gi) diag_uniform<R, MODE>(v, p.g[gi], tpart, sbase_p, sc, snz);
-    if (ph.kind[RB] == 1) {
-        dense1_shaped<R, RB, MODE>(v, sc + p.g[gi].coef_off, p.g[gi].shape);
-        ++gi;
-        if constexpr (RB + 1 < R) seq_steps<R, MODE, RB + 1>(v, p, ph, gi, tpart, sbase_p, sc, snz);
-    } else if (ph.kind[RB] == 2) {
-        if constexpr (RB + 1 < R) {
-            dense2_full<R, RB, RB + 1, MODE>(v, sc + p.g[gi].coef_off);
-            ++gi;
-            if constexpr (RB + 2 < R) seq_steps<R, MODE, RB + 2>(v, p, ph, gi, tpart, sbase_p, sc, snz);
-        }
-    }
-}
-
 template <int R, int MODE>
 __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(const __grid_constant__ TileParams p) {
-    // dynamic smem: nbuf tiles, then the row-offset table, then (gperm) the
-    // global-map table -- sized by T, so small tiles leave room for 3 CTAs
-    extern __shared__ double2 tile[];
-    const int T = p.tbits;
-    const uint32_t tsize = 1u << T;
-    uint64_t *hi_off = (uint64_t *)(tile + ((size_t)p.nbuf << T));
-    uint64_t *s_ghi = hi_off + (tsize >> kLowBits);  // global map of each tile row offset
-    // per-(phase, thread) index part of the thread bits, computed once per
-    // CTA instead of once per tile (register parts ride in the phase record)
-    constexpr int kPre = kPrePhases;
-    __shared__ uint16_t s_tpart[kPre][kThreads];
-    __shared__ uint16_t s_pt[kPre][kThreads];  // folded permutations: swizzled image of the thread part
-    __shared__ uint16_t s_lt[kThreads];
-    __shared__ uint16_t s_lk[1 << (kMaxTileBits - kThreadBits)];
-    __shared__ uint64_t s_sbase;  // current tile's base | rank bits (selector lookups)
-    constexpr int NR = 1 << R;
-    const double2 *sc = p.coef;
-    const uint32_t *snz = p.nz;
-    // tile element e -> state offset: low kLowBits tile bits are state bits 0..2
-    for (uint32_t h = threadIdx.x; h < (tsize >> kLowBits); h += blockDim.x) {
-        uint64_t off = 0;
-        for (int j = kLowBits; j < T; ++j) off |= (uint64_t)((h >> (j - kLowBits)) & 1u) << p.tb[j];
-        hi_off[h] = off;
-    }
-    __syncthreads();
-    constexpr uint32_t lowmask = (1u << kLowBits) - 1u;
-    const int per_thread = (int)(tsize >> kThreadBits);
-    const int npre = p.nphases < kPre ? p.nphases : kPre;
-    for (int ph_i = 0; ph_i < npre; ++ph_i) {
-        const Phase &ph = p.ph[ph_i];
-        uint32_t tpart = 0;
-        for (int i = 0; i < T - R; ++i) tpart |= ((threadIdx.x >> i) & 1u) << ph.tpos[i];
-        s_tpart[ph_i][threadIdx.x] = (uint16_t)tpart;
-        if (ph.post.on) s_pt[ph_i][threadIdx.x] = (uint16_t)swz(aff_lin(ph.post, tpart, T));
-    }
-    if (p.pre.on) {
-        s_lt[threadIdx.x] = (uint16_t)swz(aff_lin(p.pre, threadIdx.x, T));
-        if (threadIdx.x < (tsize >> kThreadBits)) s_lk[threadIdx.x] = (uint16_t)swz(aff_lin(p.pre, threadIdx.x << kThreadBits, T));
-    }
-    __shared__ uint64_t glo[1 << kLowBits];  // global map of the in-row offsets
-    if (p.gperm) {
-        for (uint32_t h = threadIdx.x; h < (tsize >> kLowBits); h += blockDim.x) {
-            uint64_t o = hi_off[h], r = 0;
-            while (o) {
-                r ^= p.gcol[__ffsll((long long)o) - 1];
-                o &= o - 1;
-            }
-            s_ghi[h] = r;
-        }
-        if (threadIdx.x < (1u << kLowBits)) {
-            uint64_t r = 0;
-            for (int b = 0; b < kLowBits; ++b)
-                if ((threadIdx.x >> b) & 1u) r ^= p.gcol[b];
-            glo[threadIdx.x] = r;
-        }
-    }
-    // HBM -> smem with cp.async, coalesced (consecutive e are consecutive
-    // state indices in runs of 8); every element of the tile in flight at once
-    auto fetch = [&](uint64_t b, double2 *buf) {
-        const uint64_t pol = policy_evict_first();
-        if (p.pre.on) {  // element e lands in the slot of its relabelled index
-            const uint32_t lt = s_lt[threadIdx.x] ^ swz(aff_const(p.pre, b | p.gbase));
-            for (int k = 0; k < per_thread; ++k) {
-                const uint32_t e = threadIdx.x + (uint32_t)k * kThreads;
-                cp_async16(buf + (lt ^ s_lk[k]), p.x + b + (e & lowmask) + hi_off[e >> kLowBits], pol);
-            }
-        } else {
-            for (int k = 0; k < per_thread; ++k) {
-                const uint32_t e = threadIdx.x + (uint32_t)k * kThreads;
-                cp_async16(buf + swz(e), p.x + b + (e & lowmask) + hi_off[e >> kLowBits], pol);
-            }
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    __syncthreads();
-    // nbuf 2: the next tile streams into the other buffer while this one is
-    // computed (its latency hidden inside the CTA); nbuf 1: refill after the
-    // store, latency hidden only by the other resident CTAs
-    uint64_t base = insert_zero_bits_dyn((uint64_t)blockIdx.x, p.tb, T);
-    if ((int64_t)blockIdx.x < p.ntiles) fetch(base, tile);
-    int buf = 0;
-    for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-        const uint64_t nbase = next_base(base, p);
-        const bool more = t + gridDim.x < p.ntiles;
-        double2 *tl = tile + ((size_t)buf << T);
-        if (threadIdx.x == 0) s_sbase = base | p.gbase;  // full-state index bits for selectors
-        if (p.nbuf == 2 && more) {
-            fetch(nbase, tile + ((size_t)(buf ^ 1) << T));
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-        } else {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-        }
-        __syncthreads();
-        for (int ph_i = 0; ph_i < p.nphases; ++ph_i) {
-            const Phase &ph = p.ph[ph_i];
-            if (ph.generic) {
-                for (int gi = ph.g0; gi < ph.g1; ++gi) {
-                    smem_gate<MODE>(tl, T, p.g[gi], ld_base(&s_sbase), sc, snz);
-                    __syncthreads();
-                }
-                continue;
-            }
-            double2 v[NR];
-            uint32_t tpart;
-            if (ph_i < kPre) {
-                tpart = s_tpart[ph_i][threadIdx.x];
-            } else {
-                tpart = 0;
-                for (int i = 0; i < T - R; ++i) tpart |= ((threadIdx.x >> i) & 1u) << ph.tpos[i];
-            }
-            const uint32_t tsw = swz(tpart);
-#pragma unroll
-            for (int j = 0; j < NR; ++j) v[j] = tl[tsw ^ ph.pj[j]];
-            if (ph.seq) {
-                int gi = ph.g0;
-                seq_steps<R, MODE, 0>(v, p, ph, gi, tpart, &s_sbase, sc, snz);
-#pragma unroll 2
-                for (int c = 0; c < ph.nd_before[R]; ++c, ++gi) diag_uniform<R, MODE>(v, p.g[gi], tpart, &s_sbase, sc, snz);
-            } else {
-                for (int gi = ph.g0; gi < ph.g1; ++gi) dispatch_gate<R, MODE>(v, p.g[gi], tpart, &s_sbase, sc, snz);
-            }
-            if (ph.post.on) {
-                __syncthreads();  // relabelled slots belong to other threads' registers: all reads first
-                const uint32_t bc = swz(aff_const(ph.post, ld_base(&s_sbase)));
-                const uint32_t pt = (ph_i < kPre ? (uint32_t)s_pt[ph_i][threadIdx.x] : swz(aff_lin(ph.post, tpart, T))) ^ bc;
-#pragma unroll
-                for (int j = 0; j < NR; ++j) tl[pt ^ ph.ppj[j]] = v[j];
-            } else {
-#pragma unroll
-                for (int j = 0; j < NR; ++j) tl[tsw ^ ph.pj[j]] = v[j];
-            }
-            __syncthreads();
-        }
-        if (p.gperm) {  // trailing permutation run: element i goes to A i ^ c in the other buffer
-            uint64_t ab = p.gconst, o = base;
-            while (o) {
-                ab ^= p.gcol[__ffsll((long long)o) - 1];
-                o &= o - 1;
-            }
-            for (int k = 0; k < per_thread; ++k) {
-                const uint32_t e = threadIdx.x + (uint32_t)k * kThreads;
-                st_stream(p.y + (ab ^ s_ghi[e >> kLowBits] ^ glo[e & lowmask]), tl[swz(e)]);
-            }
-        } else {
-            for (int k = 0; k < per_thread; ++k) {
-                const uint32_t e = threadIdx.x + (uint32_t)k * kThreads;
-                st_stream(p.y + base + (e & lowmask) + hi_off[e >> kLowBits], tl[swz(e)]);
-            }
-        }
-        __syncthreads();
-        base = nbase;
-        if (p.nbuf == 2) buf ^= 1;
-        else if (more) fetch(base, tile);  // refill as soon as the tile is drained
-    }
+    tile_pass_body<R, MODE>(p, p);
 }
 
 // ---- host: analysis, scheduling, packing ------------------------------------
@@ -1306,6 +769,18 @@ struct Program {
     std::vector<char> key;
     std::vector<PassPlan> plan;
     std::vector<TileParams> params;  // per tiled pass (x, gbase and the grid are filled in at launch)
+    // specialised kernels of the tiled passes (fused_jit.cu), per cmul mode:
+    // looked up once per program, then read on every call
+    mutable std::mutex jit_mu;
+    mutable std::vector<std::shared_ptr<JitPass>> jit[2];
+    mutable bool jit_requested[2] = {false, false};
+
+    std::vector<const TileParams *> tiled() const {
+        std::vector<const TileParams *> v(plan.size(), nullptr);
+        for (size_t i = 0; i < plan.size(); ++i)
+            if (!(plan[i].bits.empty() || plan[i].members.size() == 1)) v[i] = &params[i];
+        return v;
+    }
 };
 
 static void debug_plan(const std::vector<PassPlan> &plan) {
@@ -1462,6 +937,18 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
     const int R = T - kThreadBits;
     const std::vector<PassPlan> &plan = prog->plan;
     if (npasses) *npasses = (int)plan.size();
+    // specialised kernels: requested once per (program, mode); passes whose
+    // kernel is not compiled yet run the AOT interpreter (bitwise the same)
+    std::vector<std::shared_ptr<JitPass>> jit;
+    const int jit_knob = tuning().fused_jit;
+    if (jit_knob != 0 && (cmul_mode == 0 || cmul_mode == 1)) {
+        std::lock_guard<std::mutex> lk(prog->jit_mu);
+        if (!prog->jit_requested[cmul_mode]) {
+            jit_request(prog->tiled(), R, cmul_mode, jit_knob == 2, prog->jit[cmul_mode]);
+            prog->jit_requested[cmul_mode] = true;
+        }
+        jit = prog->jit[cmul_mode];
+    }
     const size_t smem_max = 2 * (sizeof(double2) << kMaxTileBits) + 2 * (sizeof(uint64_t) << (kMaxTileBits - kLowBits));
     static bool attr_set[64] = {false};  // per device (one process may drive several)
     int cur_dev = 0;
@@ -1538,6 +1025,12 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
             auto smem_for = [&](int nb) {
                 return ((sizeof(double2) * nb) << p.tbits) + ((sizeof(uint64_t) * (p.gperm ? 2 : 1)) << (p.tbits - kLowBits));
             };
+            if (pi < jit.size() && jit[pi] &&
+                jit_launch(jit[pi], p, R, smem_for(1), smem_for(2), tuning().fused_nbuf, s, rc)) {
+                if (events && rc == DIAQ_OK) cudaEventRecord((cudaEvent_t)events[ps.members.back() + 1], s);
+                cur = nxt;
+                continue;
+            }
             // two tile buffers (prefetch) unless that costs a resident CTA
             const int knob = tuning().fused_nbuf;
             int per_sm = occupancy(f, kThreads, smem_for(1));
@@ -1550,6 +1043,7 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
                 }
             }
             const size_t smem = smem_for(p.nbuf);
+            p.gstore = tuning().fused_gstore;
             const int64_t grid =
                 std::max<int64_t>(1, std::min<int64_t>(p.ntiles, (int64_t)sm_count() * std::max(1, per_sm)));
             p.gstep = 0;  // deposit grid into the non-tile bits, low to high
@@ -1614,6 +1108,28 @@ extern "C" int diaq_fused_plan(int n_bits, int local_bits, int ngates, const dia
         for (const Phase &ph : ps.phases) stats[4] += ph.generic;
     }
     return DIAQ_OK;
+}
+
+// Host-only: schedule the program and compile its specialised passes now
+// (NVRTC, no device); *seconds the compile time, *kernels the pass count.
+extern "C" int diaq_fused_jit_compile(int n_bits, int local_bits, int ngates, const diaq_gate_t *gates, int tile_bits,
+                                      int cmul_mode, double *seconds, int *kernels) {
+    if (ngates < 0 || (ngates > 0 && !gates) || !kernels)
+        return set_error(DIAQ_ERR_VALUE, "diaq_fused_jit_compile: bad arguments");
+    if (local_bits < 1 || local_bits > n_bits) return set_error(DIAQ_ERR_SHAPE, "local_bits %d invalid", local_bits);
+    if (cmul_mode != 0 && cmul_mode != 1) return set_error(DIAQ_ERR_VALUE, "cmul_mode %d", cmul_mode);
+    const int T = tile_bits >= kThreadBits + 4 ? kThreadBits + 4 : kThreadBits + 3;
+    int rc = DIAQ_OK;
+    std::shared_ptr<const Program> prog = build_program(n_bits, local_bits, T, ngates, gates, rc);
+    if (!prog) return rc;
+    if (!seconds) {  // submit to the background compile queue (as a first run_gates call would)
+        std::vector<std::shared_ptr<JitPass>> out;
+        jit_request(prog->tiled(), T - kThreadBits, cmul_mode, false, out);
+        *kernels = 0;
+        for (auto &e : out) *kernels += e ? 1 : 0;
+        return DIAQ_OK;
+    }
+    return jit_compile_now(prog->tiled(), T - kThreadBits, cmul_mode, *seconds, *kernels);
 }
 
 extern "C" int diaq_run_gates_local(int n_bits, int local_bits, int64_t rank, int ngates, const diaq_gate_t *gates,

@@ -13,6 +13,7 @@ import os
 import numpy as np
 import pytest
 
+from _circuits import fuzz_circuit
 import paper_2405_01250_b200 as D
 from conftest import GOLDEN, dense_from_pairs, digest, pairs_to_complex, rel_l2
 from oracle import oracle as O
@@ -632,35 +633,7 @@ def test_fused_scheduler_fuzz(cmul, seed):
     CCX, dense and controlled two-qubit gates), fused at every tile setting
     and with every scheduling switch, bitwise against gate by gate."""
     from paper_2405_01250_b200 import _lib as L
-    rng = np.random.default_rng(1000 + seed)
-    n = int(rng.integers(11, 19))
-    names1 = ["h", "x", "y", "z", "s", "t", "rx", "ry", "rz", "u3", "sdg"]
-    pls = []
-    for _ in range(int(rng.integers(40, 90))):
-        kind = rng.integers(8)
-        q = [int(v) for v in rng.choice(n, size=3, replace=False)]
-        if kind <= 2:
-            nm = names1[int(rng.integers(len(names1)))]
-            par = {"rx": (0.7,), "ry": (1.1,), "rz": (2.3,), "u3": (0.1, 0.2, 0.3)}.get(nm, ())
-            ops = [(nm, (q[0],), par)]
-        elif kind == 3:
-            ops = [("cx", (q[0], q[1]), ()), ("cx", (q[1], q[2]), ()), ("swap", (q[0], q[2]), ())]
-        elif kind == 4:
-            ops = [("cz", (q[0], q[1]), ()), ("ccx", (q[0], q[1], q[2]), ())]
-        else:
-            ops = []
-            if kind == 5:
-                g, qs = W.haar(rng, 4), [q[0], q[1]]
-            elif kind == 6:
-                g = np.eye(8, dtype=complex)
-                g[4:, 4:] = W.haar(rng, 4)
-                qs = q
-            else:
-                g, qs = _perm_gate([2, 0, 3, 1]), [q[0], q[1]]
-            lo, hi = min(qs), max(qs)
-            pls.append(D.Placement(2**lo, None, 2 ** (n - 1 - hi), lo, hi, "u", gate=(g, [v - lo for v in qs])))
-        if ops:
-            pls += D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
+    n, pls, rng = fuzz_circuit(seed)
     x0 = D.StateVector(n, W.random_state(rng, 2**n))
     want = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=0).amps
     switches = [{}, {"fused_seq": 0}, {"fused_gperm": 0}, {"fused_dense2": 0}, {"fused_perm": 0},
@@ -678,3 +651,50 @@ def test_fused_scheduler_fuzz(cmul, seed):
         for k, v in (("fused_seq", 1), ("fused_gperm", 1), ("fused_dense2", 1), ("fused_perm", 1),
                      ("fused_gperm_rows", 0)):
             L.tune(k, v)
+
+
+def _jit_stats():
+    import ctypes
+    st = (ctypes.c_int64 * 6)()
+    L.call("diaq_jit_stats", ctypes.addressof(st))
+    return dict(zip(["compiled", "failed", "launches", "modules", "pending", "compile_ms"], list(st)))
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_fused_jit_matches_interpreter(cmul, seed):
+    """Runtime-specialised passes (NVRTC, structure constant) against the AOT
+    interpreter kernel and gate by gate: bitwise, and the specialised kernels
+    are the ones that ran (no compile failures, launches counted)."""
+    n, pls, rng = fuzz_circuit(seed)
+    x0 = D.StateVector(n, W.random_state(rng, 2**n))
+    want = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=0).amps
+    try:
+        for tb in (11, 12):
+            L.tune("fused_jit", 0)
+            aot = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=tb).amps
+            L.tune("fused_jit", 2)
+            before = _jit_stats()
+            got = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=tb).amps
+            after = _jit_stats()
+            assert np.array_equal(got, want) and np.array_equal(aot, want), (seed, n, tb)
+            assert after["failed"] == 0, L.load().diaq_jit_last_error()
+            assert after["launches"] > before["launches"], (before, after)
+    finally:
+        L.tune("fused_jit", 1)
+
+
+def test_fused_jit_layer_n24_async(cmul):
+    """The default (asynchronous) mode: the first calls run the AOT kernel
+    while the passes compile, later calls the specialised kernels -- the
+    state is bitwise the same either way."""
+    n = 24
+    ops = W.random_layered_ops(n, 2, seed=5)
+    pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
+    x0 = D.init_state(n)
+    want = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=0).amps
+    first = D.run_gates(x0, pls, cmul_mode=cmul).amps
+    L.call("diaq_jit_wait", -1.0)
+    before = _jit_stats()
+    second = D.run_gates(x0, pls, cmul_mode=cmul).amps
+    assert _jit_stats()["launches"] > before["launches"]
+    assert np.array_equal(first, want) and np.array_equal(second, want)
