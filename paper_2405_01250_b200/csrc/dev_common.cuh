@@ -85,6 +85,11 @@ __device__ __forceinline__ void cp_async16(void *dst, const void *src, uint64_t 
                  : "memory");
 }
 
+// same, without an L2 policy operand
+__device__ __forceinline__ void cp_async16_nohint(void *dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
 // 256-bit streaming store of two adjacent elements (p must be 32-byte aligned)
 __device__ __forceinline__ void st_stream2(double2 *p, double2 a, double2 b) {
     asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y)
@@ -97,6 +102,22 @@ __device__ __forceinline__ void st_hint(double2 *p, double2 v, uint64_t pol) {
 
 __device__ __forceinline__ void st_plain(double2 *p, double2 v) {
     asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+
+// ---- thread-block clusters (distributed shared memory) ---------------------
+
+// all threads of all CTAs of the cluster; release/acquire on shared::cluster
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+
+// 16-byte load from CTA `rank`'s shared memory at this CTA's offset `local`
+__device__ __forceinline__ double2 ld_dsmem(uint32_t local, uint32_t rank) {
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local), "r"(rank));
+    double2 v;
+    asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(ra) : "memory");
+    return v;
 }
 
 // ---- exact-rounding complex arithmetic ------------------------------------

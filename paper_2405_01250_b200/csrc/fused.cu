@@ -804,9 +804,9 @@ static std::vector<char> program_key(int n_total, int n_bits, int T, int ngates,
         key.insert(key.end(), c, c + n);
     };
     // every tuning switch the schedule depends on is part of the key
-    const int head[9] = {n_total, n_bits, T, ngates, tuning().fused_perm,
-                         tuning().fused_gperm && !t_no_gperm, tuning().fused_seq, tuning().fused_dense2,
-                         tuning().fused_gperm_rows};
+    const int head[10] = {n_total, n_bits, T, ngates, tuning().fused_perm,
+                          tuning().fused_gperm && !t_no_gperm, tuning().fused_seq, tuning().fused_dense2,
+                          tuning().fused_gperm_rows, tuning().fused_pair_store};
     put(head, sizeof(head));
     for (int i = 0; i < ngates; ++i) {
         const diaq_gate_t &gt = gates[i];
@@ -816,6 +816,100 @@ static std::vector<char> program_key(int n_total, int n_bits, int T, int ngates,
         put(gt.g, sizeof(double) * 2 * ((size_t)1 << (2 * gt.k)));
     }
     return key;
+}
+
+// Linear algebra over GF(2) on 64-bit vectors: span membership and
+// solutions of A x = v for A given by its columns.
+struct Gf2 {
+    std::vector<std::pair<uint64_t, uint64_t>> rows;  // (reduced vector, combination of inputs), distinct top bits
+    // reduce v against the rows (highest pivots first); c tracks the combination
+    void reduce(uint64_t &v, uint64_t &c) const {
+        for (const auto &r : rows)
+            if (v & (1ull << (63 - __builtin_clzll(r.first)))) {
+                v ^= r.first;
+                c ^= r.second;
+            }
+    }
+    bool add(uint64_t v, uint64_t tag) {  // false if v is in the span already
+        uint64_t c = tag;
+        reduce(v, c);
+        if (!v) return false;
+        rows.emplace_back(v, c);
+        std::sort(rows.begin(), rows.end(), [](const auto &a, const auto &b) { return a.first > b.first; });
+        // keep the rows fully reduced against each other's pivots (a new pivot
+        // may sit inside an older row)
+        for (size_t i = 0; i < rows.size(); ++i)
+            for (size_t j = 0; j < rows.size(); ++j)
+                if (i != j && (rows[j].first & (1ull << (63 - __builtin_clzll(rows[i].first))))) {
+                    rows[j].first ^= rows[i].first;
+                    rows[j].second ^= rows[i].second;
+                }
+        std::sort(rows.begin(), rows.end(), [](const auto &a, const auto &b) { return a.first > b.first; });
+        return true;
+    }
+    bool solve(uint64_t v, uint64_t &x) const {
+        uint64_t c = 0;
+        reduce(v, c);
+        x = c;
+        return v == 0;
+    }
+};
+
+// Pair store of a pass's global tail (TileParams::gnp): the extra bit G
+// whose tiles must be stored together so every 32-byte destination sector
+// (rows, when cheap) is written whole by one CTA.  gcol = A's columns.
+static void plan_pair_store(const PassPlan &ps, int n_bits, TileParams &p) {
+    p.gnp = 0;
+    if (!ps.gon || n_bits > 63) return;
+    Gf2 a;
+    for (int j = 0; j < n_bits; ++j) a.add(ps.gcol[(size_t)j], 1ull << j);
+    if ((int)a.rows.size() != n_bits) return;  // not invertible (cannot happen for permutations)
+    uint64_t tmask = 0;
+    for (int b : ps.bits) tmask |= 1ull << b;
+    uint64_t x[3];
+    for (int j = 0; j < 3; ++j)
+        if (!a.solve(1ull << j, x[j])) return;
+    uint64_t G = (x[0] | x[1] | x[2]) & ~tmask;         // whole rows
+    if (__builtin_popcountll(G) > 1) G = x[0] & ~tmask;  // whole sectors
+    if (__builtin_popcountll(G) != 1) return;           // rows whole already / a pair does not close them
+    const int T = (int)ps.bits.size();
+    p.gnp = (int8_t)__builtin_popcountll(G);
+    for (int k = 0, b = 0; b < 64; ++b)
+        if ((G >> b) & 1ull) p.gpb[k++] = (int8_t)b;
+    p.emask = tmask | G;
+    for (int k = 0, b = 0; b < 64; ++b)
+        if ((p.emask >> b) & 1ull) p.eb[k++] = (int8_t)b;
+    // destination basis: e0 (e1, e2 when in the span) first, then images of the group bits
+    Gf2 span, basis;
+    std::vector<int> gbits;
+    for (int b = 0; b < 64; ++b)
+        if ((p.emask >> b) & 1ull) gbits.push_back(b);
+    for (int b : gbits) span.add(ps.gcol[(size_t)b], 0);
+    std::vector<uint64_t> w;
+    for (int j = 0; j < 3; ++j) {
+        uint64_t dummy;
+        if (span.solve(1ull << j, dummy) && basis.add(1ull << j, 0)) w.push_back(1ull << j);
+    }
+    for (int b : gbits)
+        if ((int)w.size() < T + p.gnp && basis.add(ps.gcol[(size_t)b], 0)) w.push_back(ps.gcol[(size_t)b]);
+    if ((int)w.size() != T + p.gnp) {
+        p.gnp = 0;
+        return;
+    }
+    for (int k = 0; k < T + p.gnp; ++k) {
+        uint64_t src;
+        if (!a.solve(w[(size_t)k], src) || (src & ~p.emask)) {
+            p.gnp = 0;
+            return;
+        }
+        uint32_t off = 0, rank = 0;
+        for (int j = 0; j < T; ++j)
+            if ((src >> ps.bits[(size_t)j]) & 1ull) off |= 1u << j;
+        for (int j = 0; j < p.gnp; ++j)
+            if ((src >> p.gpb[j]) & 1ull) rank |= 1u << j;
+        p.gw[k] = w[(size_t)k];
+        p.gsrc[k] = (uint16_t)(off | (rank << 12));
+    }
 }
 
 static std::shared_ptr<const Program> build_program(int n_total, int n_bits, int T, int ngates, const diaq_gate_t *gates,
@@ -859,6 +953,7 @@ static std::shared_ptr<const Program> build_program(int n_total, int n_bits, int
         if (ps.gon) {
             for (size_t j = 0; j < ps.gcol.size() && j < 64; ++j) p.gcol[j] = ps.gcol[j];
             p.gconst = ps.gc;  // rank bits folded in at launch
+            if (tuning().fused_pair_store) plan_pair_store(ps, n_bits, p);
         }
         std::copy(ps.phases.begin(), ps.phases.end(), p.ph);
         std::copy(ps.gates.begin(), ps.gates.end(), p.g);

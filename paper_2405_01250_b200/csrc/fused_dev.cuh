@@ -130,6 +130,20 @@ struct TileParams {
     int gstore;               // global-map store: 0 streaming (.cs), 1 write-back default, 2 L2 evict_last
     uint64_t gconst;          // its constant, rank bits folded in
     uint64_t gcol[64];        // image of local state bit j
+    // Pair store of a global tail that splits 32-byte sectors (specialised
+    // passes only): a tile and its partner across the extra state bit gpb[0]
+    // run in one CTA, which writes whole destination sectors (rows, when the
+    // map allows) gathered from both -- no partial-sector writes (DRAM
+    // read-modify-write).  Pairs enumerate over eb[] (tile bits and gpb[0],
+    // ascending; emask); the destination set of a pair is ab ^ span(gw[]),
+    // gw[0..] = e0 (e1, e2) first, and gsrc[k] = tile offset | (half << 12)
+    // of gw[k]'s source.  gnp = 0: per-element scatter store.
+    int8_t gnp;
+    int8_t gpb[3];
+    int8_t eb[kMaxTileBits + 3];
+    uint64_t emask;
+    uint64_t gw[kMaxTileBits + 3];
+    uint16_t gsrc[kMaxTileBits + 3];
     Phase ph[kMaxPhases];
     RegGate g[kMaxPassGates]; // pass-relative order
     double2 coef[kMaxCoef];
@@ -147,7 +161,8 @@ __host__ __device__ __forceinline__ uint32_t swz(uint32_t e) {
     return e ^ (((e >> 3) ^ (e >> 6) ^ (e >> 9)) & 7u);
 }
 
-__device__ __forceinline__ uint64_t insert_zero_bits_dyn(uint64_t g, const int *sh, int k) {
+template <class I>
+__device__ __forceinline__ uint64_t insert_zero_bits_dyn(uint64_t g, const I *sh, int k) {
     DIAQ_SUNROLL
     for (int i = 0; i < k; ++i) {
         const uint64_t low = g & ((1ull << sh[i]) - 1ull);
@@ -470,7 +485,39 @@ __device__ __forceinline__ void tile_pass_body(const TileParams &p, const TilePa
         if (threadIdx.x < (tsize >> kThreadBits)) s_lk[threadIdx.x] = (uint16_t)swz(aff_lin(S.pre, threadIdx.x << kThreadBits, T));
     }
     __shared__ uint64_t glo[1 << kLowBits];  // global map of the in-row offsets
-    if (S.gperm) {
+#ifdef DIAQ_JIT
+    // pair store (see TileParams::gnp): destination offsets / sources of the
+    // high enumeration bits (uniform table) and of this thread's low bits
+    const bool pairing = S.gnp > 0;
+    __shared__ uint64_t s_pw[1 << (kMaxTileBits + 1 - kThreadBits)];
+    __shared__ uint16_t s_ps[1 << (kMaxTileBits + 1 - kThreadBits)];
+    uint64_t pw_t = 0;
+    uint32_t ps_t = 0;
+    if (pairing) {
+        const int dims = T + S.gnp;
+        DIAQ_SUNROLL
+        for (int k = 0; k < kThreadBits; ++k)
+            if ((threadIdx.x >> k) & 1u) {
+                pw_t ^= S.gw[k];
+                ps_t ^= S.gsrc[k];
+            }
+        if (threadIdx.x < (1u << (dims - kThreadBits))) {
+            uint64_t w = 0;
+            uint32_t sr = 0;
+            DIAQ_SUNROLL
+            for (int k = kThreadBits; k < dims; ++k)
+                if ((threadIdx.x >> (k - kThreadBits)) & 1u) {
+                    w ^= S.gw[k];
+                    sr ^= S.gsrc[k];
+                }
+            s_pw[threadIdx.x] = w;
+            s_ps[threadIdx.x] = (uint16_t)sr;
+        }
+    }
+#else
+    constexpr bool pairing = false;
+#endif
+    if (S.gperm && !pairing) {
         for (uint32_t h = threadIdx.x; h < (tsize >> kLowBits); h += blockDim.x) {
             uint64_t o = hi_off[h], r = 0;
             while (o) {
@@ -495,7 +542,14 @@ __device__ __forceinline__ void tile_pass_body(const TileParams &p, const TilePa
         #pragma unroll 1
             for (int k = 0; k < NR; ++k) {
                 const uint32_t e = threadIdx.x + (uint32_t)k * kThreads;
+#ifdef DIAQ_JIT
+                // (ptxas 12.9 emitted a malformed LDGSTS for the policy form of
+                // this permuted-slot copy in specialised kernels: illegal
+                // instruction at run time; the plain form is used here)
+                cp_async16_nohint(buf + (lt ^ s_lk[k]), p.x + b + (e & lowmask) + hi_off[e >> kLowBits]);
+#else
                 cp_async16(buf + (lt ^ s_lk[k]), p.x + b + (e & lowmask) + hi_off[e >> kLowBits], pol);
+#endif
             }
         } else {
         #pragma unroll 1
@@ -507,24 +561,9 @@ __device__ __forceinline__ void tile_pass_body(const TileParams &p, const TilePa
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     __syncthreads();
-    // nbuf 2: the next tile streams into the other buffer while this one is
-    // computed (its latency hidden inside the CTA); nbuf 1: refill after the
-    // store, latency hidden only by the other resident CTAs
-    uint64_t base = insert_zero_bits_dyn((uint64_t)blockIdx.x, S.tb, T);
-    if ((int64_t)blockIdx.x < p.ntiles) fetch(base, tile);
-    int buf = 0;
-    for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-        const uint64_t nbase = next_base(base, p, S);
-        const bool more = t + gridDim.x < p.ntiles;
-        double2 *tl = tile + ((size_t)buf << T);
-        if (threadIdx.x == 0) s_sbase = base | p.gbase;  // full-state index bits for selectors
-        if (p.nbuf == 2 && more) {
-            fetch(nbase, tile + ((size_t)(buf ^ 1) << T));
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-        } else {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-        }
-        __syncthreads();
+    // one tile's phases, in place in its smem buffer (s_sbase: the tile's
+    // full-state base, written by the caller before the barrier it passes)
+    auto phases = [&](double2 *tl) {
         DIAQ_SUNROLL
         for (int ph_i = 0; ph_i < S.nphases; ++ph_i) {
             const Phase &ph = S.ph[ph_i];
@@ -573,6 +612,69 @@ __device__ __forceinline__ void tile_pass_body(const TileParams &p, const TilePa
             }
             __syncthreads();
         }
+    };
+#ifdef DIAQ_JIT
+    if (pairing) {
+        // Pair store: the tile and its partner across the extra bit gpb[0]
+        // run in one CTA (both smem buffers), then every destination sector
+        // (row) of the pair is written whole, gathered from the two buffers.
+        // Units are pairs; their bases enumerate the bits outside emask.
+        const uint64_t pbit = 1ull << S.gpb[0];
+        const int64_t nunits = p.ntiles >> 1;
+        uint64_t gb = insert_zero_bits_dyn((uint64_t)blockIdx.x, S.eb, T + 1);
+        if ((int64_t)blockIdx.x < nunits) {
+            fetch(gb, tile);
+            fetch(gb | pbit, tile + ((size_t)1 << T));
+        }
+        for (int64_t t = blockIdx.x; t < nunits; t += gridDim.x) {
+            const uint64_t ngb = ((gb | S.emask) + p.gstep) & ~S.emask;
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        #pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                if (threadIdx.x == 0) s_sbase = (gb | (h ? pbit : 0ull)) | p.gbase;
+                __syncthreads();
+                phases(tile + ((size_t)h << T));
+            }
+            __syncthreads();
+            uint64_t ab = p.gconst, o = gb;
+            while (o) {
+                ab ^= p.gcol[__ffsll((long long)o) - 1];
+                o &= o - 1;
+            }
+        #pragma unroll 4
+            for (int i = 0; i < 2 * NR; ++i) {
+                const uint32_t src = ps_t ^ s_ps[i];
+                st_stream(p.y + (ab ^ pw_t ^ s_pw[i]), tile[((size_t)(src >> 12) << T) + swz(src & 0xfffu)]);
+            }
+            __syncthreads();
+            gb = ngb;
+            if (t + gridDim.x < nunits) {
+                fetch(gb, tile);
+                fetch(gb | pbit, tile + ((size_t)1 << T));
+            }
+        }
+        return;
+    }
+#endif
+    // nbuf 2: the next tile streams into the other buffer while this one is
+    // computed (its latency hidden inside the CTA); nbuf 1: refill after the
+    // store, latency hidden only by the other resident CTAs
+    uint64_t base = insert_zero_bits_dyn((uint64_t)blockIdx.x, S.tb, T);
+    if ((int64_t)blockIdx.x < p.ntiles) fetch(base, tile);
+    int buf = 0;
+    for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+        const uint64_t nbase = next_base(base, p, S);
+        const bool more = t + gridDim.x < p.ntiles;
+        double2 *tl = tile + ((size_t)buf << T);
+        if (threadIdx.x == 0) s_sbase = base | p.gbase;  // full-state index bits for selectors
+        if (p.nbuf == 2 && more) {
+            fetch(nbase, tile + ((size_t)(buf ^ 1) << T));
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        phases(tl);
         if (S.gperm) {  // trailing permutation run: element i goes to A i ^ c in the other buffer
             uint64_t ab = p.gconst, o = base;
             while (o) {
@@ -583,9 +685,6 @@ __device__ __forceinline__ void tile_pass_body(const TileParams &p, const TilePa
             for (int k = 0; k < NR; ++k) {
                 const uint32_t e = threadIdx.x + (uint32_t)k * kThreads;
                 double2 *dst = p.y + (ab ^ s_ghi[e >> kLowBits] ^ glo[e & lowmask]);
-                // rows split by the map (a low-bit control) are completed by
-                // another CTA: keep partial sectors in L2 until the partner
-                // half lands instead of evicting them first (DRAM RMW)
                 if (p.gstore == 0) st_stream(dst, tl[swz(e)]);
                 else if (p.gstore == 1) st_plain(dst, tl[swz(e)]);
                 else st_hint(dst, tl[swz(e)], policy_evict_last());

@@ -678,7 +678,7 @@ def test_fused_jit_matches_interpreter(cmul, seed):
             after = _jit_stats()
             assert np.array_equal(got, want) and np.array_equal(aot, want), (seed, n, tb)
             assert after["failed"] == 0, L.load().diaq_jit_last_error()
-            assert after["launches"] > before["launches"], (before, after)
+            assert after["launches"] > before["launches"], (before, after, L.load().diaq_jit_last_error())
     finally:
         L.tune("fused_jit", 1)
 
