@@ -90,7 +90,7 @@ def main():
             if "spmv" in rec["kernel"]:
                 summ["spmv_dram_bytes_per_launch"] = tot
                 summ["spmv_source"] = f"profiles/{args.tag}_ncu_full.json ({name})"
-            elif "gate_kernel" in rec["kernel"] or "tile_pass_kernel" in rec["kernel"]:
+            elif any(k in rec["kernel"] for k in ("gate_kernel", "tile_pass_kernel", "diaq_jit_pass")):
                 summ["gate_dram_bytes_per_launch"] = tot
                 summ["gate_source"] = f"profiles/{args.tag}_ncu_full.json ({name})"
     with open(summ_path, "w") as f:
