@@ -460,7 +460,7 @@ def sharded_gates(args, D, L, W, torch, dist, n, world, x, s, dev):
         st = ShardedState(ns, x / world ** 0.5, comm)
     ops = W.random_layered_ops(ns, 1, seed=0)
     pls = D.compile_circuit(D.Circuit(ns, [D.GateOp(*o) for o in ops]), span_limit=ns)
-    st.apply_placements(pls)
+    st.apply_placements(pls, remap=args.remap)
     torch.cuda.synchronize()
     dist.barrier()
     g_steps = max(2, min(args.steps, 5))
@@ -469,13 +469,13 @@ def sharded_gates(args, D, L, W, torch, dist, n, world, x, s, dev):
     gl0 = L.launch_count()
     ge0.record(s)
     for _ in range(g_steps):
-        st.apply_placements(pls)
+        st.apply_placements(pls, remap=args.remap)
     ge1.record(s)
     torch.cuda.synchronize()
     g_launches = L.launch_count() - gl0
     g_ms = max_over_ranks(dist, ge0.elapsed_time(ge1), dev)
     extra = {"gates_per_step": len(pls), "steps": g_steps, "mode": f"sharded over {world} ranks",
-             "transport": transport, "stats": dict(st.stats)}
+             "transport": transport, "remap": bool(args.remap), "stats": dict(st.stats)}
     return len(pls) * g_steps, g_ms, g_launches, st.norm(), ns, extra
 
 
@@ -534,20 +534,25 @@ def secondary_workloads(args, D, L, W, torch) -> dict:
     e2e_s = time.perf_counter() - t0
     # config 5 shape on one GPU: a 2^29-amplitude state split into 2 emulated
     # shards (same plans and kernels as the NCCL path; the exchange is a
-    # device copy here), one random layer drawn over all 29 qubits
+    # device copy here), 4 random layers drawn over all 29 qubits, without
+    # and with qubit remapping (shard.remap_plan)
     from paper_2405_01250_b200.shard import run_emulated
-    ops5 = W.random_layered_ops(29, 1, seed=0)
+    ops5 = W.random_layered_ops(29, 4, seed=0)
     pls5 = D.compile_circuit(D.Circuit(29, [D.GateOp(*o) for o in ops5]), span_limit=29)
-    run_emulated(29, 2, pls5)  # warm-up
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    shards, st5 = run_emulated(29, 2, pls5)
-    torch.cuda.synchronize()
-    dt5 = time.perf_counter() - t0
-    out["config5_sharded_emulated_n29_p2"] = {"gates": len(pls5), "s_per_layer": round(dt5, 4),
-                                             "gates_per_s": round(len(pls5) / dt5, 1), "stats": st5,
-                                             "note": "2 shards on one GPU; exchange = device copy (NVLink unmeasured)"}
-    del shards
+    for remap in (False, True):
+        run_emulated(29, 2, pls5, remap=remap)  # warm-up
+        L.call("diaq_jit_wait", -1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        shards, st5 = run_emulated(29, 2, pls5, remap=remap)
+        torch.cuda.synchronize()
+        dt5 = time.perf_counter() - t0
+        key = "config5_sharded_emulated_n29_p2" + ("_remap" if remap else "")
+        out[key] = {"gates": len(pls5), "layers": 4, "s_per_circuit": round(dt5, 4),
+                    "gates_per_s": round(len(pls5) / dt5, 1), "stats": st5,
+                    "note": "2 shards on one GPU, wall clock; exchange = device copy (NVLink unmeasured); "
+                            "partner_shards_read = what in-place peer reads fetch"}
+        del shards
     # the metric's Haar4 gate kind at n=28: a layer of 14 Haar-random two-qubit
     # gates on a seeded random matching (fused passes, device time per layer)
     rng = np.random.default_rng(0)
@@ -605,6 +610,8 @@ def main():
                     help="N>1: measure gates on a state sharded over the ranks instead of replicas")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent spmv replicas instead of the row-sharded product")
+    ap.add_argument("--remap", action="store_true",
+                    help="--sharded-gates: swap global qubits into local positions before cross-shard gates")
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
                     help="sharded gates: partner shards read in place over peer memory, or NCCL-staged")
     args = ap.parse_args()

@@ -69,6 +69,114 @@ def exchange_schedule(n_bits: int, local_bits: int, g, shifts, world: int):
     return needs
 
 
+def partner_rows(local_bits: int, g: np.ndarray, shifts, rank: int) -> dict[int, float]:
+    """{column block: fraction of this rank's rows that read it} -- what a
+    kernel reading partner data in place (peer transport) fetches: RX on a
+    global bit reads the whole partner shard, SWAP(global, local) half."""
+    g = np.asarray(g)
+    k = len(shifts)
+    gs = global_shifts(shifts, local_bits)
+    loc = [i for i in range(k) if shifts[i] < local_bits]
+    glo = {i: (rank >> (shifts[i] - local_bits)) & 1 for i in range(k) if shifts[i] >= local_bits}
+    use: dict[int, int] = {}
+    for pat in range(1 << len(loc)):
+        rg = 0
+        for i in range(k):
+            bit = glo[i] if i in glo else (pat >> loc.index(i)) & 1
+            rg |= bit << (k - 1 - i)
+        blocks = set()
+        for c in np.nonzero(g[rg])[0]:
+            b = 0
+            for j, sh in enumerate(gs):
+                i = list(shifts).index(sh)
+                b |= ((int(c) >> (k - 1 - i)) & 1) << (len(gs) - 1 - j)
+            blocks.add(b)
+        for b in blocks:
+            use[b] = use.get(b, 0) + 1
+    return {b: u / (1 << len(loc)) for b, u in use.items()}
+
+
+_SWAP = np.array([[1, 0, 0, 0], [0, 0, 1, 0], [0, 1, 0, 0], [0, 0, 0, 1]], dtype=np.complex128)
+
+
+def mixing_operands(g: np.ndarray, k: int) -> list[int]:
+    """Operands a k-qubit gate mixes: i is NOT mixing when g is block
+    diagonal in it (g[r, c] == 0 whenever bit i of r and c differ) -- a
+    control or a diagonal operand, which selects rows but moves nothing."""
+    g = np.asarray(g)
+    idx = np.arange(1 << k)
+    out = []
+    for i in range(k):
+        b = (idx >> (k - 1 - i)) & 1
+        if np.any(g[b[:, None] != b[None, :]] != 0):
+            out.append(i)
+    return out
+
+
+def remap_plan(n_bits: int, local_bits: int, world: int, comps, restore: bool = True):
+    """Qubit remapping for cross-shard gates ("ways to push
+    toward linear"): before a gate that would read a partner shard because
+    it mixes global bit g, swap g with a local bit v, so the gate (and every
+    later gate on that qubit until it is displaced) runs locally.  The swap is
+    a SWAP(g, v) gate through the ordinary exchange path; it moves half a
+    shard each way (rows whose v bit differs from the rank's g bit) instead
+    of the whole partner shard a cross-shard rotation reads.  Victim v:
+    the local bit whose qubit's next mixing use is farthest ahead (Belady;
+    controls and diagonal gates do not count), ties to the highest bit.
+    Host-only and deterministic, so every rank plans the same swaps.
+
+    comps: logical (g, shifts).  Returns (physical (g, shifts) list,
+    number of swaps).  restore: end with the identity layout (swaps back),
+    so the caller's amplitudes are in logical order after the run.
+
+    Rounding: one-qubit and permutation gates are bitwise the unremapped
+    path; a dense multi-qubit gate whose operands change relative order is
+    summed in the physical column order (equal within fp64 rounding)."""
+    l2p = list(range(n_bits))
+    p2l = list(range(n_bits))
+    mix = [[shifts[i] for i in mixing_operands(g, len(shifts))] for g, shifts in comps]
+    # next mixing use of each logical bit after gate i (scanned backwards)
+    nxt = [None] * len(comps)
+    far = [len(comps)] * n_bits
+    for i in range(len(comps) - 1, -1, -1):
+        nxt[i] = far.copy()
+        for s in mix[i]:
+            far[s] = i
+    out = []
+    swaps = 0
+
+    def swap(a: int, b: int):
+        nonlocal swaps
+        out.append((_SWAP, [a, b]))
+        la, lb_ = p2l[a], p2l[b]
+        p2l[a], p2l[b] = lb_, la
+        l2p[la], l2p[lb_] = b, a
+        swaps += 1
+
+    for i, (g, shifts) in enumerate(comps):
+        phys = [l2p[s] for s in shifts]
+        if world > 1 and any(l2p[s] >= local_bits for s in mix[i]):
+            needs = exchange_schedule(n_bits, local_bits, g, phys, world)
+            if any(src != r for r, nd in enumerate(needs) for src in nd.values()):
+                busy = set(phys)
+                for s in mix[i]:
+                    if l2p[s] < local_bits:
+                        continue
+                    cand = [v for v in range(local_bits) if v not in busy]
+                    if not cand:
+                        break
+                    v = max(cand, key=lambda v: (nxt[i][p2l[v]], v))
+                    busy.add(v)
+                    swap(l2p[s], v)
+                phys = [l2p[s] for s in shifts]
+        out.append((g, phys))
+    if restore:
+        for q in range(n_bits):
+            if l2p[q] != q:
+                swap(l2p[q], q)
+    return out, swaps
+
+
 def _ptr(t):
     """device address of a source block: a tensor, a raw (peer) pointer, or None"""
     if t is None:
@@ -272,9 +380,10 @@ class ShardedState:
         srcs = [None] * (1 << kg)
         for b, src in needs[me].items():
             srcs[b] = self.local if src == me else self._peer[src][self._cur]
-        remote = sorted({src for src in needs[me].values() if src != me})
+        frac = partner_rows(lb, g, shifts, me)
         self.stats["exchanged"] += 1
-        self.stats["bytes_received"] += 16 * self.local.numel() * len(remote)
+        self.stats["bytes_received"] += int(16 * self.local.numel() *
+                                            sum(f for b, f in frac.items() if needs[me].get(b, me) != me))
         nxt = self._bufs[self._cur ^ 1]
         self.apply_fn(n, lb, g, shifts, me, srcs, nxt, cmul_mode)
         self._cur ^= 1
@@ -287,12 +396,15 @@ class ShardedState:
         needs = exchange_schedule(self.n_qubits, lb, g, shifts, self.comm.world)
         return any(src != r for r, nd in enumerate(needs) for src in nd.values())
 
-    def apply_placements(self, placements: list[Placement], cmul_mode: int | None = None) -> None:
+    def apply_placements(self, placements: list[Placement], cmul_mode: int | None = None,
+                         remap: bool = False) -> None:
         """Apply gates in order.  On the GPU every maximal run of gates that
         needs no partner data (the same decision on every rank) goes through
         one fused native call (diaq_run_gates_local: shared-memory multi-gate
         passes, global-bit controls read from the rank index); cross-shard
-        gates exchange and use the multi-source kernel."""
+        gates exchange and use the multi-source kernel.  remap: swap a
+        global qubit with a local one before a gate that would read a
+        partner shard (remap_plan); the layout is restored at the end."""
         from . import sim
         mode = sim.CMUL_MODE if cmul_mode is None else cmul_mode
         comps = []
@@ -301,6 +413,9 @@ class ShardedState:
             if comp is None:
                 raise ValueError(f"sharded apply needs compact placements, got {p!r}")
             comps.append(comp)
+        if remap:
+            comps, nsw = remap_plan(self.n_qubits, self.local_bits, self.comm.world, comps)
+            self.stats["swaps"] = self.stats.get("swaps", 0) + nsw
         if self.apply_fn is not _cuda_apply or sim.FUSE_TILE_BITS == 0:
             for g, shifts in comps:
                 self.apply_gate(g, shifts, mode)
@@ -350,10 +465,10 @@ class EmulatedComm:
 
 
 def run_emulated(n_qubits: int, world: int, placements: list[Placement], cmul_mode: int | None = None,
-                 device=None):
+                 device=None, remap: bool = False):
     """Apply placements to |0..0> split over `world` emulated ranks on one
     device; returns (list of local shards, stats).  Same plans and kernels as
-    the multi-process path."""
+    the multi-process path (remap: ShardedState.apply_placements)."""
     import torch
 
     from . import sim
@@ -368,6 +483,8 @@ def run_emulated(n_qubits: int, world: int, placements: list[Placement], cmul_mo
     lb = states[0].local_bits
     stats = {"gates": 0, "local": 0, "no_comm_global": 0, "exchanged": 0}
     comps = [p.compact() for p in placements]
+    if remap:
+        comps, stats["swaps"] = remap_plan(n_qubits, lb, world, comps)
     fuse = sim.FUSE_TILE_BITS != 0
 
     def crosses(g, shifts):
@@ -402,6 +519,10 @@ def run_emulated(n_qubits: int, world: int, placements: list[Placement], cmul_mo
             i += 1
             continue
         stats["exchanged" if cross else "no_comm_global"] += 1
+        if cross:  # shard-equivalents each rank reads from partners (in-place peer reads)
+            rd = sum(f for r in range(world) for b, f in partner_rows(lb, g, shifts, r).items()
+                     if needs[r].get(b, r) != r) / world
+            stats["partner_shards_read"] = round(stats.get("partner_shards_read", 0.0) + rd, 6)
         snap = {}
         if cross:  # partner data as it was before this gate
             for r in range(world):

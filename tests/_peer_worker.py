@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--tile", type=int, default=12)
     ap.add_argument("--out", required=True)
     ap.add_argument("--mode", default="gates", choices=["gates", "spmv"])
+    ap.add_argument("--remap", type=int, default=0)
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -43,7 +44,7 @@ def main():
             ("cx", (a.n - 1, 0), ()), ("u3", (0,), (0.3, 0.2, 0.1))]
     pls = D.compile_circuit(D.Circuit(a.n, [D.GateOp(*o) for o in ops]), span_limit=a.n)
     st = ShardedState.basis(a.n, comm)
-    st.apply_placements(pls, cmul_mode=a.cmul)
+    st.apply_placements(pls, cmul_mode=a.cmul, remap=bool(a.remap))
     norm = st.norm()
     full = st.gather()
     comm.barrier()  # nobody unmaps or frees while a partner may still read

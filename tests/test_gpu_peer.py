@@ -27,14 +27,15 @@ def _port() -> int:
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("n,tile", [(12, 12), (14, 0), (16, 11)])
-def test_peer_sharded_matches_unsharded(tmp_path, configs, n, tile):
+@pytest.mark.parametrize("n,tile,remap", [(12, 12, 0), (14, 0, 0), (16, 11, 0), (14, 0, 1), (16, 11, 1)])
+def test_peer_sharded_matches_unsharded(tmp_path, configs, n, tile, remap):
     cmul = L.CMUL_FMA if configs["meta"]["numpy_cmul"] == "fma" else L.CMUL_PLAIN
     out = str(tmp_path / "state.npy")
     port = _port()
     worker = os.path.join(ROOT, "tests", "_peer_worker.py")
     procs = [subprocess.Popen([sys.executable, worker, "--rank", str(r), "--world", "2", "--port", str(port),
-                               "--n", str(n), "--cmul", str(cmul), "--tile", str(tile), "--out", out],
+                               "--n", str(n), "--cmul", str(cmul), "--tile", str(tile), "--out", out,
+                               "--remap", str(remap)],
                               stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True) for r in range(2)]
     logs = []
     try:
@@ -48,6 +49,8 @@ def test_peer_sharded_matches_unsharded(tmp_path, configs, n, tile):
     got = np.load(out)
     info = ast.literal_eval(open(out + ".stats").read())
     assert info["stats"]["exchanged"] > 0 and abs(info["norm"] - 1.0) < 1e-12
+    if remap:  # half-shard swaps instead of whole-shard partner reads
+        assert info["stats"]["swaps"] > 0
     ops = W.random_layered_ops(n, 2, seed=0)
     ops += [("h", (0,), ()), ("cx", (0, n - 1), ()), ("ry", (1,), (0.7,)), ("swap", (0, 2), ()),
             ("cx", (n - 1, 0), ()), ("u3", (0,), (0.3, 0.2, 0.1))]
@@ -91,10 +94,11 @@ def test_bench_multi_rank_paths_on_one_gpu(tmp_path):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"),
            "--gpus", "2", "--steps", "2", "--warmup", "3", "--no-e2e", "--no-cpu", "--no-secondary",
-           "--qubits", "23", "--sharded-gates"]
+           "--qubits", "23", "--sharded-gates", "--remap"]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
     assert p.returncode == 0, p.stderr[-3000:]
     line = json.loads(p.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and "peer loads" in line["config"]["parallelism"]
     assert line["gates"]["transport"] == "peer" and line["gates"]["stats"]["exchanged"] > 0
     assert abs(line["gates"]["norm_after"] - 1.0) < 1e-10
+    assert line["gates"]["remap"] is True

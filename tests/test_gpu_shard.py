@@ -46,13 +46,18 @@ def test_sharded_n12_matches_reference(configs, cmul, world):
     assert stats["exchanged"] > 0
 
 
+@pytest.mark.parametrize("remap", [False, True], ids=["plain", "remap"])
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_sharded_n20_matches_reference_digest(configs, cmul, world):
+def test_sharded_n20_matches_reference_digest(configs, cmul, world, remap):
+    """remap: global qubits swapped into local positions before cross-shard
+    gates (shard.remap_plan) -- still bitwise the reference (config-5 mix)."""
     rec = configs["circuits"]["20"]
     ops = W.random_layered_ops(20, rec["layers"], rec["seed"])
     pls = D.compile_circuit(D.Circuit(20, [D.GateOp(*o) for o in ops]), span_limit=20)
-    shards, stats = run_emulated(20, world, pls, cmul_mode=cmul)
+    shards, stats = run_emulated(20, world, pls, cmul_mode=cmul, remap=remap)
     assert digest(_full(shards)) == rec["digest"]
+    if remap:
+        assert stats["swaps"] > 0
 
 
 def test_sharded_mixed_gates_match_unsharded(cmul):
@@ -66,6 +71,8 @@ def test_sharded_mixed_gates_match_unsharded(cmul):
     for world in (2, 4, 8):
         shards, _ = run_emulated(n, world, pls, cmul_mode=cmul)
         assert np.array_equal(_full(shards), want), world
+        shards, _ = run_emulated(n, world, pls, cmul_mode=cmul, remap=True)
+        assert np.array_equal(_full(shards), want), ("remap", world)
 
 
 @pytest.mark.parametrize("world", [2, 4, 8])

@@ -60,7 +60,7 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, ops, out_q):
+def _worker(rank, world, port, n, ops, out_q, remap=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     import torch.distributed as dist
@@ -71,7 +71,7 @@ def _worker(rank, world, port, n, ops, out_q):
         comm = TorchDistComm()
         st = ShardedState.basis(n, comm, device=torch.device("cpu"), apply_fn=numpy_apply)
         pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
-        st.apply_placements(pls, cmul_mode=O.numpy_cmul_mode())
+        st.apply_placements(pls, cmul_mode=O.numpy_cmul_mode(), remap=remap)
         nrm = st.norm()
         full = st.gather()
         if rank == 0:
@@ -80,11 +80,11 @@ def _worker(rank, world, port, n, ops, out_q):
         dist.destroy_process_group()
 
 
-def run_world(world: int, n: int, ops):
+def run_world(world: int, n: int, ops, remap: bool = False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, ops, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, ops, q, remap)) for r in range(world)]
     for p in procs:
         p.start()
     import queue
@@ -166,3 +166,93 @@ def test_cross_shard_fraction_matches_survey():
             if any(src != r for r in range(world) for src in needs[r].values()):
                 crosses += 1
         assert crosses == want, (n, world, crosses)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_remap_matches_oracle(world):
+    """Qubit remapping (shard.remap_plan): global qubits swapped into local
+    positions before cross-shard gates, layout restored at the end; the
+    gathered state is still bitwise the oracle's (one-qubit and permutation
+    gates only), with fewer partner reads than without remapping."""
+    n = 8
+    ops = W.random_layered_ops(n, 4, seed=7)
+    ops += [("ccx", (0, 5, 1), ()), ("swap", (1, 6), ()), ("cz", (0, 1), ()), ("cx", (7, 0), ())]
+    full, nrm, stats = run_world(world, n, ops, remap=True)
+    want = O.run_circuit(n, ops, cmul_mode=O.numpy_cmul_mode())
+    assert np.array_equal(full, want)
+    assert abs(nrm - 1.0) < 1e-12
+    assert stats["swaps"] > 0
+    _, _, base = run_world(world, n, ops)
+    assert stats["bytes_received"] < base["bytes_received"]
+
+
+def _dense_apply(x, g, shifts):
+    """numpy reference of one compact gate on a full 2^n vector (host test)."""
+    n = int(np.log2(len(x)))
+    k = len(shifts)
+    idx = np.arange(len(x))
+    rg = np.zeros_like(idx)
+    for i, s in enumerate(shifts):
+        rg |= ((idx >> s) & 1) << (k - 1 - i)
+    free = idx & ~sum(1 << s for s in shifts)
+    y = np.zeros_like(x)
+    for c in range(1 << k):
+        col = free.copy()
+        for i, s in enumerate(shifts):
+            col |= ((c >> (k - 1 - i)) & 1) << s
+        y += np.asarray(g)[rg, c] * x[col]
+    return y
+
+
+@pytest.mark.parametrize("n,world", [(8, 2), (9, 4), (10, 8)])
+def test_remap_plan_is_a_relabelling(n, world):
+    """The physical program (swaps + relabelled gates, layout restored)
+    computes the logical circuit; swaps are SWAP gates on one global and one
+    local bit, and every remaining cross-shard gate still needs its partner."""
+    from paper_2405_01250_b200 import gates as G
+    from paper_2405_01250_b200.shard import remap_plan
+    rng = np.random.default_rng(n)
+    ops = W.random_layered_ops(n, 3, seed=n)
+    ops.append(("u3", (0,), (0.1, 0.2, 0.3)))
+    comps = [(np.asarray(G.GATE_DEFS[nm][2](*pr), dtype=np.complex128), [n - 1 - q for q in qs]) for nm, qs, pr in ops]
+    lb = n - (world.bit_length() - 1)
+    phys, nsw = remap_plan(n, lb, world, comps)
+    assert nsw > 0 and len(phys) == len(comps) + nsw
+    x = rng.normal(size=2**n) + 1j * rng.normal(size=2**n)
+    a, b = x.copy(), x.copy()
+    for g, sh in comps:
+        a = _dense_apply(a, g, sh)
+    for g, sh in phys:
+        b = _dense_apply(b, g, sh)
+    assert np.allclose(a, b, rtol=0, atol=1e-12)
+    # no remapping needed on one shard
+    same, k = remap_plan(n, n, 1, comps)
+    assert k == 0 and all(sa == sb for (_, sa), (_, sb) in zip(same, comps))
+
+
+def test_remap_cuts_partner_reads_config5():
+    """Config-5 generator (seed 0, 20 layers) at n=33 on 8 shards: remapping
+    turns 65 cross-shard gates reading 52 partner shards into 36 cross-shard
+    operations (mostly half-shard swaps) reading 17.5 shards' worth."""
+    from paper_2405_01250_b200 import gates as G
+    from paper_2405_01250_b200.shard import exchange_schedule, partner_rows, remap_plan
+    n, world = 33, 8
+    lb = n - 3
+    ops = W.random_layered_ops(n, 20, seed=0)
+    comps = [(np.asarray(G.GATE_DEFS[nm][2](*pr), dtype=np.complex128), [n - 1 - q for q in qs]) for nm, qs, pr in ops]
+
+    def reads(prog):
+        cross, shards = 0, 0.0
+        for g, sh in prog:
+            if all(s < lb for s in sh):
+                continue
+            needs = exchange_schedule(n, lb, g, sh, world)
+            if any(src != r for r in range(world) for src in needs[r].values()):
+                cross += 1
+                fr = partner_rows(lb, g, sh, 0)
+                shards += sum(f for b, f in fr.items() if needs[0].get(b, 0) != 0)
+        return cross, shards
+
+    assert reads(comps) == (65, 52.0)
+    phys, nsw = remap_plan(n, lb, world, comps)
+    assert reads(phys) == (36, 17.5)
