@@ -953,7 +953,11 @@ static std::shared_ptr<const Program> build_program(int n_total, int n_bits, int
         if (ps.gon) {
             for (size_t j = 0; j < ps.gcol.size() && j < 64; ++j) p.gcol[j] = ps.gcol[j];
             p.gconst = ps.gc;  // rank bits folded in at launch
-            if (tuning().fused_pair_store) plan_pair_store(ps, n_bits, p);
+            // a pair of 12-bit tiles needs 128 KB of smem: one CTA per SM,
+            // slower than the scatter store's partial-sector writes (n=30
+            // layer 22.2 vs 20.9 ms); 11-bit pairs keep 3 CTAs per SM
+            const int pst = tuning().fused_pair_store;
+            if (pst >= 2 || (pst == 1 && (int)ps.bits.size() <= 11)) plan_pair_store(ps, n_bits, p);
         }
         std::copy(ps.phases.begin(), ps.phases.end(), p.ph);
         std::copy(ps.gates.begin(), ps.gates.end(), p.g);

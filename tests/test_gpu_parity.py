@@ -669,18 +669,21 @@ def test_fused_jit_matches_interpreter(cmul, seed):
     x0 = D.StateVector(n, W.random_state(rng, 2**n))
     want = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=0).amps
     try:
-        for tb in (11, 12):
+        # pair store: default (11-bit tiles only) and forced for 12-bit tiles
+        for tb, pst in ((11, 1), (12, 1), (12, 2)):
+            L.tune("fused_pair_store", pst)
             L.tune("fused_jit", 0)
             aot = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=tb).amps
             L.tune("fused_jit", 2)
             before = _jit_stats()
             got = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=tb).amps
             after = _jit_stats()
-            assert np.array_equal(got, want) and np.array_equal(aot, want), (seed, n, tb)
+            assert np.array_equal(got, want) and np.array_equal(aot, want), (seed, n, tb, pst)
             assert after["failed"] == 0, L.load().diaq_jit_last_error()
             assert after["launches"] > before["launches"], (before, after, L.load().diaq_jit_last_error())
     finally:
         L.tune("fused_jit", 1)
+        L.tune("fused_pair_store", 1)
 
 
 def test_fused_jit_layer_n24_async(cmul):
