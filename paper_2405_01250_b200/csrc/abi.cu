@@ -107,6 +107,7 @@ extern "C" int diaq_tune(const char *key, int64_t value) {
     else if (k == "fused_jit") t.fused_jit = (int)value;
     else if (k == "fused_gstore") t.fused_gstore = (int)value;
     else if (k == "fused_pair_store") t.fused_pair_store = (int)value;
+    else if (k == "fused_bank_spread") t.fused_bank_spread = (int)value;
     else if (k == "fused_perm") t.fused_perm = (int)value;
     else if (k == "kron_flat") t.kron_flat = (int)value;
     else if (k == "kron_ctas_per_sm") t.kron_ctas_per_sm = (int)(value < 1 ? 1 : value);

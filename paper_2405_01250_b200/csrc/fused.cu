@@ -391,6 +391,45 @@ static int pack_smem_gate(const diaq_gate_t &gt, const std::vector<int> &bits, P
 // (no room for the state-sized buffer they need)
 static thread_local bool t_no_gperm = false;
 
+// Shared-memory banks: a 16-byte access is served per quarter warp (lanes
+// differing in thread bits 0-2); its 8 slots hit 8 distinct 16-byte bank
+// groups iff the bank-group images (swz(e) & 7, linear in e) of the tile
+// positions carrying thread bits 0-2 are independent.  Thread bits may sit
+// on any tile positions (tpart is built from tpos; selectors test tile
+// positions), so pick the three positions that minimise the conflict
+// factors of the phase load (slot swz(tpart)) and, with a folded
+// permutation, of its store (slot swz(A tpart ^ c)); the rest stay ascending.
+static void spread_lane_bits(Phase &ph, int T, int R) {
+    const int nt = T - R;
+    if (nt < 4) return;
+    auto distinct = [](uint32_t a, uint32_t b, uint32_t c) {
+        uint32_t seen = 0;
+        for (int m = 0; m < 8; ++m) seen |= 1u << (((m & 1) ? a : 0) ^ ((m & 2) ? b : 0) ^ ((m & 4) ? c : 0));
+        return __builtin_popcount(seen);
+    };
+    auto ld = [&](int tp) { return swz(1u << tp) & 7u; };
+    auto st = [&](int tp) { return swz(aff_lin(ph.post, 1u << tp, T)) & 7u; };
+    int best[3] = {0, 1, 2};
+    int best_cost = 1 << 30;
+    for (int a = 0; a < nt; ++a)
+        for (int b = a + 1; b < nt; ++b)
+            for (int c = b + 1; c < nt; ++c) {
+                const int pa = ph.tpos[a], pb = ph.tpos[b], pc = ph.tpos[c];
+                int cost = 8 / distinct(ld(pa), ld(pb), ld(pc));
+                if (ph.post.on) cost += 8 / distinct(st(pa), st(pb), st(pc));
+                if (cost < best_cost) {
+                    best_cost = cost;
+                    best[0] = a, best[1] = b, best[2] = c;
+                }
+            }
+    int8_t out[kMaxTileBits];
+    int q = 0;
+    for (int i = 0; i < 3; ++i) out[q++] = ph.tpos[best[i]];
+    for (int i = 0; i < nt; ++i)
+        if (i != best[0] && i != best[1] && i != best[2]) out[q++] = ph.tpos[i];
+    for (int i = 0; i < nt; ++i) ph.tpos[i] = out[i];
+}
+
 static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t *gates, int T, int R,
                          std::vector<PassPlan> &plan, bool allow_d2) {
     const int low = std::min(kLowBits, n_bits);
@@ -593,6 +632,7 @@ static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t 
             }
             ph.g1 = (int)ps.gates.size();
             ph.post = sp.post.pack();
+            if (tuning().fused_bank_spread) spread_lane_bits(ph, (int)ps.bits.size(), R);
             for (int j = 0; j < 16; ++j) {
                 uint32_t e = 0;
                 for (int q = 0; q < R; ++q) e |= (uint32_t)((j >> q) & 1) << ph.rpos[q];
@@ -804,9 +844,9 @@ static std::vector<char> program_key(int n_total, int n_bits, int T, int ngates,
         key.insert(key.end(), c, c + n);
     };
     // every tuning switch the schedule depends on is part of the key
-    const int head[10] = {n_total, n_bits, T, ngates, tuning().fused_perm,
+    const int head[11] = {n_total, n_bits, T, ngates, tuning().fused_perm,
                           tuning().fused_gperm && !t_no_gperm, tuning().fused_seq, tuning().fused_dense2,
-                          tuning().fused_gperm_rows, tuning().fused_pair_store};
+                          tuning().fused_gperm_rows, tuning().fused_pair_store, tuning().fused_bank_spread};
     put(head, sizeof(head));
     for (int i = 0; i < ngates; ++i) {
         const diaq_gate_t &gt = gates[i];
@@ -910,6 +950,33 @@ static void plan_pair_store(const PassPlan &ps, int n_bits, TileParams &p) {
         p.gw[k] = w[(size_t)k];
         p.gsrc[k] = (uint16_t)(off | (rank << 12));
     }
+    // lanes 1-2 (thread bits 1-2; bit 0 keeps the sector partner e0): the
+    // destination basis vectors whose sources spread the quarter warp's
+    // gather reads over the most smem bank groups (fused_bank_spread & 2)
+    if (!(tuning().fused_bank_spread & 2) || T + p.gnp < 4) return;
+    auto bank = [&](int k) { return swz(p.gsrc[k] & 0xfffu) & 7u; };
+    auto distinct = [](uint32_t a, uint32_t b, uint32_t c) {
+        uint32_t seen = 0;
+        for (int m = 0; m < 8; ++m) seen |= 1u << (((m & 1) ? a : 0) ^ ((m & 2) ? b : 0) ^ ((m & 4) ? c : 0));
+        return __builtin_popcount(seen);
+    };
+    const int nw = T + p.gnp;
+    int b1 = 1, b2 = 2, best = distinct(bank(0), bank(1), bank(2));
+    for (int i = 1; i < nw && best < 8; ++i)
+        for (int j = i + 1; j < nw && best < 8; ++j) {
+            const int d = distinct(bank(0), bank(i), bank(j));
+            if (d > best) best = d, b1 = i, b2 = j;
+        }
+    if (b1 == 1 && b2 == 2) return;
+    uint64_t gw[kMaxTileBits + 3];
+    uint16_t gs[kMaxTileBits + 3];
+    int q = 0;
+    gw[q] = p.gw[0], gs[q++] = p.gsrc[0];
+    gw[q] = p.gw[b1], gs[q++] = p.gsrc[b1];
+    gw[q] = p.gw[b2], gs[q++] = p.gsrc[b2];
+    for (int k = 1; k < nw; ++k)
+        if (k != b1 && k != b2) gw[q] = p.gw[k], gs[q++] = p.gsrc[k];
+    for (int k = 0; k < nw; ++k) p.gw[k] = gw[k], p.gsrc[k] = gs[k];
 }
 
 static std::shared_ptr<const Program> build_program(int n_total, int n_bits, int T, int ngates, const diaq_gate_t *gates,
