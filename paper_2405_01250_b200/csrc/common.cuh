@@ -31,8 +31,8 @@ struct Tuning {
     int fused_gstore = 0;      // global-map (out-of-place permuted) store policy: 0 .cs, 1 default, 2 evict_last
     int fused_bank_spread = 3;  // fused passes, quarter-warp lanes on bank-spreading positions: 1 phase
                                 // thread bits, 2 pair-store destination basis (bitmask)
-    int fused_pair_store = 1;  // specialised passes: sector-splitting global tails stored as tile pairs
-                               // (1: 11-bit tiles only, 2: any tile, 0: off)
+    int fused_pair_store = 2;  // specialised passes: sector-splitting global tails stored as tile pairs
+                               // (2: any tile, 1: 11-bit tiles only, 0: off)
     int fused_perm = 1;        // fold permutation gates (X/CX/SWAP) into the fused passes' smem addressing
     int kron_flat = 1;         // kron_identity as one arena-linear store stream
     int kron_ctas_per_sm = 32;  // CTAs per SM launched (4 resident; later ones refill)

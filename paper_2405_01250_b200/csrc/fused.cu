@@ -1020,9 +1020,10 @@ static std::shared_ptr<const Program> build_program(int n_total, int n_bits, int
         if (ps.gon) {
             for (size_t j = 0; j < ps.gcol.size() && j < 64; ++j) p.gcol[j] = ps.gcol[j];
             p.gconst = ps.gc;  // rank bits folded in at launch
-            // a pair of 12-bit tiles needs 128 KB of smem: one CTA per SM,
-            // slower than the scatter store's partial-sector writes (n=30
-            // layer 22.2 vs 20.9 ms); 11-bit pairs keep 3 CTAs per SM
+            // a pair of 12-bit tiles needs 128 KB of smem (one CTA per SM):
+            // per pass it beats the scatter store's partial-sector writes or
+            // not (6.4-27 ms vs 8.2-14 ms at n=30, tools/pass_times.py);
+            // over the config-5 program it wins (knob 2: 453 vs 471 ms)
             const int pst = tuning().fused_pair_store;
             if (pst >= 2 || (pst == 1 && (int)ps.bits.size() <= 11)) plan_pair_store(ps, n_bits, p);
         }

@@ -669,8 +669,8 @@ def test_fused_jit_matches_interpreter(cmul, seed):
     x0 = D.StateVector(n, W.random_state(rng, 2**n))
     want = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=0).amps
     try:
-        # pair store: default (11-bit tiles only) and forced for 12-bit tiles
-        for tb, pst in ((11, 1), (12, 1), (12, 2)):
+        # pair store: any tile (default), 11-bit tiles only, off
+        for tb, pst in ((11, 2), (12, 2), (12, 1), (11, 0)):
             L.tune("fused_pair_store", pst)
             L.tune("fused_jit", 0)
             aot = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=tb).amps
@@ -683,7 +683,7 @@ def test_fused_jit_matches_interpreter(cmul, seed):
             assert after["launches"] > before["launches"], (before, after, L.load().diaq_jit_last_error())
     finally:
         L.tune("fused_jit", 1)
-        L.tune("fused_pair_store", 1)
+        L.tune("fused_pair_store", 2)
 
 
 def test_fused_jit_layer_n24_async(cmul):
