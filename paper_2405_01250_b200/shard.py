@@ -358,6 +358,9 @@ class ShardedState:
         if self.peer and any(src != r for r, nd in enumerate(needs) for src in nd.values()):
             self._apply_peer(g, shifts, needs, cmul_mode)
             return
+        if g is _SWAP and sum(s >= lb for s in shifts) == 1:
+            self._swap_staged(*sorted(shifts, reverse=True))
+            return
         sends = [(q, self.local) for q in range(self.comm.world) if q != me and me in needs[q].values()]
         recvs = [(src, self._recv_buffer(src)) for src in sorted(set(needs[me].values())) if src != me]
         if recvs or sends:
@@ -371,6 +374,22 @@ class ShardedState:
         for b, src in needs[me].items():
             srcs[b] = self.local if src == me else self._recv[src]
         self.apply_fn(n, lb, g, shifts, me, srcs, self.local, cmul_mode)
+
+    def _swap_staged(self, gbit: int, vbit: int) -> None:
+        """Remapping swap of global bit gbit and local bit vbit over the staged
+        transport: only the half shard whose v bit differs from this rank's g
+        bit crosses (packed, one send/recv with the partner), in place --
+        pure copies, bitwise the SWAP gate."""
+        lb, me = self.local_bits, self.comm.rank
+        a = (me >> (gbit - lb)) & 1
+        partner = me ^ (1 << (gbit - lb))
+        view = self.local.view(-1, 2, 1 << vbit)[:, 1 - a, :]
+        send = view.contiguous()
+        recv = self._recv_buffer(partner)[: send.numel()].view_as(send)
+        self.stats["exchanged"] += 1
+        self.stats["bytes_received"] += 16 * send.numel()
+        self.comm.exchange([(partner, send)], [(partner, recv)])
+        view.copy_(recv)
 
     def _apply_peer(self, g, shifts, needs, cmul_mode) -> None:
         """Cross-shard gate reading partner shards in place over peer memory."""

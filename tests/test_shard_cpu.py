@@ -184,6 +184,10 @@ def test_sharded_remap_matches_oracle(world):
     assert stats["swaps"] > 0
     _, _, base = run_world(world, n, ops)
     assert stats["bytes_received"] < base["bytes_received"]
+    # staged transport: a remapping swap moves half a shard, packed
+    shard = 16 * 2 ** (n - (world.bit_length() - 1))
+    assert stats["bytes_received"] % (shard // 2) == 0
+    assert stats["bytes_received"] < stats["exchanged"] * shard
 
 
 def _dense_apply(x, g, shifts):
