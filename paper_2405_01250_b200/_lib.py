@@ -180,15 +180,27 @@ def torch():
     return _torch
 
 
+_cuda_ok = False
+
+
 def device():
+    global _cuda_ok
     t = torch()
-    if not t.cuda.is_available():
-        raise DeviceError("no CUDA device visible: the DiaQ B200 path has no CPU fallback")
+    if not _cuda_ok:  # checked once: a visible device stays visible
+        if not t.cuda.is_available():
+            raise DeviceError("no CUDA device visible: the DiaQ B200 path has no CPU fallback")
+        _cuda_ok = True
     return t.device("cuda", t.cuda.current_device())
 
 
 def stream_handle() -> int:
-    return int(torch().cuda.current_stream().cuda_stream)
+    """cudaStream_t of torch's current stream on the current device (the raw
+    accessor avoids building a Stream object per call: ~0.1 vs 3 us)."""
+    t = torch()
+    raw = getattr(t._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return int(raw(t.cuda.current_device()))
+    return int(t.cuda.current_stream().cuda_stream)
 
 
 def empty_c128(n: int):
