@@ -8,6 +8,8 @@
   n=22 placement bitwise; a CX is an exact permutation; G then G^dagger
   returns x to 1e-13.
 * spgemm at n=20: bitwise against the oracle.
+* config 5 at n=30: norm preserved to 1e-10; 2 emulated shards with qubit
+  remapping equal the unsharded run bitwise.
 """
 from __future__ import annotations
 
@@ -102,3 +104,22 @@ def test_spgemm_n20_bitwise():
         r, i = oc.diag(d)
         got = C.get(d)
         assert np.array_equal(got.re, r) and np.array_equal(got.im, i), d
+
+
+def test_config5_n30_norm_and_sharded_remap(torch, cmul):
+    """Config 5 at its 1-GPU size (n=30, 16 GiB state): the fused run keeps
+    the norm (|1-||psi||| < 1e-10, the BASELINE criterion), and the same
+    circuit on 2 emulated shards with qubit remapping (half-shard swaps,
+    layout restored) gives the bitwise same state (config-5 gate mix)."""
+    from paper_2405_01250_b200.shard import run_emulated
+    n, layers = 30, 6
+    ops = W.random_layered_ops(n, layers, seed=0)
+    pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
+    st = D.init_state(n, max_qubits=30)
+    D.run_gates(st, pls, cmul_mode=cmul, inplace=True)
+    assert abs(1.0 - st.norm()) < 1e-10
+    shards, stats = run_emulated(n, 2, pls, cmul_mode=cmul, remap=True)
+    assert stats["swaps"] > 0
+    half = 2 ** (n - 1)
+    for r, sh in enumerate(shards):
+        assert torch.equal(sh, st.device_amps[r * half:(r + 1) * half]), r
