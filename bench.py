@@ -434,7 +434,7 @@ def replica_gates(args, D, L, W, torch, dist, n, world, x, s, dev):
     g_ms = max_over_ranks(dist, ge0.elapsed_time(ge1), dev)
     g_norm = state.norm()
     extra = {"gates_per_step": len(pls), "steps": g_steps, "mode": f"replicas x{world}",
-             "fused_tile_bits": D.sim.FUSE_TILE_BITS if D.sim.FUSE_TILE_BITS > 0 else "auto (11 or 12: fewer passes, ties 11)", "hbm_passes": int(g_launches),
+             "fused_tile_bits": D.sim.FUSE_TILE_BITS if D.sim.FUSE_TILE_BITS > 0 else "auto (11 or 12: 12 only with >12% fewer passes)", "hbm_passes": int(g_launches),
              "specialised_passes": {"launches_timed": jst1["launches"] - jst0["launches"], "compiled": jst1["compiled"],
                                     "failed": jst1["failed"], "compile_cpu_ms": jst1["compile_ms"],
                                     "wait_after_warmup_s": round(jit_wait_s, 3),

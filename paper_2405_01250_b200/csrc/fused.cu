@@ -1086,8 +1086,9 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
     const bool sharded = n_total > n_bits;
     cudaStream_t s = (cudaStream_t)stream;
     // tile_bits 12 -> 16 amplitudes per thread (R = 4), 11 -> 8 (R = 3); 256
-    // threads.  tile_bits <= 0: schedule both, keep the one with fewer HBM
-    // passes (a tie goes to 11: smaller tiles keep 3 CTAs per SM)
+    // threads.  tile_bits <= 0: schedule both and keep the cheaper: a 12-bit
+    // pass costs ~1.14x an 11-bit one (2 vs 3 CTAs per SM; measured 1.13-1.14
+    // over 20-layer programs at n=24/28/30), so 12 wins only with >12% fewer passes
     int T = tile_bits >= kThreadBits + 4 ? kThreadBits + 4 : kThreadBits + 3;
     int rc = DIAQ_OK;
     std::shared_ptr<const Program> prog = cached_program(n_total, n_bits, T, ngates, gates, rc);
@@ -1096,7 +1097,7 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
         T = kThreadBits + 3;
         std::shared_ptr<const Program> big = cached_program(n_total, n_bits, kThreadBits + 4, ngates, gates, rc);
         if (!big) return rc;
-        if (big->plan.size() < prog->plan.size()) {
+        if (114 * big->plan.size() < 100 * prog->plan.size()) {
             prog = big;
             T = kThreadBits + 4;
         }

@@ -51,9 +51,9 @@ def _probe_numpy_cmul() -> int:
 CMUL_MODE = _probe_numpy_cmul()
 
 # shared-memory tile of the fused multi-gate passes (diaq_run_gates_fused):
-# 11 or 12 bits, -1 lets the library pick per circuit (fewer HBM passes;
-# ties go to 11); 0 applies every gate as its own HBM sweep.  Results are
-# identical.
+# 11 or 12 bits, -1 lets the library pick per circuit (12 only with >12%
+# fewer HBM passes: its passes cost ~1.14x); 0 applies every gate as its own
+# HBM sweep.  Results are identical.
 FUSE_TILE_BITS = -1
 
 
