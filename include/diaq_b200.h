@@ -206,6 +206,18 @@ int diaq_free(void *ptr);
 int diaq_ipc_handle(const void *ptr, void *handle_out);
 int diaq_ipc_open(const void *handle, void **ptr_out);
 int diaq_ipc_close(void *ptr);
+/* Cross-rank ordering of the peer transport without host synchronisation:
+ * an interprocess event per rank (cudaEventInterprocess), exported with
+ * diaq_ipc_event_handle (DIAQ_IPC_HANDLE_BYTES bytes) and opened by the
+ * partners; a rank records its event before a cross-shard gate, the ranks
+ * pass a host barrier (which orders the enqueueing only), and each stream
+ * waits on the partners' events before the multi-source kernel. */
+int diaq_ipc_event_create(void **ev);
+int diaq_ipc_event_handle(void *ev, void *handle_out);
+int diaq_ipc_event_open(const void *handle, void **ev_out);
+int diaq_event_record(void *ev, void *stream);
+int diaq_stream_wait_event(void *stream, void *ev);
+int diaq_event_destroy(void *ev);
 
 /* ---- sampling (reference measure_all_sample, sim.py:142-161) -------------
  * hits[k] = min(#{i : cdf_i <= u_k}, N-1) with cdf = sequential float64

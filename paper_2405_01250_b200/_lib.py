@@ -98,6 +98,12 @@ _SIGS = {
     "diaq_ipc_handle": ([_P, _P], _INT),
     "diaq_ipc_open": ([_P, _P], _INT),
     "diaq_ipc_close": ([_P], _INT),
+    "diaq_ipc_event_create": ([_P], _INT),
+    "diaq_ipc_event_handle": ([_P, _P], _INT),
+    "diaq_ipc_event_open": ([_P, _P], _INT),
+    "diaq_event_record": ([_P, _P], _INT),
+    "diaq_stream_wait_event": ([_P, _P], _INT),
+    "diaq_event_destroy": ([_P], _INT),
     "diaq_sample_hits": ([_I64, _P, _P, _I64, _P, _P, _P], _INT),
     "diaq_timer_create": ([_INT, _P], _INT),
     "diaq_timer_record": ([_P, _P], _INT),
@@ -318,3 +324,33 @@ def ipc_open(handle: bytes) -> int:
 
 def ipc_close(ptr: int) -> None:
     call("diaq_ipc_close", ctypes.c_void_p(ptr))
+
+
+def ipc_event_create() -> int:
+    e = ctypes.c_void_p()
+    call("diaq_ipc_event_create", ctypes.byref(e))
+    return int(e.value)
+
+
+def ipc_event_handle(ev: int) -> bytes:
+    buf = ctypes.create_string_buffer(DIAQ_IPC_HANDLE_BYTES)
+    call("diaq_ipc_event_handle", ctypes.c_void_p(ev), buf)
+    return buf.raw
+
+
+def ipc_event_open(handle: bytes) -> int:
+    e = ctypes.c_void_p()
+    call("diaq_ipc_event_open", ctypes.create_string_buffer(handle, DIAQ_IPC_HANDLE_BYTES), ctypes.byref(e))
+    return int(e.value)
+
+
+def event_record(ev: int) -> None:
+    call("diaq_event_record", ctypes.c_void_p(ev), stream_handle())
+
+
+def stream_wait_event(ev: int) -> None:
+    call("diaq_stream_wait_event", stream_handle(), ctypes.c_void_p(ev))
+
+
+def event_destroy(ev: int) -> None:
+    call("diaq_event_destroy", ctypes.c_void_p(ev))

@@ -27,10 +27,12 @@ struct Tuning {
     int fused_gperm = 1;       // trailing permutation runs leaving the tile folded into the pass's store
     int fused_seq = 1;         // sequence phases (compile-time register bit per dense step)
     int fused_nbuf = 0;        // fused pass tile buffers: 0 auto (2 unless it costs occupancy), 1, 2
+    int fused_tbits = 7;       // thread bits of the fused passes (8: 256 threads; 7: 128 threads x 16 amplitudes, T = 11)
     int fused_jit = 1;         // fused passes specialised per structure (NVRTC): 0 off, 1 async, 2 compile first
     int fused_gstore = 0;      // global-map (out-of-place permuted) store policy: 0 .cs, 1 default, 2 evict_last
     int fused_bank_spread = 3;  // fused passes, quarter-warp lanes on bank-spreading positions: 1 phase
                                 // thread bits, 2 pair-store destination basis (bitmask)
+    int fused_plain_pair = 1;  // specialised passes over 128-byte tile rows: tiles paired across bit 3 (256-byte DRAM runs)
     int fused_pair_store = 2;  // specialised passes: sector-splitting global tails stored as tile pairs
                                // (2: any tile, 1: 11-bit tiles only, 0: off)
     int fused_perm = 1;        // fold permutation gates (X/CX/SWAP) into the fused passes' smem addressing

@@ -36,11 +36,20 @@
 #include "fused_dev.cuh"
 #include "fused_jit.cuh"
 
+extern "C" const char *diaq_jit_last_error(void);
+
 namespace diaq {
 
 template <int R, int MODE>
 __global__ void __launch_bounds__(kThreads, R >= 4 ? 2 : 3) tile_pass_kernel(const __grid_constant__ TileParams p) {
     tile_pass_body<R, MODE>(p, p);
+}
+
+// 128 threads x 16 amplitudes (T = 11, R = 4): the layout of the default
+// specialised passes (fused_tbits 7), interpreted while they compile
+template <int MODE>
+__global__ void __launch_bounds__(128, 4) tile_pass_kernel_t7(const __grid_constant__ TileParams p) {
+    tile_pass_body<4, MODE, 7>(p, p);
 }
 
 // ---- host: analysis, scheduling, packing ------------------------------------
@@ -390,6 +399,11 @@ static int pack_smem_gate(const diaq_gate_t &gt, const std::vector<int> &bits, P
 // set while re-planning a call without the out-of-place permutation tails
 // (no room for the state-sized buffer they need)
 static thread_local bool t_no_gperm = false;
+
+// thread bits of a tiled pass: 8 (256 threads; T = 11 -> R = 3, T = 12 -> R = 4)
+// or 7 (128 threads, T = 11, R = 4: a phase covers one more qubit, so a pass
+// needs fewer smem round trips, and CTAs are smaller -- the default)
+static int pass_tbits() { return tuning().fused_tbits == 7 ? 7 : 8; }
 
 // Shared-memory banks: a 16-byte access is served per quarter warp (lanes
 // differing in thread bits 0-2); its 8 slots hit 8 distinct 16-byte bank
@@ -844,9 +858,9 @@ static std::vector<char> program_key(int n_total, int n_bits, int T, int ngates,
         key.insert(key.end(), c, c + n);
     };
     // every tuning switch the schedule depends on is part of the key
-    const int head[11] = {n_total, n_bits, T, ngates, tuning().fused_perm,
+    const int head[13] = {n_total, n_bits, T, pass_tbits(), ngates, tuning().fused_perm,
                           tuning().fused_gperm && !t_no_gperm, tuning().fused_seq, tuning().fused_dense2,
-                          tuning().fused_gperm_rows, tuning().fused_pair_store, tuning().fused_bank_spread};
+                          tuning().fused_gperm_rows, tuning().fused_pair_store, tuning().fused_bank_spread, tuning().fused_plain_pair};
     put(head, sizeof(head));
     for (int i = 0; i < ngates; ++i) {
         const diaq_gate_t &gt = gates[i];
@@ -984,7 +998,7 @@ static std::shared_ptr<const Program> build_program(int n_total, int n_bits, int
     auto prog = std::make_shared<Program>();
     std::vector<PassPlan> &plan = prog->plan;
     if (n_bits >= T) {
-        rc = schedule(n_bits, n_total, ngates, gates, T, T - kThreadBits, plan);
+        rc = schedule(n_bits, n_total, ngates, gates, T, T - pass_tbits(), plan);
         if (rc) return nullptr;
     } else {  // state smaller than a tile: gate by gate (standalone path)
         for (int i = 0; i < ngates; ++i) {
@@ -1026,6 +1040,17 @@ static std::shared_ptr<const Program> build_program(int n_total, int n_bits, int
             // over the config-5 program it wins (knob 2: 453 vs 471 ms)
             const int pst = tuning().fused_pair_store;
             if (pst >= 2 || (pst == 1 && (int)ps.bits.size() <= 11)) plan_pair_store(ps, n_bits, p);
+        }
+        if (!ps.gon && tuning().fused_plain_pair && n_bits > p.tbits) {
+            int lowest = 0;  // lowest state bit outside the tile: tile rows are 2^lowest amplitudes
+            while (lowest < n_bits && ((p.tmask >> lowest) & 1ull)) ++lowest;
+            if (lowest == kLowBits) {
+                p.ppair = 1;
+                p.gpb[0] = (int8_t)lowest;
+                p.emask = p.tmask | (1ull << lowest);
+                for (int k = 0, b = 0; b < 64; ++b)
+                    if ((p.emask >> b) & 1ull) p.eb[k++] = (int8_t)b;
+            }
         }
         std::copy(ps.phases.begin(), ps.phases.end(), p.ph);
         std::copy(ps.gates.begin(), ps.gates.end(), p.g);
@@ -1090,10 +1115,11 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
     // pass costs ~1.14x an 11-bit one (2 vs 3 CTAs per SM; measured 1.13-1.14
     // over 20-layer programs at n=24/28/30), so 12 wins only with >12% fewer passes
     int T = tile_bits >= kThreadBits + 4 ? kThreadBits + 4 : kThreadBits + 3;
+    if (pass_tbits() == 7) T = kThreadBits + 3;  // 128 threads x 16 amplitudes (R = 4 is the widest phase)
     int rc = DIAQ_OK;
     std::shared_ptr<const Program> prog = cached_program(n_total, n_bits, T, ngates, gates, rc);
     if (!prog) return rc;
-    if (tile_bits <= 0) {
+    if (tile_bits <= 0 && pass_tbits() == 8) {
         T = kThreadBits + 3;
         std::shared_ptr<const Program> big = cached_program(n_total, n_bits, kThreadBits + 4, ngates, gates, rc);
         if (!big) return rc;
@@ -1102,7 +1128,8 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
             T = kThreadBits + 4;
         }
     }
-    const int R = T - kThreadBits;
+    const int R = T - pass_tbits();
+    const int tbits = T - R;
     const std::vector<PassPlan> &plan = prog->plan;
     if (npasses) *npasses = (int)plan.size();
     // specialised kernels: requested once per (program, mode); passes whose
@@ -1129,6 +1156,8 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
         cudaFuncSetAttribute(tile_pass_kernel<3, DIAQ_CMUL_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
         cudaFuncSetAttribute(tile_pass_kernel<4, DIAQ_CMUL_FMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
         cudaFuncSetAttribute(tile_pass_kernel<4, DIAQ_CMUL_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+        cudaFuncSetAttribute(tile_pass_kernel_t7<DIAQ_CMUL_FMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+        cudaFuncSetAttribute(tile_pass_kernel_t7<DIAQ_CMUL_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
         cudaGetLastError();
         attr_set[cur_dev] = true;
     }
@@ -1189,7 +1218,10 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
             if (p.gperm && sharded)  // controls on global bits: constants of this rank
                 for (int g = 0; g < 64 && g < n_total - n_bits; ++g)
                     if (((uint64_t)rank >> g) & 1ull) p.gconst ^= ps.ggcol[(size_t)g];
-            const void *f = R >= 4 ? tile_kernel_ptr<4>(cmul_mode) : tile_kernel_ptr<3>(cmul_mode);
+            const void *f = tbits == 7 ? (cmul_mode == DIAQ_CMUL_FMA ? (const void *)tile_pass_kernel_t7<DIAQ_CMUL_FMA>
+                                                                    : (const void *)tile_pass_kernel_t7<DIAQ_CMUL_PLAIN>)
+                            : R >= 4 ? tile_kernel_ptr<4>(cmul_mode) : tile_kernel_ptr<3>(cmul_mode);
+            const int nthreads = 1 << tbits;
             auto smem_for = [&](int nb) {
                 return ((sizeof(double2) * nb) << p.tbits) + ((sizeof(uint64_t) * (p.gperm ? 2 : 1)) << (p.tbits - kLowBits));
             };
@@ -1201,10 +1233,10 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
             }
             // two tile buffers (prefetch) unless that costs a resident CTA
             const int knob = tuning().fused_nbuf;
-            int per_sm = occupancy(f, kThreads, smem_for(1));
+            int per_sm = occupancy(f, nthreads, smem_for(1));
             p.nbuf = 1;
             if (knob != 1) {
-                const int per_sm2 = occupancy(f, kThreads, smem_for(2));
+                const int per_sm2 = occupancy(f, nthreads, smem_for(2));
                 if (knob == 2 || per_sm2 >= per_sm) {
                     p.nbuf = 2;
                     per_sm = per_sm2;
@@ -1218,7 +1250,7 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
             for (int b = 0, k = 0; b < 64 && ((uint64_t)grid >> k) != 0; ++b)
                 if (!((p.tmask >> b) & 1ull)) p.gstep |= (((uint64_t)grid >> k++) & 1ull) << b;
             void *args[] = {(void *)&p};
-            cudaLaunchKernel(f, dim3((unsigned)grid), dim3(kThreads), args, smem, s);
+            cudaLaunchKernel(f, dim3((unsigned)grid), dim3((unsigned)nthreads), args, smem, s);
             count_launch();
             rc = check_launch("tile_pass_kernel");
         }
@@ -1255,14 +1287,14 @@ extern "C" int diaq_fused_plan(int n_bits, int local_bits, int ngates, const dia
                                int *stats) {
     if (ngates < 0 || (ngates > 0 && !gates) || !stats) return set_error(DIAQ_ERR_VALUE, "diaq_fused_plan: bad arguments");
     if (local_bits < 1 || local_bits > n_bits) return set_error(DIAQ_ERR_SHAPE, "local_bits %d invalid", local_bits);
-    const int T = tile_bits >= kThreadBits + 4 ? kThreadBits + 4 : kThreadBits + 3;
+    const int T = (tile_bits >= kThreadBits + 4 && pass_tbits() == 8) ? kThreadBits + 4 : kThreadBits + 3;
     for (int i = 0; i < 5; ++i) stats[i] = 0;
     if (local_bits < T) {  // gate by gate
         stats[0] = stats[1] = ngates;
         return DIAQ_OK;
     }
     std::vector<PassPlan> plan;
-    const int rc = schedule(local_bits, n_bits, ngates, gates, T, T - kThreadBits, plan);
+    const int rc = schedule(local_bits, n_bits, ngates, gates, T, T - pass_tbits(), plan);
     if (rc) return rc;
     if (getenv("DIAQ_PLAN_DEBUG")) debug_plan(plan);
     for (const PassPlan &ps : plan) {
@@ -1286,18 +1318,18 @@ extern "C" int diaq_fused_jit_compile(int n_bits, int local_bits, int ngates, co
         return set_error(DIAQ_ERR_VALUE, "diaq_fused_jit_compile: bad arguments");
     if (local_bits < 1 || local_bits > n_bits) return set_error(DIAQ_ERR_SHAPE, "local_bits %d invalid", local_bits);
     if (cmul_mode != 0 && cmul_mode != 1) return set_error(DIAQ_ERR_VALUE, "cmul_mode %d", cmul_mode);
-    const int T = tile_bits >= kThreadBits + 4 ? kThreadBits + 4 : kThreadBits + 3;
+    const int T = (tile_bits >= kThreadBits + 4 && pass_tbits() == 8) ? kThreadBits + 4 : kThreadBits + 3;
     int rc = DIAQ_OK;
     std::shared_ptr<const Program> prog = build_program(n_bits, local_bits, T, ngates, gates, rc);
     if (!prog) return rc;
     if (!seconds) {  // submit to the background compile queue (as a first run_gates call would)
         std::vector<std::shared_ptr<JitPass>> out;
-        jit_request(prog->tiled(), T - kThreadBits, cmul_mode, false, out);
+        jit_request(prog->tiled(), T - pass_tbits(), cmul_mode, false, out);
         *kernels = 0;
         for (auto &e : out) *kernels += e ? 1 : 0;
         return DIAQ_OK;
     }
-    return jit_compile_now(prog->tiled(), T - kThreadBits, cmul_mode, *seconds, *kernels);
+    return jit_compile_now(prog->tiled(), T - pass_tbits(), cmul_mode, *seconds, *kernels);
 }
 
 extern "C" int diaq_run_gates_local(int n_bits, int local_bits, int64_t rank, int ngates, const diaq_gate_t *gates,

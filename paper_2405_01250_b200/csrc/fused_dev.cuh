@@ -139,6 +139,13 @@ struct TileParams {
     // gw[0..] = e0 (e1, e2) first, and gsrc[k] = tile offset | (half << 12)
     // of gw[k]'s source.  gnp = 0: per-element scatter store.
     int8_t gnp;
+    // Plain pair (specialised passes, no global tail): the tile and its
+    // partner across gpb[0] (the lowest non-tile bit, when that is bit 3)
+    // are loaded, computed and stored together by one CTA, so every DRAM
+    // access is a 256-byte run instead of two 128-byte halves visited by
+    // different CTAs at different times (row-buffer locality: a pass over
+    // high tile bits ran 1.98 ms against 1.50 ms with 256-byte runs, r02e)
+    int8_t ppair;
     int8_t gpb[3];
     int8_t eb[kMaxTileBits + 3];
     uint64_t emask;
@@ -441,7 +448,7 @@ __device__ __forceinline__ void seq_steps(double2 (&v)[1 << R], const TileParams
 // a runtime-specialised kernel (fused_jit.cu) binds S to a constant copy, so
 // every loop over phases and gates unrolls and every branch on the gate
 // records folds at compile time -- same arithmetic, same order, no decode.
-template <int R, int MODE>
+template <int R, int MODE, int TB = kThreadBits>
 __device__ __forceinline__ void tile_pass_body(const TileParams &p, const TileParams &S) {
     // dynamic smem: nbuf tiles, then the row-offset table, then (gperm) the
     // global-map table -- sized by T, so small tiles leave room for 3 CTAs
@@ -453,10 +460,11 @@ __device__ __forceinline__ void tile_pass_body(const TileParams &p, const TilePa
     // per-(phase, thread) index part of the thread bits, computed once per
     // CTA instead of once per tile (register parts ride in the phase record)
     constexpr int kPre = kPrePhases;
-    __shared__ uint16_t s_tpart[kPre][kThreads];
-    __shared__ uint16_t s_pt[kPre][kThreads];  // folded permutations: swizzled image of the thread part
-    __shared__ uint16_t s_lt[kThreads];
-    __shared__ uint16_t s_lk[1 << (kMaxTileBits - kThreadBits)];
+    constexpr int NT = 1 << TB;  // threads
+    __shared__ uint16_t s_tpart[kPre][NT];
+    __shared__ uint16_t s_pt[kPre][NT];  // folded permutations: swizzled image of the thread part
+    __shared__ uint16_t s_lt[NT];
+    __shared__ uint16_t s_lk[1 << (kMaxTileBits - TB)];
     __shared__ uint64_t s_sbase;  // current tile's base | rank bits (selector lookups)
     constexpr int NR = 1 << R;
     const double2 *sc = p.coef;
@@ -482,31 +490,31 @@ __device__ __forceinline__ void tile_pass_body(const TileParams &p, const TilePa
     }
     if (S.pre.on) {
         s_lt[threadIdx.x] = (uint16_t)swz(aff_lin(S.pre, threadIdx.x, T));
-        if (threadIdx.x < (tsize >> kThreadBits)) s_lk[threadIdx.x] = (uint16_t)swz(aff_lin(S.pre, threadIdx.x << kThreadBits, T));
+        if (threadIdx.x < (tsize >> TB)) s_lk[threadIdx.x] = (uint16_t)swz(aff_lin(S.pre, threadIdx.x << TB, T));
     }
     __shared__ uint64_t glo[1 << kLowBits];  // global map of the in-row offsets
 #ifdef DIAQ_JIT
     // pair store (see TileParams::gnp): destination offsets / sources of the
     // high enumeration bits (uniform table) and of this thread's low bits
     const bool pairing = S.gnp > 0;
-    __shared__ uint64_t s_pw[1 << (kMaxTileBits + 1 - kThreadBits)];
-    __shared__ uint16_t s_ps[1 << (kMaxTileBits + 1 - kThreadBits)];
+    __shared__ uint64_t s_pw[1 << (kMaxTileBits + 1 - TB)];
+    __shared__ uint16_t s_ps[1 << (kMaxTileBits + 1 - TB)];
     uint64_t pw_t = 0;
     uint32_t ps_t = 0;
     if (pairing) {
         const int dims = T + S.gnp;
         DIAQ_SUNROLL
-        for (int k = 0; k < kThreadBits; ++k)
+        for (int k = 0; k < TB; ++k)
             if ((threadIdx.x >> k) & 1u) {
                 pw_t ^= S.gw[k];
                 ps_t ^= S.gsrc[k];
             }
-        if (threadIdx.x < (1u << (dims - kThreadBits))) {
+        if (threadIdx.x < (1u << (dims - TB))) {
             uint64_t w = 0;
             uint32_t sr = 0;
             DIAQ_SUNROLL
-            for (int k = kThreadBits; k < dims; ++k)
-                if ((threadIdx.x >> (k - kThreadBits)) & 1u) {
+            for (int k = TB; k < dims; ++k)
+                if ((threadIdx.x >> (k - TB)) & 1u) {
                     w ^= S.gw[k];
                     sr ^= S.gsrc[k];
                 }
@@ -541,7 +549,7 @@ __device__ __forceinline__ void tile_pass_body(const TileParams &p, const TilePa
             const uint32_t lt = s_lt[threadIdx.x] ^ swz(aff_const(S.pre, b | p.gbase));
         #pragma unroll 1
             for (int k = 0; k < NR; ++k) {
-                const uint32_t e = threadIdx.x + (uint32_t)k * kThreads;
+                const uint32_t e = threadIdx.x + ((uint32_t)k << TB);
 #ifdef DIAQ_JIT
                 // (ptxas 12.9 emitted a malformed LDGSTS for the policy form of
                 // this permuted-slot copy in specialised kernels: illegal
@@ -554,7 +562,7 @@ __device__ __forceinline__ void tile_pass_body(const TileParams &p, const TilePa
         } else {
         #pragma unroll 1
             for (int k = 0; k < NR; ++k) {
-                const uint32_t e = threadIdx.x + (uint32_t)k * kThreads;
+                const uint32_t e = threadIdx.x + ((uint32_t)k << TB);
                 cp_async16(buf + swz(e), p.x + b + (e & lowmask) + hi_off[e >> kLowBits], pol);
             }
         }
@@ -683,7 +691,7 @@ __device__ __forceinline__ void tile_pass_body(const TileParams &p, const TilePa
             }
         #pragma unroll 1
             for (int k = 0; k < NR; ++k) {
-                const uint32_t e = threadIdx.x + (uint32_t)k * kThreads;
+                const uint32_t e = threadIdx.x + ((uint32_t)k << TB);
                 double2 *dst = p.y + (ab ^ s_ghi[e >> kLowBits] ^ glo[e & lowmask]);
                 if (p.gstore == 0) st_stream(dst, tl[swz(e)]);
                 else if (p.gstore == 1) st_plain(dst, tl[swz(e)]);
@@ -692,7 +700,7 @@ __device__ __forceinline__ void tile_pass_body(const TileParams &p, const TilePa
         } else {
         #pragma unroll 1
             for (int k = 0; k < NR; ++k) {
-                const uint32_t e = threadIdx.x + (uint32_t)k * kThreads;
+                const uint32_t e = threadIdx.x + ((uint32_t)k << TB);
                 st_stream(p.y + base + (e & lowmask) + hi_off[e >> kLowBits], tl[swz(e)]);
             }
         }
@@ -702,5 +710,299 @@ __device__ __forceinline__ void tile_pass_body(const TileParams &p, const TilePa
         else if (more) fetch(base, tile);  // refill as soon as the tile is drained
     }
 }
+
+#ifdef DIAQ_JIT
+// ---- specialised pass body (NVRTC; the structure S is a compile-time constant) --
+//
+// Same schedule, arithmetic and results as tile_pass_body; what changes is the
+// address arithmetic, which the profile of the interpreted form put at about
+// half of the pass's non-FP64 instructions and a third of its stall samples
+// (r02b: the tile load/store loops waited on a shared-memory offset table):
+//   * tile element e = tid + 256 k lies at state offset
+//       b + (tid & 7) + dep(tid >> 3) + dep(32 k)
+//     (dep deposits row bits into the tile's state bits): the thread part is
+//     computed once per kernel, the k part is a constant of the pass, so a
+//     tile load/store costs one 64-bit add per element -- no table lookups;
+//   * the tile buffers are 1024-byte aligned, so for a slot s = sh | sl
+//     (sl its low three bits) and a per-phase thread part T = th | tl whose
+//     high bits are disjoint from sh, the byte address base + 16 (T ^ s) is
+//     (base + 16 T) ^ 16 sl + 16 sh: one LOP3, and the rest is the load's
+//     immediate offset.
+
+__device__ __forceinline__ double2 lds128(uint32_t a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void sts128(uint32_t a, double2 v) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+
+__device__ __forceinline__ void cp_async16_s(uint32_t dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+
+// byte address of slot s relative to a 128-byte aligned t16 = base + 16 T
+// whose high part is disjoint from s's (see above)
+__device__ __forceinline__ uint32_t slot_addr(uint32_t t16, uint32_t s) {
+    return (t16 ^ ((s & 7u) << 4)) + ((s & ~7u) << 4);
+}
+
+// state offset of tile rows h (bits of h -> tile bits 3.. of S)
+__device__ __forceinline__ uint64_t row_dep(const TileParams &S, uint32_t h) {
+    uint64_t off = 0;
+#pragma unroll
+    for (int j = kLowBits; j < kMaxTileBits; ++j)
+        if (j < S.tbits) off |= (uint64_t)((h >> (j - kLowBits)) & 1u) << S.tb[j];
+    return off;
+}
+
+// image of state offset o under the global permutation map (columns S.gcol)
+__device__ __forceinline__ uint64_t gmap(const TileParams &S, uint64_t o) {
+    uint64_t r = 0;
+#pragma unroll
+    for (int j = 0; j < 64; ++j)
+        if ((o >> j) & 1ull) r ^= S.gcol[j];
+    return r;
+}
+
+template <int R, int MODE>
+__device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const TileParams &S) {
+    extern __shared__ __align__(1024) double2 tile[];
+    const int T = S.tbits;
+    const int TB = T - R;  // thread bits: 2^TB threads (a constant of the pass)
+    constexpr int NR = 1 << R;
+    constexpr uint32_t lowmask = (1u << kLowBits) - 1u;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t tile0 = smem_u32(tile);
+    constexpr int kPre = kPrePhases;
+    __shared__ uint16_t s_t16[kPre][kThreads];  // 16 * swz(tpart) per phase (T <= 12: fits 16 bits)
+    __shared__ uint16_t s_pt[kPre][kThreads];   // folded permutations: swizzled image of the thread part
+    __shared__ uint16_t s_lt[kThreads];
+    __shared__ uint64_t s_sbase;  // current tile's base | rank bits (selector lookups)
+    __shared__ uint64_t s_ab;     // global-map image of the current tile / pair base
+    const double2 *sc = p.coef;
+    const uint32_t *snz = p.nz;
+    const int npre = S.nphases < kPre ? S.nphases : kPre;
+    DIAQ_SUNROLL
+    for (int ph_i = 0; ph_i < npre; ++ph_i) {
+        const Phase &ph = S.ph[ph_i];
+        uint32_t tpart = 0;
+        DIAQ_SUNROLL
+        for (int i = 0; i < TB; ++i) tpart |= ((tid >> i) & 1u) << ph.tpos[i];
+        s_t16[ph_i][tid] = (uint16_t)(swz(tpart) << 4);
+        if (ph.post.on) s_pt[ph_i][tid] = (uint16_t)swz(aff_lin(ph.post, tpart, T));
+    }
+    if (S.pre.on) s_lt[tid] = (uint16_t)swz(aff_lin(S.pre, tid, T));
+    // element k of this thread: state offset base + t_off + kdep(k)
+    const uint64_t t_off = (tid & lowmask) + row_dep(S, tid >> kLowBits);
+    auto kdep = [&](int k) -> uint64_t { return row_dep(S, (uint32_t)k << (TB - kLowBits)); };
+    const uint32_t t16 = swz(tid) << 4;
+    auto fetch = [&](uint64_t b, uint32_t buf) {
+        const double2 *src = p.x + (b + t_off);
+        if (S.pre.on) {  // element e lands in the slot of its relabelled index
+            const uint32_t lt = s_lt[tid] ^ swz(aff_const(S.pre, b | p.gbase));
+#pragma unroll
+            for (int k = 0; k < NR; ++k)
+                cp_async16_s(buf + ((lt ^ swz(aff_lin(S.pre, (uint32_t)k << TB, T))) << 4), src + kdep(k));
+        } else {
+            const uint32_t a = buf + t16;
+#pragma unroll
+            for (int k = 0; k < NR; ++k) cp_async16_s(slot_addr(a, swz((uint32_t)k << TB)), src + kdep(k));
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    __syncthreads();
+    auto phases = [&](uint32_t buf) {
+        double2 *tl = tile + ((buf - tile0) >> 4);
+        DIAQ_SUNROLL
+        for (int ph_i = 0; ph_i < S.nphases; ++ph_i) {
+            const Phase &ph = S.ph[ph_i];
+            if (ph.generic) {
+                DIAQ_SUNROLL
+                for (int gi = ph.g0; gi < ph.g1; ++gi) {
+                    smem_gate<MODE>(tl, T, S.g[gi], ld_base(&s_sbase), sc, snz);
+                    __syncthreads();
+                }
+                continue;
+            }
+            double2 v[NR];
+            // thread part of the phase's slots (dead code unless a selector or
+            // a folded store needs it; the address comes from the table)
+            uint32_t tpart = 0;
+            DIAQ_SUNROLL
+            for (int i = 0; i < TB; ++i) tpart |= ((tid >> i) & 1u) << ph.tpos[i];
+            const uint32_t a = buf + (ph_i < kPre ? (uint32_t)s_t16[ph_i][tid] : (swz(tpart) << 4));
+#pragma unroll
+            for (int j = 0; j < NR; ++j) v[j] = lds128(slot_addr(a, ph.pj[j]));
+            if (ph.seq) {
+                int gi = ph.g0;
+                seq_steps<R, MODE, 0>(v, S, ph, gi, tpart, &s_sbase, sc, snz);
+#pragma unroll
+                for (int c = 0; c < ph.nd_before[R]; ++c, ++gi) diag_uniform<R, MODE>(v, S.g[gi], tpart, &s_sbase, sc, snz);
+            } else {
+                DIAQ_SUNROLL
+                for (int gi = ph.g0; gi < ph.g1; ++gi) dispatch_gate<R, MODE>(v, S.g[gi], tpart, &s_sbase, sc, snz);
+            }
+            if (ph.post.on) {
+                __syncthreads();  // relabelled slots belong to other threads' registers: all reads first
+                const uint32_t bc = swz(aff_const(ph.post, ld_base(&s_sbase)));
+                const uint32_t pt = (ph_i < kPre ? (uint32_t)s_pt[ph_i][tid] : swz(aff_lin(ph.post, tpart, T))) ^ bc;
+#pragma unroll
+                for (int j = 0; j < NR; ++j) sts128(buf + ((pt ^ ph.ppj[j]) << 4), v[j]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < NR; ++j) sts128(slot_addr(a, ph.pj[j]), v[j]);
+            }
+            __syncthreads();
+        }
+    };
+    if (S.gnp > 0) {
+        // Pair store (see TileParams::gnp): the tile and its partner across
+        // gpb[0] in both buffers, every destination sector written whole.
+        // Destination / source of pair element i = tid + 256 m: pw_t ^ gw(m),
+        // ps_t ^ gsrc(m) with the m parts constants of the pass.
+        const int dims = T + S.gnp;
+        uint64_t pw_t = 0;
+        uint32_t ps_t = 0;
+#pragma unroll
+        for (int k = 0; k < TB; ++k)
+            if ((tid >> k) & 1u) {
+                pw_t ^= S.gw[k];
+                ps_t ^= S.gsrc[k];
+            }
+        // smem slot of a source (tile offset | half << 12), linear over GF(2)
+        auto pslot = [&](uint32_t src) -> uint32_t { return ((src >> 12) << T) ^ swz(src & 0xfffu); };
+        const uint32_t ps_slot = pslot(ps_t);
+        const uint64_t pbit = 1ull << S.gpb[0];
+        const int64_t nunits = p.ntiles >> 1;
+        const uint32_t buf1 = tile0 + (16u << T);
+        uint64_t gb = insert_zero_bits_dyn((uint64_t)blockIdx.x, S.eb, T + 1);
+        if ((int64_t)blockIdx.x < nunits) {
+            fetch(gb, tile0);
+            fetch(gb | pbit, buf1);
+        }
+        for (int64_t t = blockIdx.x; t < nunits; t += gridDim.x) {
+            const uint64_t ngb = ((gb | S.emask) + p.gstep) & ~S.emask;
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                if (tid == 0) {
+                    s_sbase = (gb | (h ? pbit : 0ull)) | p.gbase;
+                    if (h == 0) s_ab = p.gconst ^ gmap(S, gb);
+                }
+                __syncthreads();
+                phases(h ? buf1 : tile0);
+            }
+            __syncthreads();
+            const uint64_t ab = s_ab ^ pw_t;
+#pragma unroll
+            for (int i = 0; i < 2 * NR; ++i) {
+                if (i >= (1 << (dims - TB))) break;
+                uint64_t cw = 0;
+                uint32_t cs = 0;
+#pragma unroll
+                DIAQ_SUNROLL
+                for (int m = 0; m < dims - TB; ++m)
+                    if ((i >> m) & 1) {
+                        cw ^= S.gw[TB + m];
+                        cs ^= S.gsrc[TB + m];
+                    }
+                st_stream(p.y + (ab ^ cw), lds128(tile0 + ((ps_slot ^ pslot(cs)) << 4)));
+            }
+            __syncthreads();
+            gb = ngb;
+            if (t + gridDim.x < nunits) {
+                fetch(gb, tile0);
+                fetch(gb | pbit, buf1);
+            }
+        }
+        return;
+    }
+    if (S.ppair) {
+        const uint64_t pbit = 1ull << S.gpb[0];
+        const int64_t nunits = p.ntiles >> 1;
+        const uint32_t buf1 = tile0 + (16u << T);
+        const uint32_t a0 = tile0 + t16, a1 = buf1 + t16;
+        // both halves' elements k interleaved: adjacent 128-byte rows in flight together
+        auto fetch2 = [&](uint64_t b) {
+            const double2 *src = p.x + (b + t_off);
+#pragma unroll
+            for (int k = 0; k < NR; ++k) {
+                const uint32_t sl = swz((uint32_t)k << TB);
+                cp_async16_s(slot_addr(a0, sl), src + kdep(k));
+                cp_async16_s(slot_addr(a1, sl), src + (kdep(k) | pbit));
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        uint64_t gb = insert_zero_bits_dyn((uint64_t)blockIdx.x, S.eb, T + 1);
+        if ((int64_t)blockIdx.x < nunits) fetch2(gb);
+        for (int64_t t = blockIdx.x; t < nunits; t += gridDim.x) {
+            const uint64_t ngb = ((gb | S.emask) + p.gstep) & ~S.emask;
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                if (tid == 0) s_sbase = (gb | (h ? pbit : 0ull)) | p.gbase;
+                __syncthreads();
+                phases(h ? buf1 : tile0);
+            }
+            double2 *dst = p.y + (gb + t_off);
+#pragma unroll
+            for (int k = 0; k < NR; ++k) {
+                const uint32_t sl = swz((uint32_t)k << TB);
+                st_stream(dst + kdep(k), lds128(slot_addr(a0, sl)));
+                st_stream(dst + (kdep(k) | pbit), lds128(slot_addr(a1, sl)));
+            }
+            __syncthreads();
+            gb = ngb;
+            if (t + gridDim.x < nunits) fetch2(gb);
+        }
+        return;
+    }
+    // gperm scatter store: element e -> gconst ^ G(base) ^ G(t_off) ^ G(kdep(k))
+    const uint64_t g_t = S.gperm ? gmap(S, t_off) : 0ull;
+    uint64_t base = insert_zero_bits_dyn((uint64_t)blockIdx.x, S.tb, T);
+    if ((int64_t)blockIdx.x < p.ntiles) fetch(base, tile0);
+    uint32_t buf = tile0;
+    const uint32_t tstride = 16u << T;
+    for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+        const uint64_t nbase = next_base(base, p, S);
+        const bool more = t + gridDim.x < p.ntiles;
+        if (tid == 0) {
+            s_sbase = base | p.gbase;  // full-state index bits for selectors
+            if (S.gperm) s_ab = p.gconst ^ gmap(S, base);
+        }
+        if (p.nbuf == 2 && more) {
+            fetch(nbase, buf == tile0 ? tile0 + tstride : tile0);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        phases(buf);
+        const uint32_t a = buf + t16;
+        if (S.gperm) {  // trailing permutation run: element i goes to A i ^ c in the other buffer
+            const uint64_t ab = s_ab ^ g_t;
+#pragma unroll
+            for (int k = 0; k < NR; ++k) {
+                double2 *dst = p.y + (ab ^ gmap(S, kdep(k)));
+                const double2 v = lds128(slot_addr(a, swz((uint32_t)k << TB)));
+                if (p.gstore == 0) st_stream(dst, v);
+                else if (p.gstore == 1) st_plain(dst, v);
+                else st_hint(dst, v, policy_evict_last());
+            }
+        } else {
+            double2 *dst = p.y + (base + t_off);
+#pragma unroll
+            for (int k = 0; k < NR; ++k) st_stream(dst + kdep(k), lds128(slot_addr(a, swz((uint32_t)k << TB))));
+        }
+        __syncthreads();
+        base = nbase;
+        if (p.nbuf == 2) buf = (buf == tile0) ? tile0 + tstride : tile0;
+        else if (more) fetch(base, buf);  // refill as soon as the tile is drained
+    }
+}
+#endif  // DIAQ_JIT
 
 }  // namespace diaq

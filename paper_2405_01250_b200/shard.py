@@ -192,6 +192,19 @@ def _cuda_apply(n_bits, local_bits, g, shifts, rank, srcs, y, cmul_mode):
            arr, y.data_ptr(), int(cmul_mode), L.stream_handle())
 
 
+def collective_device(backend: str, like_device):
+    """Device the tensors of a host-side collective must live on for
+    `backend`: NCCL only moves CUDA tensors (torch registers it for "cuda"
+    only), gloo moves CPU tensors everywhere and CUDA tensors for some ops
+    only -- so CPU for everything but NCCL."""
+    import torch
+    if str(backend).lower() == "nccl":
+        if like_device is not None and torch.device(like_device).type == "cuda":
+            return torch.device(like_device)
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
 class TorchDistComm:
     """torch.distributed transport (NCCL on GPUs, gloo on CPU)."""
 
@@ -201,6 +214,10 @@ class TorchDistComm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        self.backend = str(dist.get_backend(group))
+
+    def _dev(self, like=None):
+        return collective_device(self.backend, getattr(like, "device", None))
 
     def exchange(self, sends, recvs) -> None:
         """sends: [(peer, tensor)], recvs: [(peer, tensor)] -- one batched group."""
@@ -212,18 +229,27 @@ class TorchDistComm:
             for req in self.dist.batch_isend_irecv(ops):
                 req.wait()
 
-    def allreduce_sum(self, value: float, like) -> float:
+    def allreduce_sum(self, value: float, like=None) -> float:
         import torch
-        t = torch.tensor([value], dtype=torch.float64, device=like.device)
+        t = torch.tensor([value], dtype=torch.float64, device=self._dev(like))
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
         return float(t.item())
 
-    def gather(self, local):
+    def allreduce_max(self, value: float, like=None) -> float:
         import torch
-        lr = torch.view_as_real(local)
+        t = torch.tensor([value], dtype=torch.float64, device=self._dev(like))
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+    def gather(self, local):
+        """Full state on rank 0 (tests only): every shard travels on the
+        backend's device, the result is returned on `local`'s device."""
+        import torch
+        dev = self._dev(local)
+        lr = torch.view_as_real(local).to(dev)
         parts = [torch.empty_like(lr) for _ in range(self.world)] if self.rank == 0 else None
         self.dist.gather(lr, parts, dst=0, group=self.group)
-        return torch.view_as_complex(torch.cat(parts)) if self.rank == 0 else None
+        return torch.view_as_complex(torch.cat(parts)).to(local.device) if self.rank == 0 else None
 
 
 class PeerComm(TorchDistComm):
@@ -231,17 +257,58 @@ class PeerComm(TorchDistComm):
     (CUDA IPC, NVLink/NVSwitch peer access) and the multi-source kernel reads
     partner amplitudes directly inside the gate pass -- no staging copy, the
     transfer overlaps the arithmetic.  Cross-shard gates then run out of
-    place into a second buffer (partners read this rank's current one), with
-    one host barrier per such gate: a rank only overwrites a buffer after
-    every partner finished reading it, and only reads a partner's buffer
-    after the partner finished writing it.  torch.distributed (any backend)
-    carries the handles, the barrier and the reductions."""
+    place into a second buffer (partners read this rank's current one): a
+    rank only overwrites a buffer after every partner finished reading it,
+    and only reads a partner's buffer after the partner finished writing it.
+
+    That ordering is device-side (order()): each rank records an
+    interprocess CUDA event on its stream, the ranks pass a host barrier on
+    a gloo side group (it orders the enqueueing only -- no GPU is drained),
+    and each stream waits on the partners' events.  Two events per rank
+    alternate between consecutive cross-shard gates, so a fast rank cannot
+    re-record an event a slow partner has yet to wait on.  torch.distributed
+    (any backend; collectives on the backend's device) carries the handles
+    and the reductions."""
 
     peer = True
 
     def __init__(self, group=None):
         super().__init__(group)
         self._opened: list[int] = []
+        # host barriers on a CPU side group: an NCCL barrier would launch a
+        # device collective and block the host on it
+        if self.backend.lower() == "gloo":
+            self.host_group = group
+        else:
+            ranks = list(range(self.dist.get_world_size())) if group is None else \
+                self.dist.get_process_group_ranks(group)
+            self.host_group = self.dist.new_group(ranks=ranks, backend="gloo")
+        self._events = None  # ([own event x2], [[partner event x2] per rank])
+        self._phase = 0
+
+    def host_barrier(self) -> None:
+        self.dist.barrier(group=self.host_group)
+
+    def _share_events(self) -> None:
+        own = [L.ipc_event_create() for _ in range(2)]
+        handles = [L.ipc_event_handle(e) for e in own]
+        allh = [None] * self.world
+        self.dist.all_gather_object(allh, handles, group=self.host_group)
+        peers = [[None, None] if q == self.rank else [L.ipc_event_open(h) for h in hs] for q, hs in enumerate(allh)]
+        self._events = (own, peers)
+
+    def order(self) -> None:
+        """Device-side ordering before a cross-shard gate (see the class doc)."""
+        if self._events is None:
+            self._share_events()
+        own, peers = self._events
+        k = self._phase
+        L.event_record(own[k])
+        self.host_barrier()
+        for q in range(self.world):
+            if q != self.rank:
+                L.stream_wait_event(peers[q][k])
+        self._phase ^= 1
 
     def share(self, ptrs: list[int]) -> list[list[int]]:
         """table[q][i] = this process's address of rank q's buffer i.  Every
@@ -254,7 +321,7 @@ class PeerComm(TorchDistComm):
         except Exception as e:  # noqa: BLE001 -- reported to every rank below
             mine, err = None, repr(e)
         allh = [None] * self.world
-        self.dist.all_gather_object(allh, mine, group=self.group)
+        self.dist.all_gather_object(allh, mine, group=self.host_group)
         table, opened = [], []
         if err is None and all(h is not None for h in allh):
             try:
@@ -272,7 +339,7 @@ class PeerComm(TorchDistComm):
         else:
             err = err or "a partner could not export its buffers"
         errs = [None] * self.world
-        self.dist.all_gather_object(errs, err, group=self.group)
+        self.dist.all_gather_object(errs, err, group=self.host_group)
         bad = [e for e in errs if e is not None]
         if bad:
             for ptr in opened:
@@ -282,22 +349,19 @@ class PeerComm(TorchDistComm):
         return table
 
     def barrier(self) -> None:
+        """Full barrier (setup and teardown): every rank's device work done."""
         L.torch().cuda.synchronize()
-        self.dist.barrier(group=self.group)
-
-    def allreduce_sum(self, value: float, like) -> float:
-        import torch
-        t = torch.tensor([value], dtype=torch.float64)
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
-        return float(t.item())
-
-    def gather(self, local):
-        return super().gather(local.cpu())
+        self.host_barrier()
 
     def close(self) -> None:
         for p in self._opened:
             L.ipc_close(p)
         self._opened = []
+        if self._events is not None:
+            own, _ = self._events
+            for e in own:
+                L.event_destroy(e)
+            self._events = None
 
 
 class ShardedState:
@@ -394,7 +458,7 @@ class ShardedState:
     def _apply_peer(self, g, shifts, needs, cmul_mode) -> None:
         """Cross-shard gate reading partner shards in place over peer memory."""
         n, lb, me = self.n_qubits, self.local_bits, self.comm.rank
-        self.comm.barrier()  # partners finished writing their current buffers / reading our next one
+        self.comm.order()  # partners finished writing their current buffers / reading our next one (device-side)
         kg = len(global_shifts(shifts, lb))
         srcs = [None] * (1 << kg)
         for b, src in needs[me].items():

@@ -66,31 +66,51 @@ class StateVector:
 
     def __init__(self, n_qubits: int, amps):
         self.n_qubits = int(n_qubits)
+        self._set(amps)
+
+    def _set(self, amps) -> None:
         t = L.torch()
         if isinstance(amps, t.Tensor) and amps.device.type == "cuda":
             self._dev = L.to_device_c128(amps.reshape(-1))
             self._host = None
         else:
-            self._host = np.ascontiguousarray(amps, dtype=np.complex128).reshape(-1)
+            # the caller's array is copied: the state owns its amplitudes, and
+            # the copy is the authoritative one until the first upload
+            self._host = np.array(amps, dtype=np.complex128, copy=True).reshape(-1)
             self._dev = None
 
     @property
     def device_amps(self):
         if self._dev is None:
             self._dev = L.to_device_c128(self._host)
+            # from now on the device copy is authoritative: the host copy is a
+            # read-only snapshot (an edit could not reach the device)
+            self._host.flags.writeable = False
         return self._dev
+
+    def _device_modified(self) -> None:
+        """The device amplitudes changed in place: drop the host snapshot."""
+        self._host = None
 
     @property
     def amps(self) -> np.ndarray:
-        """Host view of the amplitudes.  For a device-resident state this is a
-        read-only snapshot (writing to it could not reach the device copy)."""
+        """Host view of the amplitudes.  Writable only while the state has
+        never been uploaded; afterwards a read-only snapshot of the device
+        copy.  Assign `state.amps = array` to replace the amplitudes."""
         if self._host is None:
             self._host = self._dev.cpu().numpy()
             self._host.flags.writeable = False
         return self._host
 
+    @amps.setter
+    def amps(self, value) -> None:
+        value = np.asarray(value)
+        if value.size != len(self):
+            raise ShapeError(f"state has {len(self)} amplitudes, got {value.size}")
+        self._set(value)
+
     def __len__(self) -> int:
-        return int(self._dev.numel()) if self._host is None else len(self._host)
+        return int(self._dev.numel()) if self._dev is not None else len(self._host)
 
     def norm(self) -> float:
         return float(np.sqrt(norm2(self.device_amps)))

@@ -49,7 +49,7 @@ def main():
     full = st.gather()
     comm.barrier()  # nobody unmaps or frees while a partner may still read
     if a.rank == 0:
-        np.save(a.out, full.numpy())
+        np.save(a.out, full.cpu().numpy())
         with open(a.out + ".stats", "w") as f:
             f.write(repr({"stats": st.stats, "norm": norm}))
     comm.close()
@@ -80,7 +80,7 @@ def run_spmv(a, comm):
     comm.barrier()  # partners done reading our slice
     parts = comm.gather(y)
     if a.rank == 0:
-        np.save(a.out, parts.numpy())
+        np.save(a.out, parts.cpu().numpy())
     comm.barrier()
     comm.close()
     dist.destroy_process_group()

@@ -102,3 +102,40 @@ def test_bench_multi_rank_paths_on_one_gpu(tmp_path):
     assert line["gates"]["transport"] == "peer" and line["gates"]["stats"]["exchanged"] > 0
     assert abs(line["gates"]["norm_after"] - 1.0) < 1e-10
     assert line["gates"]["remap"] is True
+
+
+_NCCL_SCRIPT = r"""
+import sys
+sys.path.insert(0, {root!r})
+import torch, torch.distributed as dist
+import paper_2405_01250_b200 as D
+from paper_2405_01250_b200 import workloads as W
+from paper_2405_01250_b200.shard import PeerComm, ShardedState, TorchDistComm
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", init_method="tcp://127.0.0.1:{port}", rank=0, world_size=1)
+for comm in (PeerComm(), TorchDistComm()):
+    st = ShardedState.basis(10, comm)
+    ops = W.random_layered_ops(10, 2, seed=0)
+    st.apply_placements(D.compile_circuit(D.Circuit(10, [D.GateOp(*o) for o in ops]), span_limit=10))
+    if isinstance(comm, PeerComm):
+        comm.order()   # events + gloo side-group barrier under an NCCL default group
+    n = st.norm()      # all-reduce on the backend's device
+    full = st.gather() # gather on the backend's device
+    assert abs(n - 1.0) < 1e-12 and full.numel() == 1024 and full.device.type == "cuda", (n, full.device)
+    assert comm.allreduce_max(3.0, st.local) == 3.0
+    if isinstance(comm, PeerComm):
+        comm.close()
+dist.destroy_process_group()
+print("nccl-ok")
+"""
+
+
+def test_peer_comm_collectives_under_nccl():
+    """under an NCCL process group every host-side collective of
+    PeerComm / TorchDistComm must hand CUDA tensors to NCCL (CPU tensors
+    raise "No backend type associated with device type cpu"); the event
+    ordering's host barrier runs on a gloo side group.  One rank (NCCL
+    refuses two ranks on one GPU)."""
+    script = _NCCL_SCRIPT.format(root=ROOT, port=_port())
+    p = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert p.returncode == 0 and "nccl-ok" in p.stdout, p.stdout[-2000:] + p.stderr[-3000:]

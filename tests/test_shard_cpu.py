@@ -260,3 +260,62 @@ def test_remap_cuts_partner_reads_config5():
     assert reads(comps) == (65, 52.0)
     phys, nsw = remap_plan(n, lb, world, comps)
     assert reads(phys) == (36, 17.5)
+
+
+def test_collective_device_follows_backend():
+    """host-side collectives must use CUDA tensors under NCCL
+    (torch registers NCCL for "cuda" only) and CPU tensors under gloo."""
+    from paper_2405_01250_b200.shard import collective_device
+    assert collective_device("nccl", torch.device("cuda", 3)) == torch.device("cuda", 3)
+    assert collective_device("NCCL", "cuda:1").type == "cuda"
+    assert collective_device("gloo", torch.device("cuda", 0)).type == "cpu"
+    assert collective_device("gloo", None).type == "cpu"
+
+
+def _order_worker(rank, world, port, out_q):
+    """PeerComm.order() protocol with the device calls recorded instead of
+    issued: record own event k, gloo barrier, wait on every partner's event
+    k; k alternates between consecutive cross-shard gates."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2405_01250_b200 import _lib as L
+        from paper_2405_01250_b200.shard import PeerComm
+        log = []
+        made = []
+        L.ipc_event_create = lambda: made.append(1000 * (rank + 1) + len(made)) or made[-1]
+        L.ipc_event_handle = lambda ev: str(ev).encode()
+        L.ipc_event_open = lambda h: int(h.decode())
+        L.event_record = lambda ev: log.append(("record", ev))
+        L.stream_wait_event = lambda ev: log.append(("wait", ev))
+        comm = PeerComm()
+        assert comm.host_group is None or comm.backend == "gloo"
+        for _ in range(3):
+            comm.order()
+        out_q.put((rank, log))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_order_protocol_gloo():
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_order_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    logs = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r, log in logs.items():
+        assert len(log) == 3 * world  # per gate: 1 record + (world - 1) waits
+        for g in range(3):
+            step = log[g * world:(g + 1) * world]
+            # own event g % 2 (two alternate), then event g % 2 of every partner
+            assert step[0] == ("record", 1000 * (r + 1) + g % 2)
+            assert sorted(ev for _, ev in step[1:]) == [1000 * (q + 1) + g % 2 for q in range(world) if q != r]
+            assert all(kind == "wait" for kind, _ in step[1:])
