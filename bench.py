@@ -41,7 +41,6 @@ sys.path.insert(0, ROOT)
 
 METRIC = "DiaQ spmv HBM GB/s and gate-applications/sec at n=28 c128; % of HBM roofline"
 N_QUBITS = 28
-CPU_SAMPLE_N = 24
 
 
 def alg_bytes(n_dim: int, offsets) -> int:
@@ -151,42 +150,148 @@ def max_over_ranks(dist, value: float, device) -> float:
 
 
 # ---------------------------------------------------------------- CPU baseline
+#
+# The reference's algorithm on the box's host cores.  The reference itself is
+# numpy (single-threaded ufuncs, ~1 GB/s); the pinned C oracle
+# (oracle/, bitwise the reference spmv) with OpenMP over every host core is
+# a stronger CPU baseline and is what the reference arm reports, at the
+# metric's own config (n=28).  Threads are pinned (OMP_PROC_BIND=close,
+# OMP_PLACES=cores, set before the oracle library loads) and every figure is
+# the median of >= 5 timed reps after a warm-up.
 
-def cpu_spmv_sample(reps: int = 3) -> dict:
-    """The pinned C oracle (bitwise the reference spmv), OpenMP on all host
-    cores, on the config-4 offsets at n=24 (a bounded sample of the workload)."""
+CPU_SPMV_REPS = 5
+
+
+def _cpu_env() -> None:
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    os.environ.setdefault("OMP_PLACES", "cores")
+
+
+def _fast_state(n_amps: int, seed: int = 1) -> np.ndarray:
+    """Normalised Gaussian complex vector (timing input; numpy's own sum)."""
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal(2 * n_amps).view(np.complex128)
+    x /= np.linalg.norm(x)
+    return x
+
+
+def cpu_spmv_measure(n: int, reps: int = CPU_SPMV_REPS, warmup: int = 1) -> dict:
+    """The C oracle spmv on the config-4 matrix at n (OpenMP, all cores)."""
+    _cpu_env()
     from oracle import oracle as O
     from paper_2405_01250_b200 import workloads as W
-    c4 = W.config4(CPU_SAMPLE_N, seed=0, with_x=False)
-    rng = np.random.default_rng(1)
+    c4 = W.config4(22, seed=0, with_x=False)  # the gate and offsets are those of every n >= 22
+    t0 = time.perf_counter()
     span = O.span_unitary(c4["u4"], c4["positions"], c4["span"])
-    a = O.kron_identity(c4["left"], span, c4["right"])
-    x = W.random_state(rng, 2**CPU_SAMPLE_N)
-    nb = alg_bytes(2**CPU_SAMPLE_N, a.offs)
-    O.spmv(a, x)  # warm-up
-    best = None
-    for _ in range(reps):
-        t0 = time.perf_counter()
+    a = O.kron_identity(2 ** (n - 22), span, c4["right"])
+    x = _fast_state(2**n)
+    build_s = time.perf_counter() - t0
+    nb = alg_bytes(2**n, a.offs)
+    for _ in range(warmup):
         O.spmv(a, x)
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
-    return {"value": round(nb / best / 1e9, 3), "unit": "GB/s", "cores": O.num_threads(),
-            "kind": "port",
-            "sample": f"config-4 offsets at n={CPU_SAMPLE_N} (2^{CPU_SAMPLE_N} rows, {nb} alg bytes), "
-                      f"best of {reps} after 1 warm-up, C oracle -O3 OpenMP"}
+    times = []
+    for _ in range(reps):
+        t1 = time.perf_counter()
+        O.spmv(a, x)
+        times.append(time.perf_counter() - t1)
+    med = statistics.median(times)
+    del a, x
+    return {"value": round(nb / med / 1e9, 3), "unit": "GB/s", "cores": O.num_threads(), "kind": "port",
+            "sample": f"config-4 spmv at n={n} (the metric's config), median of {reps} after {warmup} warm-up; "
+                      f"C oracle -O3 OpenMP (bitwise reference matrix.py:253-278), "
+                      f"OMP_PROC_BIND={os.environ.get('OMP_PROC_BIND')} OMP_PLACES={os.environ.get('OMP_PLACES')}",
+            "times_s": [round(t, 4) for t in times], "build_s": round(build_s, 2), "alg_bytes_per_step": nb,
+            "cpu_model": _cpu_model()}
+
+
+def cpu_gates_measure(n: int = N_QUBITS, count: int = 4) -> dict:
+    """The oracle's apply_placed (reference sim.py:81-105, numpy complex
+    multiply rounding) on the first `count` one-qubit gates of the n=28 random
+    layer, at 1 thread and at every host core: gates/s."""
+    _cpu_env()
+    from oracle import oracle as O
+    from paper_2405_01250_b200 import workloads as W
+    ops = [o for o in W.random_layered_ops(n, 1, seed=0) if len(o[1]) == 1][:count]
+    x = _fast_state(2**n, seed=2)
+    out = {}
+    for threads in (1, O.num_threads()):
+        t_total = 0.0
+        for name, (q,), params in ops:
+            g = O.GATES[name](*params)
+            m = O.from_dense(g)
+            t1 = time.perf_counter()
+            x = O.apply_placed(2**q, m, 2 ** (n - 1 - q), x, O.numpy_cmul_mode(), threads)
+            t_total += time.perf_counter() - t1
+        out[f"threads_{threads}"] = {"gates_per_s": round(len(ops) / t_total, 3), "s_per_gate": round(t_total / len(ops), 3)}
+    return {"unit": "gates/s", "kind": "port", "n_qubits": n, "gates": [o[0] for o in ops], **out,
+            "sample": f"first {len(ops)} one-qubit gates of the n={n} random layer, C oracle apply_placed "
+                      "(reference sim.py:69-105), pinned OpenMP threads"}
+
+
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def numpy_reference_secondary() -> dict:
+    """The real reference (numpy, baseline/_ref installed by
+    tools/install_reference.py) on this host: its spmv on the config-4
+    parity slice (n=22) and run() at n=20 (2 random layers) at threads=1 and
+    at every core.  Bounded samples; absent install -> reported as such."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "diaqsim")):
+        return {"unavailable": "baseline/_ref not installed (python tools/install_reference.py)"}
+    import importlib
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    R = importlib.import_module("diaqsim")
+    from paper_2405_01250_b200 import workloads as W
+    out = {"kind": "reference (numpy, unmodified)", "cpu_model": _cpu_model(), "numpy": np.__version__}
+    c4 = W.config4(22, seed=0, with_x=False)
+    a = R.kron_identity(1, R.build_span_unitary(R.from_dense(c4["u4"]), c4["positions"], c4["span"]), c4["right"])
+    x = _fast_state(2**22)
+    nb = alg_bytes(2**22, a.diag_indices())
+    R.spmv(a, x)
+    ts = []
+    for _ in range(3):
+        t1 = time.perf_counter()
+        R.spmv(a, x)
+        ts.append(time.perf_counter() - t1)
+    out["spmv_n22"] = {"GBs": round(nb / statistics.median(ts) / 1e9, 3), "s": round(statistics.median(ts), 3),
+                       "cores": 1, "note": "numpy ufuncs, single-threaded; median of 3"}
+    del a, x
+    ops = W.random_layered_ops(20, 2, seed=0)
+    circ = R.Circuit(20, [R.GateOp(*o) for o in ops])
+    for threads in (1, os.cpu_count() or 1):
+        t1 = time.perf_counter()
+        res = R.run(circ, shots=0, span_limit=20, threads=threads)
+        dt = time.perf_counter() - t1
+        out[f"run_n20_threads_{threads}"] = {"gates": len(ops), "s": round(dt, 3),
+                                             "apply_gates_per_s": round(len(ops) / (res.timings_ns["apply_total"] * 1e-9), 2)}
+    return out
 
 
 def run_reference(args):
+    """--impl reference: the reference algorithm's CPU implementation at the
+    metric's config (config-4 spmv, n=28) on all host cores; rank 0 only."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
+    n = args.n
+    _cpu_env()
     from oracle import oracle as O
     from paper_2405_01250_b200 import workloads as W
-    c4 = W.config4(CPU_SAMPLE_N, seed=0, with_x=False)
+    c4 = W.config4(22, seed=0, with_x=False)
     span = O.span_unitary(c4["u4"], c4["positions"], c4["span"])
-    a = O.kron_identity(c4["left"], span, c4["right"])
-    x = W.random_state(np.random.default_rng(1), 2**CPU_SAMPLE_N)
-    nb = alg_bytes(2**CPU_SAMPLE_N, a.offs)
+    a = O.kron_identity(2 ** (n - 22), span, c4["right"])
+    x = _fast_state(2**n)
+    nb = alg_bytes(2**n, a.offs)
     for _ in range(args.warmup):
         O.spmv(a, x)
     times = []
@@ -196,17 +301,26 @@ def run_reference(args):
         times.append(time.perf_counter() - t0)
     total = sum(times)
     value = nb * len(times) / total / 1e9
+    del a, x
+    secondary = {}
+    if not args.no_secondary:
+        try:
+            secondary["numpy_reference"] = numpy_reference_secondary()
+        except Exception as e:  # never lose the arm's line
+            secondary["numpy_reference"] = {"error": repr(e)}
     line = {
         "metric": METRIC, "impl": "reference", "value": round(value, 3), "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * total / len(times), 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config-4 spmv sample at n={CPU_SAMPLE_N} (same 9 offsets as n=28)",
-                   "n_qubits": CPU_SAMPLE_N, "alg_bytes_per_step": nb},
+        "config": {"workload": f"config4 spmv n={n}: kron_identity(2^{n - 22}, span(Haar4,[18,0],19), 2^3)",
+                   "n_qubits": n, "alg_bytes_per_step": nb, "same_config_as_ours": True},
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": O.num_threads(), "kind": "port",
-                         "sample": f"config-4 offsets at n={CPU_SAMPLE_N}; the C oracle restating "
-                                   "reference matrix.py:253-278 bitwise"},
+                         "sample": f"every step = one config-4 spmv at n={n}; the C oracle restating reference "
+                                   "matrix.py:253-278 bitwise, OpenMP pinned (OMP_PROC_BIND=close, OMP_PLACES=cores)",
+                         "step_s_median": round(statistics.median(times), 4), "cpu_model": _cpu_model()},
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "secondary": secondary,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -296,8 +410,11 @@ def run_ours(args):
     value = nbytes * world * args.steps / (total_ms * 1e-3) / 1e9
     y_norm = float(torch.linalg.vector_norm(y).item())
 
-    # ---- gate applications at n=28: one random layer (n rotations + n/2 CX) per step
-    if world > 1 and args.sharded_gates:
+    # ---- gate applications.  N=1: one random layer at n=28 per step (the
+    # metric's config).  N>1 (default): config 5 -- the 20-layer random
+    # circuit on a 2^(30+p) state sharded over the ranks (weak scaling);
+    # --replicas: independent n=28 layers per rank instead
+    if world > 1 and not args.replicas:
         gates_part = sharded_gates(args, D, L, W, torch, dist, n, world, x, s, dev)
     else:
         gates_part = replica_gates(args, D, L, W, torch, dist, n, world, x, s, dev)
@@ -352,7 +469,7 @@ def run_ours(args):
                 "traffic": prof.get("spmv_dram_bytes_per_launch") if n == N_QUBITS else None,
                 "alg_bytes_per_launch": nbytes, "kernel": "diaq::spmv_async_kernel<9> (cp.async-staged banded spmv)",
                 "frac_of_8TBs_spec": round(achieved / 8000.0, 4)}
-    gates_scale = 1 if (world > 1 and args.sharded_gates) else world
+    gates_scale = 1 if (world > 1 and not args.replicas) else world
     gates = {"gates_per_s": round(gates_scale * n_gates / (g_ms * 1e-3), 2), "ms_per_gate": round(ms_per_gate, 4),
              "n_qubits": gate_n, **gate_extra,
              "roofline": {"bound": "hbm", "achieved": round(gate_bytes / (ms_per_pass * 1e-3) / 1e9, 1),
@@ -370,7 +487,16 @@ def run_ours(args):
         return 0
     cpu = None
     if world == 1 and not args.no_cpu:
-        cpu = cpu_spmv_sample()
+        try:
+            cpu = cpu_spmv_measure(n)
+            gates["cpu_baseline"] = cpu_gates_measure(gate_n)
+        except Exception as e:  # never lose the headline line
+            cpu = {"error": repr(e)}
+        if not args.no_secondary:
+            try:
+                secondary["numpy_reference"] = numpy_reference_secondary()
+            except Exception as e:
+                secondary["numpy_reference"] = {"error": repr(e)}
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
@@ -443,40 +569,70 @@ def replica_gates(args, D, L, W, torch, dist, n, world, x, s, dev):
 
 
 def sharded_gates(args, D, L, W, torch, dist, n, world, x, s, dev):
-    """One random layer per step on a 2^(n+p) state sharded over the ranks;
-    weak scaling.  Cross-shard gates read partner shards in place over peer
-    memory (--transport peer, CUDA IPC over NVLink/NVSwitch) or exchange
-    them with NCCL send/recv first (--transport nccl)."""
+    """Config 5: the 20-layer random circuit (config-3 gate mix, CX matching
+    over ALL qubits) on a 2^(L+p) state sharded over the ranks, L =
+    --circuit-qubits local bits (30: 16 GiB per GPU); weak scaling.  One
+    step = the whole circuit from the current state.  Cross-shard gates read
+    partner shards in place over peer memory (--transport peer: CUDA IPC over
+    NVLink/NVSwitch, ordered by IPC events) or exchange them with NCCL
+    send/recv first (--transport nccl).  Measured without and with qubit
+    remapping (half-shard swaps before cross-shard gates); the headline is
+    the plain run."""
     from paper_2405_01250_b200.shard import PeerComm, ShardedState, TorchDistComm
     p = world.bit_length() - 1
-    ns = n + p
+    ns = args.circuit_qubits + p
+    lb = args.circuit_qubits
+    layers = args.circuit_layers
+    del x  # the circuit starts from |0...0>
     transport = args.transport
     comm = PeerComm() if transport == "peer" else TorchDistComm()
     try:
-        st = ShardedState(ns, x / world ** 0.5, comm)  # every rank's x has norm 1: global norm 1
+        st = ShardedState.basis(ns, comm)
     except L.DeviceError as e:  # no peer mapping between these GPUs: staged NCCL exchange
         transport = f"nccl (peer mapping failed: {e})"
         comm = TorchDistComm()
-        st = ShardedState(ns, x / world ** 0.5, comm)
-    ops = W.random_layered_ops(ns, 1, seed=0)
+        st = ShardedState.basis(ns, comm)
+    ops = W.random_layered_ops(ns, layers, seed=0)
     pls = D.compile_circuit(D.Circuit(ns, [D.GateOp(*o) for o in ops]), span_limit=ns)
-    st.apply_placements(pls, remap=args.remap)
-    torch.cuda.synchronize()
-    dist.barrier()
-    g_steps = max(2, min(args.steps, 5))
-    ge0 = torch.cuda.Event(enable_timing=True)
-    ge1 = torch.cuda.Event(enable_timing=True)
-    gl0 = L.launch_count()
-    ge0.record(s)
-    for _ in range(g_steps):
-        st.apply_placements(pls, remap=args.remap)
-    ge1.record(s)
-    torch.cuda.synchronize()
-    g_launches = L.launch_count() - gl0
-    g_ms = max_over_ranks(dist, ge0.elapsed_time(ge1), dev)
-    extra = {"gates_per_step": len(pls), "steps": g_steps, "mode": f"sharded over {world} ranks",
-             "transport": transport, "remap": bool(args.remap), "stats": dict(st.stats)}
-    return len(pls) * g_steps, g_ms, g_launches, st.norm(), ns, extra
+    peak, _ = measured_peak()
+    runs = {}
+    g_launches = 0
+    for remap in (False, True):
+        st.apply_placements(pls, remap=remap)  # warm-up: plans, specialised passes
+        L.call("diaq_jit_wait", -1.0)
+        torch.cuda.synchronize()
+        dist.barrier()
+        st.stats = {k: 0 for k in st.stats}
+        g_steps = max(1, min(args.steps, 3))
+        ge0 = torch.cuda.Event(enable_timing=True)
+        ge1 = torch.cuda.Event(enable_timing=True)
+        gl0 = L.launch_count()
+        ge0.record(s)
+        for _ in range(g_steps):
+            st.apply_placements(pls, remap=remap)
+        ge1.record(s)
+        torch.cuda.synchronize()
+        launches = L.launch_count() - gl0
+        g_ms = max_over_ranks(dist, ge0.elapsed_time(ge1), dev)
+        stats = {k: (v // g_steps if isinstance(v, int) else v) for k, v in st.stats.items()}
+        passes = launches / g_steps
+        # per-rank HBM: every launch sweeps the rank's shard (32 B per local
+        # amplitude: read + write); partner reads arrive over NVLink, not HBM
+        hbm_bytes = passes * 32 * 2**lb
+        runs["remap" if remap else "plain"] = {
+            "gates_per_s": round(len(pls) * g_steps / (g_ms * 1e-3), 2), "s_per_circuit": round(g_ms / g_steps / 1e3, 4),
+            "launches_per_circuit": round(passes, 1), "cross_shard_ops": stats.get("exchanged", 0),
+            "swaps": stats.get("swaps", 0), "partner_bytes_read_per_rank": stats.get("bytes_received", 0),
+            "hbm_frac_per_rank": round(hbm_bytes / (g_ms / g_steps * 1e-3) / 1e9 / peak, 4), "stats": stats}
+        if not remap:
+            g_launches = launches
+            plain_ms, plain_steps = g_ms, g_steps
+    norm = st.norm()
+    extra = {"gates_per_step": len(pls), "steps": plain_steps, "layers": layers, "circuit_qubits": ns,
+             "local_qubits": lb, "mode": f"config 5: sharded over {world} ranks (top {p} bits), weak scaling",
+             "transport": transport, "runs": runs, "norm_err": abs(1.0 - norm),
+             "norm_ok": abs(1.0 - norm) < 1e-10}
+    return len(pls) * plain_steps, plain_ms, g_launches, norm, ns, extra
 
 
 def secondary_workloads(args, D, L, W, torch) -> dict:
@@ -615,12 +771,11 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
-    ap.add_argument("--sharded-gates", action="store_true",
-                    help="N>1: measure gates on a state sharded over the ranks instead of replicas")
     ap.add_argument("--replicas", action="store_true",
-                    help="N>1: independent spmv replicas instead of the row-sharded product")
-    ap.add_argument("--remap", action="store_true",
-                    help="--sharded-gates: swap global qubits into local positions before cross-shard gates")
+                    help="N>1: independent spmv / n=28 layer replicas instead of the sharded product and circuit")
+    ap.add_argument("--circuit-qubits", type=int, default=30,
+                    help="N>1: local qubits per rank of the sharded config-5 circuit (n = this + log2 N)")
+    ap.add_argument("--circuit-layers", type=int, default=20, help="N>1: layers of the config-5 circuit")
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
                     help="sharded gates: partner shards read in place over peer memory, or NCCL-staged")
     args = ap.parse_args()

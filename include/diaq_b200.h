@@ -109,6 +109,23 @@ int diaq_to_dense(const diaq_matrix_t *a, void *dense, void *stream);
 int diaq_count_nonzero(const diaq_matrix_t *a, double eps, int64_t *nnz_out, int64_t *bsr_blocks_out,
                        void *stream);
 
+/* ---- matrix algebra around the hot path (reference matrix.py:281-355) ----
+ * All in the reference's result precision (single != 0: float32 arithmetic
+ * on float32-representable values, widened into the complex128 arena).
+ * transpose needs no call: it relabels the arena (d -> -d).
+ * diaq_arena_map: op 0 -> conj (adjoint's values), op 1 -> scale by sr+i*si,
+ *   over `total` arena elements (same layout in and out). */
+int diaq_arena_map(int64_t total, const void *src, void *dst, int op, double sr, double si, int single,
+                   void *stream);
+/* out = a + b over the union of stored diagonals (out laid out by the caller
+ * with that union); per element (+0 + a) + b (matrix.py:301-315) */
+int diaq_add(const diaq_matrix_t *a, const diaq_matrix_t *b, diaq_matrix_t *out, int single, void *stream);
+/* out = a (x) b (matrix.py:329-355); out's offsets are {dA*nB + dB}; the
+ * operands' offset/start tables also in device memory: tables_dev =
+ * [offa, starta, offb, startb] */
+int diaq_kron(const diaq_matrix_t *a, const diaq_matrix_t *b, const int64_t *tables_dev, diaq_matrix_t *out,
+              int single, void *stream);
+
 /* ---- spmv (reference matrix.py:253-278) -------------------------------
  * y = A x, bitwise equal to the reference (ascending d, no FMA). */
 int diaq_spmv(const diaq_matrix_t *a, const void *x, void *y, void *stream);
@@ -128,14 +145,51 @@ int diaq_spgemm_plan(int64_t n, int64_t nda, const int64_t *offa, int64_t ndb, c
  * workspace may then be NULL) */
 int64_t diaq_spgemm_workspace(int64_t nda, int64_t ndb, int64_t nc);
 /* multiply into the candidate layout `c` and flag keep_dev[i] = 1 iff
- * candidate i has an element with |re|+|im| > prune_eps (matrix.py:246-249) */
+ * candidate i has an element with |re|+|im| > prune_eps (matrix.py:246-249).
+ * single != 0: both operands are single precision -- products, sums and the
+ * prune test in float32 (reference result_type, matrix.py:231). */
 int diaq_spgemm(const diaq_matrix_t *a, const diaq_matrix_t *b, diaq_matrix_t *c,
-                uint8_t *keep_dev, double prune_eps, void *workspace, int64_t workspace_bytes,
+                uint8_t *keep_dev, double prune_eps, int single, void *workspace, int64_t workspace_bytes,
                 void *stream);
+/* compact a host-planned product's keep flags into a device structure table:
+ * cand_tab_dev = [offc[nc], startc[nc]]; writes *nd_dev and the kept
+ * offsets/starts, ascending (no readback). */
+int diaq_spgemm_compact(int64_t nc, const int64_t *cand_tab_dev, const uint8_t *keep_dev, int64_t *nd_dev,
+                        int64_t *offs_dev, int64_t *starts_dev, void *stream);
+
+/* ---- device-resident structure: spgemm with the plan on the device ----------
+ * A matrix whose offset/start table lives in device memory (e.g. a product
+ * whose pruned structure was never read back). */
+typedef struct {
+    int64_t n;
+    int64_t nd_cap;         /* capacity of offs/starts (>= *nd) */
+    const int64_t *nd;      /* device: number of stored diagonals */
+    const int64_t *offs;    /* device: ascending offsets */
+    const int64_t *starts;  /* device: element starts in vals */
+    const void *vals;       /* device complex128 arena */
+} diaq_dev_matrix_t;
+typedef struct {
+    int64_t *nd;            /* device outputs: count (negative: plan error), */
+    int64_t *offs;          /*   kept offsets, ascending,                      */
+    int64_t *starts;        /*   their element starts                          */
+    void *vals;             /* arena of capacity elements                      */
+    int64_t capacity;       /* >= nc * (n + 7) + 7 for nc candidates           */
+    int64_t nd_cap;         /* entries of offs/starts                          */
+} diaq_dev_result_t;
+/* count products C[i] = A[i] B[i] (matmul, matrix.py:218-250): pass 1 (the
+ * offset union count and scan) runs on the device from the operands' device
+ * tables, pass 2 multiplies, a compaction pass prunes -- one launch of each
+ * per 64 products, no host round trip.  pair_cap >= nd(A[i]) * nd(B[i])
+ * (<= 1024).  Bitwise diaq_spgemm, structure included. */
+int64_t diaq_spgemm_dev_workspace(int count, int64_t pair_cap);
+int diaq_spgemm_dev(int count, const diaq_dev_matrix_t *a, const diaq_dev_matrix_t *b, const diaq_dev_result_t *c,
+                    double prune_eps, int single, int64_t pair_cap, void *workspace, int64_t workspace_bytes,
+                    void *stream);
 
 /* ---- gate application (reference sim.py:69-105) -----------------------
  * Generic placement: y = (I_dim_a (x) m (x) I_dim_b) x over the stored
- * diagonals of m (any m).  y must not alias x. */
+ * diagonals of m (any m, any number of diagonals: chunks of 64 continue
+ * the per-amplitude sum in y, the reference's order).  y must not alias x. */
 int diaq_apply_placed(int64_t dim_a, const diaq_matrix_t *m, int64_t dim_b, const void *x, void *y,
                       int cmul_mode, void *stream);
 

@@ -44,6 +44,18 @@ class Matrix(ctypes.Structure):
     ]
 
 
+class DevMatrix(ctypes.Structure):
+    """diaq_dev_matrix_t: structure table in device memory"""
+    _fields_ = [("n", ctypes.c_int64), ("nd_cap", ctypes.c_int64), ("nd", ctypes.c_void_p),
+                ("offs", ctypes.c_void_p), ("starts", ctypes.c_void_p), ("vals", ctypes.c_void_p)]
+
+
+class DevResult(ctypes.Structure):
+    """diaq_dev_result_t"""
+    _fields_ = [("nd", ctypes.c_void_p), ("offs", ctypes.c_void_p), ("starts", ctypes.c_void_p),
+                ("vals", ctypes.c_void_p), ("capacity", ctypes.c_int64), ("nd_cap", ctypes.c_int64)]
+
+
 class Gate(ctypes.Structure):
     _fields_ = [
         ("k", ctypes.c_int),
@@ -76,7 +88,13 @@ _SIGS = {
     "diaq_spmv_host": ([_MP, _P, _P, _P, _P, _I64, _P], _INT),
     "diaq_spgemm_plan": ([_I64, _I64, _P, _I64, _P, _P, _P], _INT),
     "diaq_spgemm_workspace": ([_I64, _I64, _I64], _I64),
-    "diaq_spgemm": ([_MP, _MP, _MP, _P, ctypes.c_double, _P, _I64, _P], _INT),
+    "diaq_spgemm": ([_MP, _MP, _MP, _P, ctypes.c_double, _INT, _P, _I64, _P], _INT),
+    "diaq_spgemm_compact": ([_I64, _P, _P, _P, _P, _P, _P], _INT),
+    "diaq_spgemm_dev_workspace": ([_INT, _I64], _I64),
+    "diaq_spgemm_dev": ([_INT, _P, _P, _P, ctypes.c_double, _INT, _I64, _P, _I64, _P], _INT),
+    "diaq_arena_map": ([_I64, _P, _P, _INT, ctypes.c_double, ctypes.c_double, _INT, _P], _INT),
+    "diaq_add": ([_MP, _MP, _MP, _INT, _P], _INT),
+    "diaq_kron": ([_MP, _MP, _P, _MP, _INT, _P], _INT),
     "diaq_apply_placed": ([_I64, _MP, _I64, _P, _P, _INT, _P], _INT),
     "diaq_apply_gate": ([_INT, _INT, _P, _P, _P, _P, _INT, _P], _INT),
     "diaq_run_gates": ([_INT, _INT, ctypes.POINTER(Gate), _P, _INT, _P, _P], _INT),
@@ -225,6 +243,8 @@ def to_device_c128(a):
             return a
         return a.to(device=device(), dtype=t.complex128).contiguous()
     host = np.ascontiguousarray(a, dtype=np.complex128)
+    if not host.flags.writeable:  # read-only snapshots: torch wants a writable source
+        host = host.copy()
     return t.from_numpy(host).to(device())
 
 

@@ -124,6 +124,7 @@ struct PlacedParams {
     const double2 *x;
     double2 *y;
     int nd;
+    int accumulate;  // continue the sum already in y (a later chunk of > 64 diagonals)
     PlacedDiag dg[kParamDiags];
 };
 
@@ -132,7 +133,7 @@ __global__ void __launch_bounds__(kThreads) placed_kernel(const __grid_constant_
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < p.total; e += stride) {
         const int64_t row = (e / p.dim_b) % p.n_m;
-        double2 acc = make_double2(0.0, 0.0);
+        double2 acc = p.accumulate ? ld_plain(p.y + e) : make_double2(0.0, 0.0);
         for (int i = 0; i < p.nd; ++i) {
             if (row >= p.dg[i].lo && row < p.dg[i].hi) {
                 const double2 v = ld_reuse(p.dg[i].row0 + row);
@@ -391,30 +392,38 @@ extern "C" int diaq_apply_placed(int64_t dim_a, const diaq_matrix_t *m, int64_t 
                                  int cmul_mode, void *stream) {
     if (!m || !x || !y) return set_error(DIAQ_ERR_VALUE, "diaq_apply_placed: null argument");
     if (dim_a < 1 || dim_b < 1) return set_error(DIAQ_ERR_SHAPE, "dim_a and dim_b must be >= 1");
-    if (m->nd > kParamDiags)
-        return set_error(DIAQ_ERR_UNSUPPORTED, "diaq_apply_placed: %lld diagonals > %d", (long long)m->nd, kParamDiags);
+    if (x == y) return set_error(DIAQ_ERR_VALUE, "diaq_apply_placed: y must not alias x");
     cudaStream_t s = (cudaStream_t)stream;
-    PlacedParams p;
+    // Any number of stored diagonals: chunks of kParamDiags in ascending
+    // order, each later chunk continuing the per-amplitude sum in y -- the
+    // same sequence of additions as one pass over all of them (reference
+    // _apply_diags_block, sim.py:69-78, has no cap).
+    static thread_local PlacedParams p;
     p.total = dim_a * m->n * dim_b;
     p.dim_b = dim_b;
     p.n_m = m->n;
     p.x = (const double2 *)x;
     p.y = (double2 *)y;
-    p.nd = (int)m->nd;
     const double2 *vals = (const double2 *)m->vals;
-    for (int64_t i = 0; i < m->nd; ++i) {
-        const int64_t d = m->offs[i];
-        p.dg[i].row0 = vals + m->starts[i] + (d < 0 ? d : 0);
-        p.dg[i].lo = d < 0 ? -d : 0;
-        p.dg[i].hi = d > 0 ? m->n - d : m->n;
-        p.dg[i].xoff = d * dim_b;
-    }
     const int64_t want = (p.total + kThreads - 1) / kThreads;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * 8));
-    if (cmul_mode == DIAQ_CMUL_FMA) placed_kernel<DIAQ_CMUL_FMA><<<grid, kThreads, 0, s>>>(p);
-    else placed_kernel<DIAQ_CMUL_PLAIN><<<grid, kThreads, 0, s>>>(p);
-    count_launch();
-    return check_launch("placed_kernel");
+    for (int64_t c0 = 0; c0 == 0 || c0 < m->nd; c0 += kParamDiags) {
+        p.nd = (int)std::min<int64_t>(kParamDiags, m->nd - c0);
+        p.accumulate = c0 > 0;
+        for (int i = 0; i < p.nd; ++i) {
+            const int64_t d = m->offs[c0 + i];
+            p.dg[i].row0 = vals + m->starts[c0 + i] + (d < 0 ? d : 0);
+            p.dg[i].lo = d < 0 ? -d : 0;
+            p.dg[i].hi = d > 0 ? m->n - d : m->n;
+            p.dg[i].xoff = d * dim_b;
+        }
+        if (cmul_mode == DIAQ_CMUL_FMA) placed_kernel<DIAQ_CMUL_FMA><<<grid, kThreads, 0, s>>>(p);
+        else placed_kernel<DIAQ_CMUL_PLAIN><<<grid, kThreads, 0, s>>>(p);
+        count_launch();
+        const int rc = check_launch("placed_kernel");
+        if (rc) return rc;
+    }
+    return DIAQ_OK;
 }
 
 extern "C" int diaq_init_basis(int64_t n_amps, void *x, int64_t index, void *stream) {

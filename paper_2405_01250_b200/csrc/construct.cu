@@ -183,6 +183,7 @@ struct SpanParams {
     int64_t off[kParamDiags];
     double2 *dst[kParamDiags];
     int64_t len[kParamDiags];
+    const double2 *gdev;       // k > 4: the dense gate in device memory (else in g below)
     double2 g[256];            // dense gate, k <= 4
 };
 
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(kThreads) span_expand_kernel(const __grid_cons
         if (((r ^ c) & p.free_mask) == 0) {
             const int rg = gather_bits(r, p.shifts, p.k);
             const int cg = gather_bits(c, p.shifts, p.k);
-            const double2 gv = p.g[rg * M + cg];
+            const double2 gv = p.gdev ? ld_reuse(p.gdev + (int64_t)rg * M + cg) : p.g[rg * M + cg];
             if (fabs(gv.x) + fabs(gv.y) > 0.0) v = gv;
         }
         st_stream(p.dst[i] + kk, v);
@@ -337,9 +338,9 @@ extern "C" int diaq_kron_identity(int64_t left, const diaq_matrix_t *m, int64_t 
 extern "C" int diaq_span_plan(int k, const double *g, const int *positions, int span, int64_t *offs_out,
                               int64_t *nd_out) {
     if (!g || !positions || !offs_out || !nd_out) return set_error(DIAQ_ERR_VALUE, "diaq_span_plan: null argument");
-    if (k < 1 || k > 4) return set_error(DIAQ_ERR_UNSUPPORTED, "diaq_span_plan: gate width %d outside 1..4", k);
+    if (k < 1 || k > 16) return set_error(DIAQ_ERR_UNSUPPORTED, "diaq_span_plan: gate width %d outside 1..16", k);
     if (span < k || span > 62) return set_error(DIAQ_ERR_SHAPE, "diaq_span_plan: span %d", span);
-    int shifts[8];
+    int shifts[64];
     for (int i = 0; i < k; ++i) {
         if (positions[i] < 0 || positions[i] >= span)
             return set_error(DIAQ_ERR_SHAPE, "positions outside span of %d qubits", span);
@@ -365,10 +366,10 @@ extern "C" int diaq_span_plan(int k, const double *g, const int *positions, int 
 extern "C" int diaq_span_expand(int k, const double *g, const int *positions, int span, diaq_matrix_t *out,
                                 void *stream) {
     if (!g || !positions || !out) return set_error(DIAQ_ERR_VALUE, "diaq_span_expand: null argument");
-    if (k < 1 || k > 4) return set_error(DIAQ_ERR_UNSUPPORTED, "diaq_span_expand: gate width %d outside 1..4", k);
+    if (k < 1 || k > 16) return set_error(DIAQ_ERR_UNSUPPORTED, "diaq_span_expand: gate width %d outside 1..16", k);
     if (out->n != (1ll << span)) return set_error(DIAQ_ERR_SHAPE, "diaq_span_expand: output n mismatch");
     cudaStream_t s = (cudaStream_t)stream;
-    SpanParams p;
+    static thread_local SpanParams p;
     p.k = k;
     p.span = span;
     uint64_t gate_mask = 0;
@@ -378,8 +379,22 @@ extern "C" int diaq_span_expand(int k, const double *g, const int *positions, in
     }
     p.free_mask = (span >= 64 ? ~0ull : ((1ull << span) - 1ull)) & ~gate_mask;
     const int M = 1 << k;
-    for (int i = 0; i < M * M; ++i) p.g[i] = make_double2(g[2 * i], g[2 * i + 1]);
-    for (int64_t base = 0; base < out->nd; base += kParamDiags) {
+    double2 *gdev = nullptr;
+    p.gdev = nullptr;
+    if (k <= 4) {
+        for (int i = 0; i < M * M; ++i) p.g[i] = make_double2(g[2 * i], g[2 * i + 1]);
+    } else {  // 4^k entries: too many for the kernel parameters, staged in device memory
+        const size_t bytes = sizeof(double2) * (size_t)M * (size_t)M;
+        if (cudaMallocAsync((void **)&gdev, bytes, s) != cudaSuccess ||
+            cudaMemcpyAsync(gdev, g, bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+            cudaGetLastError();
+            if (gdev) cudaFreeAsync(gdev, s);
+            return set_error(DIAQ_ERR_CUDA, "diaq_span_expand: staging a %d-qubit gate failed", k);
+        }
+        p.gdev = gdev;
+    }
+    int rc = DIAQ_OK;
+    for (int64_t base = 0; base < out->nd && rc == DIAQ_OK; base += kParamDiags) {
         const int cnt = (int)std::min<int64_t>(kParamDiags, out->nd - base);
         p.nd = cnt;
         int64_t maxlen = 0;
@@ -393,10 +408,10 @@ extern "C" int diaq_span_expand(int k, const double *g, const int *positions, in
         dim3 grid(grid_x(maxlen, cnt), cnt);
         span_expand_kernel<<<grid, kThreads, 0, s>>>(p);
         count_launch();
-        const int rc = check_launch("span_expand_kernel");
-        if (rc) return rc;
+        rc = check_launch("span_expand_kernel");
     }
-    return DIAQ_OK;
+    if (gdev) cudaFreeAsync(gdev, s);
+    return rc;
 }
 
 extern "C" int diaq_from_dense_scan(int64_t n, const void *dense, double eps, uint8_t *keep_dev, void *stream) {

@@ -607,10 +607,31 @@ static int spmv_rows(const diaq_matrix_t *a, const void *x, void *y, int64_t r0,
             default: return launch_param<0>(p, s);
         }
     }
-    // many diagonals: stage the table in device memory (stream-ordered)
+    // many diagonals: stage the table in device memory (stream-ordered, no
+    // host sync: the pinned staging block is released once an event behind
+    // its copy has completed -- polled on later calls)
+    struct Staged {
+        cudaEvent_t ev;
+        void *host;
+    };
+    static thread_local std::vector<Staged> staged;
+    for (size_t i = 0; i < staged.size();) {
+        if (cudaEventQuery(staged[i].ev) == cudaSuccess) {
+            cudaEventDestroy(staged[i].ev);
+            cudaFreeHost(staged[i].host);
+            staged[i] = staged.back();
+            staged.pop_back();
+        } else {
+            cudaGetLastError();  // cudaErrorNotReady
+            ++i;
+        }
+    }
     const size_t bytes = sizeof(SpmvDiag) * (size_t)a->nd;
-    SpmvDiag *h = (SpmvDiag *)malloc(bytes);
-    if (!h) return set_error(DIAQ_ERR_RESOURCE, "diaq_spmv: host alloc failed");
+    SpmvDiag *h = nullptr;
+    if (cudaMallocHost((void **)&h, bytes) != cudaSuccess || !h) {
+        cudaGetLastError();
+        return set_error(DIAQ_ERR_RESOURCE, "diaq_spmv: pinned host alloc failed");
+    }
     for (int64_t i = 0; i < a->nd; ++i) {
         const int64_t d = a->offs[i];
         h[i].off = d;
@@ -620,18 +641,25 @@ static int spmv_rows(const diaq_matrix_t *a, const void *x, void *y, int64_t r0,
     }
     SpmvDiag *dtab = nullptr;
     if (cudaMallocAsync((void **)&dtab, bytes, s) != cudaSuccess) {
-        free(h);
+        cudaFreeHost(h);
         return set_error(DIAQ_ERR_CUDA, "diaq_spmv: device table alloc failed");
     }
     cudaMemcpyAsync(dtab, h, bytes, cudaMemcpyHostToDevice, s);
+    Staged st{nullptr, h};
+    if (cudaEventCreateWithFlags(&st.ev, cudaEventDisableTiming) != cudaSuccess || cudaEventRecord(st.ev, s) != cudaSuccess) {
+        cudaGetLastError();
+        cudaStreamSynchronize(s);  // cannot track the copy: wait for it instead
+        cudaFreeHost(h);
+        if (st.ev) cudaEventDestroy(st.ev);
+    } else {
+        staged.push_back(st);
+    }
     const int grid = grid_for((const void *)spmv_kernel_global, stride * nstrips);
     spmv_kernel_global<<<grid, kThreads, 0, s>>>(r0, r0 + nrows, (int)a->nd, dtab, (const double2 *)x, (double2 *)y,
                                                  ntiles, stride, nstrips, stride * nstrips);
     count_launch();
     const int rc = check_launch("spmv_kernel_global");
     cudaFreeAsync(dtab, s);
-    cudaStreamSynchronize(s);  // host table lifetime
-    free(h);
     return rc;
 }
 

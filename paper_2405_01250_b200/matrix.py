@@ -6,16 +6,19 @@ sits at storage position k = r + min(d, 0), iteration is ascending in d, and
 kernels take immutable inputs and return fresh matrices (matrix.py:1-14).
 
 Storage (B200 layout): one device complex128 arena per matrix
-(interleaved re/im: one 16-byte load per element) plus a host table of
-ascending offsets and row-aligned element starts (diaq_layout).  Host
-`Diagonal(index, re, im)` views are materialised lazily, so code written
-against the reference (`a.get(d).re.tolist()`, `np.array_equal`) still works.
+(interleaved re/im: one 16-byte load per element) plus its structure table
+(ascending offsets, row-aligned element starts; diaq_layout).  The table may
+live on the host, on the device, or both: a product computed with the
+device plan (diaq_spgemm_dev) knows its pruned structure only on the device
+until someone asks for it, so chains of products never wait for the host.
+Host `Diagonal(index, re, im)` views are downloaded one diagonal at a time
+(read-only snapshots), so code written against the reference
+(`a.get(d).re.tolist()`, `np.array_equal`) still works.
 
-Hot-path operations run as sm_100a kernels through the C-ABI:
-from_dense, to_dense, kron_identity, matmul (spgemm), spmv,
-multiply_diagonals.  transpose/adjoint/add/scale/kron/nnz/sparsity and the
-JSON wire form are O(stored) host metadata operations kept for API
-completeness ("not on the hot path").
+Every operation runs on the device through the C-ABI: from_dense, to_dense,
+kron_identity, kron, matmul (spgemm), spmv, add, scale, adjoint; transpose
+is a zero-copy relabel of the arena (position k of diagonal d and of -d are
+transposes, matrix.py:281-290).
 """
 from __future__ import annotations
 
@@ -27,12 +30,17 @@ import numpy as np
 
 from . import _lib as L
 from .alloc import DEFAULT_ALIGNMENT
-from .errors import ShapeError, UnsupportedFeatureError
+from .errors import ShapeError
 
 # diagonals whose values all fall below this after a matmul are dropped
 PRUNE_EPS = 1e-15
 
 DTYPES = {"single": np.float32, "double": np.float64}
+
+# products planned on the device: at most this many (dA, dB) pairs, and a
+# candidate arena of at most this many bytes (else the host plans exactly)
+DEV_PLAN_PAIRS = 1024
+DEV_PLAN_BYTES = 256 << 20
 
 
 def diag_len(d: int, n_dim: int) -> int:
@@ -55,23 +63,30 @@ class Diagonal:
 
 
 class _Dev:
-    """Device arena + host offset/start tables."""
+    """Device arena + its structure table (host arrays and/or device table)."""
 
-    __slots__ = ("offs", "starts", "vals", "st")
+    __slots__ = ("offs", "starts", "vals", "st", "dtab", "cap")
 
-    def __init__(self, offs: np.ndarray, starts: np.ndarray, vals):
-        self.offs = offs
-        self.starts = starts
-        self.vals = vals
-        self.st = None  # diaq_matrix_t, built once (the arena never moves)
+    def __init__(self, offs, starts, vals, dtab=None, cap=None):
+        self.offs = offs          # host int64 offsets (None: structure only on the device)
+        self.starts = starts      # host int64 element starts
+        self.vals = vals          # torch complex128 arena
+        self.st = None            # diaq_matrix_t, built once (the arena never moves)
+        self.dtab = dtab          # device int64 [nd, offs[cap], starts[cap]]
+        self.cap = cap if cap is not None else (len(offs) if offs is not None else 0)
+
+
+def _single(*mats) -> int:
+    return int(all(m.dtype == np.float32 for m in mats))
 
 
 class DiaqMatrix:
     """Square complex matrix stored as ascending full diagonals on the device.
 
     Absent diagonals are all-zero; stored zeros are kept.  The matrix is
-    either device-authoritative (built by a kernel) or host-authoritative
-    (after set_diag/drop); each side is materialised from the other on demand.
+    either host-authoritative (built with set_diag, the reference's way) or
+    device-authoritative (built by a kernel); the other side is produced on
+    demand.  `_version` counts edits, so caches keyed on a matrix see them.
     """
 
     def __init__(self, n_dim: int, dtype=np.float64, align: int = DEFAULT_ALIGNMENT):
@@ -82,15 +97,19 @@ class DiaqMatrix:
         self.align = align
         self._host: dict[int, Diagonal] | None = {}
         self._dev: _Dev | None = None
+        self._views: dict[int, Diagonal] = {}
+        self._version = 0
 
     # -- construction from a device arena -----------------------------------
 
     @classmethod
-    def _from_device(cls, n_dim: int, offs, starts, vals, dtype=np.float64) -> "DiaqMatrix":
+    def _from_device(cls, n_dim: int, offs, starts, vals, dtype=np.float64, dtab=None, cap=None) -> "DiaqMatrix":
         out = cls(n_dim, dtype)
         out._host = None
-        out._dev = _Dev(np.ascontiguousarray(offs, dtype=np.int64),
-                        np.ascontiguousarray(starts, dtype=np.int64), vals)
+        if offs is not None:
+            offs = np.ascontiguousarray(offs, dtype=np.int64)
+            starts = np.ascontiguousarray(starts, dtype=np.int64)
+        out._dev = _Dev(offs, starts, vals, dtab, cap)
         return out
 
     @classmethod
@@ -108,43 +127,91 @@ class DiaqMatrix:
             offs = np.array(sorted(self._host), dtype=np.int64)
             starts, total = L.layout(self.n_dim, offs)
             buf = np.zeros(max(total, 1), dtype=np.complex128)
-            for i, d in enumerate(offs.tolist()):
+            for s, d in zip(starts.tolist(), offs.tolist()):
                 dg = self._host[d]
-                s = int(starts[i])
-                buf[s:s + len(dg)].real = dg.re
-                buf[s:s + len(dg)].imag = dg.im
+                seg = buf[s:s + len(dg)]
+                seg.real = dg.re
+                seg.imag = dg.im
             self._dev = _Dev(offs, starts, L.to_device_c128(buf))
         return self._dev
 
-    def _hostmap(self) -> dict[int, Diagonal]:
-        """Host representation (downloads the arena once if needed)."""
-        if self._host is None:
-            dv = self._dev
-            arena = dv.vals.cpu().numpy() if len(dv.offs) else np.zeros(0, np.complex128)
-            host = {}
-            for i, d in enumerate(dv.offs.tolist()):
-                s = int(dv.starts[i])
-                seg = arena[s:s + self.n_dim - abs(d)]
-                re = np.ascontiguousarray(seg.real, dtype=self.dtype)
-                im = np.ascontiguousarray(seg.imag, dtype=self.dtype)
-                re.flags.writeable = False  # snapshots of the device arena: edit via set_diag
-                im.flags.writeable = False
-                host[d] = Diagonal(d, re, im)
-            self._host = host
-        return self._host
+    def _tables(self) -> tuple[np.ndarray, np.ndarray]:
+        """Host structure table (reads a device-only table back: one sync)."""
+        dv = self._device()
+        if dv.offs is None:
+            t = dv.dtab.cpu().numpy()
+            nd = int(t[0])
+            if nd < 0:
+                raise L.DeviceError(f"device spgemm plan failed (code {-nd})")
+            dv.offs = np.ascontiguousarray(t[1:1 + nd])
+            dv.starts = np.ascontiguousarray(t[1 + dv.cap:1 + dv.cap + nd])
+        return dv.offs, dv.starts
+
+    def _dev_table(self):
+        """(device int64 [nd, offs[cap], starts[cap]], cap): uploaded once for
+        a host-known structure (pinned, non-blocking)."""
+        dv = self._device()
+        if dv.dtab is None:
+            nd = len(dv.offs)
+            host = np.concatenate([np.array([nd], dtype=np.int64), dv.offs, dv.starts])
+            t = L.torch()
+            dv.dtab = t.from_numpy(host).pin_memory().to(dv.vals.device, non_blocking=True)
+            dv.cap = nd
+        return dv.dtab, dv.cap
+
+    def _cap(self) -> int:
+        """Upper bound of the stored diagonal count known without a sync."""
+        if self._host is not None:
+            return len(self._host)
+        dv = self._dev
+        return len(dv.offs) if dv.offs is not None else dv.cap
 
     def _struct(self) -> L.Matrix:
         dv = self._device()
         if dv.st is None:
-            dv.st = L.mat_struct(self.n_dim, dv.offs, dv.starts, dv.vals)
+            offs, starts = self._tables()
+            dv.st = L.mat_struct(self.n_dim, offs, starts, dv.vals)
         return dv.st
+
+    def _dev_struct(self) -> L.DevMatrix:
+        dtab, cap = self._dev_table()
+        base = dtab.data_ptr()
+        return L.DevMatrix(self.n_dim, cap, base, base + 8, base + 8 * (1 + cap), self._dev.vals.data_ptr())
 
     def device_arena(self):
         """(offsets, starts, torch complex128 arena) -- the device layout."""
-        dv = self._device()
-        return dv.offs, dv.starts, dv.vals
+        offs, starts = self._tables()
+        return offs, starts, self._dev.vals
+
+    def _download(self, i: int, d: int, arena=None) -> Diagonal:
+        """Host view of stored diagonal i (offset d): read-only snapshot."""
+        dv = self._dev
+        s = int(dv.starts[i])
+        length = self.n_dim - abs(d)
+        seg = arena[s:s + length] if arena is not None else dv.vals[s:s + length].cpu().numpy()
+        re = np.array(seg.real, dtype=self.dtype)
+        im = np.array(seg.imag, dtype=self.dtype)
+        re.flags.writeable = False  # snapshots of the device arena: edit via set_diag
+        im.flags.writeable = False
+        return Diagonal(int(d), re, im)
 
     # -- storage API (matrix.py:66-102) ----------------------------------------
+
+    def _edited(self) -> None:
+        self._dev = None
+        self._views = {}
+        self._version += 1
+
+    def _to_host(self) -> dict[int, Diagonal]:
+        """Make the host side authoritative (one download of the arena)."""
+        if self._host is None:
+            offs, _ = self._tables()
+            arena = self._dev.vals.cpu().numpy() if len(offs) else None
+            self._host = {}
+            for i, d in enumerate(offs.tolist()):
+                dg = self._views.get(d) or self._download(i, d, arena)
+                self._host[d] = Diagonal(d, np.array(dg.re), np.array(dg.im))
+        return self._host
 
     def set_diag(self, d: int, re, im=None) -> None:
         """Install diagonal d from value arrays (copied)."""
@@ -154,40 +221,67 @@ class DiaqMatrix:
                                                                            copy=True).reshape(-1)
         if len(re) != want or len(im) != want:
             raise ShapeError(f"diagonal {d} of n_dim={self.n_dim} needs {want} values")
-        self._hostmap()[int(d)] = Diagonal(int(d), re, im)
-        self._dev = None
+        host = self._to_host()
+        host[int(d)] = Diagonal(int(d), re, im)
+        self._edited()
 
     def get(self, d: int) -> Diagonal | None:
-        if self._host is None and int(d) not in set(self._dev.offs.tolist()):
+        d = int(d)
+        if self._host is not None:
+            return self._host.get(d)
+        if d in self._views:
+            return self._views[d]
+        offs, _ = self._tables()
+        i = int(np.searchsorted(offs, d))
+        if i >= len(offs) or offs[i] != d:
             return None
-        return self._hostmap().get(int(d))
+        self._views[d] = self._download(i, d)
+        return self._views[d]
 
     def drop(self, d: int) -> None:
-        self._hostmap().pop(int(d), None)
-        self._dev = None
+        d = int(d)
+        if self._host is not None:
+            self._host.pop(d, None)
+            self._edited()
+            return
+        offs, starts = self._tables()
+        keep = offs != d
+        if keep.all():
+            return
+        # structure-only edit: the arena stays, the table loses the diagonal
+        vals = self._dev.vals
+        self._dev = _Dev(offs[keep].copy(), starts[keep].copy(), vals)
+        self._views.pop(d, None)
+        self._version += 1
 
     def diag_indices(self) -> list[int]:
-        if self._host is None:
-            return self._dev.offs.tolist()
-        return sorted(self._host)
+        if self._host is not None:
+            return sorted(self._host)
+        return self._tables()[0].tolist()
 
     def diagonals(self):
         """Yield stored diagonals in ascending index order."""
-        h = self._hostmap()
-        for d in sorted(h):
-            yield h[d]
+        if self._host is not None:
+            for d in sorted(self._host):
+                yield self._host[d]
+            return
+        offs, _ = self._tables()
+        missing = [d for d in offs.tolist() if d not in self._views]
+        arena = self._dev.vals.cpu().numpy() if len(missing) > 1 else None
+        for i, d in enumerate(offs.tolist()):
+            if d not in self._views:
+                self._views[d] = self._download(i, d, arena)
+            yield self._views[d]
 
     def diag_count(self) -> int:
-        return len(self._dev.offs) if self._host is None else len(self._host)
+        return len(self._host) if self._host is not None else len(self._tables()[0])
 
     def copy(self) -> "DiaqMatrix":
         if self._host is None:
-            dv = self._dev
-            return DiaqMatrix._from_device(self.n_dim, dv.offs.copy(), dv.starts.copy(),
-                                           dv.vals.clone(), self.dtype)
+            offs, starts = self._tables()
+            return DiaqMatrix._from_device(self.n_dim, offs.copy(), starts.copy(), self._dev.vals.clone(), self.dtype)
         out = DiaqMatrix(self.n_dim, self.dtype, self.align)
-        for diag in self.diagonals():
-            out.set_diag(diag.index, diag.re, diag.im)
+        out._host = {d: Diagonal(d, dg.re.copy(), dg.im.copy()) for d, dg in self._host.items()}
         return out
 
     # -- convenience -----------------------------------------------------------
@@ -203,10 +297,19 @@ class DiaqMatrix:
             return NotImplemented
         if self.n_dim != other.n_dim or self.diag_indices() != other.diag_indices():
             return False
-        return all(
-            np.array_equal(a.re, b.re) and np.array_equal(a.im, b.im)
-            for a, b in zip(self.diagonals(), other.diagonals())
-        )
+        if self._host is None and other._host is None:  # both on the device: compare there
+            t = L.torch()
+            oa, sa = self._tables()
+            _, sb = other._tables()
+            va, vb = self._dev.vals, other._dev.vals
+            for d, s1, s2 in zip(oa.tolist(), sa.tolist(), sb.tolist()):
+                n = self.n_dim - abs(d)
+                a, b = t.view_as_real(va[s1:s1 + n]), t.view_as_real(vb[s2:s2 + n])
+                if not bool((a == b).all()):  # == semantics: -0 equals +0, NaN never equal
+                    return False
+            return True
+        return all(np.array_equal(x.re, y.re) and np.array_equal(x.im, y.im)
+                   for x, y in zip(self.diagonals(), other.diagonals()))
 
     __hash__ = None
 
@@ -267,7 +370,7 @@ def to_dense(a: DiaqMatrix) -> np.ndarray:
     return dense.cpu().numpy().reshape(n, n)
 
 
-# -- kernels -----------------------------------------------------------------------
+# -- spgemm ------------------------------------------------------------------------
 
 
 def _pair_range(d_a: int, d_b: int, n: int) -> tuple[int, int]:
@@ -276,53 +379,141 @@ def _pair_range(d_a: int, d_b: int, n: int) -> tuple[int, int]:
     return max(0, -d_a, -d_c), min(n, n - d_a, n - d_c)
 
 
-def _spgemm(a: DiaqMatrix, b: DiaqMatrix, prune_eps: float):
-    """Run the device spgemm; return (candidate offsets, keep flags, C arena, starts)."""
+def _dev_plan_capacity(n: int, pair_cap: int) -> tuple[int, int]:
+    """(candidate slots, arena elements) bounding a device-planned product."""
+    ncap = max(1, min(pair_cap, 2 * n - 1))
+    return ncap, ncap * (n + 7) + 8
+
+
+def _use_dev_plan(a: DiaqMatrix, b: DiaqMatrix) -> bool:
+    pc = a._cap() * b._cap()
+    if pc < 1 or pc > DEV_PLAN_PAIRS:
+        return False
+    return 16 * _dev_plan_capacity(a.n_dim, pc)[1] <= DEV_PLAN_BYTES
+
+
+def _spgemm_host(a: DiaqMatrix, b: DiaqMatrix, prune_eps: float):
+    """Host-planned product (exact layout): returns (candidate offsets,
+    starts, C arena, device keep flags)."""
     t = L.torch()
     n = a.n_dim
-    da, db = a._device(), b._device()
-    cap = max(1, len(da.offs) * len(db.offs))
+    oa, _ = a._tables()
+    ob, _ = b._tables()
+    cap = max(1, len(oa) * len(ob))
     offc = np.zeros(cap, dtype=np.int64)
     nc = ctypes.c_int64(0)
-    L.call("diaq_spgemm_plan", n, len(da.offs), da.offs.ctypes.data if len(da.offs) else None,
-           len(db.offs), db.offs.ctypes.data if len(db.offs) else None, offc.ctypes.data,
-           ctypes.addressof(nc))
+    L.call("diaq_spgemm_plan", n, len(oa), oa.ctypes.data if len(oa) else None,
+           len(ob), ob.ctypes.data if len(ob) else None, offc.ctypes.data, ctypes.addressof(nc))
     offc = offc[: nc.value].copy()
     starts, total = L.layout(n, offc)
     cvals = L.empty_c128(max(total, 1))
+    keep = t.empty(max(1, len(offc)), dtype=t.uint8, device=cvals.device)
     if len(offc) == 0:
-        return offc, np.zeros(0, np.uint8), cvals, starts
-    keep = t.empty(len(offc), dtype=t.uint8, device=cvals.device)
-    if len(offc) <= 128 and len(da.offs) * len(db.offs) <= 512:
+        return offc, starts, cvals, keep
+    if len(offc) <= 128 and len(oa) * len(ob) <= 512:
         ws, ws_bytes = None, 0  # the plan travels in the kernel parameters
     else:
-        ws_bytes = int(L.load().diaq_spgemm_workspace(len(da.offs), len(db.offs), len(offc)))
+        ws_bytes = int(L.load().diaq_spgemm_workspace(len(oa), len(ob), len(offc)))
         ws = t.empty(ws_bytes, dtype=t.uint8, device=cvals.device)
-    sa = L.mat_struct(n, da.offs, da.starts, da.vals)
-    sb = L.mat_struct(n, db.offs, db.starts, db.vals)
     sc = L.mat_struct(n, offc, starts, cvals)
-    L.call("diaq_spgemm", ctypes.byref(sa), ctypes.byref(sb), ctypes.byref(sc), keep.data_ptr(),
-           float(prune_eps), ws.data_ptr() if ws is not None else None, ws_bytes, L.stream_handle())
-    return offc, keep.cpu().numpy(), cvals, starts
+    L.call("diaq_spgemm", ctypes.byref(a._struct()), ctypes.byref(b._struct()), ctypes.byref(sc), keep.data_ptr(),
+           float(prune_eps), _single(a, b), ws.data_ptr() if ws is not None else None, ws_bytes, L.stream_handle())
+    return offc, starts, cvals, keep
+
+
+def _matmul_host(a: DiaqMatrix, b: DiaqMatrix, dtype) -> DiaqMatrix:
+    """Host plan + device multiply; the prune is compacted on the device
+    (no read back of the keep flags)."""
+    t = L.torch()
+    offc, starts, cvals, keep = _spgemm_host(a, b, PRUNE_EPS)
+    nc = len(offc)
+    if nc == 0:
+        return DiaqMatrix._from_device(a.n_dim, offc, starts, cvals, dtype)
+    cand = t.from_numpy(np.concatenate([offc, starts])).pin_memory().to(cvals.device, non_blocking=True)
+    dtab = t.empty(1 + 2 * nc, dtype=t.int64, device=cvals.device)
+    base = dtab.data_ptr()
+    L.call("diaq_spgemm_compact", nc, cand.data_ptr(), keep.data_ptr(), base, base + 8, base + 8 * (1 + nc),
+           L.stream_handle())
+    # (cand is freed stream-ordered: its memory is reused only after the compaction ran)
+    return DiaqMatrix._from_device(a.n_dim, None, None, cvals, dtype, dtab=dtab, cap=nc)
+
+
+def matmul_batch(pairs) -> list[DiaqMatrix]:
+    """Products of many (A, B) pairs (a sweep, config 2) in one native call:
+    the structure of every product is planned on the device (offset union,
+    count and scan), multiplied and pruned in one launch of each kernel per
+    64 products -- no host round trip.  Each result equals matmul(A, B)."""
+    t = L.torch()
+    pairs = list(pairs)
+    if not pairs:
+        return []
+    out: list[DiaqMatrix | None] = [None] * len(pairs)
+    dev_idx = []
+    for i, (a, b) in enumerate(pairs):
+        if a.n_dim != b.n_dim:
+            raise ShapeError(f"not multiplyable: {a.n_dim}x{a.n_dim} by {b.n_dim}x{b.n_dim}")
+        if _use_dev_plan(a, b):
+            dev_idx.append(i)
+        else:
+            out[i] = matmul(a, b)
+    if dev_idx:
+        pair_cap = max(pairs[i][0]._cap() * pairs[i][1]._cap() for i in dev_idx)
+        caps = [_dev_plan_capacity(pairs[i][0].n_dim, pair_cap) for i in dev_idx]
+        elem_off = np.cumsum([0] + [(c[1] + 31) & ~31 for c in caps])  # 512-byte aligned result arenas
+        dev = L.device()
+        arena = L.empty_c128(int(elem_off[-1]))
+        ncap_max = max(c[0] for c in caps)
+        dtabs = t.empty((len(dev_idx), 1 + 2 * ncap_max), dtype=t.int64, device=dev)
+        count = len(dev_idx)
+        A = (L.DevMatrix * count)()
+        B = (L.DevMatrix * count)()
+        C = (L.DevResult * count)()
+        abase, tbase = arena.data_ptr(), dtabs.data_ptr()
+        row = 8 * (1 + 2 * ncap_max)
+        for j, i in enumerate(dev_idx):
+            a, b = pairs[i]
+            A[j] = a._dev_struct()
+            B[j] = b._dev_struct()
+            tb = tbase + j * row
+            C[j] = L.DevResult(tb, tb + 8, tb + 8 * (1 + ncap_max), abase + 16 * int(elem_off[j]), caps[j][1],
+                               ncap_max)
+        ws_bytes = int(L.load().diaq_spgemm_dev_workspace(count, pair_cap))
+        ws = t.empty(ws_bytes, dtype=t.uint8, device=dev)
+        single = int(all(_single(*pairs[i]) for i in dev_idx))
+        if single or not any(_single(*pairs[i]) for i in dev_idx):
+            L.call("diaq_spgemm_dev", count, A, B, C, float(PRUNE_EPS), single, pair_cap, ws.data_ptr(), ws_bytes,
+                   L.stream_handle())
+        else:  # mixed precisions in one sweep: one call per precision
+            for j, i in enumerate(dev_idx):
+                L.call("diaq_spgemm_dev", 1, ctypes.byref(A[j]), ctypes.byref(B[j]), ctypes.byref(C[j]),
+                       float(PRUNE_EPS), _single(*pairs[i]), pair_cap, ws.data_ptr(), ws_bytes, L.stream_handle())
+        for j, i in enumerate(dev_idx):
+            a, b = pairs[i]
+            vals = arena[int(elem_off[j]):int(elem_off[j + 1])]
+            out[i] = DiaqMatrix._from_device(a.n_dim, None, None, vals, np.result_type(a.dtype, b.dtype),
+                                             dtab=dtabs[j], cap=ncap_max)
+    return out
 
 
 def matmul(a: DiaqMatrix, b: DiaqMatrix) -> DiaqMatrix:
     """Sparse product A @ B over diagonal pairs (matrix.py:218-250).
 
-    Device two-pass spgemm: bitwise equal to the reference (each result
-    diagonal accumulates its pairs in ascending d_a from zero), structure
-    included; result diagonals entirely below PRUNE_EPS are dropped.
+    Bitwise equal to the reference (each result diagonal accumulates its
+    pairs in ascending d_a from zero, in the result precision), structure
+    included; result diagonals entirely below PRUNE_EPS are dropped.  Small
+    structures are planned on the device (north-star pass 1: offset union,
+    count and scan), larger ones on the host; either way the prune is
+    compacted on the device and nothing is read back.
     """
     if a.n_dim != b.n_dim:
         raise ShapeError(
             f"not multiplyable: {a.n_dim}x{a.n_dim} by {b.n_dim}x{b.n_dim}"
         )
-    dtype = np.result_type(a.dtype, b.dtype)
-    if dtype != np.float64:
-        raise UnsupportedFeatureError("device spgemm computes in double precision only")
-    offc, keep, cvals, starts = _spgemm(a, b, PRUNE_EPS)
-    kept = keep.astype(bool)
-    return DiaqMatrix._from_device(a.n_dim, offc[kept], starts[kept], cvals, dtype)
+    if a._cap() == 0 or b._cap() == 0:
+        return DiaqMatrix(a.n_dim, np.result_type(a.dtype, b.dtype))
+    if _use_dev_plan(a, b):
+        return matmul_batch([(a, b)])[0]
+    return _matmul_host(a, b, np.result_type(a.dtype, b.dtype))
 
 
 def multiply_diagonals(diag_a: Diagonal, diag_b: Diagonal, n_dim: int):
@@ -342,9 +533,12 @@ def multiply_diagonals(diag_a: Diagonal, diag_b: Diagonal, n_dim: int):
     a.set_diag(d_a, diag_a.re, diag_a.im)
     b = DiaqMatrix(n_dim, diag_b.re.dtype)
     b.set_diag(d_b, diag_b.re, diag_b.im)
-    offc, _, cvals, starts = _spgemm(a, b, -1.0)
+    offc, starts, cvals, _ = _spgemm_host(a, b, -1.0)  # no prune: the partial diagonal as is
     c = DiaqMatrix._from_device(n_dim, offc, starts, cvals, diag_a.re.dtype)
     return d_c, c.get(d_c)
+
+
+# -- spmv ----------------------------------------------------------------------------
 
 
 def _as_device_vector(x, n: int):
@@ -360,6 +554,14 @@ def _as_device_vector(x, n: int):
     return L.to_device_c128(x), "numpy"
 
 
+def _overlaps(a, b) -> bool:
+    """Do two tensors share any byte of storage?"""
+    if a.device != b.device:
+        return False
+    a0, b0 = a.data_ptr(), b.data_ptr()
+    return a0 < b0 + b.numel() * b.element_size() and b0 < a0 + a.numel() * a.element_size()
+
+
 HOST_PIPELINE_MIN = 1 << 21  # rows; above this host vectors take the pipelined path
 HOST_CHUNK_ROWS = 1 << 22
 
@@ -370,15 +572,18 @@ def spmv(a: DiaqMatrix, x, out=None):
     Bitwise equal to the reference.  A host numpy `x` returns a host
     complex128 array (reference behaviour); a CUDA tensor returns a CUDA
     tensor.  `out` (extension): a complex128 torch tensor, on the device or in
-    (pinned) host memory, that receives y.  Large host vectors go through
-    diaq_spmv_host, which overlaps the H2D of x, the kernel and the D2H of y
-    chunk by chunk.
+    (pinned) host memory, that receives y; it must not overlap x (the
+    kernel stages windows of x while other rows of y are written).  Large
+    host vectors go through diaq_spmv_host, which overlaps the H2D of x, the
+    kernel and the D2H of y chunk by chunk.
     """
     n = a.n_dim
     t = L.torch()
     if out is not None and (not isinstance(out, t.Tensor) or tuple(out.shape) != (n,)
                             or out.dtype != t.complex128):
         raise ShapeError(f"out must be a complex128 tensor of shape ({n},)")
+    if out is not None and isinstance(x, t.Tensor) and _overlaps(out, x):
+        raise ValueError("spmv: out must not share storage with x")
     on_host = not (isinstance(x, t.Tensor) and x.device.type == "cuda")
     if on_host and n >= HOST_PIPELINE_MIN and (out is None or out.device.type == "cpu"):
         if isinstance(x, t.Tensor):
@@ -412,23 +617,43 @@ def spmv(a: DiaqMatrix, x, out=None):
     return y if kind == "cuda" else y.cpu()
 
 
-# -- metadata operations (host side; not on the hot path) ---------------------
+# -- matrix algebra (device kernels, ops.cu) --------------------------------------
 
 
 def transpose(a: DiaqMatrix) -> DiaqMatrix:
-    """Transpose: diagonal d moves to -d, value arrays unchanged (matrix.py:281-290)."""
-    out = DiaqMatrix(a.n_dim, a.dtype, a.align)
-    for diag in a.diagonals():
-        out.set_diag(-diag.index, diag.re, diag.im)
+    """Transpose: diagonal d becomes -d over the SAME arena (matrix.py:281-290:
+    position k of diagonal d and of -d are transposes) -- no data moves."""
+    if a.diag_count() == 0:
+        return DiaqMatrix(a.n_dim, a.dtype, a.align)
+    offs, starts = a._tables()
+    out = DiaqMatrix._from_device(a.n_dim, -offs[::-1], starts[::-1], a._dev.vals, a.dtype)
+    out.align = a.align
     return out
+
+
+def _arena_map(a: DiaqMatrix, op: int, s: complex = 0j) -> DiaqMatrix:
+    offs, starts = a._tables()
+    src = a._dev.vals
+    dst = L.empty_c128(src.numel())
+    L.call("diaq_arena_map", int(src.numel()), src.data_ptr(), dst.data_ptr(), int(op), float(s.real), float(s.imag),
+           _single(a), L.stream_handle())
+    return DiaqMatrix._from_device(a.n_dim, offs.copy(), starts.copy(), dst, a.dtype)
 
 
 def adjoint(a: DiaqMatrix) -> DiaqMatrix:
-    """Conjugate transpose (matrix.py:293-298)."""
-    out = DiaqMatrix(a.n_dim, a.dtype, a.align)
-    for diag in a.diagonals():
-        out.set_diag(-diag.index, diag.re, -diag.im)
-    return out
+    """Conjugate transpose (matrix.py:293-298): a conj pass over the arena,
+    then the transpose relabel."""
+    if a.diag_count() == 0:
+        return DiaqMatrix(a.n_dim, a.dtype, a.align)
+    return transpose(_arena_map(a, 0))
+
+
+def scale(a: DiaqMatrix, s: complex) -> DiaqMatrix:
+    """Every stored value times s: (sr*re - si*im, sr*im + si*re) in a's
+    precision (matrix.py:318-323)."""
+    if a.diag_count() == 0:
+        return DiaqMatrix(a.n_dim, a.dtype, a.align)
+    return _arena_map(a, 1, complex(s))
 
 
 def add(a: DiaqMatrix, b: DiaqMatrix) -> DiaqMatrix:
@@ -436,52 +661,30 @@ def add(a: DiaqMatrix, b: DiaqMatrix) -> DiaqMatrix:
     if a.n_dim != b.n_dim:
         raise ShapeError(f"shape mismatch: {a.n_dim} vs {b.n_dim}")
     dtype = np.result_type(a.dtype, b.dtype)
-    out = DiaqMatrix(a.n_dim, dtype)
-    for d in sorted(set(a.diag_indices()) | set(b.diag_indices())):
-        length = diag_len(d, a.n_dim)
-        re = np.zeros(length, dtype=dtype)
-        im = np.zeros(length, dtype=dtype)
-        for src in (a.get(d), b.get(d)):
-            if src is not None:
-                re += src.re
-                im += src.im
-        out.set_diag(d, re, im)
-    return out
-
-
-def scale(a: DiaqMatrix, s: complex) -> DiaqMatrix:
-    """Multiply every stored value by the complex scalar s (matrix.py:318-323)."""
-    sr, si = s.real, s.imag
-    out = DiaqMatrix(a.n_dim, a.dtype, a.align)
-    for diag in a.diagonals():
-        out.set_diag(diag.index, sr * diag.re - si * diag.im, sr * diag.im + si * diag.re)
+    union = np.union1d(np.asarray(a.diag_indices(), dtype=np.int64), np.asarray(b.diag_indices(), dtype=np.int64))
+    out = DiaqMatrix._empty_device(a.n_dim, union, dtype)
+    if len(union):
+        L.call("diaq_add", ctypes.byref(a._struct()), ctypes.byref(b._struct()), ctypes.byref(out._struct()),
+               int(dtype == np.float32), L.stream_handle())
     return out
 
 
 def kron(a: DiaqMatrix, b: DiaqMatrix) -> DiaqMatrix:
-    """General Kronecker product A (x) B (matrix.py:329-355; test-level API).
-
-    Source pair (d_a, d_b) lands on result diagonal d_a*n_b + d_b at rows
-    r_a*n_b + r_b; distinct pairs feeding one result diagonal never overlap.
-    """
-    n_a, n_b = a.n_dim, b.n_dim
-    n = n_a * n_b
+    """General Kronecker product A (x) B (matrix.py:329-355; test-level API):
+    result diagonal d = d_a*n_b + d_b; each output element finds its unique
+    source pair from its row and column on the device."""
+    t = L.torch()
+    nb = b.n_dim
+    n = a.n_dim * nb
     dtype = np.result_type(a.dtype, b.dtype)
-    bufs: dict[int, tuple[np.ndarray, np.ndarray]] = {}
-    for diag_a in a.diagonals():
-        rows_a = np.arange(len(diag_a)) - min(diag_a.index, 0)
-        for diag_b in b.diagonals():
-            rows_b = np.arange(len(diag_b)) - min(diag_b.index, 0)
-            d = diag_a.index * n_b + diag_b.index
-            if d not in bufs:
-                bufs[d] = (np.zeros(n - abs(d), dtype=dtype), np.zeros(n - abs(d), dtype=dtype))
-            re, im = bufs[d]
-            k = (rows_a[:, None] * n_b + rows_b[None, :] + min(d, 0)).ravel()
-            re[k] = (np.outer(diag_a.re, diag_b.re) - np.outer(diag_a.im, diag_b.im)).ravel()
-            im[k] = (np.outer(diag_a.re, diag_b.im) + np.outer(diag_a.im, diag_b.re)).ravel()
-    out = DiaqMatrix(n, dtype)
-    for d in sorted(bufs):
-        out.set_diag(d, *bufs[d])
+    oa, sa = a._tables()
+    ob, sb = b._tables()
+    offs = np.unique((oa[:, None] * nb + ob[None, :]).reshape(-1)) if len(oa) and len(ob) else np.zeros(0, np.int64)
+    out = DiaqMatrix._empty_device(n, offs, dtype)
+    if len(offs):
+        tabs = t.from_numpy(np.concatenate([oa, sa, ob, sb]).astype(np.int64)).to(L.device())
+        L.call("diaq_kron", ctypes.byref(a._struct()), ctypes.byref(b._struct()), tabs.data_ptr(),
+               ctypes.byref(out._struct()), int(dtype == np.float32), L.stream_handle())
     return out
 
 
@@ -521,24 +724,34 @@ def sparsity(a: DiaqMatrix, eps: float = 1e-15) -> float:
 
 
 # -- serialization (wire form of the kernel protocol, cli.py:251-287) -------------
+#
+# {"n": N, "diags": {"<d>": [[re, im], ...]}} (reference matrix.py:410-434).
+# Values travel as Python floats of the stored precision.
 
 
 def to_json_dict(a: DiaqMatrix) -> dict:
-    """Wire form: {"n": N, "diags": {"<d>": [[re, im], ...]}} (matrix.py:410-418)."""
-    return {
-        "n": a.n_dim,
-        "diags": {
-            str(diag.index): [[float(r), float(i)] for r, i in zip(diag.re, diag.im)]
-            for diag in a.diagonals()
-        },
-    }
+    diags = {}
+    for dg in a.diagonals():
+        pairs = np.empty((len(dg), 2), dtype=np.float64)
+        pairs[:, 0] = dg.re
+        pairs[:, 1] = dg.im
+        diags[str(dg.index)] = pairs.tolist()
+    return {"n": a.n_dim, "diags": diags}
 
 
 def from_json_dict(obj: dict, dtype=np.float64) -> DiaqMatrix:
-    out = DiaqMatrix(int(obj["n"]), dtype)
+    """Build the matrix in one piece: all wire diagonals parsed, then one
+    host table (uploaded on first device use)."""
+    n = int(obj["n"])
+    out = DiaqMatrix(n, dtype)
+    table = {}
     for key, pairs in obj.get("diags", {}).items():
+        d = int(key)
         arr = np.asarray(pairs, dtype=np.float64).reshape(-1, 2)
-        out.set_diag(int(key), arr[:, 0], arr[:, 1])
+        if len(arr) != diag_len(d, n):
+            raise ShapeError(f"diagonal {d} of n_dim={n} needs {diag_len(d, n)} values")
+        table[d] = Diagonal(d, np.ascontiguousarray(arr[:, 0], dtype=dtype), np.ascontiguousarray(arr[:, 1], dtype=dtype))
+    out._host = table
     return out
 
 

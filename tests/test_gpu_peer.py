@@ -94,14 +94,16 @@ def test_bench_multi_rank_paths_on_one_gpu(tmp_path):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"),
            "--gpus", "2", "--steps", "2", "--warmup", "3", "--no-e2e", "--no-cpu", "--no-secondary",
-           "--qubits", "23", "--sharded-gates", "--remap"]
+           "--qubits", "23", "--circuit-qubits", "16", "--circuit-layers", "3"]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
     assert p.returncode == 0, p.stderr[-3000:]
     line = json.loads(p.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and "peer loads" in line["config"]["parallelism"]
-    assert line["gates"]["transport"] == "peer" and line["gates"]["stats"]["exchanged"] > 0
-    assert abs(line["gates"]["norm_after"] - 1.0) < 1e-10
-    assert line["gates"]["remap"] is True
+    g = line["gates"]
+    # the default N>1 gate measurement is the sharded config-5 circuit
+    assert g["mode"].startswith("config 5") and g["circuit_qubits"] == 17 and g["transport"] == "peer"
+    assert g["runs"]["plain"]["cross_shard_ops"] > 0 and g["runs"]["remap"]["swaps"] > 0
+    assert g["norm_ok"] and abs(g["norm_after"] - 1.0) < 1e-10
 
 
 _NCCL_SCRIPT = r"""
