@@ -144,6 +144,10 @@ def load():
         raise DeviceError(
             f"{LIB_PATH} is missing: build it with `python -m paper_2405_01250_b200.build` "
             "(no CPU fallback exists)")
+    # specialised-pass cubins persist in the tree next to the library (built
+    # by __graft_entry__.build() for the benchmark's programs, and travelling
+    # with the snapshot); DIAQ_JIT_CACHE overrides, "0" disables
+    os.environ.setdefault("DIAQ_JIT_CACHE", os.path.join(os.path.dirname(os.path.dirname(LIB_PATH)), "build", "jit_cache"))
     lib = ctypes.CDLL(LIB_PATH)
     for name, (args, res) in _SIGS.items():
         fn = getattr(lib, name)

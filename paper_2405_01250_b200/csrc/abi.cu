@@ -107,6 +107,8 @@ extern "C" int diaq_tune(const char *key, int64_t value) {
     else if (k == "fused_jit") t.fused_jit = (int)value;
     else if (k == "fused_tbits") t.fused_tbits = (int)(value <= 7 ? 7 : 8);
     else if (k == "fused_gstore") t.fused_gstore = (int)value;
+    else if (k == "fused_dstore") t.fused_dstore = (int)value;
+    else if (k == "fused_ppipe") t.fused_ppipe = (int)(value < 0 ? 0 : value > 3 ? 3 : value);
     else if (k == "fused_plain_pair") t.fused_plain_pair = (int)value;
     else if (k == "fused_pair_store") t.fused_pair_store = (int)value;
     else if (k == "fused_bank_spread") t.fused_bank_spread = (int)value;

@@ -32,6 +32,8 @@ struct Tuning {
     int fused_gstore = 0;      // global-map (out-of-place permuted) store policy: 0 .cs, 1 default, 2 evict_last
     int fused_bank_spread = 3;  // fused passes, quarter-warp lanes on bank-spreading positions: 1 phase
                                 // thread bits, 2 pair-store destination basis (bitmask)
+    int fused_dstore = 0;      // plain-pair passes: last phase stored from registers (TileParams::dstore; measured 1.72 vs 1.68 ms, r02o)
+    int fused_ppipe = 0;       // plain-pair schedule (TileParams::ppipe)
     int fused_plain_pair = 1;  // specialised passes over 128-byte tile rows: tiles paired across bit 3 (256-byte DRAM runs)
     int fused_pair_store = 2;  // specialised passes: sector-splitting global tails stored as tile pairs
                                // (2: any tile, 1: 11-bit tiles only, 0: off)

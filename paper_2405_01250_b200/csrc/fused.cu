@@ -858,9 +858,9 @@ static std::vector<char> program_key(int n_total, int n_bits, int T, int ngates,
         key.insert(key.end(), c, c + n);
     };
     // every tuning switch the schedule depends on is part of the key
-    const int head[13] = {n_total, n_bits, T, pass_tbits(), ngates, tuning().fused_perm,
+    const int head[15] = {n_total, n_bits, T, pass_tbits(), ngates, tuning().fused_perm,
                           tuning().fused_gperm && !t_no_gperm, tuning().fused_seq, tuning().fused_dense2,
-                          tuning().fused_gperm_rows, tuning().fused_pair_store, tuning().fused_bank_spread, tuning().fused_plain_pair};
+                          tuning().fused_gperm_rows, tuning().fused_pair_store, tuning().fused_bank_spread, tuning().fused_plain_pair, tuning().fused_ppipe, tuning().fused_dstore};
     put(head, sizeof(head));
     for (int i = 0; i < ngates; ++i) {
         const diaq_gate_t &gt = gates[i];
@@ -1046,6 +1046,8 @@ static std::shared_ptr<const Program> build_program(int n_total, int n_bits, int
             while (lowest < n_bits && ((p.tmask >> lowest) & 1ull)) ++lowest;
             if (lowest == kLowBits) {
                 p.ppair = 1;
+                p.ppipe = (int8_t)tuning().fused_ppipe;
+
                 p.gpb[0] = (int8_t)lowest;
                 p.emask = p.tmask | (1ull << lowest);
                 for (int k = 0, b = 0; b < 64; ++b)
@@ -1053,6 +1055,21 @@ static std::shared_ptr<const Program> build_program(int n_total, int n_bits, int
             }
         }
         std::copy(ps.phases.begin(), ps.phases.end(), p.ph);
+        if (p.ppair && p.ppipe == 0 && tuning().fused_dstore && p.nphases > 0) {
+            Phase &lp = p.ph[p.nphases - 1];
+            const int R = p.tbits - pass_tbits();
+            bool ok = !lp.generic && !lp.post.on && p.tbits - R >= kLowBits;
+            for (int q = 0; q < R && ok; ++q) ok = lp.rpos[q] >= kLowBits;
+            if (ok) {  // thread bits 0-2 on tile positions 0-2 (the lane-contiguous rows), the rest as before
+                int8_t tp[kMaxTileBits];
+                int m = 0;
+                for (int b = 0; b < kLowBits; ++b) tp[m++] = (int8_t)b;
+                for (int k = 0; k < p.tbits - R; ++k)
+                    if (lp.tpos[k] >= kLowBits) tp[m++] = lp.tpos[k];
+                for (int k = 0; k < p.tbits - R; ++k) lp.tpos[k] = tp[k];
+                p.dstore = 1;
+            }
+        }
         std::copy(ps.gates.begin(), ps.gates.end(), p.g);
         std::copy(ps.pk.coef.begin(), ps.pk.coef.end(), p.coef);
         std::copy(ps.pk.nz.begin(), ps.pk.nz.end(), p.nz);

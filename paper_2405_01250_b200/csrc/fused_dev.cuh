@@ -146,6 +146,11 @@ struct TileParams {
     // different CTAs at different times (row-buffer locality: a pass over
     // high tile bits ran 1.98 ms against 1.50 ms with 256-byte runs, r02e)
     int8_t ppair;
+    int8_t dstore;  // specialised passes: the last phase stores to HBM from registers (its register bits
+                    // avoid tile positions 0-2, thread bits 0-2 sit on them: 128-byte rows per 8 lanes)
+    int8_t ppipe;   // plain pair schedule: 0 both halves land before either computes, 1 half A computes
+                    // while B lands, 2 half A is stored and the next A fetched while B computes,
+                    // 3 the halves run on the two CTAs of a cluster (fetches aligned by a cluster barrier)
     int8_t gpb[3];
     int8_t eb[kMaxTileBits + 3];
     uint64_t emask;
@@ -814,11 +819,16 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     __syncthreads();
-    auto phases = [&](uint32_t buf) {
+    // dbase / on_loaded: with S.dstore the last phase writes its registers
+    // straight to y + dbase (no smem round trip), and on_loaded() runs once
+    // every thread has read its last-phase registers (the tile buffers are
+    // free from then on: the next unit's fetch can start under the compute)
+    auto phases = [&](uint32_t buf, uint64_t dbase, auto &&on_loaded) {
         double2 *tl = tile + ((buf - tile0) >> 4);
         DIAQ_SUNROLL
         for (int ph_i = 0; ph_i < S.nphases; ++ph_i) {
             const Phase &ph = S.ph[ph_i];
+            const bool direct = S.dstore && ph_i == S.nphases - 1;
             if (ph.generic) {
                 DIAQ_SUNROLL
                 for (int gi = ph.g0; gi < ph.g1; ++gi) {
@@ -836,6 +846,10 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
             const uint32_t a = buf + (ph_i < kPre ? (uint32_t)s_t16[ph_i][tid] : (swz(tpart) << 4));
 #pragma unroll
             for (int j = 0; j < NR; ++j) v[j] = lds128(slot_addr(a, ph.pj[j]));
+            if (direct) {
+                __syncthreads();  // every thread holds its registers: the buffers are free
+                on_loaded();
+            }
             if (ph.seq) {
                 int gi = ph.g0;
                 seq_steps<R, MODE, 0>(v, S, ph, gi, tpart, &s_sbase, sc, snz);
@@ -845,7 +859,22 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
                 DIAQ_SUNROLL
                 for (int gi = ph.g0; gi < ph.g1; ++gi) dispatch_gate<R, MODE>(v, S.g[gi], tpart, &s_sbase, sc, snz);
             }
-            if (ph.post.on) {
+            if (direct) {
+                // register j of this thread = tile position tpart | e_j: state
+                // offset dep(tpart) + dep(e_j), the latter a constant
+                uint64_t toff = 0;
+                DIAQ_SUNROLL
+                for (int i = 0; i < TB; ++i) toff |= (uint64_t)((tid >> i) & 1u) << S.tb[ph.tpos[i]];
+                double2 *dst = p.y + (dbase + toff);
+#pragma unroll
+                for (int j = 0; j < NR; ++j) {
+                    uint64_t roff = 0;
+#pragma unroll
+                    for (int q = 0; q < R; ++q)
+                        if ((j >> q) & 1) roff |= 1ull << S.tb[ph.rpos[q]];
+                    st_stream(dst + roff, v[j]);
+                }
+            } else if (ph.post.on) {
                 __syncthreads();  // relabelled slots belong to other threads' registers: all reads first
                 const uint32_t bc = swz(aff_const(ph.post, ld_base(&s_sbase)));
                 const uint32_t pt = (ph_i < kPre ? (uint32_t)s_pt[ph_i][tid] : swz(aff_lin(ph.post, tpart, T))) ^ bc;
@@ -893,7 +922,7 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
                     if (h == 0) s_ab = p.gconst ^ gmap(S, gb);
                 }
                 __syncthreads();
-                phases(h ? buf1 : tile0);
+                phases(h ? buf1 : tile0, 0ull, [] {});
             }
             __syncthreads();
             const uint64_t ab = s_ab ^ pw_t;
@@ -920,6 +949,37 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
         }
         return;
     }
+    if (S.ppair && S.ppipe == 3) {
+        // Plain pair across a CTA pair (thread-block cluster of 2): CTA rank h
+        // owns half h of every pair unit.  Both CTAs pass a cluster barrier
+        // before each fetch, so the two halves of every 256-byte DRAM run are
+        // requested together (the locality of the one-CTA pair) while each
+        // CTA holds one tile (32 KB) -- more resident CTAs per SM to hide the
+        // fetch latency.
+        uint32_t half;
+        asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(half));
+        const uint64_t hb = half ? (1ull << S.gpb[0]) : 0ull;
+        const int64_t nunits = p.ntiles >> 1;
+        const int64_t u0 = blockIdx.x >> 1, ustep = gridDim.x >> 1;
+        const uint32_t a = tile0 + t16;
+        uint64_t gb = insert_zero_bits_dyn((uint64_t)u0, S.eb, T + 1);
+        for (int64_t t = u0; t < nunits; t += ustep) {
+            const uint64_t ngb = ((gb | S.emask) + p.gstep) & ~S.emask;
+            cluster_sync();
+            fetch(gb | hb, tile0);
+            if (tid == 0) s_sbase = (gb | hb) | p.gbase;
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncthreads();
+            phases(tile0, 0ull, [] {});
+            double2 *dst = p.y + ((gb | hb) + t_off);
+#pragma unroll
+            for (int k = 0; k < NR; ++k) st_stream(dst + kdep(k), lds128(slot_addr(a, swz((uint32_t)k << TB))));
+            __syncthreads();
+            gb = ngb;
+        }
+        cluster_sync();  // no CTA of a cluster exits while its partner may still arrive
+        return;
+    }
     if (S.ppair) {
         const uint64_t pbit = 1ull << S.gpb[0];
         const int64_t nunits = p.ntiles >> 1;
@@ -936,8 +996,82 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
         };
+        auto fetch1 = [&](uint64_t b, uint32_t a) {  // one half, its own commit group
+            const double2 *src = p.x + (b + t_off);
+#pragma unroll
+            for (int k = 0; k < NR; ++k) cp_async16_s(slot_addr(a, swz((uint32_t)k << TB)), src + kdep(k));
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        auto store1 = [&](uint64_t b, uint32_t a) {
+            double2 *dst = p.y + (b + t_off);
+#pragma unroll
+            for (int k = 0; k < NR; ++k) st_stream(dst + kdep(k), lds128(slot_addr(a, swz((uint32_t)k << TB))));
+        };
         uint64_t gb = insert_zero_bits_dyn((uint64_t)blockIdx.x, S.eb, T + 1);
+        if (S.ppipe) {
+            if ((int64_t)blockIdx.x < nunits) {
+                fetch1(gb, a0);
+                fetch1(gb | pbit, a1);
+            }
+            for (int64_t t = blockIdx.x; t < nunits; t += gridDim.x) {
+                const uint64_t ngb = ((gb | S.emask) + p.gstep) & ~S.emask;
+                const bool more = t + gridDim.x < nunits;
+                asm volatile("cp.async.wait_group 1;" ::: "memory");  // half A landed (B may still fly)
+                if (tid == 0) s_sbase = gb | p.gbase;
+                __syncthreads();
+                phases(tile0, 0ull, [] {});
+                if (S.ppipe == 2) {  // A leaves now; its buffer takes the next A while B computes
+                    store1(gb, a0);
+                    __syncthreads();
+                    if (more) fetch1(ngb, a0);
+                    else asm volatile("cp.async.commit_group;" ::: "memory");  // keep the group count
+                    asm volatile("cp.async.wait_group 1;" ::: "memory");      // half B landed
+                } else {
+                    asm volatile("cp.async.wait_group 0;" ::: "memory");
+                }
+                if (tid == 0) s_sbase = (gb | pbit) | p.gbase;
+                __syncthreads();
+                phases(buf1, 0ull, [] {});
+                if (S.ppipe == 2) {
+                    store1(gb | pbit, a1);
+                    __syncthreads();
+                    if (more) fetch1(ngb | pbit, a1);
+                } else {
+                    double2 *dst = p.y + (gb + t_off);
+#pragma unroll
+                    for (int k = 0; k < NR; ++k) {
+                        const uint32_t sl = swz((uint32_t)k << TB);
+                        st_stream(dst + kdep(k), lds128(slot_addr(a0, sl)));
+                        st_stream(dst + (kdep(k) | pbit), lds128(slot_addr(a1, sl)));
+                    }
+                    __syncthreads();
+                    if (more) {
+                        fetch1(ngb, a0);
+                        fetch1(ngb | pbit, a1);
+                    }
+                }
+                gb = ngb;
+            }
+            return;
+        }
         if ((int64_t)blockIdx.x < nunits) fetch2(gb);
+        if (S.dstore) {  // both halves store from registers; the next pair lands under B's last phase
+            for (int64_t t = blockIdx.x; t < nunits; t += gridDim.x) {
+                const uint64_t ngb = ((gb | S.emask) + p.gstep) & ~S.emask;
+                const bool more = t + gridDim.x < nunits;
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+                if (tid == 0) s_sbase = gb | p.gbase;
+                __syncthreads();
+                phases(tile0, gb, [] {});
+                if (tid == 0) s_sbase = (gb | pbit) | p.gbase;
+                __syncthreads();
+                phases(buf1, gb | pbit, [&] {
+                    if (more) fetch2(ngb);
+                });
+                gb = ngb;
+            }
+            return;
+        }
         for (int64_t t = blockIdx.x; t < nunits; t += gridDim.x) {
             const uint64_t ngb = ((gb | S.emask) + p.gstep) & ~S.emask;
             asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -945,7 +1079,7 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
             for (int h = 0; h < 2; ++h) {
                 if (tid == 0) s_sbase = (gb | (h ? pbit : 0ull)) | p.gbase;
                 __syncthreads();
-                phases(h ? buf1 : tile0);
+                phases(h ? buf1 : tile0, 0ull, [] {});
             }
             double2 *dst = p.y + (gb + t_off);
 #pragma unroll
@@ -980,7 +1114,7 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
             asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
         __syncthreads();
-        phases(buf);
+        phases(buf, 0ull, [] {});
         const uint32_t a = buf + t16;
         if (S.gperm) {  // trailing permutation run: element i goes to A i ^ c in the other buffer
             const uint64_t ab = s_ab ^ g_t;

@@ -196,8 +196,10 @@ __global__ void __launch_bounds__(kThreads) spmv_banded_kernel(const __grid_cons
 constexpr int kAsyncThreads = 128;
 
 
+// parameters sized by the diagonal count (a launch copies the whole block:
+// the 64-diagonal table was ~4 KB per call of a 3-diagonal product)
 template <int ND, bool kParts>
-__global__ void __launch_bounds__(kAsyncThreads) spmv_async_kernel(const __grid_constant__ SpmvParams<kParamDiags> p) {
+__global__ void __launch_bounds__(kAsyncThreads) spmv_async_kernel(const __grid_constant__ SpmvParams<ND> p) {
     __shared__ __align__(16) double2 sd[ND > 0 ? ND : 1][kAsyncThreads];
     __shared__ __align__(16) double2 xs[kMaxBands][kAsyncThreads + 2 * kMaxHalo];
     const uint64_t pol = policy_evict_first();
@@ -455,10 +457,34 @@ static int launch_param_x(const SpmvParams<kParamDiags> &p, cudaStream_t s) {
     return check_launch("spmv_kernel");
 }
 
+template <int ND>
+static void shrink_params(const SpmvParams<kParamDiags> &p, SpmvParams<ND> &q) {
+    q.n = p.n;
+    q.part_bits = p.part_bits;
+    memcpy(q.parts, p.parts, sizeof(q.parts));
+    q.r0 = p.r0;
+    q.rend = p.rend;
+    q.ntiles = p.ntiles;
+    q.stride_tiles = p.stride_tiles;
+    q.nstrips = p.nstrips;
+    q.nitems = p.nitems;
+    q.nchunks = p.nchunks;
+    q.raster = p.raster;
+    q.chunk = p.chunk;
+    q.x = p.x;
+    q.y = p.y;
+    q.nd = p.nd;
+    q.nbands = p.nbands;
+    q.halo = p.halo;
+    for (int b = 0; b < kMaxBands; ++b) q.center[b] = p.center[b];
+    for (int i = 0; i < ND; ++i) q.dg[i] = p.dg[i];
+}
+
 template <int ND, bool kParts>
 static int launch_async(const SpmvParams<kParamDiags> &p, cudaStream_t s) {
     const void *f = (const void *)spmv_async_kernel<ND, kParts>;
-    SpmvParams<kParamDiags> q = p;
+    SpmvParams<ND> q;
+    shrink_params(p, q);
     const int64_t nrows = q.rend - q.r0;
     const int64_t nt = (nrows + kAsyncThreads - 1) / kAsyncThreads;
     const int64_t scale = kThreads / kAsyncThreads;  // strip stride in 128-row tiles
@@ -489,8 +515,8 @@ static int launch_param(const SpmvParams<kParamDiags> &p, cudaStream_t s) {
             const size_t stage_bytes = 16 * (size_t)(ND * kThreads + q.nbands * (kThreads + 2 * q.halo));
             const size_t smem = stage_bytes * (size_t)nstages;
             cudaFuncSetAttribute(spmv_tma_kernel<ND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            int per_sm = 1, dev = 0, sms = kSms;
-            if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            int per_sm = 1;
+            const int sms = sm_count();
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kThreads, smem);
             cudaGetLastError();
             if (tuning().spmv_ctas_per_sm > 0) per_sm = std::min(per_sm, tuning().spmv_ctas_per_sm);
@@ -792,7 +818,7 @@ extern "C" int diaq_spmv_sharded(int64_t n, int64_t nd, const int64_t *offs, con
             }
         }
     }
-    int dev = 0, sms = kSms;    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((nrows + kThreads - 1) / kThreads, (int64_t)sms * 8));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((nrows + kThreads - 1) / kThreads, (int64_t)sm_count() * 8));
     switch (nd) {
 #define DIAQ_SHARD_ND(K) \
     case K: spmv_sharded_kernel<K><<<(unsigned)grid, kThreads, 0, s>>>(p); break;

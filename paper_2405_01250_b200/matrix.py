@@ -65,13 +65,15 @@ class Diagonal:
 class _Dev:
     """Device arena + its structure table (host arrays and/or device table)."""
 
-    __slots__ = ("offs", "starts", "vals", "st", "dtab", "cap")
+    __slots__ = ("offs", "starts", "vals", "st", "st_ref", "dtab", "cap", "rec")
 
     def __init__(self, offs, starts, vals, dtab=None, cap=None):
         self.offs = offs          # host int64 offsets (None: structure only on the device)
         self.starts = starts      # host int64 element starts
         self.vals = vals          # torch complex128 arena
         self.st = None            # diaq_matrix_t, built once (the arena never moves)
+        self.st_ref = None        # ctypes.byref(st), for the per-call fast paths
+        self.rec = None           # diaq_dev_matrix_t fields (device table), built once
         self.dtab = dtab          # device int64 [nd, offs[cap], starts[cap]]
         self.cap = cap if cap is not None else (len(offs) if offs is not None else 0)
 
@@ -104,8 +106,13 @@ class DiaqMatrix:
 
     @classmethod
     def _from_device(cls, n_dim: int, offs, starts, vals, dtype=np.float64, dtab=None, cap=None) -> "DiaqMatrix":
-        out = cls(n_dim, dtype)
+        out = cls.__new__(cls)  # (a kernel's output: no validation, cheap per product of a sweep)
+        out.n_dim = int(n_dim)
+        out.dtype = dtype if isinstance(dtype, np.dtype) else np.dtype(dtype)
+        out.align = DEFAULT_ALIGNMENT
         out._host = None
+        out._views = {}
+        out._version = 0
         if offs is not None:
             offs = np.ascontiguousarray(offs, dtype=np.int64)
             starts = np.ascontiguousarray(starts, dtype=np.int64)
@@ -172,6 +179,11 @@ class DiaqMatrix:
             offs, starts = self._tables()
             dv.st = L.mat_struct(self.n_dim, offs, starts, dv.vals)
         return dv.st
+
+    def _struct_ref(self):
+        st = self._struct()
+        self._dev.st_ref = ctypes.byref(st)
+        return self._dev.st_ref
 
     def _dev_struct(self) -> L.DevMatrix:
         dtab, cap = self._dev_table()
@@ -438,6 +450,87 @@ def _matmul_host(a: DiaqMatrix, b: DiaqMatrix, dtype) -> DiaqMatrix:
     return DiaqMatrix._from_device(a.n_dim, None, None, cvals, dtype, dtab=dtab, cap=nc)
 
 
+_WS: dict = {}
+
+
+def _workspace(nbytes: int, dev):
+    """Scratch for the device plan, reused across calls (stream-ordered: a
+    later product on the same stream reuses it only after the earlier one
+    consumed it)."""
+    t = L.torch()
+    key = (dev.index, L.stream_handle())
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = t.empty(max(nbytes, 1 << 16), dtype=t.uint8, device=dev)
+        _WS[key] = ws
+    return ws
+
+
+# diaq_dev_matrix_t / diaq_dev_result_t as numpy records: a sweep's tables
+# are filled column-wise (no per-product ctypes objects)
+_DEVMAT = np.dtype([("n", "<i8"), ("nd_cap", "<i8"), ("nd", "<u8"), ("offs", "<u8"), ("starts", "<u8"),
+                    ("vals", "<u8")])
+_DEVRES = np.dtype([("nd", "<u8"), ("offs", "<u8"), ("starts", "<u8"), ("vals", "<u8"), ("capacity", "<i8"),
+                    ("nd_cap", "<i8")])
+
+
+def _dev_record(m: DiaqMatrix):
+    """(n, cap, nd*, offs*, starts*, vals*) of m's device table, cached on m."""
+    dv = m._dev
+    if dv is not None and dv.rec is not None:
+        return dv.rec
+    dtab, cap = m._dev_table()
+    base = dtab.data_ptr()
+    m._dev.rec = (m.n_dim, cap, base, base + 8, base + 8 * (1 + cap), m._dev.vals.data_ptr())
+    return m._dev.rec
+
+
+def _dev_products(pairs, idx, out) -> None:
+    """Device-planned products of `pairs` (all pass _use_dev_plan) into
+    out[idx[j]]: one arena and one structure-table block for the sweep,
+    carved into per-product views with one split each."""
+    t = L.torch()
+    count = len(pairs)
+    pair_cap = max(a._cap() * b._cap() for a, b in pairs)
+    n0 = pairs[0][0].n_dim
+    same_n = all(a.n_dim == n0 for a, _ in pairs)
+    caps = [_dev_plan_capacity(n0, pair_cap)] * count if same_n else \
+        [_dev_plan_capacity(a.n_dim, pair_cap) for a, _ in pairs]
+    sizes = [(c[1] + 31) & ~31 for c in caps]  # 512-byte aligned result arenas
+    ncap_max = max(c[0] for c in caps)
+    dev = L.device()
+    arena = L.empty_c128(sum(sizes))
+    row = 1 + 2 * ncap_max
+    dtabs = t.empty((count, row), dtype=t.int64, device=dev)
+    A = np.empty(count, dtype=_DEVMAT)
+    B = np.empty(count, dtype=_DEVMAT)
+    C = np.empty(count, dtype=_DEVRES)
+    A[:] = [_dev_record(a) for a, _ in pairs]
+    B[:] = [_dev_record(b) for _, b in pairs]
+    tb = dtabs.data_ptr() + 8 * row * np.arange(count, dtype=np.uint64)
+    C["nd"] = tb
+    C["offs"] = tb + 8
+    C["starts"] = tb + 8 * (1 + ncap_max)
+    C["vals"] = arena.data_ptr() + 16 * np.concatenate([[0], np.cumsum(sizes[:-1])]).astype(np.uint64)
+    C["capacity"] = [c[1] for c in caps]
+    C["nd_cap"] = ncap_max
+    singles = [_single(a, b) for a, b in pairs]
+    ws_bytes = int(L.load().diaq_spgemm_dev_workspace(count, pair_cap))
+    ws = _workspace(ws_bytes, dev)
+    if all(singles) or not any(singles):
+        L.call("diaq_spgemm_dev", count, A.ctypes.data, B.ctypes.data, C.ctypes.data, float(PRUNE_EPS),
+               int(singles[0]), pair_cap, ws.data_ptr(), ws_bytes, L.stream_handle())
+    else:  # mixed precisions in one sweep: one call per product
+        for j in range(count):
+            L.call("diaq_spgemm_dev", 1, A[j:].ctypes.data, B[j:].ctypes.data, C[j:].ctypes.data, float(PRUNE_EPS),
+                   singles[j], pair_cap, ws.data_ptr(), ws_bytes, L.stream_handle())
+    views = arena.split(sizes)
+    rows = dtabs.unbind(0)
+    for j, (a, b) in enumerate(pairs):
+        out[idx[j]] = DiaqMatrix._from_device(a.n_dim, None, None, views[j], np.result_type(a.dtype, b.dtype),
+                                              dtab=rows[j], cap=ncap_max)
+
+
 def matmul_batch(pairs) -> list[DiaqMatrix]:
     """Products of many (A, B) pairs (a sweep, config 2) in one native call:
     the structure of every product is planned on the device (offset union,
@@ -457,41 +550,7 @@ def matmul_batch(pairs) -> list[DiaqMatrix]:
         else:
             out[i] = matmul(a, b)
     if dev_idx:
-        pair_cap = max(pairs[i][0]._cap() * pairs[i][1]._cap() for i in dev_idx)
-        caps = [_dev_plan_capacity(pairs[i][0].n_dim, pair_cap) for i in dev_idx]
-        elem_off = np.cumsum([0] + [(c[1] + 31) & ~31 for c in caps])  # 512-byte aligned result arenas
-        dev = L.device()
-        arena = L.empty_c128(int(elem_off[-1]))
-        ncap_max = max(c[0] for c in caps)
-        dtabs = t.empty((len(dev_idx), 1 + 2 * ncap_max), dtype=t.int64, device=dev)
-        count = len(dev_idx)
-        A = (L.DevMatrix * count)()
-        B = (L.DevMatrix * count)()
-        C = (L.DevResult * count)()
-        abase, tbase = arena.data_ptr(), dtabs.data_ptr()
-        row = 8 * (1 + 2 * ncap_max)
-        for j, i in enumerate(dev_idx):
-            a, b = pairs[i]
-            A[j] = a._dev_struct()
-            B[j] = b._dev_struct()
-            tb = tbase + j * row
-            C[j] = L.DevResult(tb, tb + 8, tb + 8 * (1 + ncap_max), abase + 16 * int(elem_off[j]), caps[j][1],
-                               ncap_max)
-        ws_bytes = int(L.load().diaq_spgemm_dev_workspace(count, pair_cap))
-        ws = t.empty(ws_bytes, dtype=t.uint8, device=dev)
-        single = int(all(_single(*pairs[i]) for i in dev_idx))
-        if single or not any(_single(*pairs[i]) for i in dev_idx):
-            L.call("diaq_spgemm_dev", count, A, B, C, float(PRUNE_EPS), single, pair_cap, ws.data_ptr(), ws_bytes,
-                   L.stream_handle())
-        else:  # mixed precisions in one sweep: one call per precision
-            for j, i in enumerate(dev_idx):
-                L.call("diaq_spgemm_dev", 1, ctypes.byref(A[j]), ctypes.byref(B[j]), ctypes.byref(C[j]),
-                       float(PRUNE_EPS), _single(*pairs[i]), pair_cap, ws.data_ptr(), ws_bytes, L.stream_handle())
-        for j, i in enumerate(dev_idx):
-            a, b = pairs[i]
-            vals = arena[int(elem_off[j]):int(elem_off[j + 1])]
-            out[i] = DiaqMatrix._from_device(a.n_dim, None, None, vals, np.result_type(a.dtype, b.dtype),
-                                             dtab=dtabs[j], cap=ncap_max)
+        _dev_products([pairs[i] for i in dev_idx], dev_idx, out)
     return out
 
 
@@ -579,6 +638,17 @@ def spmv(a: DiaqMatrix, x, out=None):
     """
     n = a.n_dim
     t = L.torch()
+    if out is None and type(x) is t.Tensor and x.is_cuda and x.dtype is t.complex128 and x.shape == (n,) \
+            and x.is_contiguous():
+        # fast path (device vector in, device vector out): one allocation,
+        # one C call with the matrix's cached descriptor
+        dv = a._dev
+        ref = dv.st_ref if dv is not None and dv.st_ref is not None else a._struct_ref()
+        y = t.empty_like(x)
+        rc = L._lib.diaq_spmv(ref, x.data_ptr(), y.data_ptr(), L.stream_handle())
+        if rc:
+            L.check(rc, "diaq_spmv")
+        return y
     if out is not None and (not isinstance(out, t.Tensor) or tuple(out.shape) != (n,)
                             or out.dtype != t.complex128):
         raise ShapeError(f"out must be a complex128 tensor of shape ({n},)")
