@@ -481,6 +481,10 @@ def run_ours(args):
                                  "a fused pass applies several gates)",
                           "ms_per_pass": round(ms_per_pass, 4)},
              "norm_after": g_norm, "gpu_launches": int(g_launches)}
+    gates["roofline_fp64"] = fp64_roofline(prof.get("gate_fp64_warp_inst_per_launch"), ms_per_pass)
+    if isinstance(gates.get("contracted"), dict) and n == N_QUBITS:
+        gates["contracted"]["roofline_fp64"] = fp64_roofline(
+            prof.get("gate_contracted_fp64_warp_inst_per_launch"), gates["contracted"]["ms_per_pass"])
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -523,6 +527,24 @@ def run_ours(args):
     return 0
 
 
+def fp64_roofline(warp_inst, ms_per_pass) -> dict | None:
+    """FP64-pipe roofline of a gate pass: DMUL+DADD+DFMA warp instructions
+    per launch (committed ncu opcode mix) over the measured pass time,
+    against 148 SMs x 2 FP64 warp instructions per clock at the max SM clock."""
+    if not warp_inst:
+        return None
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f).get("sm_max_mhz", 1965.0))
+    except Exception:
+        mhz = 1965.0
+    peak = 148 * 2 * mhz * 1e6  # warp instructions / s
+    achieved = warp_inst / (ms_per_pass * 1e-3)
+    return {"bound": "fp64", "achieved": round(achieved * 32 / 1e12, 3), "peak": round(peak * 32 / 1e12, 3),
+            "unit": "T FP64 instr/s (DFMA = 1)", "frac": round(achieved / peak, 4),
+            "fp64_warp_inst_per_launch": int(warp_inst), "source": "profiles/ncu_summary.json (ncu opcode mix)"}
+
+
 def jit_stats(L):
     import ctypes
     st = (ctypes.c_int64 * 6)()
@@ -559,13 +581,49 @@ def replica_gates(args, D, L, W, torch, dist, n, world, x, s, dev):
     jst1 = jit_stats(L)
     g_ms = max_over_ranks(dist, ge0.elapsed_time(ge1), dev)
     g_norm = state.norm()
+    contracted = contracted_gates(D, L, torch, dist, pls, x, g_steps, s, dev)
     extra = {"gates_per_step": len(pls), "steps": g_steps, "mode": f"replicas x{world}",
+             "numerics": "reference (numpy complex-multiply rounding; bitwise the reference)",
+             "contracted": contracted,
              "fused_tile_bits": D.sim.FUSE_TILE_BITS if D.sim.FUSE_TILE_BITS > 0 else "auto (11 or 12: 12 only with >12% fewer passes)", "hbm_passes": int(g_launches),
              "specialised_passes": {"launches_timed": jst1["launches"] - jst0["launches"], "compiled": jst1["compiled"],
                                     "failed": jst1["failed"], "compile_cpu_ms": jst1["compile_ms"],
                                     "wait_after_warmup_s": round(jit_wait_s, 3),
                                     "note": "NVRTC per pass structure, background thread; one-time"}}
     return len(pls) * g_steps, g_ms, g_launches, g_norm, n, extra
+
+
+def contracted_gates(D, L, torch, dist, pls, x, g_steps, s, dev):
+    """The same layer under the contracted arithmetic (DIAQ_CMUL_CONTRACT:
+    FMA chains, folded diagonal runs; within 1e-12 rel L2 of the reference,
+    not bitwise): device time per step, and its parity on one layer from x
+    against the reference-rounded layer."""
+    C = L.CMUL_CONTRACT
+    ref1 = D.run_gates(D.StateVector(x.numel().bit_length() - 1, x), pls).device_amps
+    st = D.StateVector(x.numel().bit_length() - 1, x.clone())
+    st = D.run_gates(st, pls, cmul_mode=C, inplace=True)
+    d = st.device_amps
+    rel = float(torch.linalg.vector_norm(d - ref1).item() / torch.linalg.vector_norm(ref1).item())
+    del ref1
+    L.call("diaq_jit_wait", -1.0)
+    st = D.run_gates(st, pls, cmul_mode=C, inplace=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = L.launch_count()
+    e0.record(s)
+    for _ in range(g_steps):
+        st = D.run_gates(st, pls, cmul_mode=C, inplace=True)
+    e1.record(s)
+    torch.cuda.synchronize()
+    launches = L.launch_count() - l0
+    ms = max_over_ranks(dist, e0.elapsed_time(e1), dev)
+    peak, _ = measured_peak()
+    ms_pass = ms / max(1, launches)
+    gbs = 32 * x.numel() / (ms_pass * 1e-3) / 1e9
+    return {"numerics": "contracted (FMA chains, folded diagonal runs; 1e-12 rel L2 tolerance, not bitwise)",
+            "gates_per_s": round(len(pls) * g_steps / (ms * 1e-3), 2), "ms_per_pass": round(ms_pass, 4),
+            "hbm_passes": int(launches), "roofline_frac": round(gbs / peak, 4), "achieved_GBs": round(gbs, 1),
+            "rel_l2_vs_reference_one_layer": rel, "norm_err": abs(1.0 - st.norm())}
 
 
 def sharded_gates(args, D, L, W, torch, dist, n, world, x, s, dev):
@@ -719,41 +777,43 @@ def secondary_workloads(args, D, L, W, torch) -> dict:
         lo, hi = min(qa, qb), max(qa, qb)
         pls_h.append(D.Placement(2**lo, None, 2 ** (27 - hi), lo, hi, "haar",
                                  gate=(W.haar(rng, 4), [qa - lo, qb - lo])))
-    st_h = D.init_state(28)
-    D.run_gates(st_h, pls_h, inplace=True)
-    L.call("diaq_jit_wait", -1.0)
-    ms_h = dev_time(lambda: D.run_gates(st_h, pls_h, inplace=True), 3)
-    out["haar4_layer_n28"] = {"gates": len(pls_h), "ms_per_layer": round(ms_h, 3),
-                              "gates_per_s": round(len(pls_h) / ms_h * 1e3, 1)}
-    del st_h
+    for mode, tag in ((None, ""), (L.CMUL_CONTRACT, "_contracted")):
+        st_h = D.init_state(28)
+        D.run_gates(st_h, pls_h, cmul_mode=mode, inplace=True)
+        L.call("diaq_jit_wait", -1.0)
+        ms_h = dev_time(lambda: D.run_gates(st_h, pls_h, cmul_mode=mode, inplace=True), 3)
+        out["haar4_layer_n28" + tag] = {"gates": len(pls_h), "ms_per_layer": round(ms_h, 3),
+                                        "gates_per_s": round(len(pls_h) / ms_h * 1e3, 1)}
+        del st_h
     # config 5 at its 1-GPU size: n=30 (16 GB state), 20 random layers, norm check
     ops30 = W.random_layered_ops(30, 20, seed=0)
     pls30 = D.compile_circuit(D.Circuit(30, [D.GateOp(*o) for o in ops30]), span_limit=30)
-    st30 = D.init_state(30, max_qubits=30)
-    D.run_gates(st30, pls30, inplace=True)  # warm-up (program cache, specialised passes)
-    L.call("diaq_jit_wait", -1.0)
-    del st30
-    reps30 = []
-    for _ in range(3):  # each rep from |0..0>: device time of the whole 900-gate circuit
+    for mode, tag in ((None, ""), (L.CMUL_CONTRACT, "_contracted")):
         st30 = D.init_state(30, max_qubits=30)
-        spec0 = jit_stats(L)["launches"]
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        e0.record(s)
-        D.run_gates(st30, pls30, inplace=True)
-        e1.record(s)
-        torch.cuda.synchronize()
-        reps30.append((e0.elapsed_time(e1), jit_stats(L)["launches"] - spec0))
-        if len(reps30) < 3:
-            del st30
-    ms30 = sorted(r[0] for r in reps30)[1]
-    out["config5_n30_1gpu"] = {"gates": len(pls30), "layers": 20, "s_per_circuit": round(ms30 / 1e3, 4),
-                               "gates_per_s": round(len(pls30) / ms30 * 1e3, 1),
-                               "norm_err": abs(1.0 - st30.norm()),
-                               "reps_s": [round(r[0] / 1e3, 4) for r in reps30],
-                               "specialised_launches": [r[1] for r in reps30],
-                               "note": "device time (CUDA events) of run_gates on |0..0>, fused passes; median of 3"}
-    del st30
+        D.run_gates(st30, pls30, cmul_mode=mode, inplace=True)  # warm-up (program cache, specialised passes)
+        L.call("diaq_jit_wait", -1.0)
+        del st30
+        reps30 = []
+        for _ in range(3):  # each rep from |0..0>: device time of the whole 900-gate circuit
+            st30 = D.init_state(30, max_qubits=30)
+            spec0 = jit_stats(L)["launches"]
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(s)
+            D.run_gates(st30, pls30, cmul_mode=mode, inplace=True)
+            e1.record(s)
+            torch.cuda.synchronize()
+            reps30.append((e0.elapsed_time(e1), jit_stats(L)["launches"] - spec0))
+            if len(reps30) < 3:
+                del st30
+        ms30 = sorted(r[0] for r in reps30)[1]
+        out["config5_n30_1gpu" + tag] = {
+            "gates": len(pls30), "layers": 20, "s_per_circuit": round(ms30 / 1e3, 4),
+            "gates_per_s": round(len(pls30) / ms30 * 1e3, 1), "norm_err": abs(1.0 - st30.norm()),
+            "reps_s": [round(r[0] / 1e3, 4) for r in reps30], "specialised_launches": [r[1] for r in reps30],
+            "numerics": "contracted" if mode else "reference rounding (bitwise)",
+            "note": "device time (CUDA events) of run_gates on |0..0>, fused passes; median of 3"}
+        del st30
     out["config3_circuit_n20"] = {"gates": len(pls), "ms_per_circuit": round(ms, 3),
                                   "gates_per_s": round(len(pls) / ms * 1e3, 1),
                                   "run_api_wall_s": round(e2e_s, 4),

@@ -49,6 +49,12 @@ typedef enum {
  * (reference sim.py:76-78); PLAIN is the textbook four-product form. */
 #define DIAQ_CMUL_PLAIN 0
 #define DIAQ_CMUL_FMA 1
+/* CONTRACT: not the reference's rounding but fused multiply-add chains
+ * (a 2x2 rotation costs 4 FP64 operations per amplitude instead of 6, runs
+ * of diagonal gates on non-register bits fold into one factor); results
+ * agree with the reference within 1e-12 relative L2 (north_star tolerance),
+ * not bitwise.  Standalone gate kernels use the FMA form under it. */
+#define DIAQ_CMUL_CONTRACT 2
 
 /* a device-resident DiaQ matrix (replaces reference DiaqMatrix,
  * matrix.py:50-123; the dict of Diagonal objects becomes offs/starts/vals) */

@@ -28,6 +28,7 @@ DIAQ_IPC_HANDLE_BYTES = 64
 
 CMUL_PLAIN = 0
 CMUL_FMA = 1
+CMUL_CONTRACT = 2  # fused multiply-add chains: 1e-12 rel L2 of the reference, not bitwise
 
 
 class DeviceError(DiaqError, RuntimeError):

@@ -248,7 +248,7 @@ static int launch_gate(int n_bits, const double *g, const int *shifts, const voi
     const int64_t want = (p.ngroups + kThreads - 1) / kThreads;
     const int grid = (int)std::max<int64_t>(
         1, std::min<int64_t>(want, (int64_t)sm_count() * tuning().gate_ctas_per_sm));
-    if (cmul_mode == DIAQ_CMUL_FMA) gate_kernel<K, DIAQ_CMUL_FMA><<<grid, kThreads, 0, s>>>(p);
+    if (cmul_mode != DIAQ_CMUL_PLAIN) gate_kernel<K, DIAQ_CMUL_FMA><<<grid, kThreads, 0, s>>>(p);
     else gate_kernel<K, DIAQ_CMUL_PLAIN><<<grid, kThreads, 0, s>>>(p);
     count_launch();
     return check_launch("gate_kernel");
@@ -357,7 +357,7 @@ static int launch_multi(const ShardView &v, int local_bits, const double *g, con
     const int64_t want = (p.ngroups + kThreads - 1) / kThreads;
     const int grid = (int)std::max<int64_t>(
         1, std::min<int64_t>(want, (int64_t)sm_count() * tuning().gate_ctas_per_sm));
-    if (cmul_mode == DIAQ_CMUL_FMA) gate_kernel_multi<KL, KG, DIAQ_CMUL_FMA><<<grid, kThreads, 0, s>>>(p);
+    if (cmul_mode != DIAQ_CMUL_PLAIN) gate_kernel_multi<KL, KG, DIAQ_CMUL_FMA><<<grid, kThreads, 0, s>>>(p);
     else gate_kernel_multi<KL, KG, DIAQ_CMUL_PLAIN><<<grid, kThreads, 0, s>>>(p);
     count_launch();
     return check_launch("gate_kernel_multi");
@@ -417,7 +417,7 @@ extern "C" int diaq_apply_placed(int64_t dim_a, const diaq_matrix_t *m, int64_t 
             p.dg[i].hi = d > 0 ? m->n - d : m->n;
             p.dg[i].xoff = d * dim_b;
         }
-        if (cmul_mode == DIAQ_CMUL_FMA) placed_kernel<DIAQ_CMUL_FMA><<<grid, kThreads, 0, s>>>(p);
+        if (cmul_mode != DIAQ_CMUL_PLAIN) placed_kernel<DIAQ_CMUL_FMA><<<grid, kThreads, 0, s>>>(p);
         else placed_kernel<DIAQ_CMUL_PLAIN><<<grid, kThreads, 0, s>>>(p);
         count_launch();
         const int rc = check_launch("placed_kernel");

@@ -136,8 +136,30 @@ __device__ __forceinline__ double2 cmul_fma(double2 v, double2 x) {
 
 template <int MODE>
 __device__ __forceinline__ double2 cmul(double2 v, double2 x) {
-    if constexpr (MODE == DIAQ_CMUL_FMA) return cmul_fma(v, x);
-    else return cmul_plain(v, x);
+    if constexpr (MODE == DIAQ_CMUL_PLAIN) return cmul_plain(v, x);
+    else return cmul_fma(v, x);
+}
+
+// ---- contracted forms (DIAQ_CMUL_CONTRACT; 1e-12 tolerance, not bitwise) ----
+// a x + b y as one chain of fused multiply-adds: 1 DMUL + 3 DFMA per part
+__device__ __forceinline__ double2 cmac2_c(double2 a, double2 x, double2 b, double2 y) {
+    return make_double2(__fma_rn(a.x, x.x, __fma_rn(-a.y, x.y, __fma_rn(b.x, y.x, -__dmul_rn(b.y, y.y)))),
+                        __fma_rn(a.x, x.y, __fma_rn(a.y, x.x, __fma_rn(b.x, y.y, __dmul_rn(b.y, y.x)))));
+}
+
+// real a, b: a x + b y (RY, H): 1 DMUL + 1 DFMA per part
+__device__ __forceinline__ double2 cmac2_rr(double a, double2 x, double b, double2 y) {
+    return make_double2(__fma_rn(a, x.x, __dmul_rn(b, y.x)), __fma_rn(a, x.y, __dmul_rn(b, y.y)));
+}
+
+// real a, imaginary b = i bi: a x + i bi y (RX rows)
+__device__ __forceinline__ double2 cmac2_ri(double a, double2 x, double bi, double2 y) {
+    return make_double2(__fma_rn(a, x.x, -__dmul_rn(bi, y.y)), __fma_rn(a, x.y, __dmul_rn(bi, y.x)));
+}
+
+// acc + a x (continuing a contracted chain)
+__device__ __forceinline__ double2 cfma_c(double2 a, double2 x, double2 acc) {
+    return make_double2(__fma_rn(a.x, x.x, __fma_rn(-a.y, x.y, acc.x)), __fma_rn(a.x, x.y, __fma_rn(a.y, x.x, acc.y)));
 }
 
 // products with a coefficient whose other part is an exact zero (see

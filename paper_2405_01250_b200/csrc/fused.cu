@@ -807,8 +807,15 @@ int apply_gate_sharded_own(int n_bits, int local_bits, int k, const double *g, c
 
 template <int R>
 static const void *tile_kernel_ptr(int cmul_mode) {
-    return cmul_mode == DIAQ_CMUL_FMA ? (const void *)tile_pass_kernel<R, DIAQ_CMUL_FMA>
-                                      : (const void *)tile_pass_kernel<R, DIAQ_CMUL_PLAIN>;
+    return cmul_mode == DIAQ_CMUL_CONTRACT ? (const void *)tile_pass_kernel<R, DIAQ_CMUL_CONTRACT>
+           : cmul_mode == DIAQ_CMUL_FMA    ? (const void *)tile_pass_kernel<R, DIAQ_CMUL_FMA>
+                                           : (const void *)tile_pass_kernel<R, DIAQ_CMUL_PLAIN>;
+}
+
+static const void *tile_kernel_t7_ptr(int cmul_mode) {
+    return cmul_mode == DIAQ_CMUL_CONTRACT ? (const void *)tile_pass_kernel_t7<DIAQ_CMUL_CONTRACT>
+           : cmul_mode == DIAQ_CMUL_FMA    ? (const void *)tile_pass_kernel_t7<DIAQ_CMUL_FMA>
+                                           : (const void *)tile_pass_kernel_t7<DIAQ_CMUL_PLAIN>;
 }
 
 }  // namespace diaq
@@ -826,8 +833,8 @@ struct Program {
     // specialised kernels of the tiled passes (fused_jit.cu), per cmul mode:
     // looked up once per program, then read on every call
     mutable std::mutex jit_mu;
-    mutable std::vector<std::shared_ptr<JitPass>> jit[2];
-    mutable bool jit_requested[2] = {false, false};
+    mutable std::vector<std::shared_ptr<JitPass>> jit[3];
+    mutable bool jit_requested[3] = {false, false, false};
 
     std::vector<const TileParams *> tiled() const {
         std::vector<const TileParams *> v(plan.size(), nullptr);
@@ -1125,6 +1132,8 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
                      int cmul_mode, int tile_bits, void **events, int *npasses, void *stream) {
     if (ngates < 0 || (ngates > 0 && !gates) || !state)
         return set_error(DIAQ_ERR_VALUE, "diaq_run_gates_fused: bad arguments");
+    if (cmul_mode < DIAQ_CMUL_PLAIN || cmul_mode > DIAQ_CMUL_CONTRACT)
+        return set_error(DIAQ_ERR_VALUE, "diaq_run_gates_fused: cmul_mode %d", cmul_mode);
     const bool sharded = n_total > n_bits;
     cudaStream_t s = (cudaStream_t)stream;
     // tile_bits 12 -> 16 amplitudes per thread (R = 4), 11 -> 8 (R = 3); 256
@@ -1153,7 +1162,7 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
     // kernel is not compiled yet run the AOT interpreter (bitwise the same)
     std::vector<std::shared_ptr<JitPass>> jit;
     const int jit_knob = tuning().fused_jit;
-    if (jit_knob != 0 && (cmul_mode == 0 || cmul_mode == 1)) {
+    if (jit_knob != 0 && cmul_mode >= 0 && cmul_mode <= 2) {
         std::lock_guard<std::mutex> lk(prog->jit_mu);
         if (!prog->jit_requested[cmul_mode]) {
             jit_request(prog->tiled(), R, cmul_mode, jit_knob == 2, prog->jit[cmul_mode]);
@@ -1175,6 +1184,9 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
         cudaFuncSetAttribute(tile_pass_kernel<4, DIAQ_CMUL_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
         cudaFuncSetAttribute(tile_pass_kernel_t7<DIAQ_CMUL_FMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
         cudaFuncSetAttribute(tile_pass_kernel_t7<DIAQ_CMUL_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+        cudaFuncSetAttribute(tile_pass_kernel<3, DIAQ_CMUL_CONTRACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+        cudaFuncSetAttribute(tile_pass_kernel<4, DIAQ_CMUL_CONTRACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+        cudaFuncSetAttribute(tile_pass_kernel_t7<DIAQ_CMUL_CONTRACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
         cudaGetLastError();
         attr_set[cur_dev] = true;
     }
@@ -1235,8 +1247,7 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
             if (p.gperm && sharded)  // controls on global bits: constants of this rank
                 for (int g = 0; g < 64 && g < n_total - n_bits; ++g)
                     if (((uint64_t)rank >> g) & 1ull) p.gconst ^= ps.ggcol[(size_t)g];
-            const void *f = tbits == 7 ? (cmul_mode == DIAQ_CMUL_FMA ? (const void *)tile_pass_kernel_t7<DIAQ_CMUL_FMA>
-                                                                    : (const void *)tile_pass_kernel_t7<DIAQ_CMUL_PLAIN>)
+            const void *f = tbits == 7 ? tile_kernel_t7_ptr(cmul_mode)
                             : R >= 4 ? tile_kernel_ptr<4>(cmul_mode) : tile_kernel_ptr<3>(cmul_mode);
             const int nthreads = 1 << tbits;
             auto smem_for = [&](int nb) {
@@ -1334,7 +1345,7 @@ extern "C" int diaq_fused_jit_compile(int n_bits, int local_bits, int ngates, co
     if (ngates < 0 || (ngates > 0 && !gates) || !kernels)
         return set_error(DIAQ_ERR_VALUE, "diaq_fused_jit_compile: bad arguments");
     if (local_bits < 1 || local_bits > n_bits) return set_error(DIAQ_ERR_SHAPE, "local_bits %d invalid", local_bits);
-    if (cmul_mode != 0 && cmul_mode != 1) return set_error(DIAQ_ERR_VALUE, "cmul_mode %d", cmul_mode);
+    if (cmul_mode < 0 || cmul_mode > 2) return set_error(DIAQ_ERR_VALUE, "cmul_mode %d", cmul_mode);
     const int T = (tile_bits >= kThreadBits + 4 && pass_tbits() == 8) ? kThreadBits + 4 : kThreadBits + 3;
     int rc = DIAQ_OK;
     std::shared_ptr<const Program> prog = build_program(n_bits, local_bits, T, ngates, gates, rc);

@@ -232,7 +232,18 @@ __device__ __forceinline__ void dense1_full(double2 (&v)[1 << R], const double2 
         const int j0 = ((g >> B1) << (B1 + 1)) | (g & ((1 << B1) - 1));
         const int j1 = j0 | (1 << B1);
         const double2 x0 = v[j0], x1 = v[j1];
-        if constexpr (SHAPE == 1) {
+        if constexpr (MODE == DIAQ_CMUL_CONTRACT) {  // 4 (shaped) / 8 FP64 operations per amplitude
+            if constexpr (SHAPE == 1) {
+                v[j0] = cmac2_rr(c00.x, x0, c01.x, x1);
+                v[j1] = cmac2_rr(c10.x, x0, c11.x, x1);
+            } else if constexpr (SHAPE == 2) {
+                v[j0] = cmac2_ri(c00.x, x0, c01.y, x1);
+                v[j1] = cmac2_ri(c11.x, x1, c10.y, x0);
+            } else {
+                v[j0] = cmac2_c(c00, x0, c01, x1);
+                v[j1] = cmac2_c(c10, x0, c11, x1);
+            }
+        } else if constexpr (SHAPE == 1) {
             v[j0] = cadd(cmul_re(c00.x, x0), cmul_re(c01.x, x1));
             v[j1] = cadd(cmul_re(c10.x, x0), cmul_re(c11.x, x1));
         } else if constexpr (SHAPE == 2) {
@@ -266,6 +277,10 @@ __device__ __forceinline__ void dense2_full(double2 (&v)[1 << R], const double2 
         const double2 x0 = v[jq[0]], x1 = v[jq[1]], x2 = v[jq[2]], x3 = v[jq[3]];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
+            if constexpr (MODE == DIAQ_CMUL_CONTRACT) {
+                v[jq[r]] = cfma_c(c[r * 4], x0, cfma_c(c[r * 4 + 1], x1, cmac2_c(c[r * 4 + 2], x2, c[r * 4 + 3], x3)));
+                continue;
+            }
             double2 a = cmul<MODE>(c[r * 4], x0);
             a = cadd(a, cmul<MODE>(c[r * 4 + 1], x1));
             a = cadd(a, cmul<MODE>(c[r * 4 + 2], x2));
@@ -321,6 +336,40 @@ __device__ __forceinline__ void diag_uniform(double2 (&v)[1 << R], const RegGate
     (void)snz;
 #pragma unroll
     for (int j = 0; j < (1 << R); ++j) v[j] = cmul<MODE>(d, v[j]);
+}
+
+// a run of `count` diagonal gates whose selectors are thread or base bits
+// (gates S.g[gi ..]): applied one by one, or under DIAQ_CMUL_CONTRACT
+// folded into one factor per thread (their product, in gate order) and
+// applied with one complex multiply per amplitude
+template <int R, int MODE>
+__device__ __forceinline__ void diag_run(double2 (&v)[1 << R], const TileParams &S, int &gi, int count, uint32_t tpart,
+                                         const uint64_t *sbase_p, const double2 *sc, const uint32_t *snz) {
+    if constexpr (MODE == DIAQ_CMUL_CONTRACT) {
+        if (count <= 0) return;
+        double2 d = make_double2(1.0, 0.0);
+        for (int c = 0; c < count; ++c, ++gi) {
+            const RegGate &G = S.g[gi];
+            const uint32_t b =
+                G.osel[0] == 0 ? (uint32_t)((ld_base(sbase_p) >> G.opos[0]) & 1ull) : (tpart >> G.opos[0]) & 1u;
+#ifdef DIAQ_JIT
+            const double2 f = b ? sc[G.coef_off + 1] : sc[G.coef_off];
+#else
+            const double2 f = sc[G.coef_off + (int)b];
+#endif
+            d = c == 0 ? f : cmul_fma(f, d);
+        }
+#pragma unroll
+        for (int j = 0; j < (1 << R); ++j) v[j] = cmul_fma(d, v[j]);
+        (void)snz;
+    } else {
+#ifdef DIAQ_JIT
+#pragma unroll
+#else
+#pragma unroll 2
+#endif
+        for (int c = 0; c < count; ++c, ++gi) diag_uniform<R, MODE>(v, S.g[gi], tpart, sbase_p, sc, snz);
+    }
 }
 
 template <int R, int MODE>
@@ -424,15 +473,10 @@ template <int R, int MODE, int RB>
 __device__ __forceinline__ void seq_steps(double2 (&v)[1 << R], const TileParams &S, const Phase &ph, int &gi,
                                           uint32_t tpart, const uint64_t *sbase_p, const double2 *sc,
                                           const uint32_t *snz) {
-    // unrolled by 2: a complex multiply cannot land in its input registers
-    // (both parts read both inputs), so a rolled loop pays a register copy of
-    // the amplitude set per gate to return to the loop-carried assignment
-#ifdef DIAQ_JIT
-#pragma unroll
-#else
-#pragma unroll 2
-#endif
-    for (int c = 0; c < ph.nd_before[RB]; ++c, ++gi) diag_uniform<R, MODE>(v, S.g[gi], tpart, sbase_p, sc, snz);
+    // (diag_run unrolls by 2: a complex multiply cannot land in its input
+    // registers, so a rolled loop pays a register copy of the amplitude set
+    // per gate to return to the loop-carried assignment)
+    diag_run<R, MODE>(v, S, gi, ph.nd_before[RB], tpart, sbase_p, sc, snz);
     if (ph.kind[RB] == 1) {
         dense1_shaped<R, RB, MODE>(v, sc + S.g[gi].coef_off, S.g[gi].shape);
         ++gi;
@@ -603,12 +647,7 @@ __device__ __forceinline__ void tile_pass_body(const TileParams &p, const TilePa
             if (ph.seq) {
                 int gi = ph.g0;
                 seq_steps<R, MODE, 0>(v, S, ph, gi, tpart, &s_sbase, sc, snz);
-#ifdef DIAQ_JIT
-#pragma unroll
-#else
-#pragma unroll 2
-#endif
-                for (int c = 0; c < ph.nd_before[R]; ++c, ++gi) diag_uniform<R, MODE>(v, S.g[gi], tpart, &s_sbase, sc, snz);
+                diag_run<R, MODE>(v, S, gi, ph.nd_before[R], tpart, &s_sbase, sc, snz);
             } else {
                 DIAQ_SUNROLL
                 for (int gi = ph.g0; gi < ph.g1; ++gi) dispatch_gate<R, MODE>(v, S.g[gi], tpart, &s_sbase, sc, snz);
@@ -853,8 +892,7 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
             if (ph.seq) {
                 int gi = ph.g0;
                 seq_steps<R, MODE, 0>(v, S, ph, gi, tpart, &s_sbase, sc, snz);
-#pragma unroll
-                for (int c = 0; c < ph.nd_before[R]; ++c, ++gi) diag_uniform<R, MODE>(v, S.g[gi], tpart, &s_sbase, sc, snz);
+                diag_run<R, MODE>(v, S, gi, ph.nd_before[R], tpart, &s_sbase, sc, snz);
             } else {
                 DIAQ_SUNROLL
                 for (int gi = ph.g0; gi < ph.g1; ++gi) dispatch_gate<R, MODE>(v, S.g[gi], tpart, &s_sbase, sc, snz);

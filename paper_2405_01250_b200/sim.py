@@ -49,6 +49,26 @@ def _probe_numpy_cmul() -> int:
 
 # rounding of the gate-apply complex multiply; defaults to this host's numpy
 CMUL_MODE = _probe_numpy_cmul()
+_REFERENCE_CMUL = CMUL_MODE
+
+
+def set_numerics(kind: str) -> None:
+    """Arithmetic of the gate loop (extension; the default is "reference").
+
+    "reference": every gate with numpy's complex-multiply rounding, states
+    bitwise equal to the reference simulator.  "contracted": fused
+    multiply-add chains (a rotation costs 4 FP64 operations per amplitude
+    instead of 6; runs of diagonal gates on non-register bits fold into one
+    factor), within 1e-12 relative L2 of the reference (the north-star
+    tolerance) but not bitwise.
+    """
+    global CMUL_MODE
+    if kind == "reference":
+        CMUL_MODE = _REFERENCE_CMUL
+    elif kind == "contracted":
+        CMUL_MODE = L.CMUL_CONTRACT
+    else:
+        raise ValueError(f"numerics must be 'reference' or 'contracted', got {kind!r}")
 
 # shared-memory tile of the fused multi-gate passes (diaq_run_gates_fused):
 # 11 or 12 bits, -1 lets the library pick per circuit (12 only with >12%

@@ -35,13 +35,22 @@ def test_jit_exports():
         L.call("diaq_jit_stats", None)
 
 
-def test_jit_compiles_benchmark_layer():
+@pytest.mark.parametrize("cmul_mode", [L.CMUL_FMA, L.CMUL_CONTRACT])
+def test_jit_compiles_benchmark_layer(cmul_mode):
     n = 28
     ops = W.random_layered_ops(n, 1, seed=0)
     pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
     for tb in (11, 12):
-        kernels, secs = _compile(n, pls, tb)
+        kernels, secs = _compile(n, pls, tb, cmul_mode=cmul_mode)
         assert kernels == 2, (tb, kernels)
+
+
+def test_jit_rejects_unknown_cmul_mode():
+    n = 12
+    ops = W.random_layered_ops(n, 1, seed=0)
+    pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
+    with pytest.raises(ValueError):
+        _compile(n, pls, 11, cmul_mode=3)
 
 
 @pytest.mark.parametrize("seed", [0, 3])
