@@ -5,6 +5,7 @@
 #include <string>
 
 #include <mutex>
+#include <unordered_set>
 #include <vector>
 
 #include "common.cuh"
@@ -116,6 +117,7 @@ extern "C" int diaq_tune(const char *key, int64_t value) {
     else if (k == "kron_flat") t.kron_flat = (int)value;
     else if (k == "kron_ctas_per_sm") t.kron_ctas_per_sm = (int)(value < 1 ? 1 : value);
     else return set_error(DIAQ_ERR_VALUE, "diaq_tune: unknown key %s", key);
+    ++t.epoch;
     return DIAQ_OK;
 }
 
@@ -173,34 +175,60 @@ extern "C" int diaq_timer_create(int n, void **events) {
 }
 
 // waits for events[n-1]; ms_out[i] = time between events[i] and events[i+1]
+// events recorded since the last diaq_timer_elapsed that read them
+static std::mutex g_marked_mu;
+static std::unordered_set<void *> g_marked;
+
+namespace diaq {
+cudaError_t timer_record(void *event, cudaStream_t s) {
+    const cudaError_t e = cudaEventRecord((cudaEvent_t)event, s);
+    if (e == cudaSuccess) {
+        std::lock_guard<std::mutex> lk(g_marked_mu);
+        g_marked.insert(event);
+    }
+    return e;
+}
+}  // namespace diaq
+
 extern "C" int diaq_timer_elapsed(int n, void **events, float *ms_out) {
     if (n < 1 || !events || !ms_out) return set_error(DIAQ_ERR_VALUE, "diaq_timer_elapsed: bad arguments");
     if (cudaEventSynchronize((cudaEvent_t)events[n - 1]) != cudaSuccess)
         return set_error(DIAQ_ERR_CUDA, "cudaEventSynchronize: %s", cudaGetErrorString(cudaGetLastError()));
     // events a fused pass did not record (all its gates but the last) read as
-    // zero-length intervals; the others are measured from the last recorded one
-    cudaEvent_t last = (cudaEvent_t)events[0];
+    // zero-length intervals; the others are measured from the last recorded
+    // one.  Only events marked by this run are read (an unrecorded event costs
+    // a failing driver call, and one left from an earlier run would be stale).
+    std::lock_guard<std::mutex> lk(g_marked_mu);
+    void *last = events[0];
+    g_marked.erase(events[0]);
     for (int i = 0; i + 1 < n; ++i) {
         float ms = 0.0f;
-        if (cudaEventElapsedTime(&ms, last, (cudaEvent_t)events[i + 1]) == cudaSuccess) {
+        auto it = g_marked.find(events[i + 1]);
+        if (it != g_marked.end() &&
+            cudaEventElapsedTime(&ms, (cudaEvent_t)last, (cudaEvent_t)events[i + 1]) == cudaSuccess) {
             ms_out[i] = ms;
-            last = (cudaEvent_t)events[i + 1];
+            last = events[i + 1];
         } else {
             cudaGetLastError();
             ms_out[i] = 0.0f;
         }
+        if (it != g_marked.end()) g_marked.erase(it);
     }
     return DIAQ_OK;
 }
 
 extern "C" int diaq_timer_destroy(int n, void **events) {
+    {
+        std::lock_guard<std::mutex> lk(g_marked_mu);
+        for (int i = 0; i < n; ++i) g_marked.erase(events[i]);
+    }
     for (int i = 0; i < n; ++i)
         if (events[i]) cudaEventDestroy((cudaEvent_t)events[i]);
     return DIAQ_OK;
 }
 
 extern "C" int diaq_timer_record(void *event, void *stream) {
-    if (cudaEventRecord((cudaEvent_t)event, (cudaStream_t)stream) != cudaSuccess)
+    if (timer_record(event, (cudaStream_t)stream) != cudaSuccess)
         return set_error(DIAQ_ERR_CUDA, "cudaEventRecord: %s", cudaGetErrorString(cudaGetLastError()));
     return DIAQ_OK;
 }

@@ -377,12 +377,12 @@ extern "C" int diaq_run_gates(int n_bits, int ngates, const diaq_gate_t *gates, 
                               void **events, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (ngates < 0 || (ngates > 0 && !gates) || !state) return set_error(DIAQ_ERR_VALUE, "diaq_run_gates: bad arguments");
-    if (events && cudaEventRecord((cudaEvent_t)events[0], s) != cudaSuccess)
+    if (events && timer_record(events[0], s) != cudaSuccess)
         return set_error(DIAQ_ERR_CUDA, "diaq_run_gates: event record failed");
     for (int i = 0; i < ngates; ++i) {
         const int rc = apply_gate(n_bits, gates[i].k, gates[i].g, gates[i].shifts, state, state, cmul_mode, s);
         if (rc) return rc;
-        if (events && cudaEventRecord((cudaEvent_t)events[i + 1], s) != cudaSuccess)
+        if (events && timer_record(events[i + 1], s) != cudaSuccess)
             return set_error(DIAQ_ERR_CUDA, "diaq_run_gates: event record failed");
     }
     return DIAQ_OK;

@@ -40,6 +40,7 @@ struct Tuning {
     int fused_perm = 1;        // fold permutation gates (X/CX/SWAP) into the fused passes' smem addressing
     int kron_flat = 1;         // kron_identity as one arena-linear store stream
     int kron_ctas_per_sm = 32;  // CTAs per SM launched (4 resident; later ones refill)
+    uint64_t epoch = 0;         // bumped by every diaq_tune (launch caches key on it)
 };
 Tuning &tuning();
 // SM count of the current device and resident CTAs per SM of a kernel,
@@ -50,4 +51,7 @@ int occupancy(const void *kernel, int threads, size_t smem);
 int set_error(int code, const char *fmt, ...);
 void count_launch(int n = 1);
 int check_launch(const char *what);
+// record a per-gate timer event and mark it as recorded for the next
+// diaq_timer_elapsed (events of gates inside a fused pass are not recorded)
+cudaError_t timer_record(void *event, cudaStream_t s);
 }  // namespace diaq

@@ -1190,7 +1190,7 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
         cudaGetLastError();
         attr_set[cur_dev] = true;
     }
-    if (events && cudaEventRecord((cudaEvent_t)events[0], s) != cudaSuccess)
+    if (events && timer_record(events[0], s) != cudaSuccess)
         return set_error(DIAQ_ERR_CUDA, "diaq_run_gates_fused: event record failed");
     thread_local TileParams tparams;
     // Buffers: a pass with a global permutation tail writes the other buffer
@@ -1255,7 +1255,7 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
             };
             if (pi < jit.size() && jit[pi] &&
                 jit_launch(jit[pi], p, R, smem_for(1), smem_for(2), tuning().fused_nbuf, s, rc)) {
-                if (events && rc == DIAQ_OK) cudaEventRecord((cudaEvent_t)events[ps.members.back() + 1], s);
+                if (events && rc == DIAQ_OK) timer_record(events[ps.members.back() + 1], s);
                 cur = nxt;
                 continue;
             }
@@ -1285,7 +1285,7 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
         // events[i]..events[i+1] bracket gate i; a fused pass records only its
         // last gate's event (one record per pass, not per gate), so the pass's
         // time lands on that gate and diaq_timer_elapsed reads the others as 0
-        if (events && rc == DIAQ_OK) cudaEventRecord((cudaEvent_t)events[ps.members.back() + 1], s);
+        if (events && rc == DIAQ_OK) timer_record(events[ps.members.back() + 1], s);
         cur = nxt;
     }
     if (rc == DIAQ_OK && cur != 0 &&

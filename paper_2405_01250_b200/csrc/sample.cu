@@ -123,105 +123,133 @@ __global__ void sample_search_kernel(const double *c, int64_t n, const double *u
 }
 
 // Small states (n <= 2^24): the whole binade walk in ONE CTA, no host round
-// trip.  The CTA scans chunks of kWalkE * 1024 elements: k_i = RNE(q_i / U)
-// in the current binade, an exclusive block scan of the per-thread sums, the
-// first element that leaves the binade or ties (block min), c written up to
-// it, the exiting element as one float64 add, then the next binade -- the
-// same arithmetic as the host-driven path below, ~0.3 ms at n = 20 instead
-// of ~45 synchronised round trips.
-constexpr int kWalkThreads = 1024;
-constexpr int kWalkE = 8;
+// trip.  The CTA scans chunks of kWalkE * kWalkThreads elements: k_i =
+// RNE(q_i / U) in the current binade, an exclusive block scan of the
+// per-thread sums, the first element that leaves the binade or ties, c
+// written up to it, the exiting element as one float64 add, then the next
+// binade -- the same arithmetic as the host-driven path below.  Each thread
+// owns kWalkE consecutive elements of a chunk; chunks move through shared
+// memory (coalesced cp.async loads, double-buffered so the next chunk lands
+// while this one is scanned; c staged back the same way for coalesced
+// stores), and a chunk that stays in its binade costs one block scan and one
+// __syncthreads_or -- the exit bookkeeping runs only at the ~45 binade ends.
+constexpr int kWalkThreads = 512;
+constexpr int kWalkE = 12;
+constexpr int kWalkChunk = kWalkE * kWalkThreads;
+constexpr size_t kWalkSmem = 2 * sizeof(double) * kWalkChunk;
 
-__global__ void __launch_bounds__(kWalkThreads) sample_walk_kernel(const double *q, int64_t n,
-                                                                   const unsigned long long *first_nz, double *c) {
-    using BlockScan = cub::BlockScan<long long, kWalkThreads>;
+__device__ __forceinline__ long long walk_k(double v) {
+    const double r = rint(v);  // round half to even
+    return r >= 9007199254740992.0 ? (1ll << 53) : (long long)r;
+}
+
+// chunk [p, p + kWalkChunk) of q into buf (zeros past n), one commit group
+__device__ __forceinline__ void walk_fetch(double *buf, const double *q, int64_t p, int64_t n) {
+    for (int k = threadIdx.x; k < kWalkChunk; k += kWalkThreads) {
+        if (p + k < n) {
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(buf + k)), "l"(q + p + k)
+                         : "memory");
+        } else {
+            buf[k] = 0.0;
+        }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kWalkThreads, 1) sample_walk_kernel(const double *__restrict__ q, int64_t n,
+                                                                      const unsigned long long *first_nz,
+                                                                      double *__restrict__ c) {
+    using BlockScan = cub::BlockScan<long long, kWalkThreads, cub::BLOCK_SCAN_WARP_SCANS>;
     __shared__ typename BlockScan::TempStorage scan_tmp;
     __shared__ long long s_exit;
     __shared__ double s_cur;
-    __shared__ int64_t s_i;
+    extern __shared__ double wbuf[];  // two chunk buffers
     const int tid = threadIdx.x;
     const unsigned long long f = *first_nz;
     const int64_t first = f == ~0ull ? n : (int64_t)f;
     for (int64_t j = tid; j < first && j < n; j += blockDim.x) c[j] = 0.0;
     if (first >= n) return;
-    if (tid == 0) {
-        s_cur = q[first];
-        c[first] = s_cur;
-        s_i = first + 1;
-    }
-    __syncthreads();
     const long long lim = 1ll << 53;
-    constexpr int64_t chunk = (int64_t)kWalkE * kWalkThreads;
-    while (true) {
-        const int64_t i = s_i;
-        const double cur = s_cur;
-        if (i >= n) break;
-        int e = 0;
-        frexp(cur, &e);  // cur in [2^(e-1), 2^e)
-        const int eb = e - 1;
-        const double U = ldexp(1.0, eb - 52);
-        const double scale = ldexp(1.0, 52 - eb);
-        long long kbase = (long long)ldexp(cur, 52 - eb);  // exact integer in [2^52, 2^53)
-        int64_t pos = i;
-        __syncthreads();
+    double cur = q[first];
+    if (tid == 0) c[first] = cur;
+    int64_t pos = first + 1;
+    int cb = 0;  // buffer of the current chunk
+    walk_fetch(wbuf, q, pos, n);
+    while (pos < n) {
+        // binade of cur (a normal double: q >= 1e-12 when nonzero): cur in [2^eb, 2^(eb+1))
+        const int eb = (int)((__double_as_longlong(cur) >> 52) & 0x7ff) - 1023;
+        const double U = __longlong_as_double((long long)(eb - 52 + 1023) << 52);
+        const double scale = __longlong_as_double((long long)(52 - eb + 1023) << 52);
+        long long kbase = (long long)__dmul_rn(cur, scale);  // exact integer in [2^52, 2^53)
         while (pos < n) {
-            long long kv[kWalkE];
-            bool ex[kWalkE];
-            long long tsum = 0;
+            double *buf = wbuf + cb * kWalkChunk;
+            double *nbuf = wbuf + (cb ^ 1) * kWalkChunk;
+            __syncthreads();  // nbuf (the previous chunk) fully drained to c
+            walk_fetch(nbuf, q, pos + kWalkChunk, n);  // the next chunk flies under this one
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+            __syncthreads();
+            double *mine = buf + tid * kWalkE;
             const int64_t b = pos + (int64_t)tid * kWalkE;
+            long long kv[kWalkE], tsum = 0;
+            unsigned ties = 0;
 #pragma unroll
-            for (int j = 0; j < kWalkE; ++j) {
-                kv[j] = 0;
-                ex[j] = false;
-                if (b + j < n) {
-                    const double v = __dmul_rn(q[b + j], scale);
-                    const double fl = floor(v);
-                    const double r = rint(v);
-                    kv[j] = r >= 9007199254740992.0 ? lim : (long long)r;
-                    ex[j] = (v - fl) == 0.5;
-                }
+            for (int j = 0; j < kWalkE; ++j) {  // q = 0 past n
+                const double v = __dmul_rn(mine[j], scale);  // exact: scaling by a power of two
+                kv[j] = walk_k(v);
+                ties |= (unsigned)((v - floor(v)) == 0.5) << j;
                 tsum += kv[j];
             }
-            long long excl;
-            long long total;
+            long long excl, total;
             BlockScan(scan_tmp).ExclusiveSum(tsum, excl, total);
-            if (tid == 0) s_exit = LLONG_MAX;
-            __syncthreads();
             long long run = kbase + excl;
-            long long my_exit = LLONG_MAX;
+            int my = -1;
+            const int64_t rem = n - b;
+            const int lim_j = rem < kWalkE ? (int)rem : kWalkE;  // valid elements of this thread
 #pragma unroll
             for (int j = 0; j < kWalkE; ++j) {
                 run += kv[j];
-                if (b + j < n && my_exit == LLONG_MAX && (ex[j] || run >= lim)) my_exit = b + j;
+                if (my < 0 && j < lim_j && (((ties >> j) & 1u) || run >= lim)) my = j;
             }
-            if (my_exit != LLONG_MAX) atomicMin(&s_exit, my_exit);
-            __syncthreads();
-            const long long xat = s_exit;
+            const bool exits = __syncthreads_or(my >= 0);
+            int64_t xat = pos + kWalkChunk;  // first element not written from the integer scan
+            if (exits) {
+                if (tid == 0) s_exit = LLONG_MAX;
+                __syncthreads();
+                if (my >= 0) atomicMin(&s_exit, (long long)(b + my));
+                __syncthreads();
+                xat = s_exit;
+            }
             run = kbase + excl;
 #pragma unroll
-            for (int j = 0; j < kWalkE; ++j) {
+            for (int j = 0; j < kWalkE; ++j) {  // own slots only: no hazard with other threads' reads
                 run += kv[j];
-                if (b + j < n && b + j < xat) c[b + j] = __dmul_rn((double)run, U);
+                mine[j] = __dmul_rn((double)run, U);
             }
-            if (xat == LLONG_MAX) {  // the whole chunk stays in the binade
+            __syncthreads();
+            int64_t wend = xat < n ? xat : n;
+            if (wend > pos + kWalkChunk) wend = pos + kWalkChunk;
+            for (int k = tid; pos + k < wend; k += kWalkThreads) c[pos + k] = buf[k];
+            if (!exits) {
                 kbase += total;
-                pos += chunk;
-                __syncthreads();
+                pos += kWalkChunk;
+                cb ^= 1;
                 continue;
             }
             __syncthreads();  // c before the exit is written
-            if (tid == 0) {  // the exiting element: one float64 add (IEEE, round to nearest even)
-                const double cprev = xat > 0 ? c[xat - 1] : 0.0;
-                const double sum = __dadd_rn(cprev, q[xat]);
+            if (tid == 0) {   // the exiting element: one float64 add (IEEE, round to nearest even)
+                const double sum = __dadd_rn(c[xat - 1], q[xat]);
                 c[xat] = sum;
                 s_cur = sum;
-                s_i = xat + 1;
             }
+            asm volatile("cp.async.wait_group 0;" ::: "memory");  // drop the prefetched chunk
             __syncthreads();
+            cur = s_cur;
+            pos = xat + 1;
+            if (pos < n) walk_fetch(wbuf + cb * kWalkChunk, q, pos, n);
             break;
         }
-        if (pos >= n) break;
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 static int grid_of(int64_t n) {
@@ -286,7 +314,8 @@ extern "C" int diaq_sample_hits(int64_t n, const void *x, const double *u_host, 
     }
     if (shots == 0) goto done;
     if (n <= ((int64_t)1 << 24)) {  // one-CTA device walk (no round trips)
-        sample_walk_kernel<<<1, kWalkThreads, 0, s>>>(q, n, flag, c);
+        cudaFuncSetAttribute(sample_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWalkSmem);
+        sample_walk_kernel<<<1, kWalkThreads, kWalkSmem, s>>>(q, n, flag, c);
         count_launch();
         DIAQ_CK(cudaGetLastError());
         goto search;

@@ -258,7 +258,10 @@ def measure_all_sample(x: StateVector, shots: int, seed: int) -> dict[str, int]:
         return {}
     outcomes, freq = np.unique(hits[:shots], return_counts=True)
     width = x.n_qubits
-    return {format(int(i), f"0{width}b"): int(c) for i, c in zip(outcomes, freq)}
+    # bitstrings q0..q(n-1), MSB first, formatted in one numpy pass
+    bits = (outcomes[:, None] >> np.arange(width - 1, -1, -1, dtype=np.int64)) & 1
+    keys = (bits.astype(np.uint8) + ord("0")).view(f"S{width}").ravel()
+    return {k.decode(): int(c) for k, c in zip(keys, freq.tolist())}
 
 
 # -- driver ----------------------------------------------------------------------
@@ -387,16 +390,30 @@ def run(
     if hit is None:
         placements = fuse_pass(compile_circuit(circuit, **kwargs), enabled=fusion)
         names = [f"{i}:{p.name}" for i, p in enumerate(placements)]
-        hit = (placements, names, L.Timer(len(placements) + 1))
+        comps = [p.compact() for p in placements]
+        # the placements are private to this cache, so the packed program
+        # cannot go stale: it is built once and replayed
+        prog = _GateProgram(comps) if all(c is not None for c in comps) else None
+        hit = (placements, names, L.Timer(len(placements) + 1), prog)
         if len(_RUN_CACHE) >= 4:
             _RUN_CACHE.pop(next(iter(_RUN_CACHE)))
         _RUN_CACHE[key] = hit
-    placements, names, timer = hit
+    placements, names, timer, prog = hit
     t_compile = time.perf_counter_ns() - t0
 
     state = init_state(circuit.n_qubits)
     t0 = time.perf_counter_ns()
-    if backend == "diaq":
+    if backend == "diaq" and prog is not None and prog.n:
+        xd = state.device_amps
+        state._device_modified()
+        n_bits = len(state).bit_length() - 1
+        if FUSE_TILE_BITS != 0:
+            L.call("diaq_run_gates_fused", n_bits, prog.n, prog.arr, xd.data_ptr(), int(CMUL_MODE),
+                   int(FUSE_TILE_BITS), timer.slice_ptr(0), None, L.stream_handle())
+        else:
+            L.call("diaq_run_gates", n_bits, prog.n, prog.arr, xd.data_ptr(), int(CMUL_MODE), timer.slice_ptr(0),
+                   L.stream_handle())
+    elif backend == "diaq":
         state = run_gates(state, placements, timer=timer, inplace=True)
     else:
         timer.record(0)

@@ -500,7 +500,8 @@ def test_spmv_host_pipeline_chunks(monkeypatch):
 def test_device_sampler_matches_reference_sampler():
     """Device sampler (exact sequential CDF) == the reference numpy sampler, shot for shot."""
     rng = np.random.default_rng(31)
-    for n, shots, seed in ((1, 100, 0), (6, 4096, 3), (10, 100000, 7), (14, 50000, 11), (18, 20000, 5)):
+    for n, shots, seed in ((1, 100, 0), (6, 4096, 3), (10, 100000, 7), (14, 50000, 11), (18, 20000, 5),
+                           (20, 1024, 0), (22, 4096, 9)):
         x = W.random_state(rng, 2**n)
         if n == 6:
             x[::3] = 0  # zero runs and a sparse CDF
