@@ -40,6 +40,9 @@ struct Tuning {
     int fused_perm = 1;        // fold permutation gates (X/CX/SWAP) into the fused passes' smem addressing
     int kron_flat = 1;         // kron_identity as one arena-linear store stream
     int kron_ctas_per_sm = 32;  // CTAs per SM launched (4 resident; later ones refill)
+    int fused_estore = 1;      // pair passes: store gathered into registers, next fetch issued before the HBM writes
+                               // (n=28 layer, contracted: 1.615 -> 1.574 ms per pass, r02f)
+    int fused_reorder = 1;     // contracted arithmetic: schedule passes with commutation-aware deferral
     uint64_t epoch = 0;         // bumped by every diaq_tune (launch caches key on it)
 };
 Tuning &tuning();

@@ -399,6 +399,9 @@ static int pack_smem_gate(const diaq_gate_t &gt, const std::vector<int> &bits, P
 // set while re-planning a call without the out-of-place permutation tails
 // (no room for the state-sized buffer they need)
 static thread_local bool t_no_gperm = false;
+// schedule with commutation-aware deferral (set for the contracted arithmetic;
+// part of the program key)
+static thread_local bool t_reorder = false;
 
 // thread bits of a tiled pass: 8 (256 threads; T = 11 -> R = 3, T = 12 -> R = 4)
 // or 7 (128 threads, T = 11, R = 4: a phase covers one more qubit, so a pass
@@ -446,6 +449,7 @@ static void spread_lane_bits(Phase &ph, int T, int R) {
 
 static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t *gates, int T, int R,
                          std::vector<PassPlan> &plan, bool allow_d2) {
+    const bool reorder = t_reorder;
     const int low = std::min(kLowBits, n_bits);
     std::vector<char> fast((size_t)ngates);  // register fast-path classification, once per gate
     std::vector<PermGate> perm((size_t)ngates);
@@ -693,9 +697,32 @@ static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t 
         return DIAQ_OK;
     };
     reset();
-    for (int i = 0; i < ngates; ++i) {
+    // reorder (contracted arithmetic only): a gate that does not fit the open
+    // pass is deferred instead of closing it, and the scan goes on -- later
+    // gates on other qubits commute with it and may still join.  Any gate
+    // sharing a qubit with a deferred one is deferred too (program order per
+    // qubit is kept), and the deferred gates, in order, form the next sweep.
+    // Reordering gates on disjoint qubits is exact in real arithmetic but
+    // changes the rounding, so the bitwise modes keep the program order.
+    std::vector<int> pending((size_t)ngates);
+    for (int i = 0; i < ngates; ++i) pending[(size_t)i] = i;
+    while (!pending.empty()) {
+    std::vector<int> deferred;
+    uint64_t blocked = 0;
+    for (const int i : pending) {
         const diaq_gate_t &gt = gates[i];
         if (gt.k < 1 || gt.k > 5) return set_error(DIAQ_ERR_UNSUPPORTED, "gate width %d outside 1..5", gt.k);
+        uint64_t qmask = 0;
+        for (int j = 0; j < gt.k; ++j)
+            if (gt.shifts[j] >= 0 && gt.shifts[j] < 64) qmask |= 1ull << gt.shifts[j];
+        auto defer = [&]() {
+            deferred.push_back(i);
+            blocked |= qmask;
+        };
+        if (reorder && (qmask & blocked)) {
+            defer();
+            continue;
+        }
         const uint32_t mix = mixing_mask(gt.k, gt.g);
         int kin = 0, kout = 0, add = 0;
         for (int j = 0; j < gt.k; ++j) {
@@ -712,6 +739,10 @@ static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t 
         }
         const bool pg = perm[(size_t)i].ok;
         if (!pg && tail != SIZE_MAX) {  // a gate after a global permutation tail opens the next pass
+            if (reorder) {
+                defer();
+                continue;
+            }
             int rc = flush();
             if (rc) return rc;
             reset();
@@ -743,6 +774,10 @@ static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t 
                     continue;
                 }
                 // it opens the next pass, where its bits can join the tile
+                if (reorder) {
+                    defer();
+                    continue;
+                }
                 int rc = flush();
                 if (rc) return rc;
                 reset();
@@ -752,6 +787,10 @@ static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t 
             }
         }
         if (pg ? (kin > T - low) : (kin > kMaxRegKin || kin > R || kout > kMaxSel)) {  // standalone pass
+            if (reorder && !members.empty()) {  // its own pass, after the open one
+                defer();
+                continue;
+            }
             int rc = flush();
             if (rc) return rc;
             reset();
@@ -770,6 +809,10 @@ static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t 
         // phases per pass are bounded too: a pass can need up to one phase per gate
         if (nb + add > T || (int)members.size() >= std::min(kMaxPassGates, kMaxPhases) ||
             (int)pbase.size() + padd > kMaxPermBase || ncoef + gcoef > kMaxCoef || nnz + gnz > kMaxNz) {
+            if (reorder && !members.empty()) {
+                defer();
+                continue;
+            }
             int rc = flush();
             if (rc) return rc;
             reset();
@@ -786,6 +829,12 @@ static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t 
         ncoef += gcoef;
         nnz += gnz;
         members.push_back(i);
+    }
+    if (!reorder) break;
+    int rc = flush();
+    if (rc) return rc;
+    reset();
+    pending.swap(deferred);
     }
     return flush();
 }
@@ -865,7 +914,7 @@ static std::vector<char> program_key(int n_total, int n_bits, int T, int ngates,
         key.insert(key.end(), c, c + n);
     };
     // every tuning switch the schedule depends on is part of the key
-    const int head[15] = {n_total, n_bits, T, pass_tbits(), ngates, tuning().fused_perm,
+    const int head[16] = {n_total, n_bits, T, pass_tbits(), ngates, (int)t_reorder, tuning().fused_perm,
                           tuning().fused_gperm && !t_no_gperm, tuning().fused_seq, tuning().fused_dense2,
                           tuning().fused_gperm_rows, tuning().fused_pair_store, tuning().fused_bank_spread, tuning().fused_plain_pair, tuning().fused_ppipe, tuning().fused_dstore};
     put(head, sizeof(head));
@@ -1134,6 +1183,7 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
         return set_error(DIAQ_ERR_VALUE, "diaq_run_gates_fused: bad arguments");
     if (cmul_mode < DIAQ_CMUL_PLAIN || cmul_mode > DIAQ_CMUL_CONTRACT)
         return set_error(DIAQ_ERR_VALUE, "diaq_run_gates_fused: cmul_mode %d", cmul_mode);
+    t_reorder = cmul_mode == DIAQ_CMUL_CONTRACT && tuning().fused_reorder;
     const bool sharded = n_total > n_bits;
     cudaStream_t s = (cudaStream_t)stream;
     // tile_bits 12 -> 16 amplitudes per thread (R = 4), 11 -> 8 (R = 3); 256
@@ -1231,9 +1281,11 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
         }
     }
     int cur = 0;
+    int ev_hi = -1;  // highest gate applied so far (reordered programs: events stay monotone)
     for (size_t pi = 0; pi < np && rc == DIAQ_OK; ++pi) {
         const int nxt = flip[pi] ? 1 - cur : cur;
         const PassPlan &ps = plan[pi];
+        for (int m : ps.members) ev_hi = std::max(ev_hi, m);
         if (ps.bits.empty() || ps.members.size() == 1) {
             const diaq_gate_t &gt = gates[ps.members[0]];
             if (sharded) rc = apply_gate_sharded_own(n_total, n_bits, gt.k, gt.g, gt.shifts, rank, bufs[cur], cmul_mode, s);
@@ -1244,6 +1296,7 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
             p.x = bufs[cur];
             p.y = bufs[nxt];
             p.gbase = sharded ? ((uint64_t)rank << n_bits) : 0ull;
+            p.estore = tuning().fused_estore;
             if (p.gperm && sharded)  // controls on global bits: constants of this rank
                 for (int g = 0; g < 64 && g < n_total - n_bits; ++g)
                     if (((uint64_t)rank >> g) & 1ull) p.gconst ^= ps.ggcol[(size_t)g];
@@ -1255,7 +1308,7 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
             };
             if (pi < jit.size() && jit[pi] &&
                 jit_launch(jit[pi], p, R, smem_for(1), smem_for(2), tuning().fused_nbuf, s, rc)) {
-                if (events && rc == DIAQ_OK) timer_record(events[ps.members.back() + 1], s);
+                if (events && rc == DIAQ_OK) timer_record(events[ev_hi + 1], s);
                 cur = nxt;
                 continue;
             }
@@ -1285,7 +1338,7 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
         // events[i]..events[i+1] bracket gate i; a fused pass records only its
         // last gate's event (one record per pass, not per gate), so the pass's
         // time lands on that gate and diaq_timer_elapsed reads the others as 0
-        if (events && rc == DIAQ_OK) timer_record(events[ps.members.back() + 1], s);
+        if (events && rc == DIAQ_OK) timer_record(events[ev_hi + 1], s);
         cur = nxt;
     }
     if (rc == DIAQ_OK && cur != 0 &&
@@ -1322,6 +1375,7 @@ extern "C" int diaq_fused_plan(int n_bits, int local_bits, int ngates, const dia
         return DIAQ_OK;
     }
     std::vector<PassPlan> plan;
+    t_reorder = false;  // the program-order schedule (the bitwise modes')
     const int rc = schedule(local_bits, n_bits, ngates, gates, T, T - pass_tbits(), plan);
     if (rc) return rc;
     if (getenv("DIAQ_PLAN_DEBUG")) debug_plan(plan);
@@ -1346,6 +1400,7 @@ extern "C" int diaq_fused_jit_compile(int n_bits, int local_bits, int ngates, co
         return set_error(DIAQ_ERR_VALUE, "diaq_fused_jit_compile: bad arguments");
     if (local_bits < 1 || local_bits > n_bits) return set_error(DIAQ_ERR_SHAPE, "local_bits %d invalid", local_bits);
     if (cmul_mode < 0 || cmul_mode > 2) return set_error(DIAQ_ERR_VALUE, "cmul_mode %d", cmul_mode);
+    t_reorder = cmul_mode == DIAQ_CMUL_CONTRACT && tuning().fused_reorder;
     const int T = (tile_bits >= kThreadBits + 4 && pass_tbits() == 8) ? kThreadBits + 4 : kThreadBits + 3;
     int rc = DIAQ_OK;
     std::shared_ptr<const Program> prog = build_program(n_bits, local_bits, T, ngates, gates, rc);

@@ -128,6 +128,7 @@ struct TileParams {
     int gperm;                // store through the global map (out of place)
     int nbuf;                 // tile buffers in dynamic smem: 2 = prefetch the next tile during this one
     int gstore;               // global-map store: 0 streaming (.cs), 1 write-back default, 2 L2 evict_last
+    int estore;               // pair passes: gather the store into registers, fetch the next unit, then store
     uint64_t gconst;          // its constant, rank bits folded in
     uint64_t gcol[64];        // image of local state bit j
     // Pair store of a global tail that splits 32-byte sectors (specialised
@@ -964,6 +965,38 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
             }
             __syncthreads();
             const uint64_t ab = s_ab ^ pw_t;
+            if (p.estore) {
+                // the whole store gathered into registers first: the tile
+                // buffers are free before any HBM write, so the next unit's
+                // fetch is in flight while this unit's stores drain
+                constexpr int NS = 2 * NR;
+                double2 sv[NS];
+#pragma unroll
+                for (int i = 0; i < NS; ++i) {
+                    if (i >= (1 << (dims - TB))) break;
+                    uint32_t cs = 0;
+#pragma unroll
+                    for (int m = 0; m < dims - TB; ++m)
+                        if ((i >> m) & 1) cs ^= S.gsrc[TB + m];
+                    sv[i] = lds128(tile0 + ((ps_slot ^ pslot(cs)) << 4));
+                }
+                __syncthreads();
+                gb = ngb;
+                if (t + gridDim.x < nunits) {
+                    fetch(gb, tile0);
+                    fetch(gb | pbit, buf1);
+                }
+#pragma unroll
+                for (int i = 0; i < NS; ++i) {
+                    if (i >= (1 << (dims - TB))) break;
+                    uint64_t cw = 0;
+#pragma unroll
+                    for (int m = 0; m < dims - TB; ++m)
+                        if ((i >> m) & 1) cw ^= S.gw[TB + m];
+                    st_stream(p.y + (ab ^ cw), sv[i]);
+                }
+                continue;
+            }
 #pragma unroll
             for (int i = 0; i < 2 * NR; ++i) {
                 if (i >= (1 << (dims - TB))) break;
@@ -1118,6 +1151,27 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
                 if (tid == 0) s_sbase = (gb | (h ? pbit : 0ull)) | p.gbase;
                 __syncthreads();
                 phases(h ? buf1 : tile0, 0ull, [] {});
+            }
+            if (p.estore) {  // gather to registers, fetch the next pair, then store (see the pair store)
+                double2 sa[NR], sb[NR];
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < NR; ++k) {
+                    const uint32_t sl = swz((uint32_t)k << TB);
+                    sa[k] = lds128(slot_addr(a0, sl));
+                    sb[k] = lds128(slot_addr(a1, sl));
+                }
+                __syncthreads();
+                const uint64_t cgb = gb;
+                gb = ngb;
+                if (t + gridDim.x < nunits) fetch2(gb);
+                double2 *dst = p.y + (cgb + t_off);
+#pragma unroll
+                for (int k = 0; k < NR; ++k) {
+                    st_stream(dst + kdep(k), sa[k]);
+                    st_stream(dst + (kdep(k) | pbit), sb[k]);
+                }
+                continue;
             }
             double2 *dst = p.y + (gb + t_off);
 #pragma unroll
