@@ -1208,6 +1208,33 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
         __syncthreads();
         phases(buf, 0ull, [] {});
         const uint32_t a = buf + t16;
+        if (p.estore && p.nbuf == 1) {
+            // one buffer: gather this tile's store into registers, refill the
+            // buffer with the next tile, then write -- the fetch is in flight
+            // during the HBM writes instead of after them
+            double2 sv[NR];
+#pragma unroll
+            for (int k = 0; k < NR; ++k) sv[k] = lds128(slot_addr(a, swz((uint32_t)k << TB)));
+            const uint64_t ab = S.gperm ? (s_ab ^ g_t) : 0ull;
+            __syncthreads();
+            const uint64_t cbase = base;
+            base = nbase;
+            if (more) fetch(base, buf);
+            if (S.gperm) {
+#pragma unroll
+                for (int k = 0; k < NR; ++k) {
+                    double2 *dst = p.y + (ab ^ gmap(S, kdep(k)));
+                    if (p.gstore == 0) st_stream(dst, sv[k]);
+                    else if (p.gstore == 1) st_plain(dst, sv[k]);
+                    else st_hint(dst, sv[k], policy_evict_last());
+                }
+            } else {
+                double2 *dst = p.y + (cbase + t_off);
+#pragma unroll
+                for (int k = 0; k < NR; ++k) st_stream(dst + kdep(k), sv[k]);
+            }
+            continue;
+        }
         if (S.gperm) {  // trailing permutation run: element i goes to A i ^ c in the other buffer
             const uint64_t ab = s_ab ^ g_t;
 #pragma unroll
