@@ -116,6 +116,7 @@ extern "C" int diaq_tune(const char *key, int64_t value) {
     else if (k == "fused_perm") t.fused_perm = (int)value;
     else if (k == "fused_estore") t.fused_estore = (int)value;
     else if (k == "fused_reorder") t.fused_reorder = (int)value;
+    else if (k == "fused_dyn") t.fused_dyn = (int)value;
     else if (k == "kron_flat") t.kron_flat = (int)value;
     else if (k == "kron_ctas_per_sm") t.kron_ctas_per_sm = (int)(value < 1 ? 1 : value);
     else return set_error(DIAQ_ERR_VALUE, "diaq_tune: unknown key %s", key);

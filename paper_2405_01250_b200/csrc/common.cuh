@@ -43,6 +43,8 @@ struct Tuning {
     int fused_estore = 1;      // pair passes: store gathered into registers, next fetch issued before the HBM writes
                                // (n=28 layer, contracted: 1.615 -> 1.574 ms per pass, r02f)
     int fused_reorder = 1;     // contracted arithmetic: schedule passes with commutation-aware deferral
+    int fused_dyn = 1;         // units handed out in order by a global counter (TileParams::uctr): adjacent DRAM runs fetched
+                               // together (n=28 layer 1.554 -> 1.434 ms per contracted pass, config 5 339 -> 305 ms, r02n)
     uint64_t epoch = 0;         // bumped by every diaq_tune (launch caches key on it)
 };
 Tuning &tuning();

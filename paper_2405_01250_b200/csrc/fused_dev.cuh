@@ -129,6 +129,12 @@ struct TileParams {
     int nbuf;                 // tile buffers in dynamic smem: 2 = prefetch the next tile during this one
     int gstore;               // global-map store: 0 streaming (.cs), 1 write-back default, 2 L2 evict_last
     int estore;               // pair passes: gather the store into registers, fetch the next unit, then store
+    // pair passes with estore: units handed out in order by a global counter
+    // (null: static blockIdx + k gridDim), so the units in flight are always
+    // a contiguous window and adjacent DRAM runs are fetched together; the
+    // last CTA to finish resets the counter pair for the slot's next launch
+    unsigned long long *uctr;
+    unsigned long long *udone;
     uint64_t gconst;          // its constant, rank bits folded in
     uint64_t gcol[64];        // image of local state bit j
     // Pair store of a global tail that splits 32-byte sectors (specialised
@@ -827,6 +833,7 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
     __shared__ uint16_t s_lt[kThreads];
     __shared__ uint64_t s_sbase;  // current tile's base | rank bits (selector lookups)
     __shared__ uint64_t s_ab;     // global-map image of the current tile / pair base
+    __shared__ int64_t s_u[2];    // dynamic unit order: the next unit, double-buffered by parity
     const double2 *sc = p.coef;
     const uint32_t *snz = p.nz;
     const int npre = S.nphases < kPre ? S.nphases : kPre;
@@ -857,6 +864,25 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
             for (int k = 0; k < NR; ++k) cp_async16_s(slot_addr(a, swz((uint32_t)k << TB)), src + kdep(k));
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    // dynamic unit order (p.uctr): the first unit, and the end-of-pass reset
+    auto first_unit = [&]() -> int64_t {
+        if (!p.uctr) return (int64_t)blockIdx.x;
+        if (tid == 0) s_u[0] = (int64_t)atomicAdd(p.uctr, 1ull);
+        __syncthreads();
+        return s_u[0];
+    };
+    auto units_done = [&]() {
+        if (!p.uctr) return;
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            if (atomicAdd(p.udone, 1ull) == (unsigned long long)gridDim.x - 1ull) {
+                *p.uctr = 0ull;
+                *p.udone = 0ull;
+                __threadfence();
+            }
+        }
     };
     __syncthreads();
     // dbase / on_loaded: with S.dstore the last phase writes its registers
@@ -946,13 +972,17 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
         const uint64_t pbit = 1ull << S.gpb[0];
         const int64_t nunits = p.ntiles >> 1;
         const uint32_t buf1 = tile0 + (16u << T);
-        uint64_t gb = insert_zero_bits_dyn((uint64_t)blockIdx.x, S.eb, T + 1);
-        if ((int64_t)blockIdx.x < nunits) {
+        const bool dyn = p.uctr && p.estore;
+        const int64_t u0 = dyn ? first_unit() : (int64_t)blockIdx.x;
+        uint64_t gb = insert_zero_bits_dyn((uint64_t)u0, S.eb, T + 1);
+        if (u0 < nunits) {
             fetch(gb, tile0);
             fetch(gb | pbit, buf1);
         }
-        for (int64_t t = blockIdx.x; t < nunits; t += gridDim.x) {
+        int par = 1;
+        for (int64_t t = u0; t < nunits; t += gridDim.x) {
             const uint64_t ngb = ((gb | S.emask) + p.gstep) & ~S.emask;
+            if (dyn && tid == 0) s_u[par] = (int64_t)atomicAdd(p.uctr, 1ull);  // lands during the compute
             asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll 1
             for (int h = 0; h < 2; ++h) {
@@ -981,8 +1011,16 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
                     sv[i] = lds128(tile0 + ((ps_slot ^ pslot(cs)) << 4));
                 }
                 __syncthreads();
-                gb = ngb;
-                if (t + gridDim.x < nunits) {
+                int64_t nt = t + gridDim.x;
+                if (dyn) {
+                    nt = s_u[par];
+                    par ^= 1;
+                    gb = insert_zero_bits_dyn((uint64_t)nt, S.eb, T + 1);
+                    t = nt - gridDim.x;  // the loop increment lands on nt
+                } else {
+                    gb = ngb;
+                }
+                if (nt < nunits) {
                     fetch(gb, tile0);
                     fetch(gb | pbit, buf1);
                 }
@@ -1018,6 +1056,7 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
                 fetch(gb | pbit, buf1);
             }
         }
+        if (dyn) units_done();
         return;
     }
     if (S.ppair && S.ppipe == 3) {
@@ -1125,6 +1164,43 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
             }
             return;
         }
+        if (p.uctr && p.estore && !S.dstore) {  // dynamic unit order (see TileParams::uctr)
+            int64_t t = first_unit();
+            gb = insert_zero_bits_dyn((uint64_t)t, S.eb, T + 1);
+            if (t < nunits) fetch2(gb);
+            int par = 1;
+            while (t < nunits) {
+                if (tid == 0) s_u[par] = (int64_t)atomicAdd(p.uctr, 1ull);  // lands during the compute
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll 1
+                for (int h = 0; h < 2; ++h) {
+                    if (tid == 0) s_sbase = (gb | (h ? pbit : 0ull)) | p.gbase;
+                    __syncthreads();
+                    phases(h ? buf1 : tile0, 0ull, [] {});
+                }
+                double2 sa[NR], sb[NR];
+#pragma unroll
+                for (int k = 0; k < NR; ++k) {
+                    const uint32_t sl = swz((uint32_t)k << TB);
+                    sa[k] = lds128(slot_addr(a0, sl));
+                    sb[k] = lds128(slot_addr(a1, sl));
+                }
+                __syncthreads();
+                const uint64_t cgb = gb;
+                t = s_u[par];
+                par ^= 1;
+                gb = insert_zero_bits_dyn((uint64_t)t, S.eb, T + 1);
+                if (t < nunits) fetch2(gb);
+                double2 *dst = p.y + (cgb + t_off);
+#pragma unroll
+                for (int k = 0; k < NR; ++k) {
+                    st_stream(dst + kdep(k), sa[k]);
+                    st_stream(dst + (kdep(k) | pbit), sb[k]);
+                }
+            }
+            units_done();
+            return;
+        }
         if ((int64_t)blockIdx.x < nunits) fetch2(gb);
         if (S.dstore) {  // both halves store from registers; the next pair lands under B's last phase
             for (int64_t t = blockIdx.x; t < nunits; t += gridDim.x) {
@@ -1188,6 +1264,48 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
     }
     // gperm scatter store: element e -> gconst ^ G(base) ^ G(t_off) ^ G(kdep(k))
     const uint64_t g_t = S.gperm ? gmap(S, t_off) : 0ull;
+    if (p.uctr && p.estore && p.nbuf == 1) {  // dynamic unit order (see TileParams::uctr), one buffer
+        int64_t t = first_unit();
+        uint64_t base = insert_zero_bits_dyn((uint64_t)t, S.tb, T);
+        if (t < p.ntiles) fetch(base, tile0);
+        int par = 1;
+        const uint32_t a = tile0 + t16;
+        while (t < p.ntiles) {
+            if (tid == 0) {
+                s_u[par] = (int64_t)atomicAdd(p.uctr, 1ull);  // lands during the compute
+                s_sbase = base | p.gbase;
+                if (S.gperm) s_ab = p.gconst ^ gmap(S, base);
+            }
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncthreads();
+            phases(tile0, 0ull, [] {});
+            double2 sv[NR];
+#pragma unroll
+            for (int k = 0; k < NR; ++k) sv[k] = lds128(slot_addr(a, swz((uint32_t)k << TB)));
+            const uint64_t ab = S.gperm ? (s_ab ^ g_t) : 0ull;
+            __syncthreads();
+            const uint64_t cbase = base;
+            t = s_u[par];
+            par ^= 1;
+            base = insert_zero_bits_dyn((uint64_t)t, S.tb, T);
+            if (t < p.ntiles) fetch(base, tile0);
+            if (S.gperm) {
+#pragma unroll
+                for (int k = 0; k < NR; ++k) {
+                    double2 *dst = p.y + (ab ^ gmap(S, kdep(k)));
+                    if (p.gstore == 0) st_stream(dst, sv[k]);
+                    else if (p.gstore == 1) st_plain(dst, sv[k]);
+                    else st_hint(dst, sv[k], policy_evict_last());
+                }
+            } else {
+                double2 *dst = p.y + (cbase + t_off);
+#pragma unroll
+                for (int k = 0; k < NR; ++k) st_stream(dst + kdep(k), sv[k]);
+            }
+        }
+        units_done();
+        return;
+    }
     uint64_t base = insert_zero_bits_dyn((uint64_t)blockIdx.x, S.tb, T);
     if ((int64_t)blockIdx.x < p.ntiles) fetch(base, tile0);
     uint32_t buf = tile0;
