@@ -14,12 +14,14 @@ def _perm_gate(q):
     return m
 
 
-def fuzz_circuit(seed):
+def fuzz_circuit(seed, n=None):
     """Seeded random circuit over every gate kind the fused scheduler routes
     differently; returns (n, placements, rng) -- also used by the CPU
-    codegen test of the specialised passes (test_jit_cpu.py)."""
+    codegen test of the specialised passes (test_jit_cpu.py).  `n` forces
+    the state size (default: drawn from 11..18)."""
     rng = np.random.default_rng(1000 + seed)
-    n = int(rng.integers(11, 19))
+    drawn = int(rng.integers(11, 19))
+    n = drawn if n is None else int(n)
     names1 = ["h", "x", "y", "z", "s", "t", "rx", "ry", "rz", "u3", "sdg"]
     pls = []
     for _ in range(int(rng.integers(40, 90))):

@@ -702,3 +702,28 @@ def test_fused_jit_layer_n24_async(cmul):
     second = D.run_gates(x0, pls, cmul_mode=cmul).amps
     assert _jit_stats()["launches"] > before["launches"]
     assert np.array_equal(first, want) and np.array_equal(second, want)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_fused_dynamic_unit_order_is_bitwise(cmul, seed):
+    """The dynamic unit order (fused_dyn: units handed out by a global
+    counter, active when every CTA runs several units) changes only which
+    CTA computes which unit: at n=24 the scheduler fuzz circuits -- pair
+    store, plain pair and scatter passes, both numerics -- give bitwise the
+    same state with it on and off, and (reference rounding) the gate-by-gate
+    state."""
+    n, pls, rng = fuzz_circuit(seed, n=24)
+    x0 = D.StateVector(n, W.random_state(rng, 2**n))
+    want = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=0).amps
+    try:
+        for mode in (cmul, L.CMUL_CONTRACT):
+            L.tune("fused_dyn", 0)
+            static = D.run_gates(x0, pls, cmul_mode=mode).amps
+            L.tune("fused_dyn", 1)
+            dyn = D.run_gates(x0, pls, cmul_mode=mode).amps
+            again = D.run_gates(x0, pls, cmul_mode=mode).amps  # fresh counter slots, same result
+            assert np.array_equal(static, dyn) and np.array_equal(dyn, again), (seed, mode)
+            if mode == cmul:
+                assert np.array_equal(dyn, want), seed
+    finally:
+        L.tune("fused_dyn", 1)
