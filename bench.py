@@ -655,8 +655,11 @@ def sharded_gates(args, D, L, W, torch, dist, n, world, x, s, dev):
     peak, _ = measured_peak()
     runs = {}
     g_launches = 0
-    for remap in (False, True):
-        st.apply_placements(pls, remap=remap)  # warm-up: plans, specialised passes
+    # plain and remapped with reference rounding (bitwise), then the
+    # contracted arithmetic (1e-12 tolerance; commutation-aware scheduling of
+    # the local runs) without remapping
+    for remap, mode in ((False, None), (True, None), (False, L.CMUL_CONTRACT)):
+        st.apply_placements(pls, cmul_mode=mode, remap=remap)  # warm-up: plans, specialised passes
         L.call("diaq_jit_wait", -1.0)
         torch.cuda.synchronize()
         dist.barrier()
@@ -667,7 +670,7 @@ def sharded_gates(args, D, L, W, torch, dist, n, world, x, s, dev):
         gl0 = L.launch_count()
         ge0.record(s)
         for _ in range(g_steps):
-            st.apply_placements(pls, remap=remap)
+            st.apply_placements(pls, cmul_mode=mode, remap=remap)
         ge1.record(s)
         torch.cuda.synchronize()
         launches = L.launch_count() - gl0
@@ -677,12 +680,12 @@ def sharded_gates(args, D, L, W, torch, dist, n, world, x, s, dev):
         # per-rank HBM: every launch sweeps the rank's shard (32 B per local
         # amplitude: read + write); partner reads arrive over NVLink, not HBM
         hbm_bytes = passes * 32 * 2**lb
-        runs["remap" if remap else "plain"] = {
+        runs["contracted" if mode else ("remap" if remap else "plain")] = {
             "gates_per_s": round(len(pls) * g_steps / (g_ms * 1e-3), 2), "s_per_circuit": round(g_ms / g_steps / 1e3, 4),
             "launches_per_circuit": round(passes, 1), "cross_shard_ops": stats.get("exchanged", 0),
             "swaps": stats.get("swaps", 0), "partner_bytes_read_per_rank": stats.get("bytes_received", 0),
             "hbm_frac_per_rank": round(hbm_bytes / (g_ms / g_steps * 1e-3) / 1e9 / peak, 4), "stats": stats}
-        if not remap:
+        if not remap and mode is None:
             g_launches = launches
             plain_ms, plain_steps = g_ms, g_steps
     norm = st.norm()

@@ -103,6 +103,7 @@ def test_bench_multi_rank_paths_on_one_gpu(tmp_path):
     # the default N>1 gate measurement is the sharded config-5 circuit
     assert g["mode"].startswith("config 5") and g["circuit_qubits"] == 17 and g["transport"] == "peer"
     assert g["runs"]["plain"]["cross_shard_ops"] > 0 and g["runs"]["remap"]["swaps"] > 0
+    assert g["runs"]["contracted"]["gates_per_s"] > 0  # the contracted arithmetic on the sharded path
     assert g["norm_ok"] and abs(g["norm_after"] - 1.0) < 1e-10
 
 
