@@ -317,6 +317,10 @@ int diaq_trim_pool(void);
  * [4] shared-memory (generic) phases.  local_bits < n_bits: one rank's
  * shard, as diaq_run_gates_local. */
 int diaq_fused_plan(int n_bits, int local_bits, int ngates, const diaq_gate_t *gates, int tile_bits, int *stats);
+/* The same for the schedule a numerics mode runs: DIAQ_CMUL_CONTRACT takes
+ * the commutation-aware schedule when it needs fewer passes. */
+int diaq_fused_plan_mode(int n_bits, int local_bits, int ngates, const diaq_gate_t *gates, int tile_bits,
+                         int cmul_mode, int *stats);
 
 /* ---- specialised fused passes (NVRTC) ------------------------------------
  * Each tiled pass is also compiled at run time with its structure (tile

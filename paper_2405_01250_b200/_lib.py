@@ -102,6 +102,7 @@ _SIGS = {
     "diaq_run_gates_fused": ([_INT, _INT, ctypes.POINTER(Gate), _P, _INT, _INT, _P, _P, _P], _INT),
     "diaq_trim_pool": ([], _INT),
     "diaq_fused_plan": ([_INT, _INT, _INT, ctypes.POINTER(Gate), _INT, _P], _INT),
+    "diaq_fused_plan_mode": ([_INT, _INT, _INT, ctypes.POINTER(Gate), _INT, _INT, _P], _INT),
     "diaq_jit_wait": ([ctypes.c_double], _INT),
     "diaq_jit_stats": ([_P], _INT),
     "diaq_jit_last_error": ([], ctypes.c_char_p),

@@ -117,6 +117,9 @@ extern "C" int diaq_tune(const char *key, int64_t value) {
     else if (k == "fused_estore") t.fused_estore = (int)value;
     else if (k == "fused_reorder") t.fused_reorder = (int)value;
     else if (k == "fused_dyn") t.fused_dyn = (int)value;
+    else if (k == "fused_lookahead") t.fused_lookahead = (int)value;
+    else if (k == "fused_unit") t.fused_unit = (int)value;
+    else if (k == "fused_maxph") t.fused_maxph = (int)(value < 1 ? 1 : value);
     else if (k == "kron_flat") t.kron_flat = (int)value;
     else if (k == "kron_ctas_per_sm") t.kron_ctas_per_sm = (int)(value < 1 ? 1 : value);
     else return set_error(DIAQ_ERR_VALUE, "diaq_tune: unknown key %s", key);

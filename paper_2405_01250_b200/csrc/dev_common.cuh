@@ -157,6 +157,17 @@ __device__ __forceinline__ double2 cmac2_ri(double a, double2 x, double bi, doub
     return make_double2(__fma_rn(a, x.x, -__dmul_rn(bi, y.y)), __fma_rn(a, x.y, __dmul_rn(bi, y.x)));
 }
 
+// unit-diagonal rows (contracted rotations with the common diagonal entry
+// factored out of the pass, fused.cu unit forms): x + b y, 1 DFMA per part
+__device__ __forceinline__ double2 cmac1_r(double2 x, double b, double2 y) {
+    return make_double2(__fma_rn(b, y.x, x.x), __fma_rn(b, y.y, x.y));
+}
+
+// x + i bi y
+__device__ __forceinline__ double2 cmac1_i(double2 x, double bi, double2 y) {
+    return make_double2(__fma_rn(-bi, y.y, x.x), __fma_rn(bi, y.x, x.y));
+}
+
 // acc + a x (continuing a contracted chain)
 __device__ __forceinline__ double2 cfma_c(double2 a, double2 x, double2 acc) {
     return make_double2(__fma_rn(a.x, x.x, __fma_rn(-a.y, x.y, acc.x)), __fma_rn(a.x, x.y, __fma_rn(a.y, x.x, acc.y)));

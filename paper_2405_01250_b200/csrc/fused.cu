@@ -402,6 +402,9 @@ static thread_local bool t_no_gperm = false;
 // schedule with commutation-aware deferral (set for the contracted arithmetic;
 // part of the program key)
 static thread_local bool t_reorder = false;
+// contracted arithmetic: rotations in unit-diagonal form (unit_forms below;
+// part of the program key -- the coefficient tables differ)
+static thread_local bool t_unit = false;
 
 // thread bits of a tiled pass: 8 (256 threads; T = 11 -> R = 3, T = 12 -> R = 4)
 // or 7 (128 threads, T = 11, R = 4: a phase covers one more qubit, so a pass
@@ -447,6 +450,39 @@ static void spread_lane_bits(Phase &ph, int T, int R) {
     for (int i = 0; i < nt; ++i) ph.tpos[i] = out[i];
 }
 
+// Contracted arithmetic: a rotation [[a, b], [c, a]] with a real (RX, RY)
+// is applied as [[1, b/a], [c/a, 1]] -- one DFMA per part, 2 FP64
+// operations per amplitude instead of 4 -- and the scalar a is carried to
+// the pass's last such gate, which keeps its form with every entry scaled
+// by the product of the scalars (a scalar commutes with every gate of the
+// pass, so the pass computes the same operator; the rounding differs, as
+// everywhere under this arithmetic).  |b/a| stays below 2^10.
+static void unit_forms(PassPlan &ps) {
+    std::vector<size_t> el;
+    for (size_t gi = 0; gi < ps.gates.size(); ++gi) {
+        const RegGate &G = ps.gates[gi];
+        if (G.op != 1 || (G.shape != 1 && G.shape != 2)) continue;
+        const double2 *c = &ps.pk.coef[(size_t)G.coef_off];
+        if ((ps.pk.nz[(size_t)G.nz_off] & ps.pk.nz[(size_t)G.nz_off + 1] & 3u) != 3u) continue;
+        if (c[0].x != c[3].x || !(fabs(c[0].x) >= 0x1p-10) || !(fabs(c[0].x) <= 1.0)) continue;
+        el.push_back(gi);
+    }
+    if (el.size() < 2) return;
+    double scale = 1.0;
+    for (size_t e = 0; e + 1 < el.size(); ++e) {
+        RegGate &G = ps.gates[el[e]];
+        double2 *c = &ps.pk.coef[(size_t)G.coef_off];
+        const double a = c[0].x;
+        scale *= a;
+        c[1] = make_double2(c[1].x / a, c[1].y / a);
+        c[2] = make_double2(c[2].x / a, c[2].y / a);
+        c[0] = c[3] = make_double2(1.0, 0.0);
+        G.shape = (int8_t)(G.shape + 2);
+    }
+    double2 *c = &ps.pk.coef[(size_t)ps.gates[el.back()].coef_off];
+    for (int e = 0; e < 4; ++e) c[e] = make_double2(c[e].x * scale, c[e].y * scale);
+}
+
 static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t *gates, int T, int R,
                          std::vector<PassPlan> &plan, bool allow_d2) {
     const bool reorder = t_reorder;
@@ -470,7 +506,6 @@ static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t 
     }
     std::vector<int> members;
     std::vector<char> inb(64, 0);
-    std::vector<int> pbase;  // non-mixing operand bits of the pass's permutation gates (fold bound)
     int nb = 0;
     int ncoef = 0, nnz = 0;  // the pass's coefficient / mask table entries (kernel parameter bound)
     size_t tail = SIZE_MAX;  // members[tail..]: permutation run folded over the whole index (final store)
@@ -480,7 +515,6 @@ static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t 
         nb = 0;
         for (int b = 0; b < low; ++b) { inb[b] = 1; ++nb; }
         members.clear();
-        pbase.clear();
         ncoef = nnz = 0;
         tail = SIZE_MAX;
     };
@@ -693,10 +727,27 @@ static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t 
         }
         if ((int)ps.phases.size() > kMaxPhases || (int)ps.gates.size() > kMaxPassGates)
             return set_error(DIAQ_ERR_VALUE, "fused pass too long");
+        if (t_unit) unit_forms(ps);
         plan.push_back(ps);
         return DIAQ_OK;
     };
-    reset();
+    // per-gate facts the sweep needs (once per schedule)
+    std::vector<uint32_t> gmix((size_t)ngates, 0);
+    std::vector<uint64_t> gqm((size_t)ngates, 0);
+    for (int i = 0; i < ngates; ++i) {
+        const diaq_gate_t &gt = gates[i];
+        if (gt.k < 1 || gt.k > 5) return set_error(DIAQ_ERR_UNSUPPORTED, "gate width %d outside 1..5", gt.k);
+        gmix[(size_t)i] = mixing_mask(gt.k, gt.g);
+        for (int j = 0; j < gt.k; ++j) {
+            if (gt.shifts[j] < 0 || gt.shifts[j] >= n_total || gt.shifts[j] >= 64)
+                return set_error(DIAQ_ERR_SHAPE, "gate shift %d outside state of %d qubits", gt.shifts[j], n_total);
+            gqm[(size_t)i] |= 1ull << gt.shifts[j];
+            if (((gmix[(size_t)i] >> j) & 1u) && gt.shifts[j] >= n_bits)
+                return set_error(DIAQ_ERR_VALUE, "gate mixes global bit %d: it needs the partner shard", gt.shifts[j]);
+        }
+    }
+    const uint64_t allq = n_total >= 64 ? ~0ull : ((1ull << n_total) - 1ull);
+    // One sweep over `pending` builds one pass (program order: every pass).
     // reorder (contracted arithmetic only): a gate that does not fit the open
     // pass is deferred instead of closing it, and the scan goes on -- later
     // gates on other qubits commute with it and may still join.  Any gate
@@ -704,139 +755,296 @@ static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t 
     // qubit is kept), and the deferred gates, in order, form the next sweep.
     // Reordering gates on disjoint qubits is exact in real arithmetic but
     // changes the rounding, so the bitwise modes keep the program order.
-    std::vector<int> pending((size_t)ngates);
-    for (int i = 0; i < ngates; ++i) pending[(size_t)i] = i;
-    while (!pending.empty()) {
-    std::vector<int> deferred;
-    uint64_t blocked = 0;
-    for (const int i : pending) {
-        const diaq_gate_t &gt = gates[i];
-        if (gt.k < 1 || gt.k > 5) return set_error(DIAQ_ERR_UNSUPPORTED, "gate width %d outside 1..5", gt.k);
-        uint64_t qmask = 0;
-        for (int j = 0; j < gt.k; ++j)
-            if (gt.shifts[j] >= 0 && gt.shifts[j] < 64) qmask |= 1ull << gt.shifts[j];
-        auto defer = [&]() {
-            deferred.push_back(i);
-            blocked |= qmask;
-        };
-        if (reorder && (qmask & blocked)) {
-            defer();
-            continue;
-        }
-        const uint32_t mix = mixing_mask(gt.k, gt.g);
-        int kin = 0, kout = 0, add = 0;
-        for (int j = 0; j < gt.k; ++j) {
-            if (gt.shifts[j] < 0 || gt.shifts[j] >= n_total)
-                return set_error(DIAQ_ERR_SHAPE, "gate shift %d outside state of %d qubits", gt.shifts[j], n_total);
-            if ((mix >> j) & 1u) {
-                if (gt.shifts[j] >= n_bits)
-                    return set_error(DIAQ_ERR_VALUE, "gate mixes global bit %d: it needs the partner shard", gt.shifts[j]);
-                ++kin;
-                add += inb[gt.shifts[j]] ? 0 : 1;
-            } else {
-                ++kout;
+    //   preset != 0 (lookahead): the pass's tile bits are fixed before the
+    // sweep, and a gate whose mixing bits are not among them is deferred.
+    //   dry: a lookahead trial -- nothing is flushed or emitted; *score is
+    // the value of the pass this sweep would build.
+    // reorder: phases per pass are capped where the shared-memory round trips
+    // stop hiding under the pass's HBM time (each phase moves every amplitude
+    // through shared memory once: ncu r02u shows deep passes at 73-81% of the
+    // shared-memory pipe); a gate that would open one more phase is deferred
+    const int maxph = reorder ? std::max(1, std::min(tuning().fused_maxph, kMaxPhases)) : kMaxPhases;
+    uint64_t preset = 0;
+    uint64_t tailq = 0;      // qubits of the tail's permutation gates
+    int nrec = 0;            // gate records of the open pass (its non-permutation members)
+    // phases the open pass needs so far -- the count flush() will arrive at
+    // (exact without dense two-qubit gates, an upper bound with them)
+    int nph = 0;
+    bool ph_open = false, ph_generic = false, has_d2 = false;
+    uint64_t ph_used = 0;
+    std::vector<int> run_base;  // operands outside the tile of the open permutation run (one folded map)
+    auto reset2 = [&]() {
+        reset();
+        if (preset) {
+            nb = 0;
+            for (int b = 0; b < 64; ++b) {
+                inb[b] = (char)((preset >> b) & 1ull);
+                nb += inb[b];
             }
         }
-        const bool pg = perm[(size_t)i].ok;
-        if (!pg && tail != SIZE_MAX) {  // a gate after a global permutation tail opens the next pass
-            if (reorder) {
+        tailq = 0;
+        nrec = nph = 0;
+        ph_open = ph_generic = has_d2 = false;
+        ph_used = 0;
+        run_base.clear();
+    };
+    auto sweep = [&](const std::vector<int> &pending, std::vector<int> *deferred_out, bool dry, int *score) -> int {
+        uint64_t blocked = 0;
+        int sc = 0;
+        const bool fixed = preset != 0;
+        for (size_t pi = 0; pi < pending.size(); ++pi) {
+            const int i = pending[pi];
+            if (reorder && blocked == allq) {  // nothing further can join
+                if (deferred_out) deferred_out->insert(deferred_out->end(), pending.begin() + (long)pi, pending.end());
+                break;
+            }
+            const diaq_gate_t &gt = gates[i];
+            const uint64_t qmask = gqm[(size_t)i];
+            auto defer = [&]() {
+                if (deferred_out) deferred_out->push_back(i);
+                blocked |= qmask;
+            };
+            if (reorder && (qmask & blocked)) {
                 defer();
                 continue;
             }
-            int rc = flush();
-            if (rc) return rc;
-            reset();
-            add = 0;
-            for (int j = 0; j < gt.k; ++j)
-                if (((mix >> j) & 1u) && !inb[gt.shifts[j]]) ++add;
-        }
-        if (pg && !members.empty() && tuning().fused_gperm && !t_no_gperm) {
-            // a permutation that does not fit the tile (or follows one that did
-            // not) joins the pass's global tail instead of opening a pass
-            int padd0 = 0;
-            for (int j = 0; j < gt.k; ++j)
-                if (!((mix >> j) & 1u) && std::find(pbase.begin(), pbase.end(), gt.shifts[j]) == pbase.end()) ++padd0;
-            if (tail != SIZE_MAX || kin > T - low || nb + add > T || (int)pbase.size() + padd0 > kMaxPermBase ||
-                (int)members.size() >= std::min(kMaxPassGates, kMaxPhases)) {
-                // the tail must keep 128-byte rows whole (its store writes whole
-                // rows): no output bit above the row may depend on a row bit,
-                // else partial-sector writes cost read-modify-write traffic
-                GlobalAffine trial;
-                if (tail == SIZE_MAX) trial.init(n_bits);
-                else trial = tail_map;
-                bool rows = trial.fold(gt, perm[(size_t)i]);
-                for (int o = low; o < n_bits && rows && tuning().fused_gperm_rows; ++o)
-                    if (trial.row[o].m & ((1ull << low) - 1ull)) rows = false;
-                if (rows) {
-                    tail_map = trial;
-                    if (tail == SIZE_MAX) tail = members.size();
-                    members.push_back(i);
-                    continue;
+            const uint32_t mix = gmix[(size_t)i];
+            uint64_t mixq = 0;
+            int kin = 0, kout = 0, add = 0;
+            for (int j = 0; j < gt.k; ++j) {
+                if ((mix >> j) & 1u) {
+                    ++kin;
+                    add += inb[gt.shifts[j]] ? 0 : 1;
+                    mixq |= 1ull << gt.shifts[j];
+                } else {
+                    ++kout;
                 }
-                // it opens the next pass, where its bits can join the tile
+            }
+            const bool pg = perm[(size_t)i].ok;
+            // reorder: an open pass never closes inside a sweep; a fixed tile also defers from an empty pass
+            const bool can_defer = reorder && (!members.empty() || fixed || dry);
+            bool before_tail = false;
+            if (!pg && tail != SIZE_MAX) {  // a gate after a global permutation tail opens the next pass ...
                 if (reorder) {
+                    if (qmask & tailq) {
+                        defer();
+                        continue;
+                    }
+                    before_tail = true;  // ... unless it shares no qubit with the tail: it commutes exactly, and joins the body
+                } else {
+                    int rc = flush();
+                    if (rc) return rc;
+                    reset2();
+                    add = kin;
+                    for (int j = 0; j < gt.k; ++j)
+                        if (((mix >> j) & 1u) && inb[gt.shifts[j]]) --add;
+                }
+            }
+            // operands outside the tile this permutation adds to the open run's folded map
+            int padd = 0;
+            if (pg)
+                for (int j = 0; j < gt.k; ++j)
+                    if (!((mix >> j) & 1u) && !inb[gt.shifts[j]] &&
+                        std::find(run_base.begin(), run_base.end(), gt.shifts[j]) == run_base.end())
+                        ++padd;
+            // phases after this gate
+            const bool isd2 = d2[(size_t)i] != 0;
+            const bool fastg = fast[(size_t)i] || isd2;
+            int nph_after = nph;
+            if (pg) {
+                nph_after += ph_generic ? 1 : 0;
+            } else if (!fastg) {
+                nph_after += 1;
+            } else if (has_d2 || isd2) {
+                nph_after += 1;
+            } else if (!(ph_open && __builtin_popcountll(ph_used | mixq) <= R)) {
+                nph_after += 1;
+            }
+            const bool room = nrec + (pg ? 0 : 1) <= kMaxPassGates && nph_after <= maxph;
+            if (pg && !members.empty() && tuning().fused_gperm && !t_no_gperm) {
+                // a permutation that does not fit the tile (or follows one that did
+                // not) joins the pass's global tail instead of opening a pass
+                if (tail != SIZE_MAX || kin > T - low || nb + add > T || (int)run_base.size() + padd > kMaxPermBase || !room) {
+                    // the tail must keep 128-byte rows whole (its store writes whole
+                    // rows): no output bit above the row may depend on a row bit,
+                    // else partial-sector writes cost read-modify-write traffic
+                    GlobalAffine trial;
+                    if (tail == SIZE_MAX) trial.init(n_bits);
+                    else trial = tail_map;
+                    bool rows = trial.fold(gt, perm[(size_t)i]);
+                    for (int o = low; o < n_bits && rows && tuning().fused_gperm_rows; ++o)
+                        if (trial.row[o].m & ((1ull << low) - 1ull)) rows = false;
+                    if (rows) {
+                        tail_map = trial;
+                        if (tail == SIZE_MAX) tail = members.size();
+                        members.push_back(i);
+                        tailq |= qmask;
+                        sc += 1;
+                        continue;
+                    }
+                    // it opens the next pass, where its bits can join the tile
+                    if (reorder) {
+                        defer();
+                        continue;
+                    }
+                    int rc = flush();
+                    if (rc) return rc;
+                    reset2();
+                    add = kin;
+                    for (int j = 0; j < gt.k; ++j)
+                        if (((mix >> j) & 1u) && inb[gt.shifts[j]]) --add;
+                    padd = 0;
+                    for (int j = 0; j < gt.k; ++j)
+                        if (!((mix >> j) & 1u) && !inb[gt.shifts[j]]) ++padd;
+                    nph_after = 0;
+                }
+            }
+            if (pg ? (kin > T - low) : (kin > kMaxRegKin || kin > R || kout > kMaxSel)) {  // standalone pass
+                if (can_defer) {  // its own pass, after the open one
                     defer();
                     continue;
                 }
                 int rc = flush();
                 if (rc) return rc;
-                reset();
-                add = 0;
+                reset2();
+                PassPlan ps;
+                ps.members = {i};
+                plan.push_back(ps);
+                continue;
+            }
+            const int gcoef = pg ? 0 : (1 << kout) << (2 * kin), gnz = pg ? 0 : (1 << kout) << kin;
+            if (nb + add > T || nrec + (pg ? 0 : 1) > kMaxPassGates || nph_after > maxph ||
+                (int)run_base.size() + padd > kMaxPermBase || ncoef + gcoef > kMaxCoef || nnz + gnz > kMaxNz) {
+                if (can_defer) {
+                    defer();
+                    continue;
+                }
+                int rc = flush();
+                if (rc) return rc;
+                reset2();
+                before_tail = false;
+                add = kin;
                 for (int j = 0; j < gt.k; ++j)
-                    if (((mix >> j) & 1u) && !inb[gt.shifts[j]]) ++add;
+                    if (((mix >> j) & 1u) && inb[gt.shifts[j]]) --add;
+            }
+            for (int j = 0; j < gt.k; ++j)
+                if (((mix >> j) & 1u) && !inb[gt.shifts[j]]) { inb[gt.shifts[j]] = 1; ++nb; }
+            // bookkeeping as flush() will build the phases
+            if (pg) {
+                for (int j = 0; j < gt.k; ++j)
+                    if (!((mix >> j) & 1u) && !inb[gt.shifts[j]] &&
+                        std::find(run_base.begin(), run_base.end(), gt.shifts[j]) == run_base.end())
+                        run_base.push_back(gt.shifts[j]);
+                if (ph_generic) ++nph;  // an empty register phase carries the run
+                ph_generic = false;
+                ph_open = false;
+                sc += 1;
+            } else {
+                run_base.clear();  // the next permutation run is a new map
+                ++nrec;
+                if (!fastg) {
+                    ++nph;
+                    ph_open = false;
+                    ph_generic = true;
+                } else {
+                    ph_generic = false;
+                    if (has_d2 || isd2) {
+                        ++nph;
+                        has_d2 = true;
+                        ph_open = false;
+                    } else if (ph_open && __builtin_popcountll(ph_used | mixq) <= R) {
+                        ph_used |= mixq;
+                    } else {
+                        ++nph;
+                        ph_open = true;
+                        ph_used = mixq;
+                    }
+                }
+                sc += kin > 0 ? 4 : 1;
+            }
+            ncoef += gcoef;
+            nnz += gnz;
+            if (before_tail) {
+                members.insert(members.begin() + (long)tail, i);
+                ++tail;
+            } else {
+                members.push_back(i);
             }
         }
-        if (pg ? (kin > T - low) : (kin > kMaxRegKin || kin > R || kout > kMaxSel)) {  // standalone pass
-            if (reorder && !members.empty()) {  // its own pass, after the open one
-                defer();
-                continue;
-            }
-            int rc = flush();
-            if (rc) return rc;
-            reset();
-            PassPlan ps;
-            ps.members = {i};
-            plan.push_back(ps);
-            continue;
-        }
-        // non-mixing operands of permutation gates may end up outside the tile;
-        // the folded maps carry at most kMaxPermBase of them
-        int padd = 0;
-        if (pg)
-            for (int j = 0; j < gt.k; ++j)
-                if (!((mix >> j) & 1u) && std::find(pbase.begin(), pbase.end(), gt.shifts[j]) == pbase.end()) ++padd;
-        const int gcoef = pg ? 0 : (1 << kout) << (2 * kin), gnz = pg ? 0 : (1 << kout) << kin;
-        // phases per pass are bounded too: a pass can need up to one phase per gate
-        if (nb + add > T || (int)members.size() >= std::min(kMaxPassGates, kMaxPhases) ||
-            (int)pbase.size() + padd > kMaxPermBase || ncoef + gcoef > kMaxCoef || nnz + gnz > kMaxNz) {
-            if (reorder && !members.empty()) {
-                defer();
-                continue;
-            }
-            int rc = flush();
-            if (rc) return rc;
-            reset();
-            add = 0;
-            for (int j = 0; j < gt.k; ++j)
-                if (((mix >> j) & 1u) && !inb[gt.shifts[j]]) ++add;
-        }
-        for (int j = 0; j < gt.k; ++j)
-            if (((mix >> j) & 1u) && !inb[gt.shifts[j]]) { inb[gt.shifts[j]] = 1; ++nb; }
-        if (pg)
-            for (int j = 0; j < gt.k; ++j)
-                if (!((mix >> j) & 1u) && std::find(pbase.begin(), pbase.end(), gt.shifts[j]) == pbase.end())
-                    pbase.push_back(gt.shifts[j]);
-        ncoef += gcoef;
-        nnz += gnz;
-        members.push_back(i);
+        if (score) *score = sc;
+        return DIAQ_OK;
+    };
+    std::vector<int> pending((size_t)ngates);
+    for (int i = 0; i < ngates; ++i) pending[(size_t)i] = i;
+    if (!reorder) {
+        reset2();
+        int rc = sweep(pending, nullptr, false, nullptr);
+        if (rc) return rc;
+        return flush();
     }
-    if (!reorder) break;
-    int rc = flush();
-    if (rc) return rc;
-    reset();
-    pending.swap(deferred);
+    // Lookahead (reorder only): first fit takes tile bits in the order the
+    // gates ask for them; a pass is worth more when its tile holds qubits
+    // whose CX partners are in the tile too, so their next layers' gates can
+    // join.  Start from the first-fit tile and exchange one bit at a time
+    // while the trial sweep's score grows.
+    const bool look = tuning().fused_lookahead != 0 && n_bits > T;
+    auto trial = [&](uint64_t bits) -> int {
+        int sc = 0;
+        preset = bits;
+        reset2();
+        if (sweep(pending, nullptr, true, &sc) != DIAQ_OK) sc = -1;
+        return sc;
+    };
+    while (!pending.empty()) {
+        uint64_t choice = 0;
+        if (look) {
+            const int sc0 = trial(0);
+            uint64_t bits = 0;
+            int nbits = 0;
+            for (int b = 0; b < 64; ++b)
+                if (inb[b]) { bits |= 1ull << b; ++nbits; }
+            for (int b = 0; nbits < T && b < n_bits; ++b)
+                if (!((bits >> b) & 1ull)) { bits |= 1ull << b; ++nbits; }
+            int best = nbits == T ? trial(bits) : -1;
+            bool improved = best >= 0;
+            for (int it = 0; improved && it < 64; ++it) {
+                improved = false;
+                for (int out = low; out < n_bits && !improved; ++out) {
+                    if (!((bits >> out) & 1ull)) continue;
+                    for (int in = low; in < n_bits && !improved; ++in) {
+                        if ((bits >> in) & 1ull) continue;
+                        const uint64_t cand = (bits & ~(1ull << out)) | (1ull << in);
+                        const int sc = trial(cand);
+                        if (sc > best) {
+                            best = sc;
+                            bits = cand;
+                            improved = true;
+                        }
+                    }
+                }
+            }
+            if (best > sc0) choice = bits;
+        }
+        std::vector<int> deferred;
+        preset = choice;
+        reset2();
+        const size_t plan0 = plan.size();
+        int rc = sweep(pending, &deferred, false, nullptr);
+        if (rc) return rc;
+        if (members.empty() && plan.size() == plan0) {
+            if (!choice) return set_error(DIAQ_ERR_VALUE, "fused schedule made no progress");
+            deferred.clear();  // the fixed tile admitted nothing: first fit
+            preset = 0;
+            reset2();
+            rc = sweep(pending, &deferred, false, nullptr);
+            if (rc) return rc;
+        }
+        rc = flush();
+        if (rc) return rc;
+        pending.swap(deferred);
     }
-    return flush();
+    preset = 0;
+    return DIAQ_OK;
 }
 
 static int schedule(int n_bits, int n_total, int ngates, const diaq_gate_t *gates, int T, int R,
@@ -914,7 +1122,8 @@ static std::vector<char> program_key(int n_total, int n_bits, int T, int ngates,
         key.insert(key.end(), c, c + n);
     };
     // every tuning switch the schedule depends on is part of the key
-    const int head[16] = {n_total, n_bits, T, pass_tbits(), ngates, (int)t_reorder, tuning().fused_perm,
+    const int head[18] = {n_total, n_bits, T, pass_tbits(), ngates, (int)t_reorder, (int)t_unit,
+                          t_reorder ? tuning().fused_lookahead + 256 * tuning().fused_maxph : 0, tuning().fused_perm,
                           tuning().fused_gperm && !t_no_gperm, tuning().fused_seq, tuning().fused_dense2,
                           tuning().fused_gperm_rows, tuning().fused_pair_store, tuning().fused_bank_spread, tuning().fused_plain_pair, tuning().fused_ppipe, tuning().fused_dstore};
     put(head, sizeof(head));
@@ -1184,6 +1393,7 @@ static int run_fused(int n_total, int n_bits, int64_t rank, int ngates, const di
     if (cmul_mode < DIAQ_CMUL_PLAIN || cmul_mode > DIAQ_CMUL_CONTRACT)
         return set_error(DIAQ_ERR_VALUE, "diaq_run_gates_fused: cmul_mode %d", cmul_mode);
     t_reorder = cmul_mode == DIAQ_CMUL_CONTRACT && tuning().fused_reorder;
+    t_unit = cmul_mode == DIAQ_CMUL_CONTRACT && tuning().fused_unit;
     const bool sharded = n_total > n_bits;
     cudaStream_t s = (cudaStream_t)stream;
     // tile_bits 12 -> 16 amplitudes per thread (R = 4), 11 -> 8 (R = 3); 256
@@ -1375,9 +1585,11 @@ extern "C" int diaq_run_gates_fused(int n_bits, int ngates, const diaq_gate_t *g
     return run_fused(n_bits, n_bits, 0, ngates, gates, state, cmul_mode, tile_bits, events, npasses, stream);
 }
 
-extern "C" int diaq_fused_plan(int n_bits, int local_bits, int ngates, const diaq_gate_t *gates, int tile_bits,
-                               int *stats) {
+extern "C" int diaq_fused_plan_mode(int n_bits, int local_bits, int ngates, const diaq_gate_t *gates, int tile_bits,
+                                    int cmul_mode, int *stats) {
     if (ngates < 0 || (ngates > 0 && !gates) || !stats) return set_error(DIAQ_ERR_VALUE, "diaq_fused_plan: bad arguments");
+    if (cmul_mode < DIAQ_CMUL_PLAIN || cmul_mode > DIAQ_CMUL_CONTRACT)
+        return set_error(DIAQ_ERR_VALUE, "diaq_fused_plan: cmul_mode %d", cmul_mode);
     if (local_bits < 1 || local_bits > n_bits) return set_error(DIAQ_ERR_SHAPE, "local_bits %d invalid", local_bits);
     const int T = (tile_bits >= kThreadBits + 4 && pass_tbits() == 8) ? kThreadBits + 4 : kThreadBits + 3;
     for (int i = 0; i < 5; ++i) stats[i] = 0;
@@ -1387,8 +1599,17 @@ extern "C" int diaq_fused_plan(int n_bits, int local_bits, int ngates, const dia
     }
     std::vector<PassPlan> plan;
     t_reorder = false;  // the program-order schedule (the bitwise modes')
-    const int rc = schedule(local_bits, n_bits, ngates, gates, T, T - pass_tbits(), plan);
+    t_unit = cmul_mode == DIAQ_CMUL_CONTRACT && tuning().fused_unit;
+    int rc = schedule(local_bits, n_bits, ngates, gates, T, T - pass_tbits(), plan);
     if (rc) return rc;
+    if (cmul_mode == DIAQ_CMUL_CONTRACT && tuning().fused_reorder) {  // as run_fused: reordered only when it saves passes
+        std::vector<PassPlan> re;
+        t_reorder = true;
+        rc = schedule(local_bits, n_bits, ngates, gates, T, T - pass_tbits(), re);
+        t_reorder = false;
+        if (rc) return rc;
+        if (re.size() < plan.size()) plan.swap(re);
+    }
     if (getenv("DIAQ_PLAN_DEBUG")) debug_plan(plan);
     for (const PassPlan &ps : plan) {
         ++stats[0];
@@ -1403,6 +1624,11 @@ extern "C" int diaq_fused_plan(int n_bits, int local_bits, int ngates, const dia
     return DIAQ_OK;
 }
 
+extern "C" int diaq_fused_plan(int n_bits, int local_bits, int ngates, const diaq_gate_t *gates, int tile_bits,
+                               int *stats) {
+    return diaq_fused_plan_mode(n_bits, local_bits, ngates, gates, tile_bits, DIAQ_CMUL_PLAIN, stats);
+}
+
 // Host-only: schedule the program and compile its specialised passes now
 // (NVRTC, no device); *seconds the compile time, *kernels the pass count.
 extern "C" int diaq_fused_jit_compile(int n_bits, int local_bits, int ngates, const diaq_gate_t *gates, int tile_bits,
@@ -1412,6 +1638,7 @@ extern "C" int diaq_fused_jit_compile(int n_bits, int local_bits, int ngates, co
     if (local_bits < 1 || local_bits > n_bits) return set_error(DIAQ_ERR_SHAPE, "local_bits %d invalid", local_bits);
     if (cmul_mode < 0 || cmul_mode > 2) return set_error(DIAQ_ERR_VALUE, "cmul_mode %d", cmul_mode);
     t_reorder = cmul_mode == DIAQ_CMUL_CONTRACT && tuning().fused_reorder;
+    t_unit = cmul_mode == DIAQ_CMUL_CONTRACT && tuning().fused_unit;
     const int T = (tile_bits >= kThreadBits + 4 && pass_tbits() == 8) ? kThreadBits + 4 : kThreadBits + 3;
     int rc = DIAQ_OK;
     std::shared_ptr<const Program> prog = build_program(n_bits, local_bits, T, ngates, gates, rc);

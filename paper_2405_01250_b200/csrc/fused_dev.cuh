@@ -46,7 +46,9 @@ struct RegGate {               // narrow fields: the records live in the kernel 
     // 2 diagonal with one selector
     int8_t op;
     // dense 1-qubit coefficient shape (host): 0 complex, 1 all entries real
-    // (RY, H), 2 real diagonal / imaginary off-diagonal (RX)
+    // (RY, H), 2 real diagonal / imaginary off-diagonal (RX); contracted
+    // arithmetic only: 3 / 4 = shapes 1 / 2 with both diagonal entries
+    // exactly 1 (their common value factored out of the pass, fused.cu)
     int8_t shape;
     int8_t mpos[kMaxRegKin];  // generic phases: tile positions of the mixing bits (relabelled order)
     int16_t coef_off;         // coef[coef_off + (b << 2kin) + r * 2^kin + c]   (pass-relative)
@@ -240,7 +242,13 @@ __device__ __forceinline__ void dense1_full(double2 (&v)[1 << R], const double2 
         const int j1 = j0 | (1 << B1);
         const double2 x0 = v[j0], x1 = v[j1];
         if constexpr (MODE == DIAQ_CMUL_CONTRACT) {  // 4 (shaped) / 8 FP64 operations per amplitude
-            if constexpr (SHAPE == 1) {
+            if constexpr (SHAPE == 3) {  // unit diagonal, real off-diagonal: 2 operations per amplitude
+                v[j0] = cmac1_r(x0, c01.x, x1);
+                v[j1] = cmac1_r(x1, c10.x, x0);
+            } else if constexpr (SHAPE == 4) {  // unit diagonal, imaginary off-diagonal
+                v[j0] = cmac1_i(x0, c01.y, x1);
+                v[j1] = cmac1_i(x1, c10.y, x0);
+            } else if constexpr (SHAPE == 1) {
                 v[j0] = cmac2_rr(c00.x, x0, c01.x, x1);
                 v[j1] = cmac2_rr(c10.x, x0, c11.x, x1);
             } else if constexpr (SHAPE == 2) {
@@ -250,10 +258,10 @@ __device__ __forceinline__ void dense1_full(double2 (&v)[1 << R], const double2 
                 v[j0] = cmac2_c(c00, x0, c01, x1);
                 v[j1] = cmac2_c(c10, x0, c11, x1);
             }
-        } else if constexpr (SHAPE == 1) {
+        } else if constexpr (SHAPE == 1 || SHAPE == 3) {
             v[j0] = cadd(cmul_re(c00.x, x0), cmul_re(c01.x, x1));
             v[j1] = cadd(cmul_re(c10.x, x0), cmul_re(c11.x, x1));
-        } else if constexpr (SHAPE == 2) {
+        } else if constexpr (SHAPE == 2 || SHAPE == 4) {
             v[j0] = cadd(cmul_re(c00.x, x0), cmul_im(c01.y, x1));
             v[j1] = cadd(cmul_im(c10.y, x0), cmul_re(c11.x, x1));
         } else {
@@ -267,6 +275,8 @@ template <int R, int B1, int MODE>
 __device__ __forceinline__ void dense1_shaped(double2 (&v)[1 << R], const double2 *c, int shape) {
     if (shape == 1) dense1_full<R, B1, MODE, 1>(v, c);
     else if (shape == 2) dense1_full<R, B1, MODE, 2>(v, c);
+    else if (MODE == DIAQ_CMUL_CONTRACT && shape == 3) dense1_full<R, B1, MODE, 3>(v, c);  // host: contracted only
+    else if (MODE == DIAQ_CMUL_CONTRACT && shape == 4) dense1_full<R, B1, MODE, 4>(v, c);
     else dense1_full<R, B1, MODE, 0>(v, c);
 }
 
@@ -1164,20 +1174,45 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
             }
             return;
         }
-        if (p.uctr && p.estore && !S.dstore) {  // dynamic unit order (see TileParams::uctr)
-            int64_t t = first_unit();
-            gb = insert_zero_bits_dyn((uint64_t)t, S.eb, T + 1);
-            if (t < nunits) fetch2(gb);
-            int par = 1;
-            while (t < nunits) {
-                if (tid == 0) s_u[par] = (int64_t)atomicAdd(p.uctr, 1ull);  // lands during the compute
+        if (S.dstore) {  // both halves store from registers; the next pair lands under B's last phase
+            if ((int64_t)blockIdx.x < nunits) fetch2(gb);
+            for (int64_t t = blockIdx.x; t < nunits; t += gridDim.x) {
+                const uint64_t ngb = ((gb | S.emask) + p.gstep) & ~S.emask;
+                const bool more = t + gridDim.x < nunits;
                 asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll 1
-                for (int h = 0; h < 2; ++h) {
-                    if (tid == 0) s_sbase = (gb | (h ? pbit : 0ull)) | p.gbase;
+                for (int h = 0; h < 2; ++h) {  // one copy of the phase code for both halves
+                    const uint64_t hb = gb | (h ? pbit : 0ull);
+                    if (tid == 0) s_sbase = hb | p.gbase;
                     __syncthreads();
-                    phases(h ? buf1 : tile0, 0ull, [] {});
+                    phases(h ? buf1 : tile0, hb, [&] {
+                        if (h && more) fetch2(ngb);
+                    });
                 }
+                gb = ngb;
+            }
+            return;
+        }
+        // One loop for both unit orders (one copy of the phase code per
+        // kernel: the unrolled gate program is most of its text): static
+        // (unit t + gridDim.x next) or dynamic (p.uctr: units handed out in
+        // order by a global counter, see TileParams::uctr).
+        const bool dyn = p.uctr && p.estore;
+        int64_t t = dyn ? first_unit() : (int64_t)blockIdx.x;
+        gb = insert_zero_bits_dyn((uint64_t)t, S.eb, T + 1);
+        if (t < nunits) fetch2(gb);
+        int par = 1;
+        while (t < nunits) {
+            if (dyn && tid == 0) s_u[par] = (int64_t)atomicAdd(p.uctr, 1ull);  // lands during the compute
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                if (tid == 0) s_sbase = (gb | (h ? pbit : 0ull)) | p.gbase;
+                __syncthreads();
+                phases(h ? buf1 : tile0, 0ull, [] {});
+            }
+            const uint64_t cgb = gb;
+            if (p.estore) {  // gather to registers, fetch the next pair, then store (see the pair store)
                 double2 sa[NR], sb[NR];
 #pragma unroll
                 for (int k = 0; k < NR; ++k) {
@@ -1186,8 +1221,7 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
                     sb[k] = lds128(slot_addr(a1, sl));
                 }
                 __syncthreads();
-                const uint64_t cgb = gb;
-                t = s_u[par];
+                t = dyn ? s_u[par] : t + gridDim.x;
                 par ^= 1;
                 gb = insert_zero_bits_dyn((uint64_t)t, S.eb, T + 1);
                 if (t < nunits) fetch2(gb);
@@ -1197,59 +1231,9 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
                     st_stream(dst + kdep(k), sa[k]);
                     st_stream(dst + (kdep(k) | pbit), sb[k]);
                 }
-            }
-            units_done();
-            return;
-        }
-        if ((int64_t)blockIdx.x < nunits) fetch2(gb);
-        if (S.dstore) {  // both halves store from registers; the next pair lands under B's last phase
-            for (int64_t t = blockIdx.x; t < nunits; t += gridDim.x) {
-                const uint64_t ngb = ((gb | S.emask) + p.gstep) & ~S.emask;
-                const bool more = t + gridDim.x < nunits;
-                asm volatile("cp.async.wait_group 0;" ::: "memory");
-                if (tid == 0) s_sbase = gb | p.gbase;
-                __syncthreads();
-                phases(tile0, gb, [] {});
-                if (tid == 0) s_sbase = (gb | pbit) | p.gbase;
-                __syncthreads();
-                phases(buf1, gb | pbit, [&] {
-                    if (more) fetch2(ngb);
-                });
-                gb = ngb;
-            }
-            return;
-        }
-        for (int64_t t = blockIdx.x; t < nunits; t += gridDim.x) {
-            const uint64_t ngb = ((gb | S.emask) + p.gstep) & ~S.emask;
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-#pragma unroll 1
-            for (int h = 0; h < 2; ++h) {
-                if (tid == 0) s_sbase = (gb | (h ? pbit : 0ull)) | p.gbase;
-                __syncthreads();
-                phases(h ? buf1 : tile0, 0ull, [] {});
-            }
-            if (p.estore) {  // gather to registers, fetch the next pair, then store (see the pair store)
-                double2 sa[NR], sb[NR];
-                __syncthreads();
-#pragma unroll
-                for (int k = 0; k < NR; ++k) {
-                    const uint32_t sl = swz((uint32_t)k << TB);
-                    sa[k] = lds128(slot_addr(a0, sl));
-                    sb[k] = lds128(slot_addr(a1, sl));
-                }
-                __syncthreads();
-                const uint64_t cgb = gb;
-                gb = ngb;
-                if (t + gridDim.x < nunits) fetch2(gb);
-                double2 *dst = p.y + (cgb + t_off);
-#pragma unroll
-                for (int k = 0; k < NR; ++k) {
-                    st_stream(dst + kdep(k), sa[k]);
-                    st_stream(dst + (kdep(k) | pbit), sb[k]);
-                }
                 continue;
             }
-            double2 *dst = p.y + (gb + t_off);
+            double2 *dst = p.y + (cgb + t_off);
 #pragma unroll
             for (int k = 0; k < NR; ++k) {
                 const uint32_t sl = swz((uint32_t)k << TB);
@@ -1257,68 +1241,32 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
                 st_stream(dst + (kdep(k) | pbit), lds128(slot_addr(a1, sl)));
             }
             __syncthreads();
-            gb = ngb;
-            if (t + gridDim.x < nunits) fetch2(gb);
+            t += gridDim.x;
+            gb = insert_zero_bits_dyn((uint64_t)t, S.eb, T + 1);
+            if (t < nunits) fetch2(gb);
         }
+        if (dyn) units_done();
         return;
     }
     // gperm scatter store: element e -> gconst ^ G(base) ^ G(t_off) ^ G(kdep(k))
     const uint64_t g_t = S.gperm ? gmap(S, t_off) : 0ull;
-    if (p.uctr && p.estore && p.nbuf == 1) {  // dynamic unit order (see TileParams::uctr), one buffer
-        int64_t t = first_unit();
-        uint64_t base = insert_zero_bits_dyn((uint64_t)t, S.tb, T);
-        if (t < p.ntiles) fetch(base, tile0);
-        int par = 1;
-        const uint32_t a = tile0 + t16;
-        while (t < p.ntiles) {
-            if (tid == 0) {
-                s_u[par] = (int64_t)atomicAdd(p.uctr, 1ull);  // lands during the compute
-                s_sbase = base | p.gbase;
-                if (S.gperm) s_ab = p.gconst ^ gmap(S, base);
-            }
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-            __syncthreads();
-            phases(tile0, 0ull, [] {});
-            double2 sv[NR];
-#pragma unroll
-            for (int k = 0; k < NR; ++k) sv[k] = lds128(slot_addr(a, swz((uint32_t)k << TB)));
-            const uint64_t ab = S.gperm ? (s_ab ^ g_t) : 0ull;
-            __syncthreads();
-            const uint64_t cbase = base;
-            t = s_u[par];
-            par ^= 1;
-            base = insert_zero_bits_dyn((uint64_t)t, S.tb, T);
-            if (t < p.ntiles) fetch(base, tile0);
-            if (S.gperm) {
-#pragma unroll
-                for (int k = 0; k < NR; ++k) {
-                    double2 *dst = p.y + (ab ^ gmap(S, kdep(k)));
-                    if (p.gstore == 0) st_stream(dst, sv[k]);
-                    else if (p.gstore == 1) st_plain(dst, sv[k]);
-                    else st_hint(dst, sv[k], policy_evict_last());
-                }
-            } else {
-                double2 *dst = p.y + (cbase + t_off);
-#pragma unroll
-                for (int k = 0; k < NR; ++k) st_stream(dst + kdep(k), sv[k]);
-            }
-        }
-        units_done();
-        return;
-    }
-    uint64_t base = insert_zero_bits_dyn((uint64_t)blockIdx.x, S.tb, T);
-    if ((int64_t)blockIdx.x < p.ntiles) fetch(base, tile0);
+    // one loop for both unit orders, as above (dynamic order: one buffer, estore)
+    const bool dyn = p.uctr && p.estore && p.nbuf == 1;
+    int64_t t = dyn ? first_unit() : (int64_t)blockIdx.x;
+    uint64_t base = insert_zero_bits_dyn((uint64_t)t, S.tb, T);
+    if (t < p.ntiles) fetch(base, tile0);
     uint32_t buf = tile0;
     const uint32_t tstride = 16u << T;
-    for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-        const uint64_t nbase = next_base(base, p, S);
-        const bool more = t + gridDim.x < p.ntiles;
+    int par = 1;
+    while (t < p.ntiles) {
+        const int64_t nt = t + gridDim.x;  // static order
         if (tid == 0) {
+            if (dyn) s_u[par] = (int64_t)atomicAdd(p.uctr, 1ull);  // lands during the compute
             s_sbase = base | p.gbase;  // full-state index bits for selectors
             if (S.gperm) s_ab = p.gconst ^ gmap(S, base);
         }
-        if (p.nbuf == 2 && more) {
-            fetch(nbase, buf == tile0 ? tile0 + tstride : tile0);
+        if (p.nbuf == 2 && nt < p.ntiles) {
+            fetch(insert_zero_bits_dyn((uint64_t)nt, S.tb, T), buf == tile0 ? tile0 + tstride : tile0);
             asm volatile("cp.async.wait_group 1;" ::: "memory");
         } else {
             asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -1336,8 +1284,10 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
             const uint64_t ab = S.gperm ? (s_ab ^ g_t) : 0ull;
             __syncthreads();
             const uint64_t cbase = base;
-            base = nbase;
-            if (more) fetch(base, buf);
+            t = dyn ? s_u[par] : nt;
+            par ^= 1;
+            base = insert_zero_bits_dyn((uint64_t)t, S.tb, T);
+            if (t < p.ntiles) fetch(base, buf);
             if (S.gperm) {
 #pragma unroll
                 for (int k = 0; k < NR; ++k) {
@@ -1369,10 +1319,12 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
             for (int k = 0; k < NR; ++k) st_stream(dst + kdep(k), lds128(slot_addr(a, swz((uint32_t)k << TB))));
         }
         __syncthreads();
-        base = nbase;
+        t = nt;
+        base = insert_zero_bits_dyn((uint64_t)t, S.tb, T);
         if (p.nbuf == 2) buf = (buf == tile0) ? tile0 + tstride : tile0;
-        else if (more) fetch(base, buf);  // refill as soon as the tile is drained
+        else if (t < p.ntiles) fetch(base, buf);  // refill as soon as the tile is drained
     }
+    if (dyn) units_done();
 }
 #endif  // DIAQ_JIT
 

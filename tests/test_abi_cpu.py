@@ -168,6 +168,37 @@ def _plan(lib, n, ops, tile_bits=12, local_bits=None):
     return dict(zip(["passes", "single", "phases", "folded", "smem_phases"], list(st)))
 
 
+def test_fused_schedule_lookahead_host_only(lib):
+    """Contracted arithmetic: the lookahead schedule of config 5 (n=30, 20
+    layers) needs about half the passes of first fit, the program-order
+    schedule of the bitwise modes is untouched by the knob, and a one-layer
+    program (the benchmark's step) keeps its two passes."""
+    import paper_2405_01250_b200 as D
+    from paper_2405_01250_b200.sim import _GateProgram
+
+    def passes(n, ops, mode):
+        pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
+        prog = _GateProgram([p.compact() for p in pls])
+        st = (ctypes.c_int * 5)()
+        L.check(lib.diaq_fused_plan_mode(n, n, prog.n, prog.arr, 0, mode, st), "diaq_fused_plan_mode")
+        assert st[3] == sum(1 for o in ops if o[0] == "cx")  # every CX folded, none executed
+        return st[0]
+
+    ops = W.random_layered_ops(30, 20, seed=0)
+    inorder = passes(30, ops, L.CMUL_FMA)
+    look = passes(30, ops, L.CMUL_CONTRACT)
+    L.tune("fused_lookahead", 0)
+    try:
+        first_fit = passes(30, ops, L.CMUL_CONTRACT)
+        assert passes(30, ops, L.CMUL_FMA) == inorder
+    finally:
+        L.tune("fused_lookahead", 1)
+    assert look < first_fit < inorder
+    assert look <= 0.6 * inorder
+    one = W.random_layered_ops(28, 1, seed=0)
+    assert passes(28, one, L.CMUL_CONTRACT) == passes(28, one, L.CMUL_FMA) == 2
+
+
 def test_fused_schedule_host_only(lib):
     """The fused-pass scheduler (host code behind diaq_run_gates_fused) on
     the benchmark layer and on permutation-heavy circuits: CX/X/SWAP runs
@@ -184,7 +215,7 @@ def test_fused_schedule_host_only(lib):
         assert _plan(lib, n, ops)["passes"] == 4  # tile-only folding: two relabelling copy passes
         many = [("cx", (27 - i, 0), ()) for i in range(12)]
         st = _plan(lib, 28, many)   # more than 8 distinct controls outside the tile start a new pass
-        assert st["folded"] == 12 and st["passes"] == 2
+        assert st["folded"] + st["single"] == 12 and st["passes"] == 2
     finally:
         L.tune("fused_gperm", 1)
     many = [("h", (27,), ())] + [("cx", (27 - i, 0), ()) for i in range(12)]

@@ -71,7 +71,8 @@ def test_contracted_fuzz_every_tile(ref_mode, seed):
     n, pls, rng = fuzz_circuit(seed)
     x0 = D.StateVector(n, W.random_state(rng, 2**n))
     want = D.run_gates(x0, pls, cmul_mode=ref_mode, tile_bits=0).amps
-    switches = [{}, {"fused_seq": 0}, {"fused_gperm": 0}, {"fused_dense2": 0}]
+    switches = [{}, {"fused_seq": 0}, {"fused_gperm": 0}, {"fused_dense2": 0}, {"fused_lookahead": 0},
+                {"fused_unit": 0}, {"fused_reorder": 0}]
     try:
         for sw in switches:
             for k, v in sw.items():
@@ -83,7 +84,7 @@ def test_contracted_fuzz_every_tile(ref_mode, seed):
             for k in sw:
                 L.tune(k, 1)
     finally:
-        for k in ("fused_seq", "fused_gperm", "fused_dense2"):
+        for k in ("fused_seq", "fused_gperm", "fused_dense2", "fused_lookahead", "fused_unit", "fused_reorder"):
             L.tune(k, 1)
 
 
@@ -151,3 +152,42 @@ def test_contracted_sharded_emulated(ref_mode):
         shards, _ = run_emulated(n, p, pls, cmul_mode=C)
         got = np.concatenate([s.cpu().numpy() for s in shards])
         assert rel_l2(got, want) < TOL, p
+
+
+@pytest.mark.parametrize("n,layers,seed", [(16, 12, 5), (22, 10, 6), (24, 8, 7)])
+def test_contracted_lookahead_deep_passes(ref_mode, n, layers, seed):
+    """Layered circuits deep enough that the lookahead schedule packs several
+    layers into a pass (tile bits chosen by trial sweeps, gates joining the
+    body ahead of a global permutation tail, rotations in unit-diagonal
+    form): within 1e-12 of the bitwise program-order state, with fewer
+    passes than first fit, and the same state from the interpreter."""
+    import ctypes
+    from paper_2405_01250_b200.sim import _GateProgram
+    ops = W.random_layered_ops(n, layers, seed=seed)
+    pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
+    rng = np.random.default_rng(seed)
+    x0 = D.StateVector(n, W.random_state(rng, 2**n))
+    want = D.run_gates(x0, pls, cmul_mode=ref_mode).amps
+    prog = _GateProgram([p.compact() for p in pls])
+
+    def passes():
+        st = (ctypes.c_int * 5)()
+        L.check(L.load().diaq_fused_plan_mode(n, n, prog.n, prog.arr, 0, C, st), "diaq_fused_plan_mode")
+        return st[0]
+
+    try:
+        L.tune("fused_lookahead", 0)
+        first_fit = passes()
+        L.tune("fused_lookahead", 1)
+        assert passes() < first_fit
+        L.tune("fused_jit", 2)
+        got = D.run_gates(x0, pls, cmul_mode=C).amps
+        assert rel_l2(got, want) < TOL
+        L.tune("fused_jit", 0)
+        assert np.array_equal(D.run_gates(x0, pls, cmul_mode=C).amps, got)
+        L.tune("fused_unit", 0)  # the same schedule without the unit forms
+        assert rel_l2(D.run_gates(x0, pls, cmul_mode=C).amps, want) < TOL
+    finally:
+        L.tune("fused_jit", 1)
+        L.tune("fused_lookahead", 1)
+        L.tune("fused_unit", 1)
