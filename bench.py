@@ -813,6 +813,26 @@ def secondary_workloads(args, D, L, W, torch) -> dict:
         out["haar4_layer_n28" + tag] = {"gates": len(pls_h), "ms_per_layer": round(ms_h, 3),
                                         "gates_per_s": round(len(pls_h) / ms_h * 1e3, 1)}
         del st_h
+    # the benchmark's layer kind as a deep program at the metric's size: n=28, 20
+    # layers (840 gates) in one run_gates call -- the schedule packs several
+    # layers into a pass (contracted arithmetic: lookahead tile bits, phase
+    # slots), which a one-layer step cannot show
+    ops28 = W.random_layered_ops(28, 20, seed=0)
+    pls28 = D.compile_circuit(D.Circuit(28, [D.GateOp(*o) for o in ops28]), span_limit=28)
+    for mode, tag in ((None, ""), (L.CMUL_CONTRACT, "_contracted")):
+        st28 = D.init_state(28)
+        D.run_gates(st28, pls28, cmul_mode=mode, inplace=True)
+        L.call("diaq_jit_wait", -1.0)
+        spec0 = jit_stats(L)["launches"]
+        D.run_gates(st28, pls28, cmul_mode=mode, inplace=True)
+        npass28 = jit_stats(L)["launches"] - spec0
+        ms28 = dev_time(lambda: D.run_gates(st28, pls28, cmul_mode=mode, inplace=True), 3)
+        out["layered_n28_20layers" + tag] = {
+            "gates": len(pls28), "ms_per_circuit": round(ms28, 3), "gates_per_s": round(len(pls28) / ms28 * 1e3, 1),
+            "hbm_passes": npass28, "ms_per_pass": round(ms28 / max(1, npass28), 3),
+            "numerics": "contracted" if mode else "reference rounding (bitwise)",
+            "norm_err": abs(1.0 - st28.norm())}
+        del st28
     # config 5 at its 1-GPU size: n=30 (16 GB state), 20 random layers, norm check
     ops30 = W.random_layered_ops(30, 20, seed=0)
     pls30 = D.compile_circuit(D.Circuit(30, [D.GateOp(*o) for o in ops30]), span_limit=30)

@@ -119,6 +119,8 @@ extern "C" int diaq_tune(const char *key, int64_t value) {
     else if (k == "fused_dyn") t.fused_dyn = (int)value;
     else if (k == "fused_lookahead") t.fused_lookahead = (int)value;
     else if (k == "fused_unit") t.fused_unit = (int)value;
+    else if (k == "fused_slots") t.fused_slots = (int)value;
+    else if (k == "fused_slot_gates") t.fused_slot_gates = (int)(value < 1 ? 1 : value);
     else if (k == "fused_maxph") t.fused_maxph = (int)(value < 1 ? 1 : value);
     else if (k == "kron_flat") t.kron_flat = (int)value;
     else if (k == "kron_ctas_per_sm") t.kron_ctas_per_sm = (int)(value < 1 ? 1 : value);

@@ -46,7 +46,9 @@ struct Tuning {
     int fused_dyn = 1;         // units handed out in order by a global counter (TileParams::uctr): adjacent DRAM runs fetched
                                // together (n=28 layer 1.554 -> 1.434 ms per contracted pass, config 5 339 -> 305 ms, r02n)
     int fused_lookahead = 1;   // contracted arithmetic: each pass's tile bits chosen by trial sweeps (fused.cu schedule_once)
-    int fused_maxph = 6;       // contracted arithmetic: phases (shared-memory round trips) per pass at most (config 5 n=30: 237/223/214/198/215/286 ms at 3/4/5/6/7/8, r02u)
+    int fused_maxph = 5;       // contracted arithmetic: phases (shared-memory round trips) per pass at most (config 5 n=30 with slots: 204/182/178/193 ms at 3/4/5/6; without: 237/223/214/198/215/286 ms at 3..8, r02u)
+    int fused_slots = 1;       // contracted arithmetic: gates placed into the earliest phase slot, X/CX/SWAP on register bits as exchanges
+    int fused_slot_gates = 6;  // ... at most this many non-diagonal gate records per slot (the specialised kernels unroll longer gate loops only partly: 8 left 3 of 23 config-5 kernels with run-time dispatch)
     int fused_unit = 1;        // contracted arithmetic: rotations in unit-diagonal form, 2 FP64 operations per amplitude
     uint64_t epoch = 0;         // bumped by every diaq_tune (launch caches key on it)
 };

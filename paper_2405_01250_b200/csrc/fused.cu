@@ -30,6 +30,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <functional>
 #include <vector>
 
 #include "common.cuh"
@@ -87,6 +88,8 @@ struct PassPlan {
     // local index and applied by the final store (out of place): new index =
     // XOR of gcol[j] over the set old bits j ^ gc ^ XOR of ggcol[g] over the
     // set global (rank) bits g
+    int nrperm = 0;               // permutation members applied as register renamings (gate records, no arithmetic)
+    int nrperm_records = 0;       // their gate records (a SWAP takes three)
     bool gon = false;
     size_t tail = SIZE_MAX;
     std::vector<uint64_t> gcol, ggcol;
@@ -345,6 +348,7 @@ static int pack_reg_gate(const diaq_gate_t &gt, const std::vector<int> &bits, co
             rx = rx && ((e == 0 || e == 3) ? c[e].y == 0.0 : c[e].x == 0.0);
         }
         G.shape = real ? 1 : (rx ? 2 : 0);
+        G.full = (pk.nz[(size_t)G.nz_off] & pk.nz[(size_t)G.nz_off + 1] & 3u) == 3u;
     }
     else if (G.kin == 0 && G.kout == 1) G.op = 2;
     else if (G.kin == 2 && G.kout == 0) {  // dense two-qubit: register path only when every entry is nonzero
@@ -450,6 +454,51 @@ static void spread_lane_bits(Phase &ph, int T, int R) {
     for (int i = 0; i < nt; ++i) ph.tpos[i] = out[i];
 }
 
+// A permutation gate as controlled exchanges of register pairs: X (one
+// operand), CX in either orientation, SWAP (three CX).  out: (control
+// operand or -1, target operand) in application order; false: not of
+// these kinds (the gate is folded into a phase store instead).
+static bool rperm_ops(const diaq_gate_t &gt, const PermGate &pg, std::vector<std::pair<int, int>> &out) {
+    out.clear();
+    if (!pg.ok) return false;
+    if (gt.k == 1) {
+        if (pg.d != 1u || pg.col[0] != 1u) return false;
+        out.push_back({-1, 0});
+        return true;
+    }
+    if (gt.k != 2 || pg.d != 0u) return false;
+    // gate-index bit m <-> operand 1 - m; col[m] = image of bit m
+    const uint32_t c0 = pg.col[0], c1 = pg.col[1];
+    if (c0 == 1u && c1 == 3u) out.push_back({0, 1});        // bit 1 (operand 0) controls bit 0 (operand 1)
+    else if (c0 == 3u && c1 == 2u) out.push_back({1, 0});   // bit 0 (operand 1) controls bit 1 (operand 0)
+    else if (c0 == 2u && c1 == 1u) out = {{0, 1}, {1, 0}, {0, 1}};  // SWAP
+    else return false;
+    return true;
+}
+
+static int pack_rperm(const diaq_gate_t &gt, const PermGate &pg, const std::vector<int> &bits, const Phase &ph, int R,
+                      std::vector<RegGate> &out) {
+    std::vector<std::pair<int, int>> ops;
+    if (!rperm_ops(gt, pg, ops)) return set_error(DIAQ_ERR_VALUE, "fused pass: permutation is not a register exchange");
+    auto regbit = [&](int operand) {
+        const int tp = tile_pos(bits, gt.shifts[operand]);
+        for (int i = 0; i < R; ++i)
+            if (tp >= 0 && ph.rpos[i] == tp) return i;
+        return -1;
+    };
+    for (const auto &op : ops) {
+        RegGate G;
+        memset(&G, 0, sizeof(G));
+        G.op = 4;
+        G.rb[0] = (int8_t)regbit(op.second);
+        G.rb[1] = (int8_t)(op.first < 0 ? -1 : regbit(op.first));
+        if (G.rb[0] < 0 || (op.first >= 0 && G.rb[1] < 0))
+            return set_error(DIAQ_ERR_VALUE, "fused pass: register exchange outside the phase registers");
+        out.push_back(G);
+    }
+    return DIAQ_OK;
+}
+
 // Contracted arithmetic: a rotation [[a, b], [c, a]] with a real (RX, RY)
 // is applied as [[1, b/a], [c/a, 1]] -- one DFMA per part, 2 FP64
 // operations per amplitude instead of 4 -- and the scalar a is carried to
@@ -518,26 +567,31 @@ static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t 
         ncoef = nnz = 0;
         tail = SIZE_MAX;
     };
-    auto flush = [&]() -> int {
-        if (members.empty()) return DIAQ_OK;
-        PassPlan ps;
+    // phase specs: register phases (<= R mixing bits), generic smem phases,
+    // and permutation runs folded into the previous phase's store (or the
+    // tile load when the pass opens with one)
+    struct Spec {
+        int generic = 0;
+        std::vector<int> mem;
+        std::vector<char> rperm;  // parallel to mem (may be shorter: 0): permutation applied in registers
+        std::vector<int> used;
+        HostAffine post;
+        bool seq_ok = true;  // still a sequence phase (dense steps on fresh register bits in order)
+        bool has_d2 = false;
+    };
+    std::function<int(PassPlan &, std::vector<Spec> &, HostAffine &, const std::vector<int> &)> finish;
+    auto tile_bits_of = [&](PassPlan &ps) {
         for (int b = 0; b < 64; ++b)
             if (inb[b]) ps.bits.push_back(b);
         for (int b = 0; (int)ps.bits.size() < T && b < n_bits; ++b)
             if (!inb[b]) ps.bits.push_back(b);
         std::sort(ps.bits.begin(), ps.bits.end());
+    };
+    auto flush = [&]() -> int {
+        if (members.empty()) return DIAQ_OK;
+        PassPlan ps;
+        tile_bits_of(ps);
         ps.members = members;
-        // 1. phase specs: register phases (<= R mixing bits), generic smem
-        //    phases, and permutation runs folded into the previous phase's
-        //    store (or the tile load when the pass opens with one)
-        struct Spec {
-            int generic = 0;
-            std::vector<int> mem;
-            std::vector<int> used;
-            HostAffine post;
-            bool seq_ok = true;  // still a sequence phase (dense steps on fresh register bits in order)
-            bool has_d2 = false;
-        };
         std::vector<Spec> specs;
         HostAffine pre;
         pre.init((int)ps.bits.size());
@@ -619,14 +673,19 @@ static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t 
             specs.push_back(sp);
             open = false;
         }
+        const std::vector<int> tailm(members.begin() + (long)body, members.end());
+        return finish(ps, specs, pre, tailm);
+    };
+    // the pass from its phase specs: global tail map, packed phases and gate records
+    finish = [&](PassPlan &ps, std::vector<Spec> &specs, HostAffine &pre, const std::vector<int> &tailm) -> int {
         ps.pre = pre.pack();
-        if (tail < members.size()) {  // trailing run leaving the tile: one map over the whole local index
+        if (!tailm.empty()) {  // trailing run leaving the tile: one map over the whole local index
             GlobalAffine ga;
             ga.init(n_bits);
-            for (size_t i = tail; i < members.size(); ++i)
-                if (!ga.fold(gates[members[i]], perm[(size_t)members[i]]))
+            for (const int gi : tailm)
+                if (!ga.fold(gates[gi], perm[(size_t)gi]))
                     return set_error(DIAQ_ERR_VALUE, "fused pass: permutation moves a global bit");
-            ps.tail = tail;
+            ps.tail = ps.members.size() - tailm.size();
             ps.gon = true;
             ps.gcol.assign((size_t)n_bits, 0);
             ps.ggcol.assign(64, 0);
@@ -676,7 +735,16 @@ static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t 
             for (int tp = 0; tp < (int)ps.bits.size(); ++tp)
                 if (std::find(rp.begin(), rp.end(), tp) == rp.end()) ph.tpos[tq++] = tp;
             ph.g0 = (int)ps.gates.size();
-            for (int gi : sp.mem) {
+            for (size_t mi = 0; mi < sp.mem.size(); ++mi) {
+                const int gi = sp.mem[mi];
+                if (mi < sp.rperm.size() && sp.rperm[mi]) {
+                    const int before = (int)ps.gates.size();
+                    const int rc = pack_rperm(gates[gi], perm[(size_t)gi], ps.bits, ph, R, ps.gates);
+                    if (rc) return rc;
+                    ++ps.nrperm;
+                    ps.nrperm_records += (int)ps.gates.size() - before;
+                    continue;
+                }
                 RegGate G;
                 const int rc = pack_reg_gate(gates[gi], ps.bits, ph, R, ps.pk, G);
                 if (rc) return rc;
@@ -720,9 +788,16 @@ static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t 
                     ph.nd_before[R] = (int8_t)cnt;
                 }
             }
-            if (!ph.seq)  // a dense two-qubit gate runs only in a sequence phase
+            if (!ph.seq) {  // a dense two-qubit gate runs only in a sequence phase
                 for (int g = ph.g0; g < ph.g1; ++g)
                     if (ps.gates[g].op == 3) return kRetryNoDense2;
+                int lead = 0;  // leading diagonals on non-register bits: applied as one run (diag_run)
+                while (ph.g0 + lead < ph.g1 && lead < 127 && ps.gates[(size_t)(ph.g0 + lead)].op == 2 &&
+                       ps.gates[(size_t)(ph.g0 + lead)].osel[0] != 2)
+                    ++lead;
+                for (int b = 0; b < 5; ++b) ph.nd_before[b] = 0;
+                ph.nd_before[0] = (int8_t)lead;
+            }
             ps.phases.push_back(ph);
         }
         if ((int)ps.phases.size() > kMaxPhases || (int)ps.gates.size() > kMaxPassGates)
@@ -974,6 +1049,304 @@ static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t 
         if (score) *score = sc;
         return DIAQ_OK;
     };
+    // ---- slot sweep (reorder only, knob fused_slots) ------------------------
+    // The pass is built as a list of phase slots instead of one open phase:
+    // a gate goes into the EARLIEST slot that follows the last gate on each
+    // of its qubits and has register bits left for it (gates on other
+    // qubits in later slots commute with it), so one phase takes several
+    // layers' gates on its four qubits.  An X / CX / SWAP whose operands are
+    // register bits of its slot is applied there as a register exchange
+    // (no arithmetic, a renaming in the specialised kernels) and the slot
+    // stays open; any other permutation is folded into its slot's store.
+    struct Slot {
+        std::vector<int> body;
+        std::vector<char> rperm;
+        std::vector<int> post;      // folded permutations, in order
+        std::vector<int> base;      // their operands outside the tile (one folded map)
+        uint64_t used = 0;          // state bits taken as register bits
+        int ndiag = 0;              // one-selector diagonal gates of the body (most lead it as one run)
+        bool generic = false, has_d2 = false, seq_ok = true;
+    };
+    std::vector<Slot> slots;
+    std::vector<int> prev, prebase, tailv;  // permutations opening the pass / their outside operands / global tail
+    int lastph[64];
+    bool lastpost[64];
+    int barrier = -1;  // slot of the last shared-memory (generic) gate: every later gate follows it
+    const bool use_slots = reorder && tuning().fused_slots != 0;
+    auto reset_slots = [&]() {
+        reset2();
+        slots.clear();
+        prev.clear();
+        prebase.clear();
+        tailv.clear();
+        for (int b = 0; b < 64; ++b) { lastph[b] = -2; lastpost[b] = false; }
+        barrier = -1;
+    };
+    auto sweep_slots = [&](const std::vector<int> &pending, std::vector<int> *deferred_out, bool dry, int *score) -> int {
+        uint64_t blocked = 0;
+        int sc = 0;
+        bool any = false;  // the pass has a member
+        std::vector<std::pair<int, int>> rops;
+        for (size_t pi = 0; pi < pending.size(); ++pi) {
+            const int i = pending[pi];
+            if (blocked == allq) {
+                if (deferred_out) deferred_out->insert(deferred_out->end(), pending.begin() + (long)pi, pending.end());
+                break;
+            }
+            const diaq_gate_t &gt = gates[i];
+            const uint64_t qmask = gqm[(size_t)i];
+            auto defer = [&]() {
+                if (deferred_out) deferred_out->push_back(i);
+                blocked |= qmask;
+            };
+            if (qmask & blocked) {
+                defer();
+                continue;
+            }
+            const uint32_t mix = gmix[(size_t)i];
+            uint64_t mixq = 0;
+            int kin = 0, kout = 0, add = 0;
+            for (int j = 0; j < gt.k; ++j) {
+                if ((mix >> j) & 1u) {
+                    ++kin;
+                    add += inb[gt.shifts[j]] ? 0 : 1;
+                    mixq |= 1ull << gt.shifts[j];
+                } else {
+                    ++kout;
+                }
+            }
+            const bool pg = perm[(size_t)i].ok;
+            const bool standalone = pg ? (kin > T - low) : (kin > kMaxRegKin || kin > R || kout > kMaxSel);
+            if (standalone) {
+                if (any || preset || dry) {
+                    defer();
+                    continue;
+                }
+                PassPlan ps;  // first in order and nothing open: its own pass now
+                ps.members = {i};
+                plan.push_back(ps);
+                continue;
+            }
+            // the slot this gate must follow on each of its qubits
+            int kmin = barrier + 1;
+            bool after_post = false;
+            for (int j = 0; j < gt.k; ++j) {
+                const int q = gt.shifts[j];
+                if (lastph[q] == -2) continue;
+                const int need = (pg || !lastpost[q]) ? lastph[q] : lastph[q] + 1;  // a permutation may join the same store
+                if (need > kmin) kmin = need;
+            }
+            if (pg) {
+                // global tail: its target leaves the tile (or it follows the tail on a shared qubit)
+                const bool fits_tile = tailv.empty() && kin <= T - low && nb + add <= T;
+                if (!fits_tile || (qmask & tailq)) {
+                    if (!any || !tuning().fused_gperm || t_no_gperm) {
+                        defer();
+                        continue;
+                    }
+                    GlobalAffine trial_map;
+                    if (tailv.empty()) trial_map.init(n_bits);
+                    else trial_map = tail_map;
+                    bool rows = trial_map.fold(gt, perm[(size_t)i]);
+                    for (int o = low; o < n_bits && rows && tuning().fused_gperm_rows; ++o)
+                        if (trial_map.row[o].m & ((1ull << low) - 1ull)) rows = false;
+                    if (!rows) {
+                        defer();
+                        continue;
+                    }
+                    tail_map = trial_map;
+                    tailv.push_back(i);
+                    tailq |= qmask;
+                    sc += 1;
+                    continue;
+                }
+                // in the tile: a register exchange in slot kmin, or folded into its store
+                for (int j = 0; j < gt.k; ++j) after_post = after_post || (lastph[gt.shifts[j]] == kmin && lastpost[gt.shifts[j]]);
+                bool done = false;
+                if (kmin >= 0 && kmin < (int)slots.size() && !after_post && rperm_ops(gt, perm[(size_t)i], rops)) {
+                    Slot &sl = slots[(size_t)kmin];
+                    bool in_tile = true;
+                    for (int j = 0; j < gt.k; ++j) in_tile = in_tile && inb[gt.shifts[j]];
+                    if (in_tile && !sl.generic && !sl.has_d2 && __builtin_popcountll(sl.used | qmask) <= R &&
+                        nrec + (int)rops.size() <= kMaxPassGates &&
+                        (int)sl.body.size() - sl.ndiag + (int)rops.size() <= tuning().fused_slot_gates) {
+                        sl.body.push_back(i);
+                        sl.rperm.push_back(1);
+                        sl.used |= qmask;
+                        sl.seq_ok = false;
+                        nrec += (int)rops.size();
+                        for (int j = 0; j < gt.k; ++j) { lastph[gt.shifts[j]] = kmin; lastpost[gt.shifts[j]] = false; }
+                        done = true;
+                    }
+                }
+                if (!done) {
+                    int k = kmin;
+                    if (k >= (int)slots.size()) k = (int)slots.size() - 1;  // (barrier + 1 past the end: the last slot's store)
+                    if (k >= 0 && slots[(size_t)k].generic) {  // a shared-memory phase has no store map: an empty register phase carries it
+                        if (k + 1 < (int)slots.size()) {
+                            k = k + 1;
+                        } else {
+                            if ((int)slots.size() + 1 > maxph) {
+                                defer();
+                                continue;
+                            }
+                            slots.emplace_back();
+                            k = (int)slots.size() - 1;
+                        }
+                    }
+                    std::vector<int> &base = k < 0 ? prebase : slots[(size_t)k].base;
+                    int padd = 0;
+                    for (int j = 0; j < gt.k; ++j)
+                        if (!((mix >> j) & 1u) && !inb[gt.shifts[j]] &&
+                            std::find(base.begin(), base.end(), gt.shifts[j]) == base.end())
+                            ++padd;
+                    if ((int)base.size() + padd > kMaxPermBase) {
+                        defer();
+                        continue;
+                    }
+                    for (int j = 0; j < gt.k; ++j)
+                        if (!((mix >> j) & 1u) && !inb[gt.shifts[j]] &&
+                            std::find(base.begin(), base.end(), gt.shifts[j]) == base.end())
+                            base.push_back(gt.shifts[j]);
+                    (k < 0 ? prev : slots[(size_t)k].post).push_back(i);
+                    for (int j = 0; j < gt.k; ++j) { lastph[gt.shifts[j]] = k; lastpost[gt.shifts[j]] = true; }
+                }
+                for (int j = 0; j < gt.k; ++j)
+                    if (((mix >> j) & 1u) && !inb[gt.shifts[j]]) { inb[gt.shifts[j]] = 1; ++nb; }
+                any = true;
+                sc += 1;
+                continue;
+            }
+            // arithmetic gates
+            if (qmask & tailq) {  // after the tail on a shared qubit
+                defer();
+                continue;
+            }
+            const int gcoef = (1 << kout) << (2 * kin), gnz = (1 << kout) << kin;
+            if (nb + add > T || nrec + 1 > kMaxPassGates || ncoef + gcoef > kMaxCoef || nnz + gnz > kMaxNz) {
+                defer();
+                continue;
+            }
+            const bool isd2 = d2[(size_t)i] != 0;
+            const bool fastg = fast[(size_t)i] || isd2;
+            if (kmin < 0) kmin = 0;
+            int k = -1;
+            if (fastg) {
+                for (int c = kmin; c < (int)slots.size() && k < 0; ++c) {
+                    const Slot &sl = slots[(size_t)c];
+                    if (sl.generic) continue;
+                    // (the specialised kernels unroll a phase's gate loop only up to a size)
+                    if ((int)sl.body.size() - sl.ndiag >= tuning().fused_slot_gates) continue;
+                    const int fresh = __builtin_popcountll(mixq & ~sl.used);
+                    if (__builtin_popcountll(sl.used | mixq) > R) continue;
+                    // as flush(): dense two-qubit gates only in sequence phases
+                    bool keeps = fresh == kin;
+                    if (kin == 0 && (qmask & sl.used)) keeps = false;
+                    if (!(keeps || (!sl.has_d2 && !isd2)) || (isd2 && !sl.seq_ok)) continue;
+                    k = c;
+                }
+            }
+            if (k < 0) {  // a new slot at the end
+                if ((int)slots.size() + 1 > maxph) {
+                    defer();
+                    continue;
+                }
+                slots.emplace_back();
+                k = (int)slots.size() - 1;
+                if (!fastg) {
+                    slots.back().generic = true;
+                    barrier = k;
+                }
+            }
+            Slot &sl = slots[(size_t)k];
+            if (fastg) {
+                const int fresh = __builtin_popcountll(mixq & ~sl.used);
+                bool keeps = fresh == kin;
+                if (kin == 0 && (qmask & sl.used)) keeps = false;
+                sl.seq_ok = sl.seq_ok && keeps;
+                sl.has_d2 = sl.has_d2 || isd2;
+                sl.used |= mixq;
+            }
+            sl.body.push_back(i);
+            sl.rperm.push_back(0);
+            if (fastg && kin == 0) ++sl.ndiag;
+            for (int j = 0; j < gt.k; ++j) {
+                lastph[gt.shifts[j]] = k;
+                lastpost[gt.shifts[j]] = sl.generic;  // nothing joins a shared-memory phase
+            }
+            for (int j = 0; j < gt.k; ++j)
+                if (((mix >> j) & 1u) && !inb[gt.shifts[j]]) { inb[gt.shifts[j]] = 1; ++nb; }
+            ++nrec;
+            ncoef += gcoef;
+            nnz += gnz;
+            any = true;
+            sc += kin > 0 ? 4 : 1;
+        }
+        if (score) *score = sc;
+        if (dry) return DIAQ_OK;
+        // members in execution order, for flush_slots()
+        members.clear();
+        members.insert(members.end(), prev.begin(), prev.end());
+        for (const Slot &sl : slots) {
+            members.insert(members.end(), sl.body.begin(), sl.body.end());
+            members.insert(members.end(), sl.post.begin(), sl.post.end());
+        }
+        members.insert(members.end(), tailv.begin(), tailv.end());
+        return DIAQ_OK;
+    };
+    auto flush_slots = [&]() -> int {
+        if (members.empty()) return DIAQ_OK;
+        PassPlan ps;
+        tile_bits_of(ps);
+        ps.members = members;
+        const int TT = (int)ps.bits.size();
+        HostAffine pre;
+        pre.init(TT);
+        for (const int gi : prev)
+            if (!pre.fold(gates[gi], perm[(size_t)gi], ps.bits))
+                return set_error(DIAQ_ERR_VALUE, "fused pass: permutation fold overflow");
+        std::vector<Spec> specs;
+        for (const Slot &sl : slots) {
+            Spec sp;
+            sp.generic = sl.generic ? 1 : 0;
+            // diagonal gates on bits that are not register bits of the slot commute with every
+            // other gate of its body (those act on register bits): they lead it, as one run
+            if (!sl.generic) {
+                for (int part = 0; part < 2; ++part)
+                    for (size_t mi = 0; mi < sl.body.size(); ++mi) {
+                        const diaq_gate_t &gt = gates[sl.body[mi]];
+                        const bool lead = !sl.rperm[mi] && gmix[(size_t)sl.body[mi]] == 0u && gt.k == 1 &&
+                                          fast[(size_t)sl.body[mi]] && !(gqm[(size_t)sl.body[mi]] & sl.used);
+                        if (lead == (part == 0)) {
+                            sp.mem.push_back(sl.body[mi]);
+                            sp.rperm.push_back(sl.rperm[mi]);
+                        }
+                    }
+            } else {
+                sp.mem = sl.body;
+                sp.rperm = sl.rperm;
+            }
+            sp.has_d2 = sl.has_d2;
+            sp.post.init(TT);
+            for (size_t mi = 0; mi < sp.mem.size(); ++mi) {  // register bits in first-use order
+                const diaq_gate_t &gt = gates[sp.mem[mi]];
+                const uint32_t mix = gmix[(size_t)sp.mem[mi]];
+                std::vector<int> ops;
+                for (int o = 0; o < gt.k; ++o)
+                    if (sp.rperm[mi] || ((mix >> o) & 1u)) ops.push_back(o);
+                std::sort(ops.begin(), ops.end(), [&](int a, int b) { return gt.shifts[a] > gt.shifts[b]; });
+                for (const int o : ops) {
+                    const int tp = tile_pos(ps.bits, gt.shifts[o]);
+                    if (!sl.generic && std::find(sp.used.begin(), sp.used.end(), tp) == sp.used.end()) sp.used.push_back(tp);
+                }
+            }
+            for (const int gi : sl.post)
+                if (!sp.post.fold(gates[gi], perm[(size_t)gi], ps.bits))
+                    return set_error(DIAQ_ERR_VALUE, "fused pass: permutation fold overflow");
+            specs.push_back(sp);
+        }
+        return finish(ps, specs, pre, tailv);
+    };
     std::vector<int> pending((size_t)ngates);
     for (int i = 0; i < ngates; ++i) pending[(size_t)i] = i;
     if (!reorder) {
@@ -991,9 +1364,22 @@ static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t 
     auto trial = [&](uint64_t bits) -> int {
         int sc = 0;
         preset = bits;
-        reset2();
-        if (sweep(pending, nullptr, true, &sc) != DIAQ_OK) sc = -1;
+        if (use_slots) {
+            reset_slots();
+            if (sweep_slots(pending, nullptr, true, &sc) != DIAQ_OK) sc = -1;
+        } else {
+            reset2();
+            if (sweep(pending, nullptr, true, &sc) != DIAQ_OK) sc = -1;
+        }
         return sc;
+    };
+    auto real_sweep = [&](std::vector<int> &deferred) -> int {
+        if (use_slots) {
+            reset_slots();
+            return sweep_slots(pending, &deferred, false, nullptr);
+        }
+        reset2();
+        return sweep(pending, &deferred, false, nullptr);
     };
     while (!pending.empty()) {
         uint64_t choice = 0;
@@ -1027,19 +1413,17 @@ static int schedule_once(int n_bits, int n_total, int ngates, const diaq_gate_t 
         }
         std::vector<int> deferred;
         preset = choice;
-        reset2();
         const size_t plan0 = plan.size();
-        int rc = sweep(pending, &deferred, false, nullptr);
+        int rc = real_sweep(deferred);
         if (rc) return rc;
         if (members.empty() && plan.size() == plan0) {
             if (!choice) return set_error(DIAQ_ERR_VALUE, "fused schedule made no progress");
             deferred.clear();  // the fixed tile admitted nothing: first fit
             preset = 0;
-            reset2();
-            rc = sweep(pending, &deferred, false, nullptr);
+            rc = real_sweep(deferred);
             if (rc) return rc;
         }
-        rc = flush();
+        rc = use_slots ? flush_slots() : flush();
         if (rc) return rc;
         pending.swap(deferred);
     }
@@ -1123,7 +1507,10 @@ static std::vector<char> program_key(int n_total, int n_bits, int T, int ngates,
     };
     // every tuning switch the schedule depends on is part of the key
     const int head[18] = {n_total, n_bits, T, pass_tbits(), ngates, (int)t_reorder, (int)t_unit,
-                          t_reorder ? tuning().fused_lookahead + 256 * tuning().fused_maxph : 0, tuning().fused_perm,
+                          t_reorder ? tuning().fused_lookahead + 2 * tuning().fused_slots + 256 * tuning().fused_maxph +
+                                          65536 * tuning().fused_slot_gates
+                                    : 0,
+                          tuning().fused_perm,
                           tuning().fused_gperm && !t_no_gperm, tuning().fused_seq, tuning().fused_dense2,
                           tuning().fused_gperm_rows, tuning().fused_pair_store, tuning().fused_bank_spread, tuning().fused_plain_pair, tuning().fused_ppipe, tuning().fused_dstore};
     put(head, sizeof(head));
@@ -1618,7 +2005,7 @@ extern "C" int diaq_fused_plan_mode(int n_bits, int local_bits, int ngates, cons
             continue;
         }
         stats[2] += (int)ps.phases.size();
-        stats[3] += (int)(ps.members.size() - ps.gates.size());
+        stats[3] += (int)(ps.members.size() - ps.gates.size()) + ps.nrperm_records;
         for (const Phase &ph : ps.phases) stats[4] += ph.generic;
     }
     return DIAQ_OK;

@@ -43,13 +43,15 @@ struct RegGate {               // narrow fields: the records live in the kernel 
     int8_t opos[kMaxSel];
     int8_t rsel;              // any osel == 2
     // fast-path classification (host): 0 generic, 1 dense 1-qubit (no selector),
-    // 2 diagonal with one selector
+    // 2 diagonal with one selector, 3 dense 2-qubit, 4 X / CX on register
+    // bits rb[0] (target) and rb[1] (control, -1: none): an exchange of registers
     int8_t op;
     // dense 1-qubit coefficient shape (host): 0 complex, 1 all entries real
     // (RY, H), 2 real diagonal / imaginary off-diagonal (RX); contracted
     // arithmetic only: 3 / 4 = shapes 1 / 2 with both diagonal entries
     // exactly 1 (their common value factored out of the pass, fused.cu)
     int8_t shape;
+    int8_t full;              // dense 1-qubit: all four entries nonzero (host) -- the branch-free form
     int8_t mpos[kMaxRegKin];  // generic phases: tile positions of the mixing bits (relabelled order)
     int16_t coef_off;         // coef[coef_off + (b << 2kin) + r * 2^kin + c]   (pass-relative)
     int16_t nz_off;           // nz[nz_off + (b << kin) + r]
@@ -389,6 +391,27 @@ __device__ __forceinline__ void diag_run(double2 (&v)[1 << R], const TileParams 
     }
 }
 
+// X / CX on register bits (RegGate::op 4): exchange of register pairs over
+// target bit rt, for the indices whose control bit rc is set (rc < 0: all).
+// Register indices are static and the exchange is predicated on the
+// (uniform) record: no arithmetic, and a pure renaming when the record is a
+// compile-time constant (the specialised kernels).
+template <int R>
+__device__ __forceinline__ void reg_cx(double2 (&v)[1 << R], int rt, int rc) {
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+        if (t != rt) continue;
+#pragma unroll
+        for (int j = 0; j < (1 << R); ++j) {
+            if ((j >> t) & 1) continue;
+            if (rc >= 0 && !((j >> rc) & 1)) continue;
+            const double2 a = v[j];
+            v[j] = v[j | (1 << t)];
+            v[j | (1 << t)] = a;
+        }
+    }
+}
+
 template <int R, int MODE>
 __device__ __forceinline__ void dispatch_gate(double2 (&v)[1 << R], const RegGate &G, uint32_t tpart, const uint64_t *sbase_p,
                                               const double2 *sc, const uint32_t *snz) {
@@ -396,9 +419,16 @@ __device__ __forceinline__ void dispatch_gate(double2 (&v)[1 << R], const RegGat
     static_assert(R == 3 || R == 4, "register fast paths cover 8 or 16 amplitudes per thread");
     if (G.op == 1) {
         const double2 *c = sc + G.coef_off;
-        const uint32_t n0 = snz[G.nz_off], n1 = snz[G.nz_off + 1];
-        if ((n0 & n1 & 3u) == 3u) DIAQ_RB_DISPATCH(R, G.rb[0], (dense1_shaped<R, RB_, MODE>(v, c, G.shape)));
-        else DIAQ_RB_DISPATCH(R, G.rb[0], (dense1<R, RB_, MODE>(v, c, n0, n1)));
+        if (G.full) {  // (a structure constant in the specialised kernels: one form compiled)
+            DIAQ_RB_DISPATCH(R, G.rb[0], (dense1_shaped<R, RB_, MODE>(v, c, G.shape)));
+        } else {
+            const uint32_t n0 = snz[G.nz_off], n1 = snz[G.nz_off + 1];
+            DIAQ_RB_DISPATCH(R, G.rb[0], (dense1<R, RB_, MODE>(v, c, n0, n1)));
+        }
+        return;
+    }
+    if (G.op == 4) {
+        reg_cx<R>(v, G.rb[0], G.rb[1]);
         return;
     }
     if (G.op == 2) {
@@ -666,8 +696,13 @@ __device__ __forceinline__ void tile_pass_body(const TileParams &p, const TilePa
                 seq_steps<R, MODE, 0>(v, S, ph, gi, tpart, &s_sbase, sc, snz);
                 diag_run<R, MODE>(v, S, gi, ph.nd_before[R], tpart, &s_sbase, sc, snz);
             } else {
+                // leading diagonals on non-register bits (nd_before[0] of them): one folded factor
+                // under the contracted arithmetic, gate by gate otherwise (diag_run)
+                int gd = ph.g0;
+                diag_run<R, MODE>(v, S, gd, ph.nd_before[0], tpart, &s_sbase, sc, snz);
                 DIAQ_SUNROLL
-                for (int gi = ph.g0; gi < ph.g1; ++gi) dispatch_gate<R, MODE>(v, S.g[gi], tpart, &s_sbase, sc, snz);
+                for (int gi = ph.g0 + ph.nd_before[0]; gi < ph.g1; ++gi)
+                    dispatch_gate<R, MODE>(v, S.g[gi], tpart, &s_sbase, sc, snz);
             }
             if (ph.post.on) {
                 __syncthreads();  // relabelled slots belong to other threads' registers: all reads first
@@ -931,8 +966,13 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
                 seq_steps<R, MODE, 0>(v, S, ph, gi, tpart, &s_sbase, sc, snz);
                 diag_run<R, MODE>(v, S, gi, ph.nd_before[R], tpart, &s_sbase, sc, snz);
             } else {
+                // leading diagonals on non-register bits (nd_before[0] of them): one folded factor
+                // under the contracted arithmetic, gate by gate otherwise (diag_run)
+                int gd = ph.g0;
+                diag_run<R, MODE>(v, S, gd, ph.nd_before[0], tpart, &s_sbase, sc, snz);
                 DIAQ_SUNROLL
-                for (int gi = ph.g0; gi < ph.g1; ++gi) dispatch_gate<R, MODE>(v, S.g[gi], tpart, &s_sbase, sc, snz);
+                for (int gi = ph.g0 + ph.nd_before[0]; gi < ph.g1; ++gi)
+                    dispatch_gate<R, MODE>(v, S.g[gi], tpart, &s_sbase, sc, snz);
             }
             if (direct) {
                 // register j of this thread = tile position tpart | e_j: state

@@ -72,7 +72,7 @@ def test_contracted_fuzz_every_tile(ref_mode, seed):
     x0 = D.StateVector(n, W.random_state(rng, 2**n))
     want = D.run_gates(x0, pls, cmul_mode=ref_mode, tile_bits=0).amps
     switches = [{}, {"fused_seq": 0}, {"fused_gperm": 0}, {"fused_dense2": 0}, {"fused_lookahead": 0},
-                {"fused_unit": 0}, {"fused_reorder": 0}]
+                {"fused_unit": 0}, {"fused_reorder": 0}, {"fused_slots": 0}, {"fused_maxph": 3}]
     try:
         for sw in switches:
             for k, v in sw.items():
@@ -82,10 +82,12 @@ def test_contracted_fuzz_every_tile(ref_mode, seed):
                 err = rel_l2(got, want)
                 assert err < TOL, (seed, n, tb, sw, err)
             for k in sw:
-                L.tune(k, 1)
+                L.tune(k, 5 if k == "fused_maxph" else 1)
     finally:
-        for k in ("fused_seq", "fused_gperm", "fused_dense2", "fused_lookahead", "fused_unit", "fused_reorder"):
+        for k in ("fused_seq", "fused_gperm", "fused_dense2", "fused_lookahead", "fused_unit", "fused_reorder",
+                  "fused_slots"):
             L.tune(k, 1)
+        L.tune("fused_maxph", 5)
 
 
 @pytest.mark.parametrize("seed", range(3))
