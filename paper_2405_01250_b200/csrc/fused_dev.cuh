@@ -1148,6 +1148,18 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
         // both halves' elements k interleaved: adjacent 128-byte rows in flight together
         auto fetch2 = [&](uint64_t b) {
             const double2 *src = p.x + (b + t_off);
+            if (S.pre.on) {  // a permutation run opens the pass: each half lands relabelled (as fetch())
+                const uint32_t lt0 = s_lt[tid] ^ swz(aff_const(S.pre, b | p.gbase));
+                const uint32_t lt1 = s_lt[tid] ^ swz(aff_const(S.pre, (b | pbit) | p.gbase));
+#pragma unroll
+                for (int k = 0; k < NR; ++k) {
+                    const uint32_t kl = swz(aff_lin(S.pre, (uint32_t)k << TB, T));
+                    cp_async16_s(tile0 + ((lt0 ^ kl) << 4), src + kdep(k));
+                    cp_async16_s(buf1 + ((lt1 ^ kl) << 4), src + (kdep(k) | pbit));
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+                return;
+            }
 #pragma unroll
             for (int k = 0; k < NR; ++k) {
                 const uint32_t sl = swz((uint32_t)k << TB);
@@ -1156,7 +1168,11 @@ __device__ __forceinline__ void tile_pass_body_jit(const TileParams &p, const Ti
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
         };
-        auto fetch1 = [&](uint64_t b, uint32_t a) {  // one half, its own commit group
+        auto fetch1 = [&](uint64_t b, uint32_t a) {  // one half (its base b, buffer address a + t16), its own commit group
+            if (S.pre.on) {
+                fetch(b, a - t16);
+                return;
+            }
             const double2 *src = p.x + (b + t_off);
 #pragma unroll
             for (int k = 0; k < NR; ++k) cp_async16_s(slot_addr(a, swz((uint32_t)k << TB)), src + kdep(k));

@@ -687,6 +687,46 @@ def test_fused_jit_matches_interpreter(cmul, seed):
         L.tune("fused_pair_store", 2)
 
 
+@pytest.mark.parametrize("seed", [8, 13, 21, 34])
+def test_fused_jit_matches_interpreter_more_seeds(cmul, seed):
+    """More circuit shapes through the specialised kernels (seed 8: a pass
+    opening with a permutation run AND running as a plain pair -- the pair
+    fetch once ignored the opening relabelling, r02x)."""
+    n, pls, rng = fuzz_circuit(seed)
+    x0 = D.StateVector(n, W.random_state(rng, 2**n))
+    want = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=0).amps
+    try:
+        L.tune("fused_jit", 2)
+        for tb in (11, 12):
+            assert np.array_equal(D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=tb).amps, want), (seed, n, tb)
+        for knob in ("fused_ppipe",):  # the pipelined pair schedules share the fetch
+            for v in (1, 2):
+                L.tune(knob, v)
+                assert np.array_equal(D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=11).amps, want), (seed, knob, v)
+            L.tune(knob, 0)
+    finally:
+        L.tune("fused_jit", 1)
+        L.tune("fused_ppipe", 0)
+
+
+def test_fused_jit_opening_permutation_plain_pair(cmul):
+    """The minimal form of that case: CX / SWAP opening a pass whose lowest
+    non-tile bit is bit 3 (plain pair), then dense gates, no global tail."""
+    n = 13
+    ops = [("cx", (2, 6), ()), ("swap", (2, 8), ()), ("swap", (10, 1), ()), ("u3", (5,), (0.1, 0.5, 0.2)),
+           ("ry", (7,), (0.9,)), ("rx", (12,), (0.4,)), ("h", (0,), ()), ("rx", (4,), (1.3,))]
+    pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
+    rng = np.random.default_rng(1)
+    x0 = D.StateVector(n, W.random_state(rng, 2**n))
+    want = D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=0).amps
+    try:
+        for jit in (0, 2):
+            L.tune("fused_jit", jit)
+            assert np.array_equal(D.run_gates(x0, pls, cmul_mode=cmul, tile_bits=11).amps, want), jit
+    finally:
+        L.tune("fused_jit", 1)
+
+
 def test_fused_jit_layer_n24_async(cmul):
     """The default (asynchronous) mode: the first calls run the AOT kernel
     while the passes compile, later calls the specialised kernels -- the
