@@ -62,6 +62,17 @@ def test_contracted_config3_vs_oracle(ref_mode):
     err = rel_l2(res.state, want)
     assert err < TOL, err
     assert abs(np.linalg.norm(res.state) - 1.0) < 1e-12
+    # the same program with every specialised kernel compiled before it runs
+    # (the default compiles in the background and interprets meanwhile), in
+    # both numerics: 1e-12 contracted, bitwise with the reference rounding
+    pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
+    try:
+        L.tune("fused_jit", 2)
+        got = D.run_gates(D.init_state(n), pls, cmul_mode=C).amps
+        assert rel_l2(got, want) < TOL
+        assert np.array_equal(D.run_gates(D.init_state(n), pls, cmul_mode=ref_mode).amps, want)
+    finally:
+        L.tune("fused_jit", 1)
 
 
 @pytest.mark.parametrize("seed", range(6))

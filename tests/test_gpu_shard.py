@@ -119,8 +119,38 @@ def test_sharded_fuzz(cmul, seed):
     targets on global bits, CZ, CCX, Haar4) on emulated shards: fused local
     runs with rank-dependent controls, permutation tails, and exchanges,
     bitwise against the single-state run."""
+    n, pls = _shard_fuzz_circuit(seed, 12, 17)
+    want = D.run_gates(D.init_state(n), pls, cmul_mode=cmul).amps
+    for world in (2, 4):
+        shards, _ = run_emulated(n, world, pls, cmul_mode=cmul)
+        assert np.array_equal(_full(shards), want), (seed, n, world)
+
+
+@pytest.mark.parametrize("seed", range(4, 10))
+def test_sharded_fuzz_specialised_passes(cmul, seed):
+    """The same circuits on shards large enough for tiled passes, with the
+    NVRTC-specialised kernels compiled before they run (fused_jit 2: rank
+    bits in the selector base, rank-dependent constants of the permutation
+    maps): bitwise against the single-state run, and within 1e-12 under the
+    contracted arithmetic."""
+    from paper_2405_01250_b200 import _lib as L
+    n, pls = _shard_fuzz_circuit(seed, 15, 19)
+    want = D.run_gates(D.init_state(n), pls, cmul_mode=cmul).amps
+    try:
+        L.tune("fused_jit", 2)
+        for world in (2, 4):
+            shards, _ = run_emulated(n, world, pls, cmul_mode=cmul)
+            assert np.array_equal(_full(shards), want), (seed, n, world)
+            shards, _ = run_emulated(n, world, pls, cmul_mode=L.CMUL_CONTRACT)
+            got = _full(shards)
+            assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-12, (seed, n, world)
+    finally:
+        L.tune("fused_jit", 1)
+
+
+def _shard_fuzz_circuit(seed, nlo, nhi):
     rng = np.random.default_rng(500 + seed)
-    n = int(rng.integers(12, 17))
+    n = int(rng.integers(nlo, nhi))
     ops = []
     for _ in range(int(rng.integers(30, 60))):
         q = [int(v) for v in rng.choice(np.arange(2, n), size=3, replace=False)]  # qubits 0, 1: the global bits
@@ -143,7 +173,4 @@ def test_sharded_fuzz(cmul, seed):
     a, b = (int(v) for v in rng.choice(n, size=2, replace=False))
     lo, hi = min(a, b), max(a, b)
     pls.append(D.Placement(2**lo, None, 2 ** (n - 1 - hi), lo, hi, "haar", gate=(W.haar(rng, 4), [a - lo, b - lo])))
-    want = D.run_gates(D.init_state(n), pls, cmul_mode=cmul).amps
-    for world in (2, 4):
-        shards, _ = run_emulated(n, world, pls, cmul_mode=cmul)
-        assert np.array_equal(_full(shards), want), (seed, n, world)
+    return n, pls
