@@ -75,7 +75,13 @@ void diaq_reset_launch_count(void);
 /* launch-geometry knobs (never change results): "spmv_raster" (0 strip-
  * fastest, 1 column chunks), "spmv_chunk", "spmv_xpol" (0 normal, 1 L2
  * evict_last for x), "spmv_ctas_per_sm" (0 = occupancy max),
- * "gate_ctas_per_sm" */
+ * "gate_ctas_per_sm"; the "fused_*" switches of the multi-gate passes
+ * (csrc/common.cuh lists them) never change results in the bitwise
+ * numerics modes.  Under DIAQ_CMUL_CONTRACT the schedule switches
+ * ("fused_reorder", "fused_lookahead", "fused_slots", "fused_maxph",
+ * "fused_slot_gates", "fused_unit") pick which gates share a pass and in
+ * which form they are applied: the state stays within the mode's 1e-12
+ * tolerance, and is deterministic for a given setting */
 int diaq_tune(const char *key, int64_t value);
 
 /* ---- layout (host only) ----------------------------------------------

@@ -176,17 +176,22 @@ def test_fused_schedule_lookahead_host_only(lib):
     import paper_2405_01250_b200 as D
     from paper_2405_01250_b200.sim import _GateProgram
 
+    phases = {}
+
     def passes(n, ops, mode):
         pls = D.compile_circuit(D.Circuit(n, [D.GateOp(*o) for o in ops]), span_limit=n)
         prog = _GateProgram([p.compact() for p in pls])
         st = (ctypes.c_int * 5)()
         L.check(lib.diaq_fused_plan_mode(n, n, prog.n, prog.arr, 0, mode, st), "diaq_fused_plan_mode")
-        assert st[3] == sum(1 for o in ops if o[0] == "cx")  # every CX folded, none executed
+        assert st[3] == sum(1 for o in ops if o[0] == "cx")  # every CX folded or a register exchange, none executed
+        assert st[1] == 0 and st[4] == 0
+        phases[(n, mode)] = st[2]
         return st[0]
 
     ops = W.random_layered_ops(30, 20, seed=0)
     inorder = passes(30, ops, L.CMUL_FMA)
     look = passes(30, ops, L.CMUL_CONTRACT)
+    ph_slots = phases[(30, L.CMUL_CONTRACT)]
     L.tune("fused_lookahead", 0)
     try:
         first_fit = passes(30, ops, L.CMUL_CONTRACT)
@@ -195,6 +200,15 @@ def test_fused_schedule_lookahead_host_only(lib):
         L.tune("fused_lookahead", 1)
     assert look < first_fit < inorder
     assert look <= 0.6 * inorder
+    # phase slots: several layers' gates per phase -- fewer shared-memory round
+    # trips at about the same pass count, and never more than the cap per pass
+    assert ph_slots <= 5 * look
+    L.tune("fused_slots", 0)
+    try:
+        flat = passes(30, ops, L.CMUL_CONTRACT)
+        assert ph_slots < phases[(30, L.CMUL_CONTRACT)] and look <= flat + 2
+    finally:
+        L.tune("fused_slots", 1)
     one = W.random_layered_ops(28, 1, seed=0)
     assert passes(28, one, L.CMUL_CONTRACT) == passes(28, one, L.CMUL_FMA) == 2
 
